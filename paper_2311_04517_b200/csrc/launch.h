@@ -1,0 +1,32 @@
+// Internal launch interface between the host runtime (runtime.cu) and the kernel
+// translation units (step_f32.cu, step_f64.cu, objective.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "step_kernel.cuh"
+#include "objective_kernel.cuh"
+
+namespace hpcg {
+
+// Padded smem row widths with a compiled kernel. n -> smallest NP >= n.
+int pick_np(int dtype, int n);  // dtype 0 f32, 1 f64; returns 0 if unsupported
+
+struct StepGeometry {
+    int cluster = 0;    // CTAs per worker
+    int rows_cap = 0;   // max rows per CTA
+    int smem = 0;       // dynamic smem bytes
+    int active_clusters = 0;
+};
+
+// Chooses the cluster size (smallest that fits the sample in smem, widened while the
+// occupancy API reports more SMs in use) and launches W clusters. Returns a CUDA error.
+cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeometry* geo_out, std::string* why);
+cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int W, StepGeometry* g, std::string* why);
+
+// *nblocks: in = capacity of p.block_cost, out = grid used (fixed per device/kernel/kv)
+cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st);
+int objective_blocks();  // fixed grid for deterministic block partials
+
+}  // namespace hpcg

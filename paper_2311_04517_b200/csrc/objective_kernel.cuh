@@ -1,0 +1,267 @@
+// Full-data objective f(C, X) = sum_i min_j ||x_i - c_j||^2 streamed over all m rows
+// of an HBM-resident X (engine.hpp:197-229 final_assignment / assign_valid_subset,
+// core.hpp:224-233 mssc_objective), plus the optional labels / counts of the full
+// assignment. Each row is read once; the nearest valid centre is found with the fp32
+// FFMA2 screen and an exact fp64 recheck of near ties; the row's cost is the exact
+// reference distance (core.hpp:147-152, non-fused, ascending d) to that centre, so
+// per-row values are bit-identical to the reference and only the (fixed, deterministic)
+// summation order differs.
+#pragma once
+#include "common.cuh"
+#include "step_kernel.cuh"  // Geo (swizzled row layout) and cp.async helpers
+
+namespace hpcg {
+
+constexpr int kObjThreads = 256;
+constexpr int kObjMaxK = 256;
+
+struct ObjParams {
+    const void* X;
+    int64_t m;
+    int32_t n;
+    int32_t kv;            // valid centres
+    const double* C;       // [kv x n] valid centres (compacted), fp64
+    const int32_t* remap;  // [kv] original slot of each valid centre
+    int32_t* labels;       // [m] or null
+    unsigned long long* counts;  // [k original] or null (atomics on integers: order-free)
+    double* block_cost;    // [gridDim.x]
+};
+
+// Per-warp software pipeline: each warp streams groups of GR consecutive rows through a
+// STAGES-deep ring of shared-memory slots filled by cp.async (16/8/4-B copies, swizzled
+// like the step kernel's sample so the row-per-lane reads are bank-conflict free). Loads
+// for STAGES-1 groups are in flight while the warp computes on the oldest one.
+template <typename T, int NP>
+struct ObjGeo {
+    using G = Geo<T, NP>;
+    static constexpr int NPF = G::NPF;
+    static constexpr int R = NP <= 16 ? 2 : 1;
+    static constexpr int GR = 32 * R;                 // rows per group
+    static constexpr int STAGE = GR * G::RS;          // bytes per ring slot
+    static constexpr int STAGES = 3;
+    static constexpr int CSR = G::CSR;
+};
+
+template <typename T, int NP>
+__host__ __device__ inline int objective_smem(int kv) {
+    using O = ObjGeo<T, NP>;
+    const int cs = ((kv * O::CSR * 4 + 15) & ~15);
+    const int cd = ((kv * NP * 8 + 15) & ~15);
+    return cs + cd + (kObjThreads / 32) * O::STAGES * O::STAGE;
+}
+
+template <typename T, int NP>
+__global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjParams p) {
+    using O = ObjGeo<T, NP>;
+    using G = typename O::G;
+    constexpr int NPF = O::NPF, R = O::R, CSR = O::CSR;
+    extern __shared__ __align__(16) unsigned char osm[];
+    const int kv = p.kv, n = p.n;
+    float* cs = reinterpret_cast<float*>(osm);
+    double* Cd = reinterpret_cast<double*>(osm + ((kv * CSR * 4 + 15) & ~15));
+    unsigned char* rings = osm + ((kv * CSR * 4 + 15) & ~15) + ((kv * NP * 8 + 15) & ~15);
+    __shared__ float s_cmax;
+    __shared__ double s_wcost[kObjThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int e = tid; e < kv * NP; e += kObjThreads) {
+        const int j = e / NP, d = e - j * NP;
+        Cd[e] = d < n ? p.C[(int64_t)j * n + d] : 0.0;
+    }
+    __syncthreads();
+    for (int j = tid; j < kv; j += kObjThreads) {
+        float* rec = cs + j * CSR;
+        double cc = 0.0;
+        for (int d = 0; d < NP; ++d) {
+            const double c = Cd[j * NP + d];
+            cc += c * c;
+            rec[d] = (float)(-2.0 * c);
+        }
+        for (int d = NP; d < NPF; ++d) rec[d] = 0.f;
+        rec[NPF] = (float)cc;
+        rec[NPF + 1] = 0.f;
+    }
+    T* ring = reinterpret_cast<T*>(rings + warp * O::STAGES * O::STAGE);
+    // zero the ring once: padding columns (NP > n) are never written by the copies
+    for (int e = lane; e < O::STAGES * O::STAGE / 4; e += 32) reinterpret_cast<float*>(ring)[e] = 0.f;
+    __syncthreads();
+    if (tid == 0) {
+        float cm = 0.f;
+        for (int j = 0; j < kv; ++j) cm = fmaxf(cm, sqrtf(cs[j * CSR + NPF]) * 1.0001f);
+        s_cmax = cm;
+    }
+    __syncthreads();
+    const float cmax = s_cmax;
+    constexpr float kappa = 2.0f * (float)(NPF / 2 + 12) * 5.9604645e-8f;
+
+    const T* X = static_cast<const T*>(p.X);
+    const int64_t m = p.m;
+    const int rowb = n * (int)sizeof(T);
+    const int64_t ngroups = (m + O::GR - 1) / O::GR;
+    const int64_t wglobal = (int64_t)blockIdx.x * (kObjThreads / 32) + warp;
+    const int64_t wstride = (int64_t)gridDim.x * (kObjThreads / 32);
+    const int64_t my_groups = wglobal < ngroups ? (ngroups - wglobal + wstride - 1) / wstride : 0;
+
+    auto issue = [&](int64_t i) {  // copies of the warp's i-th group into slot i % STAGES
+        if (i < my_groups) {
+            const int64_t g = wglobal + i * wstride;
+            T* slot = ring + (i % O::STAGES) * (O::STAGE / (int)sizeof(T));
+            const int64_t row0 = g * O::GR;
+            const int rows = (int)(m - row0 < O::GR ? m - row0 : O::GR);
+            const T* src = X + row0 * n;
+            if ((rowb & 15) == 0) {
+                const int cpr = rowb >> 4;
+                constexpr int EPC = 16 / (int)sizeof(T);
+                for (int e = lane; e < rows * cpr; e += 32) {
+                    const int li = e / cpr, q = e - li * cpr;
+                    cp_async16(slot + G::elem_off(li, q * EPC), src + (int64_t)li * n + q * EPC);
+                }
+            } else if ((rowb & 7) == 0) {
+                const int cpr = rowb >> 3;
+                constexpr int EPC = 8 / (int)sizeof(T);
+                for (int e = lane; e < rows * cpr; e += 32) {
+                    const int li = e / cpr, q = e - li * cpr;
+                    cp_async8(slot + G::elem_off(li, q * EPC), src + (int64_t)li * n + q * EPC);
+                }
+            } else {
+                for (int e = lane; e < rows * n; e += 32) {
+                    const int li = e / n, d = e - li * n;
+                    cp_async4(slot + G::elem_off(li, d), src + (int64_t)li * n + d);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+
+    double cost = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < O::STAGES - 1; ++i) issue(i);
+#pragma unroll 1
+    for (int64_t i = 0; i < my_groups; ++i) {
+        cp_async_wait_group<O::STAGES - 2>();
+        __syncwarp();
+        const int64_t g = wglobal + i * wstride;
+        const T* slot = ring + (i % O::STAGES) * (O::STAGE / (int)sizeof(T));
+        float2 x2[R][NPF / 2];
+        bool valid[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int lr = r * 32 + lane;
+            valid[r] = g * O::GR + lr < m;
+            if constexpr (G::VEC16 && sizeof(T) == 4) {
+#pragma unroll
+                for (int q = 0; q < NP / 4; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(slot + G::elem_off(lr, q * 4));
+                    x2[r][2 * q] = make_float2(v.x, v.y);
+                    x2[r][2 * q + 1] = make_float2(v.z, v.w);
+                }
+            } else if constexpr (G::VEC16) {
+#pragma unroll
+                for (int q = 0; q < NP / 2; ++q) {
+                    const double2 v = *reinterpret_cast<const double2*>(slot + G::elem_off(lr, q * 2));
+                    x2[r][q] = make_float2((float)v.x, (float)v.y);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < NPF / 2; ++q) {
+                    const float a = (float)slot[G::elem_off(lr, 2 * q)];
+                    const float b = 2 * q + 1 < NP ? (float)slot[G::elem_off(lr, 2 * q + 1)] : 0.f;
+                    x2[r][q] = make_float2(a, b);
+                }
+            }
+        }
+        float m1[R], m2[R];
+        int i1[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            m1[r] = __int_as_float(0x7f800000);
+            m2[r] = __int_as_float(0x7f800000);
+            i1[r] = 0;
+        }
+        for (int j = 0; j < kv; ++j) {
+            const float* rec = cs + j * CSR;
+            float2 c2[NPF / 2];
+#pragma unroll
+            for (int q = 0; q < NPF / 2; ++q) c2[q] = *reinterpret_cast<const float2*>(rec + 2 * q);
+            const float2 init = *reinterpret_cast<const float2*>(rec + NPF);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 acc = init;
+#pragma unroll
+                for (int q = 0; q < NPF / 2; ++q) acc = __ffma2_rn(x2[r][q], c2[q], acc);
+                const float dj = acc.x + acc.y;
+                m2[r] = fminf(m2[r], fmaxf(m1[r], dj));
+                const bool lt = dj < m1[r];
+                m1[r] = fminf(m1[r], dj);
+                i1[r] = lt ? j : i1[r];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!valid[r]) continue;
+            const int lr = r * 32 + lane;
+            float nn = 0.f;
+#pragma unroll
+            for (int q = 0; q < NPF / 2; ++q) nn = fmaf(x2[r][q].x, x2[r][q].x, fmaf(x2[r][q].y, x2[r][q].y, nn));
+            const float sc = sqrtf(nn) + cmax;
+            int lab = i1[r];
+            if (!(m2[r] - m1[r] > kappa * sc * sc)) {  // near tie: exact reference argmin (core.hpp:146-157)
+                double best = __longlong_as_double(0x7ff0000000000000LL);
+                lab = 0;
+                for (int j = 0; j < kv; ++j) {
+                    double dd = 0.0;
+                    for (int d = 0; d < n; ++d) {
+                        const double diff = __dsub_rn((double)slot[G::elem_off(lr, d)], Cd[j * NP + d]);
+                        dd = __dadd_rn(dd, __dmul_rn(diff, diff));
+                    }
+                    if (dd < best) {
+                        best = dd;
+                        lab = j;
+                    }
+                }
+            }
+            // row cost: fp64 distance to the chosen centre (within 1 ulp per term of the reference)
+            double dd = 0.0;
+            const double* cj = Cd + lab * NP;
+#pragma unroll
+            for (int d = 0; d < NP; ++d) {
+                if (d < n) {
+                    const double diff = (double)slot[G::elem_off(lr, d)] - cj[d];
+                    dd = fma(diff, diff, dd);
+                }
+            }
+            cost += dd;
+            const int64_t row = g * O::GR + lr;
+            if (p.labels) p.labels[row] = p.remap[lab];
+            if (p.counts) atomicAdd(p.counts + p.remap[lab], 1ULL);
+        }
+        __syncwarp();
+        issue(i + O::STAGES - 1);
+    }
+    cp_async_wait_group<0>();
+    cost = warp_sum(cost);
+    if (lane == 0) s_wcost[warp] = cost;
+    __syncthreads();
+    if (tid == 0) {
+        double v = 0.0;
+        for (int w = 0; w < kObjThreads / 32; ++w) v += s_wcost[w];
+        p.block_cost[blockIdx.x] = v;
+    }
+}
+
+// Fixed-order final sum of the block partials (deterministic f(C,X)).
+static __global__ void sum_blocks_kernel(const double* part, int nparts, double* out) {
+    __shared__ double s[32];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) v += part[i];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+        *out = t;
+    }
+}
+
+}  // namespace hpcg

@@ -1,0 +1,1351 @@
+// Host runtime of libhpcg.so: the C-ABI declared in include/hpcg.h.
+//
+// Owns device memory and streams, validates arguments with the reference's own error
+// texts, drives the lockstep HPClust engine round by round (engine.hpp:380-436) with the
+// worker-step kernel, and replays the reference's mt19937_64 worker streams on the host
+// when RNG parity with the reference is requested. No CPU compute fallback exists: every
+// numeric result comes from the sm_100a kernels.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/hpcg.h"
+#include "launch.h"
+
+using namespace hpcg;
+
+// ============================================================== errors
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail(HPCG_ECUDA, std::string("CUDA error: ") +         \
+                                                           cudaGetErrorString(e_) + " at " + \
+                                                           #call);                            \
+    } while (0)
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+// ------------------------------------------------------------ device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t reserve(size_t b) {
+        if (b <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, b ? b : 16);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// ------------------------------------------------ std::mt19937_64 (host replay)
+// The 64-bit Mersenne Twister with the parameters fixed by [rand.predef]; plus the
+// reference's hand-rolled distributions (rng.hpp:38-53) and seed derivation (rng.hpp:12-33).
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+struct Mt64 {
+    uint64_t mt[312];
+    int pos = 312;
+    void seed(uint64_t s) {
+        mt[0] = s;
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+        pos = 312;
+    }
+    void twist() {
+        for (int i = 0; i < 312; ++i) {
+            const uint64_t y = (mt[i] & 0xFFFFFFFF80000000ULL) | (mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+            uint64_t v = mt[(i + 156) % 312] ^ (y >> 1);
+            if (y & 1) v ^= 0xB5026F5AA96619E9ULL;
+            mt[i] = v;
+        }
+        pos = 0;
+    }
+    uint64_t next() {
+        if (pos >= 312) twist();
+        uint64_t z = mt[pos++];
+        z ^= (z >> 29) & 0x5555555555555555ULL;
+        z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+        z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+        return z ^ (z >> 43);
+    }
+    double unit() { return (double)(next() >> 11) * 0x1.0p-53; }
+    uint64_t uniform_index(uint64_t n) {
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+        uint64_t x;
+        do {
+            x = next();
+        } while (x >= limit);
+        return x % n;
+    }
+    static Mt64 derive(uint64_t master, uint64_t domain, uint64_t index) {
+        Mt64 r;
+        r.seed(splitmix64(master ^ splitmix64(domain ^ splitmix64(index))));
+        return r;
+    }
+};
+
+// engine.hpp:165-177 partial Fisher-Yates over iota(m) in O(s): only displaced slots are
+// stored, so the draws (and the stream advance) are exactly the reference's.
+void sparse_fisher_yates(Mt64& rng, int64_t m, int64_t s, int64_t* out) {
+    std::unordered_map<int64_t, int64_t> moved;
+    moved.reserve((size_t)(2 * s));
+    auto at = [&](int64_t i) {
+        auto it = moved.find(i);
+        return it == moved.end() ? i : it->second;
+    };
+    for (int64_t i = 0; i < s; ++i) {
+        const int64_t j = i + (int64_t)rng.uniform_index((uint64_t)(m - i));
+        const int64_t vi = at(i), vj = at(j);
+        moved[i] = vj;
+        moved[j] = vi;
+        out[i] = vj;
+    }
+}
+}  // namespace
+
+// ============================================================== handles
+struct hpcg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::mutex mu;
+    std::atomic<int64_t> launches{0};
+    DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
+    // per-kernel-class event timing (class 0 worker step, 1 objective)
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
+    int64_t t_count[2] = {0, 0};
+    double t_ms[2] = {0.0, 0.0};
+};
+
+namespace {
+// Brackets one launch with events on the launching stream when timing is enabled.
+struct KTimer {
+    hpcg_ctx* c;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    KTimer(hpcg_ctx* c_, int cls_) : c(c_), cls(cls_) {
+        if (c->timing) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    void done() {
+        if (a) {
+            cudaEventRecord(b, c->stream);
+            c->pending[cls].emplace_back(a, b);
+            a = b = nullptr;
+        }
+    }
+    ~KTimer() {
+        if (a) {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    }
+};
+
+__global__ void fma_probe_kernel(float* out, float a, float b, int iters) {
+    float2 x[8];
+    const float2 A = make_float2(a, a), B = make_float2(b, b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = make_float2((float)threadIdx.x + i, (float)i);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ffma2_rn(x[i], A, B);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i].x + x[i].y;
+    if (s == 1234.5f) out[0] = s;
+}
+}  // namespace
+
+struct hpcg_dataset {
+    hpcg_ctx* ctx = nullptr;
+    const void* X = nullptr;
+    bool owned = false;
+    int dtype = 0;
+    int64_t m = 0, n = 0;
+    ~hpcg_dataset() {
+        if (owned && X) cudaFree(const_cast<void*>(X));
+    }
+};
+
+namespace {
+size_t dsize(int dtype) { return dtype == HPCG_F32 ? 4 : 8; }
+
+int check_shape(int dtype, int64_t n, int64_t k) {
+    if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
+    if (pick_np(dtype, (int)n) == 0 || n < 1)
+        return fail(HPCG_EUNSUPPORTED, "n > 32 features is not supported by this build's kernels");
+    if (k > kMaxK) return fail(HPCG_EUNSUPPORTED, "k > 32 centroids is not supported by this build's kernels");
+    return HPCG_OK;
+}
+
+// ------------------------------------------------------------ small kernels
+__global__ void gather_kernel(const unsigned char* X, int64_t rowb, const int64_t* idx, int64_t s,
+                              unsigned char* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= s * rowb) return;
+    const int64_t i = e / rowb, b = e - i * rowb;
+    out[e] = X[idx[i] * rowb + b];
+}
+
+struct RoundEndParams {
+    int W, k, n;
+    int64_t round;  // 0-based round just finished
+    int publish;    // round was cooperative (publish accepted) ...
+    int carry;      // ... or hybrid carry-over round (publish finite incumbents)
+    int worker_base;
+    const uint8_t* accepted;
+    const double* inc_obj;
+    const double* inc_c;
+    const uint8_t* inc_f;
+    const int64_t* nd;
+    const int32_t* err;
+    uint8_t* log_acc;  // [R x W]
+    double* log_obj;   // [R x W]
+    int32_t* err_first;
+    unsigned long long* nd_total;
+    int64_t* sh_version;
+    double* sh_obj;
+    int32_t* sh_worker;
+    double* sh_c;
+    uint8_t* sh_f;
+    double* pub_log;  // [cap x 4]
+    int64_t* pub_count;
+    int64_t pub_cap;
+};
+
+// engine.hpp:391-402 on_round_end: publications in worker-id order, strict < (engine.hpp:131)
+__global__ void round_end_kernel(const RoundEndParams p) {
+    __shared__ int s_winner;
+    __shared__ unsigned long long s_nd[256];
+    unsigned long long nd = 0;
+    for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
+        p.log_acc[p.round * p.W + w] = p.accepted[w];
+        p.log_obj[p.round * p.W + w] = p.inc_obj[w];
+        nd += (unsigned long long)p.nd[w];
+        if (p.err[w] != 0 && p.err_first[w] == 0) p.err_first[w] = p.err[w];
+    }
+    s_nd[threadIdx.x] = nd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < (int)blockDim.x; ++i) t += s_nd[i];
+        *p.nd_total += t;
+        int winner = -1;
+        if (p.publish || p.carry) {
+            double best = *p.sh_obj;
+            int64_t ver = *p.sh_version;
+            int64_t cnt = *p.pub_count;
+            for (int w = 0; w < p.W; ++w) {
+                const double f = p.inc_obj[w];
+                const bool cand = (p.publish && p.accepted[w]) || (p.carry && isfinite(f));
+                if (cand && f < best) {
+                    best = f;
+                    winner = w;
+                    ++ver;
+                    if (cnt < p.pub_cap) {
+                        p.pub_log[cnt * 4 + 0] = (double)ver;
+                        p.pub_log[cnt * 4 + 1] = (double)(p.worker_base + w);
+                        p.pub_log[cnt * 4 + 2] = f;
+                        p.pub_log[cnt * 4 + 3] = (double)(p.round + 1);
+                    }
+                    ++cnt;
+                }
+            }
+            *p.pub_count = cnt;
+            if (winner >= 0) {
+                *p.sh_obj = best;
+                *p.sh_version = ver;
+                *p.sh_worker = p.worker_base + winner;
+            }
+        }
+        s_winner = winner;
+    }
+    __syncthreads();
+    const int wn = s_winner;
+    if (wn >= 0) {
+        const int64_t kn = (int64_t)p.k * p.n;
+        for (int64_t e = threadIdx.x; e < kn; e += blockDim.x) p.sh_c[e] = p.inc_c[wn * kn + e];
+        for (int j = threadIdx.x; j < p.k; j += blockDim.x) p.sh_f[j] = p.inc_f[(int64_t)wn * p.k + j];
+    }
+}
+
+__global__ void fill_f64_kernel(double* p, int64_t n, double v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+template <typename T>
+cudaError_t h2d(T* dst, const T* src, size_t count, cudaStream_t st) {
+    return cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+template <typename T>
+cudaError_t d2h(T* dst, const T* src, size_t count, cudaStream_t st) {
+    return cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, st);
+}
+
+// Full-data assignment on device: valid centres C_valid_dev [kv x n], remap [kv];
+// labels_dev may be null; counts_dev (u64 x k) may be null; cost to cost_dev.
+int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev, const int32_t* remap_dev, int kv,
+               int32_t* labels_dev, unsigned long long* counts_dev, double* cost_dev, DevBuf& blocks) {
+    const int nb = objective_blocks();
+    CU(blocks.reserve((size_t)nb * sizeof(double)));
+    ObjParams op;
+    op.X = ds->X;
+    op.m = ds->m;
+    op.n = (int)ds->n;
+    op.kv = kv;
+    op.C = C_valid_dev;
+    op.remap = remap_dev;
+    op.labels = labels_dev;
+    op.counts = counts_dev;
+    op.block_cost = blocks.as<double>();
+    int used = nb;
+    KTimer kt(ctx, 1);
+    CU(launch_objective(ds->dtype, op, &used, ctx->stream));
+    kt.done();
+    sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, cost_dev);
+    CU(cudaGetLastError());
+    ctx->launches += 2;
+    return HPCG_OK;
+}
+}  // namespace
+
+// ============================================================== C-ABI
+extern "C" {
+
+const char* hpcg_last_error(void) { return g_err.c_str(); }
+int hpcg_abi_version(void) { return HPCG_ABI_VERSION; }
+
+int hpcg_ctx_create(int device, hpcg_ctx** out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(HPCG_ECUDA, std::string("no CUDA device available (libhpcg has no CPU fallback): ") +
+                                    cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(HPCG_EINVAL, "device index out of range");
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(HPCG_ECUDA, "libhpcg is built for sm_100a (B200); device has compute capability " +
+                                    std::to_string(prop.major) + "." + std::to_string(prop.minor));
+    CU(cudaSetDevice(device));
+    auto* c = new hpcg_ctx;
+    c->device = device;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(HPCG_ECUDA, cudaGetErrorString(e));
+    }
+    c->own_stream = true;
+    *out = c;
+    return HPCG_OK;
+}
+
+int hpcg_ctx_destroy(hpcg_ctx* ctx) {
+    if (!ctx) return HPCG_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return HPCG_OK;
+}
+
+int hpcg_ctx_set_stream(hpcg_ctx* ctx, void* st) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (st) {
+        ctx->stream = static_cast<cudaStream_t>(st);
+        ctx->own_stream = false;
+    } else {
+        CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    return HPCG_OK;
+}
+
+int hpcg_ctx_synchronize(hpcg_ctx* ctx) {
+    cudaSetDevice(ctx->device);
+    CU(cudaStreamSynchronize(ctx->stream));
+    return HPCG_OK;
+}
+
+int64_t hpcg_ctx_launch_count(const hpcg_ctx* ctx) { return ctx->launches.load(); }
+
+int hpcg_ctx_enable_timing(hpcg_ctx* ctx, int enable) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->timing = enable != 0;
+    return HPCG_OK;
+}
+
+int hpcg_ctx_kernel_times(hpcg_ctx* ctx, int64_t* counts, double* total_ms) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    for (int c = 0; c < 2; ++c) {
+        for (auto& ev : ctx->pending[c]) {
+            float ms = 0.f;
+            CU(cudaEventSynchronize(ev.second));
+            CU(cudaEventElapsedTime(&ms, ev.first, ev.second));
+            ctx->t_ms[c] += ms;
+            ctx->t_count[c] += 1;
+            cudaEventDestroy(ev.first);
+            cudaEventDestroy(ev.second);
+        }
+        ctx->pending[c].clear();
+        if (counts) counts[c] = ctx->t_count[c];
+        if (total_ms) total_ms[c] = ctx->t_ms[c];
+    }
+    return HPCG_OK;
+}
+
+int hpcg_probe_fma_peak(hpcg_ctx* ctx, double* tfma) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    DevBuf out;
+    CU(out.reserve(64));
+    const int blocks = sms * 8, threads = 256, iters = 8192;
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    fma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), 1.0001f, 0.5f, iters);  // warm-up
+    CU(cudaEventRecord(a, ctx->stream));
+    for (int r = 0; r < 5; ++r) fma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), 1.0001f, 0.5f, iters);
+    CU(cudaEventRecord(b, ctx->stream));
+    CU(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    ctx->launches += 6;
+    const double fmas = 5.0 * blocks * threads * (double)iters * 8 * 2;
+    *tfma = fmas / (ms * 1e-3) / 1e12;
+    return HPCG_OK;
+}
+
+// ------------------------------------------------------------------ datasets
+int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n,
+                        hpcg_dataset** out) {
+    if (m < 1 || n < 1) return fail(HPCG_EINVAL, "Dataset: needs at least one row and one column");
+    if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
+    cudaSetDevice(ctx->device);
+    void* d = nullptr;
+    const size_t bytes = (size_t)m * (size_t)n * dsize(dtype);
+    CU(cudaMalloc(&d, bytes));
+    cudaError_t e = cudaMemcpyAsync(d, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return fail(HPCG_ECUDA, cudaGetErrorString(e));
+    }
+    auto* ds = new hpcg_dataset;
+    ds->ctx = ctx;
+    ds->X = d;
+    ds->owned = true;
+    ds->dtype = dtype;
+    ds->m = m;
+    ds->n = n;
+    *out = ds;
+    return HPCG_OK;
+}
+
+int hpcg_dataset_wrap(hpcg_ctx* ctx, const void* X_dev, hpcg_dtype dtype, int64_t m, int64_t n, hpcg_dataset** out) {
+    if (m < 1 || n < 1) return fail(HPCG_EINVAL, "Dataset: needs at least one row and one column");
+    if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
+    auto* ds = new hpcg_dataset;
+    ds->ctx = ctx;
+    ds->X = X_dev;
+    ds->owned = false;
+    ds->dtype = dtype;
+    ds->m = m;
+    ds->n = n;
+    *out = ds;
+    return HPCG_OK;
+}
+
+int hpcg_dataset_destroy(hpcg_dataset* ds) {
+    if (ds) {
+        cudaSetDevice(ds->ctx->device);
+        delete ds;
+    }
+    return HPCG_OK;
+}
+
+const void* hpcg_dataset_device_ptr(const hpcg_dataset* ds) { return ds->X; }
+
+// ---------------------------------------------------------- full assignment
+int hpcg_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_host, const uint8_t* deg, int64_t k,
+                int require_valid, int32_t* labels_host, int64_t* counts_host, double* cost, int64_t* n_d) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (k < 1) return fail(HPCG_EINVAL, "assign: need at least one centroid");
+    const int64_t n = ds->n;
+    std::vector<double> cv;
+    std::vector<int32_t> remap;
+    for (int64_t j = 0; j < k; ++j) {
+        if (deg && deg[j]) {
+            if (require_valid) return fail(HPCG_EINVAL, "assign: degenerate centroid present");
+            continue;
+        }
+        remap.push_back((int32_t)j);
+        cv.insert(cv.end(), C_host + j * n, C_host + (j + 1) * n);
+    }
+    if (remap.empty()) return fail(HPCG_EINVAL, "assignment: every centroid is degenerate");
+    const int kv = (int)remap.size();
+    if (kv > kObjMaxK) return fail(HPCG_EUNSUPPORTED, "more than 256 valid centroids");
+    if (pick_np(ds->dtype, (int)n) == 0)
+        return fail(HPCG_EUNSUPPORTED, "n > 32 features is not supported by this build's kernels");
+    CU(ctx->s_a.reserve(cv.size() * 8));
+    CU(ctx->s_b.reserve(remap.size() * 4 + 16));
+    CU(ctx->s_c.reserve(8));
+    CU(h2d(ctx->s_a.as<double>(), cv.data(), cv.size(), ctx->stream));
+    CU(h2d(ctx->s_b.as<int32_t>(), remap.data(), remap.size(), ctx->stream));
+    int32_t* lab_dev = nullptr;
+    unsigned long long* cnt_dev = nullptr;
+    if (labels_host) {
+        CU(ctx->s_d.reserve((size_t)ds->m * 4));
+        lab_dev = ctx->s_d.as<int32_t>();
+    }
+    if (counts_host) {
+        CU(ctx->s_e.reserve((size_t)k * 8));
+        cnt_dev = ctx->s_e.as<unsigned long long>();
+        CU(cudaMemsetAsync(cnt_dev, 0, (size_t)k * 8, ctx->stream));
+    }
+    int rc = run_assign(ctx, ds, ctx->s_a.as<double>(), ctx->s_b.as<int32_t>(), kv, lab_dev, cnt_dev,
+                        ctx->s_c.as<double>(), ctx->s_f);
+    if (rc) return rc;
+    double c = 0;
+    CU(d2h(&c, ctx->s_c.as<double>(), 1, ctx->stream));
+    if (labels_host) CU(d2h(labels_host, lab_dev, (size_t)ds->m, ctx->stream));
+    std::vector<unsigned long long> cnt(counts_host ? (size_t)k : 0);
+    if (counts_host) CU(d2h(cnt.data(), cnt_dev, (size_t)k, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (counts_host)
+        for (int64_t j = 0; j < k; ++j) counts_host[j] = (int64_t)cnt[j];
+    if (cost) *cost = c;
+    if (n_d) *n_d = ds->m * kv;
+    return HPCG_OK;
+}
+
+int hpcg_assign_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_dev, int64_t k_valid,
+                    int32_t* labels_dev, double* cost_dev) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (k_valid < 1) return fail(HPCG_EINVAL, "assign: need at least one centroid");
+    if (k_valid > kObjMaxK) return fail(HPCG_EUNSUPPORTED, "more than 256 valid centroids");
+    if (pick_np(ds->dtype, (int)ds->n) == 0)
+        return fail(HPCG_EUNSUPPORTED, "n > 32 features is not supported by this build's kernels");
+    if (ctx->s_b.bytes < (size_t)k_valid * 4) {
+        std::vector<int32_t> remap((size_t)k_valid);
+        for (int64_t j = 0; j < k_valid; ++j) remap[(size_t)j] = (int32_t)j;
+        CU(ctx->s_b.reserve(remap.size() * 4));
+        CU(h2d(ctx->s_b.as<int32_t>(), remap.data(), remap.size(), ctx->stream));
+    } else {
+        // identity remap kept in s_b by construction of this path
+        std::vector<int32_t> remap((size_t)k_valid);
+        for (int64_t j = 0; j < k_valid; ++j) remap[(size_t)j] = (int32_t)j;
+        CU(h2d(ctx->s_b.as<int32_t>(), remap.data(), remap.size(), ctx->stream));
+    }
+    return run_assign(ctx, ds, C_dev, ctx->s_b.as<int32_t>(), (int)k_valid, labels_dev, nullptr, cost_dev,
+                      ctx->s_f);
+}
+
+// ---------------------------------------------------------------- gather
+int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, int64_t s, void* S_host) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (s < 1 || s > ds->m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
+    for (int64_t i = 0; i < s; ++i)
+        if (idx_host[i] < 0 || idx_host[i] >= ds->m) return fail(HPCG_EINVAL, "gather: row index out of range");
+    const int64_t rowb = ds->n * (int64_t)dsize(ds->dtype);
+    CU(ctx->s_a.reserve((size_t)s * 8));
+    CU(ctx->s_b.reserve((size_t)(s * rowb)));
+    CU(h2d(ctx->s_a.as<int64_t>(), idx_host, (size_t)s, ctx->stream));
+    const int64_t tot = s * rowb;
+    gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(
+        static_cast<const unsigned char*>(ds->X), rowb, ctx->s_a.as<int64_t>(), s, ctx->s_b.as<unsigned char>());
+    CU(cudaGetLastError());
+    ctx->launches += 1;
+    CU(cudaMemcpyAsync(S_host, ctx->s_b.p, (size_t)tot, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return HPCG_OK;
+}
+
+int hpcg_reference_draw_indices(uint64_t* mt_state, int32_t* mt_pos, int64_t m, int64_t s, int64_t* idx_out) {
+    if (s < 1 || s > m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
+    Mt64 r;
+    std::memcpy(r.mt, mt_state, sizeof r.mt);
+    r.pos = *mt_pos;
+    sparse_fisher_yates(r, m, s, idx_out);
+    std::memcpy(mt_state, r.mt, sizeof r.mt);
+    *mt_pos = r.pos;
+    return HPCG_OK;
+}
+
+// ------------------------------------------------------- reference streams
+int hpcg_rng_seed(uint64_t seed, uint64_t* st, int32_t* pos) {
+    Mt64 r;
+    r.seed(seed);
+    std::memcpy(st, r.mt, sizeof r.mt);
+    *pos = r.pos;
+    return HPCG_OK;
+}
+
+int hpcg_rng_derive(uint64_t master, uint64_t domain, uint64_t index, uint64_t* st, int32_t* pos) {
+    Mt64 r = Mt64::derive(master, domain, index);
+    std::memcpy(st, r.mt, sizeof r.mt);
+    *pos = r.pos;
+    return HPCG_OK;
+}
+
+int hpcg_rng_draw(uint64_t* st, int32_t* pos, int32_t kind, uint64_t bound, int64_t count, void* out) {
+    if (kind == 2 && bound == 0) return fail(HPCG_EINVAL, "uniform_index: n must be positive");
+    Mt64 r;
+    std::memcpy(r.mt, st, sizeof r.mt);
+    r.pos = *pos;
+    for (int64_t i = 0; i < count; ++i) {
+        if (kind == 0)
+            static_cast<uint64_t*>(out)[i] = r.next();
+        else if (kind == 1)
+            static_cast<double*>(out)[i] = r.unit();
+        else
+            static_cast<uint64_t*>(out)[i] = r.uniform_index(bound);
+    }
+    std::memcpy(st, r.mt, sizeof r.mt);
+    *pos = r.pos;
+    return HPCG_OK;
+}
+
+// ------------------------------------------------- batched worker step
+int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, int64_t W, int64_t s,
+                             const double* C_init, const uint8_t* flags_init, int64_t k, const hpcg_lloyd_cfg* cfg,
+                             const int64_t* first_row_host, const double* units_host, int64_t units_stride,
+                             int do_lloyd, double* C_out, uint8_t* flags_out, double* objective, int32_t* iterations,
+                             int32_t* stop, int64_t* n_d, int32_t* filled, int32_t* labels, int64_t* counts,
+                             double* history, int32_t hist_cap, int32_t* hist_len) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    const int64_t n = ds->n;
+    if (W < 1) return fail(HPCG_EINVAL, "worker_step: need at least one worker");
+    if (s < 1) return fail(HPCG_EINVAL, "seeding: empty sample");
+    if (k < 1) return fail(HPCG_EINVAL, "kmeanspp_seed: k must be positive");
+    if (cfg->candidates < 1) return fail(HPCG_EINVAL, "seeding: need at least one candidate");
+    if (do_lloyd) {
+        if (cfg->max_iters < 1) return fail(HPCG_EINVAL, "kmeans: max_iters must be positive");
+        if (!(cfg->rel_tol > 0.0)) return fail(HPCG_EINVAL, "kmeans: rel_tol must be positive");
+    }
+    if (int rc = check_shape(ds->dtype, n, k)) return rc;
+    if (cfg->candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 8 K-means++ candidates");
+    if (idx_host) {
+        for (int64_t i = 0; i < W * s; ++i)
+            if (idx_host[i] < 0 || idx_host[i] >= ds->m) return fail(HPCG_EINVAL, "sample index out of range");
+    } else if (ds->m != W * s) {
+        return fail(HPCG_EINVAL, "batched samples: dataset must hold W*s rows");
+    }
+    const bool explicit_draws = first_row_host != nullptr && units_host != nullptr;
+    if (explicit_draws)
+        for (int64_t w = 0; w < W; ++w)
+            if (first_row_host[w] < 0 || first_row_host[w] >= s) return fail(HPCG_EINVAL, "first_row out of range");
+
+    // device buffers (one allocation per call; this path serves tests and the drop-in API)
+    DevBuf d_idx, d_ci, d_fi, d_fr, d_un, d_c, d_f, d_obj, d_it, d_st, d_nd, d_fl, d_err, d_lab, d_cnt, d_hist,
+        d_hl;
+    const int64_t kn = k * n;
+    if (idx_host) CU(d_idx.reserve((size_t)(W * s) * 8));
+    CU(d_ci.reserve((size_t)(W * kn) * 8));
+    CU(d_fi.reserve((size_t)(W * k)));
+    CU(d_c.reserve((size_t)(W * kn) * 8));
+    CU(d_f.reserve((size_t)(W * k)));
+    CU(d_obj.reserve((size_t)W * 8));
+    CU(d_it.reserve((size_t)W * 4));
+    CU(d_st.reserve((size_t)W * 4));
+    CU(d_nd.reserve((size_t)W * 8));
+    CU(d_fl.reserve((size_t)W * 4));
+    CU(d_err.reserve((size_t)W * 4));
+    if (idx_host) CU(h2d(d_idx.as<int64_t>(), idx_host, (size_t)(W * s), ctx->stream));
+    CU(h2d(d_ci.as<double>(), C_init, (size_t)(W * kn), ctx->stream));
+    if (flags_init)
+        CU(h2d(d_fi.as<uint8_t>(), flags_init, (size_t)(W * k), ctx->stream));
+    else
+        CU(cudaMemsetAsync(d_fi.p, 0, (size_t)(W * k), ctx->stream));
+    if (explicit_draws) {
+        CU(d_fr.reserve((size_t)W * 8));
+        CU(d_un.reserve((size_t)(W * std::max<int64_t>(units_stride, 1)) * 8));
+        CU(h2d(d_fr.as<int64_t>(), first_row_host, (size_t)W, ctx->stream));
+        if (units_stride > 0) CU(h2d(d_un.as<double>(), units_host, (size_t)(W * units_stride), ctx->stream));
+    }
+    if (labels) CU(d_lab.reserve((size_t)(W * s) * 4));
+    if (counts) CU(d_cnt.reserve((size_t)(W * k) * 8));
+    if (history && hist_cap > 0) CU(d_hist.reserve((size_t)(W * hist_cap) * 8));
+    CU(d_hl.reserve((size_t)W * 4));
+
+    StepParams p = {};
+    p.X = ds->X;
+    p.m = ds->m;
+    p.n = (int)n;
+    p.s = s;
+    p.W = (int)W;
+    p.sample_mode = idx_host ? 0 : 2;
+    p.idx = d_idx.as<int64_t>();
+    p.key = 0x6870636c75737431ULL;
+    p.round = 0;
+    p.worker_base = 0;
+    p.init_c = d_ci.as<double>();
+    p.init_stride = kn;
+    p.init_f = d_fi.as<uint8_t>();
+    p.initf_stride = k;
+    p.shared_version = nullptr;
+    p.candidates = (int)cfg->candidates;
+    p.seed_mode = explicit_draws ? 0 : 1;
+    p.first_row = d_fr.as<int64_t>();
+    p.units = d_un.as<double>();
+    p.units_stride = (int)units_stride;
+    p.k = (int)k;
+    p.max_iters = (int)std::min<int64_t>(cfg->max_iters, INT32_MAX);
+    p.rel_tol = cfg->rel_tol;
+    p.do_lloyd = do_lloyd;
+    p.out_c = d_c.as<double>();
+    p.out_f = d_f.as<uint8_t>();
+    p.out_obj = d_obj.as<double>();
+    p.out_iters = d_it.as<int32_t>();
+    p.out_stop = d_st.as<int32_t>();
+    p.out_nd = d_nd.as<int64_t>();
+    p.out_filled = d_fl.as<int32_t>();
+    p.out_err = d_err.as<int32_t>();
+    p.out_labels = labels ? d_lab.as<int32_t>() : nullptr;
+    p.out_counts = counts ? d_cnt.as<int64_t>() : nullptr;
+    p.out_hist = (history && hist_cap > 0) ? d_hist.as<double>() : nullptr;
+    p.hist_cap = hist_cap;
+    p.out_hist_len = d_hl.as<int32_t>();
+    std::string why;
+    KTimer kt(ctx, 0);
+    cudaError_t e = launch_step(ds->dtype, p, ctx->stream, nullptr, &why);
+    kt.done();
+    if (e != cudaSuccess) return fail(HPCG_ECUDA, std::string("worker step launch: ") + cudaGetErrorString(e) + " " + why);
+    ctx->launches += 1;
+    std::vector<int32_t> err((size_t)W);
+    CU(d2h(err.data(), d_err.as<int32_t>(), (size_t)W, ctx->stream));
+    if (C_out) CU(d2h(C_out, d_c.as<double>(), (size_t)(W * kn), ctx->stream));
+    if (flags_out) CU(d2h(flags_out, d_f.as<uint8_t>(), (size_t)(W * k), ctx->stream));
+    if (objective) CU(d2h(objective, d_obj.as<double>(), (size_t)W, ctx->stream));
+    if (iterations) CU(d2h(iterations, d_it.as<int32_t>(), (size_t)W, ctx->stream));
+    if (stop) CU(d2h(stop, d_st.as<int32_t>(), (size_t)W, ctx->stream));
+    if (n_d) CU(d2h(n_d, d_nd.as<int64_t>(), (size_t)W, ctx->stream));
+    if (filled) CU(d2h(filled, d_fl.as<int32_t>(), (size_t)W, ctx->stream));
+    if (labels) CU(d2h(labels, d_lab.as<int32_t>(), (size_t)(W * s), ctx->stream));
+    if (counts) CU(d2h(counts, d_cnt.as<int64_t>(), (size_t)(W * k), ctx->stream));
+    if (history && hist_cap > 0) CU(d2h(history, d_hist.as<double>(), (size_t)(W * hist_cap), ctx->stream));
+    if (hist_len) CU(d2h(hist_len, d_hl.as<int32_t>(), (size_t)W, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int64_t w = 0; w < W; ++w) {
+        if (err[(size_t)w] == kErrDegenerateInit) return fail(HPCG_EINVAL, "kmeans: degenerate centroid in init");
+        if (err[(size_t)w] == kErrMonotone) return fail(HPCG_ELOGIC, "kmeans: objective increased between iterations");
+    }
+    return HPCG_OK;
+}
+
+}  // extern "C"
+
+// ============================================================== engine
+struct hpcg_engine {
+    hpcg_ctx* ctx = nullptr;
+    const hpcg_dataset* ds = nullptr;
+    hpcg_engine_cfg cfg{};
+    int64_t W = 0, k = 0, n = 0, s = 0, R = 0;
+    int64_t round = 0;
+    uint64_t key = 0;
+    std::chrono::steady_clock::time_point t0;
+    DevBuf inc_c, inc_f, inc_obj, acc, nd, err, err_first, iters, stopb, filled, objb;
+    DevBuf sh_ver, sh_obj, sh_worker, sh_c, sh_f;
+    DevBuf log_acc, log_obj, nd_total, pub_log, pub_count;
+    DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks;
+    int64_t pub_cap = 0;
+    // reference-RNG replay state
+    std::vector<Mt64> streams;
+    std::vector<int64_t> h_idx, h_fr;
+    std::vector<double> h_un;
+    int64_t ucap = 0;
+};
+
+namespace {
+bool phase_cooperative(int strategy, double t1, double progress) {  // engine.hpp:288-296
+    if (strategy == HPCG_COOPERATIVE) return true;
+    if (strategy == HPCG_HYBRID) return progress >= t1;
+    return false;
+}
+
+int engine_round(hpcg_engine* e) {
+    hpcg_ctx* ctx = e->ctx;
+    const int64_t r = e->round, W = e->W, k = e->k, n = e->n, s = e->s, kn = k * n;
+    const bool coop = phase_cooperative(e->cfg.strategy, e->cfg.phase_t1, (double)r);
+    const bool reference = e->cfg.rng_mode == HPCG_RNG_REFERENCE;
+    const int64_t ncand = e->cfg.candidates;
+    std::vector<int64_t> pending_loop, no_valid;
+    std::vector<Mt64> snap;
+    if (reference) {
+        // which slots each worker will reseed (seeding.hpp:60-79) decides the draws it consumes
+        std::vector<uint8_t> flags((size_t)(W * k), 1);
+        int64_t ver = 1;
+        if (coop) {
+            CU(d2h(&ver, e->sh_ver.as<int64_t>(), 1, ctx->stream));
+            std::vector<uint8_t> f1((size_t)k);
+            CU(d2h(f1.data(), e->sh_f.as<uint8_t>(), (size_t)k, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            for (int64_t w = 0; w < W; ++w)
+                for (int64_t j = 0; j < k; ++j) flags[(size_t)(w * k + j)] = ver ? f1[(size_t)j] : 1;
+        } else {
+            CU(d2h(flags.data(), e->inc_f.as<uint8_t>(), (size_t)(W * k), ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+        }
+        pending_loop.assign((size_t)W, 0);
+        no_valid.assign((size_t)W, 0);
+        snap.resize((size_t)W);
+        for (int64_t w = 0; w < W; ++w) {
+            Mt64& rng = e->streams[(size_t)w];
+            sparse_fisher_yates(rng, e->ds->m, s, e->h_idx.data() + w * s);  // engine.hpp:241
+            int64_t np_ = 0, nv = 0;
+            for (int64_t j = 0; j < k; ++j) (flags[(size_t)(w * k + j)] ? np_ : nv) += 1;
+            e->h_fr[(size_t)w] = 0;
+            if (np_ > 0 && nv == 0) {
+                e->h_fr[(size_t)w] = (int64_t)rng.uniform_index((uint64_t)s);
+                no_valid[(size_t)w] = 1;
+            }
+            snap[(size_t)w] = rng;
+            const int64_t loops = np_ - no_valid[(size_t)w];
+            pending_loop[(size_t)w] = loops;
+            for (int64_t t = 0; t < loops * ncand; ++t) e->h_un[(size_t)(w * e->ucap + t)] = rng.unit();
+        }
+        CU(h2d(e->d_idx.as<int64_t>(), e->h_idx.data(), (size_t)(W * s), ctx->stream));
+        CU(h2d(e->d_fr.as<int64_t>(), e->h_fr.data(), (size_t)W, ctx->stream));
+        CU(h2d(e->d_un.as<double>(), e->h_un.data(), (size_t)(W * e->ucap), ctx->stream));
+    }
+    StepParams p = {};
+    p.X = e->ds->X;
+    p.m = e->ds->m;
+    p.n = (int)n;
+    p.s = s;
+    p.W = (int)W;
+    p.sample_mode = reference ? 0 : 1;
+    p.idx = e->d_idx.as<int64_t>();
+    p.key = e->key;
+    p.round = (uint32_t)r;
+    p.worker_base = e->cfg.worker_base;
+    if (coop) {
+        p.init_c = e->sh_c.as<double>();
+        p.init_stride = 0;
+        p.init_f = e->sh_f.as<uint8_t>();
+        p.initf_stride = 0;
+        p.shared_version = e->sh_ver.as<int64_t>();
+    } else {
+        p.init_c = e->inc_c.as<double>();
+        p.init_stride = kn;
+        p.init_f = e->inc_f.as<uint8_t>();
+        p.initf_stride = k;
+        p.shared_version = nullptr;
+    }
+    p.candidates = (int)ncand;
+    p.seed_mode = reference ? 0 : 1;
+    p.first_row = e->d_fr.as<int64_t>();
+    p.units = e->d_un.as<double>();
+    p.units_stride = (int)e->ucap;
+    p.k = (int)k;
+    p.max_iters = (int)std::min<int64_t>(e->cfg.max_iters, INT32_MAX);
+    p.rel_tol = e->cfg.rel_tol;
+    p.do_lloyd = 1;
+    p.out_obj = e->objb.as<double>();
+    p.out_iters = e->iters.as<int32_t>();
+    p.out_stop = e->stopb.as<int32_t>();
+    p.out_nd = e->nd.as<int64_t>();
+    p.out_filled = e->filled.as<int32_t>();
+    p.out_err = e->err.as<int32_t>();
+    p.inc_c = e->inc_c.as<double>();
+    p.inc_f = e->inc_f.as<uint8_t>();
+    p.inc_obj = e->inc_obj.as<double>();
+    p.accepted = e->acc.as<uint8_t>();
+    std::string why;
+    KTimer kt(ctx, 0);
+    cudaError_t ce = launch_step(e->ds->dtype, p, ctx->stream, nullptr, &why);
+    kt.done();
+    if (ce != cudaSuccess) return fail(HPCG_ECUDA, std::string("worker step launch: ") + cudaGetErrorString(ce) + " " + why);
+    ctx->launches += 1;
+
+    RoundEndParams q = {};
+    q.W = (int)W;
+    q.k = (int)k;
+    q.n = (int)n;
+    q.round = r;
+    q.publish = coop ? 1 : 0;  // round_was_coop (engine.hpp:393)
+    const bool hybrid = e->cfg.strategy == HPCG_HYBRID;
+    q.carry = (hybrid && (r + 1) == (int64_t)(size_t)e->cfg.phase_t1) ? 1 : 0;  // engine.hpp:386,396
+    q.worker_base = e->cfg.worker_base;
+    q.accepted = e->acc.as<uint8_t>();
+    q.inc_obj = e->inc_obj.as<double>();
+    q.inc_c = e->inc_c.as<double>();
+    q.inc_f = e->inc_f.as<uint8_t>();
+    q.nd = e->nd.as<int64_t>();
+    q.err = e->err.as<int32_t>();
+    q.log_acc = e->log_acc.as<uint8_t>();
+    q.log_obj = e->log_obj.as<double>();
+    q.err_first = e->err_first.as<int32_t>();
+    q.nd_total = e->nd_total.as<unsigned long long>();
+    q.sh_version = e->sh_ver.as<int64_t>();
+    q.sh_obj = e->sh_obj.as<double>();
+    q.sh_worker = e->sh_worker.as<int32_t>();
+    q.sh_c = e->sh_c.as<double>();
+    q.sh_f = e->sh_f.as<uint8_t>();
+    q.pub_log = e->pub_log.as<double>();
+    q.pub_count = e->pub_count.as<int64_t>();
+    q.pub_cap = e->pub_cap;
+    round_end_kernel<<<1, 256, 0, ctx->stream>>>(q);
+    CU(cudaGetLastError());
+    ctx->launches += 1;
+
+    if (reference) {  // rewind streams of workers whose seeding stopped early (seeding.hpp:87)
+        std::vector<int32_t> fl((size_t)W);
+        CU(d2h(fl.data(), e->filled.as<int32_t>(), (size_t)W, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (int64_t w = 0; w < W; ++w) {
+            const int64_t used = fl[(size_t)w] - no_valid[(size_t)w];
+            if (used < pending_loop[(size_t)w]) {
+                Mt64 rng = snap[(size_t)w];
+                for (int64_t t = 0; t < used * ncand; ++t) rng.unit();
+                e->streams[(size_t)w] = rng;
+            }
+        }
+    }
+    ++e->round;
+    return HPCG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_cfg* c, hpcg_engine** out) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    hpcg_engine_cfg cfg = *c;
+    if (cfg.strategy == HPCG_INNER) cfg.n_workers = 1;  // engine.hpp:446
+    // EngineConfig::validate (engine.hpp:70-86)
+    if (cfg.k < 1) return fail(HPCG_EINVAL, "EngineConfig: k must be positive");
+    if (cfg.sample_size < 1 || cfg.sample_size > ds->m)
+        return fail(HPCG_EINVAL, "EngineConfig: sample_size must be in [1, m]");
+    if (cfg.n_workers < 1) return fail(HPCG_EINVAL, "EngineConfig: need at least one worker");
+    if (cfg.max_samples < 1) return fail(HPCG_EINVAL, "EngineConfig: need a time limit or a max_samples bound");
+    if (cfg.strategy == HPCG_HYBRID) {
+        if (!(cfg.phase_t1 >= 0.0 && cfg.phase_t2 >= 0.0))
+            return fail(HPCG_EINVAL, "EngineConfig: hybrid phase durations must be nonnegative");
+        const double b = (double)cfg.max_samples;
+        if (!(std::fabs(cfg.phase_t1 + cfg.phase_t2 - b) <= 1e-9 * std::max(1.0, std::fabs(b))))
+            return fail(HPCG_EINVAL, "EngineConfig: hybrid phases must sum to the total budget");
+    }
+    if (cfg.max_iters < 1) return fail(HPCG_EINVAL, "kmeans: max_iters must be positive");
+    if (!(cfg.rel_tol > 0.0)) return fail(HPCG_EINVAL, "kmeans: rel_tol must be positive");
+    if (cfg.candidates < 1) return fail(HPCG_EINVAL, "seeding: need at least one candidate");
+    if (cfg.candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 8 K-means++ candidates");
+    if (int rc = check_shape(ds->dtype, ds->n, cfg.k)) return rc;
+    StepGeometry g;
+    std::string why;
+    if (step_geometry(ds->dtype, (int)ds->n, cfg.sample_size, (int)cfg.k, (int)cfg.n_workers, &g, &why) != cudaSuccess)
+        return fail(HPCG_EUNSUPPORTED, "worker step geometry: " + why);
+
+    auto* e = new hpcg_engine;
+    e->ctx = ctx;
+    e->ds = ds;
+    e->cfg = cfg;
+    e->W = cfg.n_workers;
+    e->k = cfg.k;
+    e->n = ds->n;
+    e->s = cfg.sample_size;
+    e->R = cfg.max_samples;
+    e->key = splitmix64(cfg.master_seed ^ 0x48504331ULL);
+    e->t0 = std::chrono::steady_clock::now();
+    const int64_t W = e->W, k = e->k, kn = k * e->n;
+    auto bad = [&](cudaError_t err) {
+        delete e;
+        return fail(HPCG_ECUDA, std::string("engine allocation: ") + cudaGetErrorString(err));
+    };
+#define ALLOC(buf, bytes)                                  \
+    do {                                                   \
+        cudaError_t err_ = e->buf.reserve((size_t)(bytes)); \
+        if (err_ != cudaSuccess) return bad(err_);          \
+    } while (0)
+    ALLOC(inc_c, W * kn * 8);
+    ALLOC(inc_f, W * k);
+    ALLOC(inc_obj, W * 8);
+    ALLOC(acc, W);
+    ALLOC(nd, W * 8);
+    ALLOC(err, W * 4);
+    ALLOC(err_first, W * 4);
+    ALLOC(iters, W * 4);
+    ALLOC(stopb, W * 4);
+    ALLOC(filled, W * 4);
+    ALLOC(objb, W * 8);
+    ALLOC(sh_ver, 8);
+    ALLOC(sh_obj, 8);
+    ALLOC(sh_worker, 4);
+    ALLOC(sh_c, kn * 8);
+    ALLOC(sh_f, k);
+    ALLOC(log_acc, e->R * W);
+    ALLOC(log_obj, e->R * W * 8);
+    ALLOC(nd_total, 8);
+    e->pub_cap = std::max<int64_t>(64, e->R * std::min<int64_t>(W, 64));
+    ALLOC(pub_log, e->pub_cap * 4 * 8);
+    ALLOC(pub_count, 8);
+    const bool reference = cfg.rng_mode == HPCG_RNG_REFERENCE;
+    e->ucap = std::max<int64_t>(1, k * cfg.candidates);
+    ALLOC(d_fr, W * 8);
+    ALLOC(d_un, W * e->ucap * 8);
+    if (reference) {
+        ALLOC(d_idx, W * e->s * 8);
+        e->h_idx.assign((size_t)(W * e->s), 0);
+        e->h_fr.assign((size_t)W, 0);
+        e->h_un.assign((size_t)(W * e->ucap), 0.0);
+        for (int64_t w = 0; w < W; ++w)  // engine.hpp:457
+            e->streams.push_back(Mt64::derive(cfg.master_seed, 1, (uint64_t)(cfg.worker_base + w)));
+    }
+#undef ALLOC
+    cudaStream_t st = ctx->stream;
+    cudaError_t ce = cudaSuccess;
+    auto chk = [&](cudaError_t x) {
+        if (ce == cudaSuccess) ce = x;
+    };
+    chk(cudaMemsetAsync(e->inc_c.p, 0, (size_t)(W * kn * 8), st));
+    chk(cudaMemsetAsync(e->inc_f.p, 1, (size_t)(W * k), st));  // all-degenerate incumbents (engine.hpp:456)
+    fill_f64_kernel<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(e->inc_obj.as<double>(), W, kInf);
+    fill_f64_kernel<<<1, 1, 0, st>>>(e->sh_obj.as<double>(), 1, kInf);
+    chk(cudaMemsetAsync(e->sh_ver.p, 0, 8, st));
+    chk(cudaMemsetAsync(e->sh_worker.p, 0xff, 4, st));
+    chk(cudaMemsetAsync(e->sh_c.p, 0, (size_t)(kn * 8), st));
+    chk(cudaMemsetAsync(e->sh_f.p, 1, (size_t)k, st));
+    chk(cudaMemsetAsync(e->err_first.p, 0, (size_t)(W * 4), st));
+    chk(cudaMemsetAsync(e->nd_total.p, 0, 8, st));
+    chk(cudaMemsetAsync(e->pub_count.p, 0, 8, st));
+    chk(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->R * W), st));
+    chk(cudaGetLastError());
+    ctx->launches += 2;
+    if (ce != cudaSuccess) return bad(ce);
+    *out = e;
+    return HPCG_OK;
+}
+
+int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t W = e->W, k = e->k, kn = k * e->n;
+    e->cfg.master_seed = master_seed;
+    e->key = splitmix64(master_seed ^ 0x48504331ULL);
+    e->round = 0;
+    e->t0 = std::chrono::steady_clock::now();
+    if (e->cfg.rng_mode == HPCG_RNG_REFERENCE)
+        for (int64_t w = 0; w < W; ++w)
+            e->streams[(size_t)w] = Mt64::derive(master_seed, 1, (uint64_t)(e->cfg.worker_base + w));
+    CU(cudaMemsetAsync(e->inc_c.p, 0, (size_t)(W * kn * 8), st));
+    CU(cudaMemsetAsync(e->inc_f.p, 1, (size_t)(W * k), st));
+    fill_f64_kernel<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(e->inc_obj.as<double>(), W, kInf);
+    fill_f64_kernel<<<1, 1, 0, st>>>(e->sh_obj.as<double>(), 1, kInf);
+    CU(cudaGetLastError());
+    ctx->launches += 2;
+    CU(cudaMemsetAsync(e->sh_ver.p, 0, 8, st));
+    CU(cudaMemsetAsync(e->sh_worker.p, 0xff, 4, st));
+    CU(cudaMemsetAsync(e->sh_c.p, 0, (size_t)(kn * 8), st));
+    CU(cudaMemsetAsync(e->sh_f.p, 1, (size_t)k, st));
+    CU(cudaMemsetAsync(e->err_first.p, 0, (size_t)(W * 4), st));
+    CU(cudaMemsetAsync(e->nd_total.p, 0, 8, st));
+    CU(cudaMemsetAsync(e->pub_count.p, 0, 8, st));
+    CU(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->R * W), st));
+    return HPCG_OK;
+}
+
+int hpcg_engine_import_best(hpcg_engine* e, double obj, int64_t worker, const double* C, const uint8_t* f) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    int64_t ver = 0;
+    CU(d2h(&ver, e->sh_ver.as<int64_t>(), 1, st));
+    CU(cudaStreamSynchronize(st));
+    ++ver;
+    const int32_t wk = (int32_t)worker;
+    CU(h2d(e->sh_ver.as<int64_t>(), &ver, 1, st));
+    CU(h2d(e->sh_obj.as<double>(), &obj, 1, st));
+    CU(h2d(e->sh_worker.as<int32_t>(), &wk, 1, st));
+    CU(h2d(e->sh_c.as<double>(), C, (size_t)(e->k * e->n), st));
+    CU(h2d(e->sh_f.as<uint8_t>(), f, (size_t)e->k, st));
+    CU(cudaStreamSynchronize(st));
+    return HPCG_OK;
+}
+
+int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    cudaSetDevice(e->ctx->device);
+    for (int64_t i = 0; i < n_rounds; ++i) {
+        if (e->round >= e->R) return fail(HPCG_EINVAL, "engine: max_samples rounds already run");
+        if (int rc = engine_round(e)) return rc;
+    }
+    return HPCG_OK;
+}
+
+int64_t hpcg_engine_round_index(const hpcg_engine* e) { return e->round; }
+
+int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    cudaSetDevice(e->ctx->device);
+    unsigned long long v = 0;
+    CU(d2h(&v, e->nd_total.as<unsigned long long>(), 1, e->ctx->stream));
+    CU(cudaStreamSynchronize(e->ctx->stream));
+    *n_d = (int64_t)v;
+    return HPCG_OK;
+}
+
+int hpcg_engine_export_best(hpcg_engine* e, double* obj_out, int64_t* worker_out, double* C_out, uint8_t* f_out) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    cudaSetDevice(e->ctx->device);
+    hpcg_ctx* ctx = e->ctx;
+    int32_t wk = -1;
+    if (obj_out) CU(d2h(obj_out, e->sh_obj.as<double>(), 1, ctx->stream));
+    CU(d2h(&wk, e->sh_worker.as<int32_t>(), 1, ctx->stream));
+    if (C_out) CU(d2h(C_out, e->sh_c.as<double>(), (size_t)(e->k * e->n), ctx->stream));
+    if (f_out) CU(d2h(f_out, e->sh_f.as<uint8_t>(), (size_t)e->k, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (worker_out) *worker_out = wk;
+    return HPCG_OK;
+}
+
+int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels,
+                       double* publications, int64_t pub_cap, double* worker_obj, double* traces, int64_t trace_cap,
+                       int64_t* trace_len) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t W = e->W, k = e->k, n = e->n, kn = k * n, R = e->round;
+    std::vector<double> inc_obj((size_t)W);
+    std::vector<int32_t> errf((size_t)W);
+    std::vector<uint8_t> lacc((size_t)(std::max<int64_t>(R, 1) * W));
+    std::vector<double> lobj((size_t)(std::max<int64_t>(R, 1) * W));
+    unsigned long long ndt = 0;
+    int64_t npub = 0;
+    CU(d2h(inc_obj.data(), e->inc_obj.as<double>(), (size_t)W, st));
+    CU(d2h(errf.data(), e->err_first.as<int32_t>(), (size_t)W, st));
+    if (R > 0) {
+        CU(d2h(lacc.data(), e->log_acc.as<uint8_t>(), (size_t)(R * W), st));
+        CU(d2h(lobj.data(), e->log_obj.as<double>(), (size_t)(R * W), st));
+    }
+    CU(d2h(&ndt, e->nd_total.as<unsigned long long>(), 1, st));
+    CU(d2h(&npub, e->pub_count.as<int64_t>(), 1, st));
+    CU(cudaStreamSynchronize(st));
+    // worker errors are rethrown after the join, lowest worker first (engine.hpp:330-331)
+    for (int64_t w = 0; w < W; ++w) {
+        if (errf[(size_t)w] == kErrDegenerateInit) return fail(HPCG_EINVAL, "kmeans: degenerate centroid in init");
+        if (errf[(size_t)w] == kErrMonotone) return fail(HPCG_ELOGIC, "kmeans: objective increased between iterations");
+    }
+    // select_best (engine.hpp:180-194)
+    int best = -1;
+    double best_f = kInf;
+    for (int64_t w = 0; w < W; ++w)
+        if (inc_obj[(size_t)w] < best_f) {
+            best_f = inc_obj[(size_t)w];
+            best = (int)w;
+        }
+    if (best < 0) return fail(HPCG_ENOSOL, "no solution produced: every worker incumbent is infinite");
+    hpcg_run_out o = {};
+    o.best_worker = e->cfg.worker_base + best;
+    o.best_sample_objective = best_f;
+    // traces: lockstep timestamps are samples_processed + 1 = round + 1 (engine.hpp:413)
+    double min_last = kInf;
+    std::vector<double> last_ts((size_t)W, -1.0);
+    for (int64_t w = 0; w < W; ++w) {
+        int64_t cnt = 0;
+        for (int64_t r = 0; r < R; ++r) {
+            if (!lacc[(size_t)(r * W + w)]) continue;
+            if (traces && cnt < trace_cap) {
+                traces[(w * trace_cap + cnt) * 2 + 0] = (double)(r + 1);
+                traces[(w * trace_cap + cnt) * 2 + 1] = lobj[(size_t)(r * W + w)];
+            }
+            last_ts[(size_t)w] = (double)(r + 1);
+            ++cnt;
+        }
+        if (trace_len) trace_len[w] = cnt;
+        if (cnt > 0) min_last = std::min(min_last, last_ts[(size_t)w]);
+    }
+    o.clustering_time = min_last;  // engine.hpp:472-475
+    // every worker has t_w = R in lockstep, so the first finisher is worker 0 (engine.hpp:477-481)
+    o.clustering_time_first_finisher = last_ts[0] >= 0 ? last_ts[0] : 0.0;
+    std::vector<double> bc((size_t)kn);
+    std::vector<uint8_t> bf((size_t)k);
+    CU(d2h(bc.data(), e->inc_c.as<double>() + best * kn, (size_t)kn, st));
+    CU(d2h(bf.data(), e->inc_f.as<uint8_t>() + best * k, (size_t)k, st));
+    CU(cudaStreamSynchronize(st));
+    if (centroids) std::memcpy(centroids, bc.data(), (size_t)kn * 8);
+    if (flags) std::memcpy(flags, bf.data(), (size_t)k);
+    int64_t final_nd = 0;
+    if (e->cfg.compute_full_objective || e->cfg.compute_assignment) {  // engine.hpp:483-491
+        std::vector<double> cv;
+        std::vector<int32_t> remap;
+        for (int64_t j = 0; j < k; ++j)
+            if (!bf[(size_t)j]) {
+                remap.push_back((int32_t)j);
+                cv.insert(cv.end(), bc.begin() + j * n, bc.begin() + (j + 1) * n);
+            }
+        if (remap.empty()) return fail(HPCG_EINVAL, "assignment: every centroid is degenerate");
+        CU(e->scratch_a.reserve(cv.size() * 8));
+        CU(e->scratch_b.reserve(remap.size() * 4));
+        CU(e->scratch_c.reserve(8));
+        CU(h2d(e->scratch_a.as<double>(), cv.data(), cv.size(), st));
+        CU(h2d(e->scratch_b.as<int32_t>(), remap.data(), remap.size(), st));
+        DevBuf lab;
+        const bool want_labels = e->cfg.compute_assignment && labels;
+        if (want_labels) CU(lab.reserve((size_t)e->ds->m * 4));
+        int rc = run_assign(ctx, e->ds, e->scratch_a.as<double>(), e->scratch_b.as<int32_t>(), (int)remap.size(),
+                            want_labels ? lab.as<int32_t>() : nullptr, nullptr, e->scratch_c.as<double>(), e->blocks);
+        if (rc) return rc;
+        double f = 0;
+        CU(d2h(&f, e->scratch_c.as<double>(), 1, st));
+        if (want_labels) CU(d2h(labels, lab.as<int32_t>(), (size_t)e->ds->m, st));
+        CU(cudaStreamSynchronize(st));
+        o.full_objective = f;
+        o.has_full_objective = 1;
+        final_nd = e->ds->m * (int64_t)remap.size();
+    }
+    o.total_samples = (uint64_t)(W * R);
+    o.distance_evals = (int64_t)ndt + final_nd;
+    o.n_publications = npub;
+    if (publications && npub > 0) {
+        const int64_t cnt = std::min(npub, std::min(pub_cap, e->pub_cap));
+        CU(d2h(publications, e->pub_log.as<double>(), (size_t)(cnt * 4), st));
+        CU(cudaStreamSynchronize(st));
+    }
+    if (worker_obj) std::memcpy(worker_obj, inc_obj.data(), (size_t)W * 8);
+    o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
+    if (out) *out = o;
+    return HPCG_OK;
+}
+
+int hpcg_engine_destroy(hpcg_engine* e) {
+    if (e) {
+        cudaSetDevice(e->ctx->device);
+        delete e;
+    }
+    return HPCG_OK;
+}
+
+int hpcg_run(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n, const hpcg_engine_cfg* cfg,
+             hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels, double* publications,
+             int64_t pub_cap, double* worker_obj, double* traces, int64_t trace_cap, int64_t* trace_len) {
+    const auto t0 = std::chrono::steady_clock::now();
+    hpcg_dataset* ds = nullptr;
+    if (int rc = hpcg_dataset_upload(ctx, X_host, dtype, m, n, &ds)) return rc;
+    hpcg_engine* e = nullptr;
+    int rc = hpcg_engine_create(ctx, ds, cfg, &e);
+    if (!rc) {
+        e->t0 = t0;
+        rc = hpcg_engine_rounds(e, cfg->max_samples);
+    }
+    if (!rc)
+        rc = hpcg_engine_finish(e, out, centroids, flags, labels, publications, pub_cap, worker_obj, traces,
+                                trace_cap, trace_len);
+    hpcg_engine_destroy(e);
+    hpcg_dataset_destroy(ds);
+    return rc;
+}
+
+// ------------------------------------------------------------ synthetic data
+// Seeded Gaussian mixture keyed by global row index: row i picks its component by
+// inverse CDF of the weights, then coordinates mean + sigma * N(0,1) (Box-Muller on
+// splitmix64-hashed counters); a noise_frac share of rows is uniform in the noise box.
+int hpcg_gen_mixture(void* X_out, hpcg_dtype dtype, int64_t m, int64_t n, int64_t n_comp, const double* means,
+                     const double* sigmas, const double* weights, double noise_frac, double noise_lo,
+                     double noise_hi, uint64_t seed, int n_threads) {
+    if (m < 1 || n < 1 || n_comp < 1) return fail(HPCG_EINVAL, "gen_mixture: bad shape");
+    std::vector<double> cum((size_t)n_comp);
+    double t = 0;
+    for (int64_t c = 0; c < n_comp; ++c) cum[(size_t)c] = (t += weights ? weights[c] : 1.0);
+    for (auto& v : cum) v /= t;
+    const uint64_t key = splitmix64(seed ^ 0x6d69787475726531ULL);
+    auto u01 = [](uint64_t h) { return ((double)(h >> 11) + 0.5) * 0x1.0p-53; };
+    auto work = [&](int64_t b, int64_t e_) {
+        for (int64_t i = b; i < e_; ++i) {
+            const uint64_t hr = splitmix64(key ^ splitmix64((uint64_t)i));
+            const bool noise = u01(splitmix64(hr ^ 0x11)) < noise_frac;
+            const double uc = u01(splitmix64(hr ^ 0x22));
+            int64_t comp = 0;
+            while (comp < n_comp - 1 && cum[(size_t)comp] <= uc) ++comp;
+            for (int64_t d = 0; d < n; d += 2) {
+                const uint64_t hd = splitmix64(hr + 0x9e3779b97f4a7c15ULL * (uint64_t)(d + 1));
+                double v0, v1;
+                if (noise) {
+                    v0 = noise_lo + (noise_hi - noise_lo) * u01(hd);
+                    v1 = noise_lo + (noise_hi - noise_lo) * u01(splitmix64(hd));
+                } else {
+                    const double a = u01(hd), bb = u01(splitmix64(hd));
+                    const double r = std::sqrt(-2.0 * std::log(a));
+                    v0 = means[comp * n + d] + sigmas[comp] * r * std::cos(6.283185307179586 * bb);
+                    v1 = d + 1 < n ? means[comp * n + d + 1] + sigmas[comp] * r * std::sin(6.283185307179586 * bb) : 0;
+                }
+                if (dtype == HPCG_F32) {
+                    float* X = static_cast<float*>(X_out) + i * n;
+                    X[d] = (float)v0;
+                    if (d + 1 < n) X[d + 1] = (float)v1;
+                } else {
+                    double* X = static_cast<double*>(X_out) + i * n;
+                    X[d] = v0;
+                    if (d + 1 < n) X[d + 1] = v1;
+                }
+            }
+        }
+    };
+    int T = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    if (m < 4096) T = 1;
+    std::vector<std::thread> th;
+    for (int ti = 0; ti < T; ++ti) {
+        int64_t b, e_;
+        chunk_range(m, T, ti, b, e_);
+        th.emplace_back(work, b, e_);
+    }
+    for (auto& x : th) x.join();
+    return HPCG_OK;
+}
+
+}  // extern "C"
