@@ -1,0 +1,403 @@
+#!/usr/bin/env python3
+"""HPClust hot-path benchmark (BASELINE.json metric: point-centroid distance evaluations/s in
+batched Lloyd; full-data f(C,X) GB/s).
+
+Workload (N=1): BASELINE.json configs[1] ("config 2"): X = 10,000,000 x 16 fp32 from a
+10-component Gaussian mixture (means U[-10,10]^16, sigma_c U[0.5,2], Zipf(1.1) weights;
+seeded synthetic stand-in), k=10, s=20,000, 256 workers per GPU, cooperative strategy,
+1,000 samples total -> max_samples=4 lockstep rounds (1,024 samples).
+
+One STEP = one complete HPClust run of that workload on the device-resident X: 4 rounds of
+{sample gather -> K-means++ reseed of degenerate slots -> Lloyd to convergence -> keep-best
+-> incumbent publication} for all 256 workers, select_best, and the full-data objective
+pass. value = distance evaluations of the step (the reference's n_d accounting:
+core.hpp:205, seeding.hpp:38) / step time. e2e = the same run through the C-ABI's one-call
+hpcg_run on HOST data (pinned), i.e. upload of X + rounds + final pass + result readback.
+
+Multi-GPU (torchrun): weak scaling, every rank runs the same per-GPU workload (its own X
+shard of 1e7 rows and 256 workers) and after every round the ranks all-gather their shared
+best (objective, global worker id, centroids) over NCCL and install the global winner
+(cooperative exchange).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built from the
+reference headers) runs hpclust::run on the same data (fp64), n_workers = host threads,
+max_samples=4, cooperative, on all host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+M, N, K, S, W_PER_GPU, ROUNDS = 10_000_000, 16, 10, 20_000, 256, 4
+METRIC = "point-centroid dist evals/s in batched Lloyd; full-data f(C,X) GB/s"
+UNIT = "evals/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+
+
+def mixture_params(seed=2311):
+    rs = np.random.default_rng(seed)
+    means = rs.uniform(-10, 10, (10, N))
+    sig = rs.uniform(0.5, 2.0, 10)
+    w = 1.0 / np.arange(1, 11) ** 1.1
+    return means, sig, w / w.sum()
+
+
+def make_data(rank: int):
+    import paper_2311_04517_b200 as hp
+    means, sig, w = mixture_params()
+    return hp.gen_mixture(M, N, means, sig, w, seed=1000 + rank, dtype=np.float32)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def exchange_best(eng, world, device):
+    """Cooperative exchange across ranks: all-gather (objective, global worker, centroids,
+    flags) and install the global winner (min objective, ties -> lowest worker id)."""
+    import torch
+    import torch.distributed as dist
+    obj, wk, C_, f = eng.export_best()
+    rec = torch.zeros(2 + C_.size + f.size, dtype=torch.float64, device=device)
+    rec[0] = obj
+    rec[1] = float(wk)
+    rec[2:2 + C_.size] = torch.from_numpy(C_.ravel())
+    rec[2 + C_.size:] = torch.from_numpy(f.astype(np.float64))
+    out = [torch.empty_like(rec) for _ in range(world)]
+    dist.all_gather(out, rec)
+    recs = [o.cpu().numpy() for o in out]
+    best = merge_records([(r[0], int(r[1])) for r in recs])
+    if best is not None and (recs[best][0] < obj or int(recs[best][1]) != wk):
+        r = recs[best]
+        eng.import_best(float(r[0]), int(r[1]), r[2:2 + C_.size].reshape(C_.shape), r[2 + C_.size:].astype(np.uint8))
+
+
+def merge_records(recs):
+    """Index of the winning (objective, worker) record: strict min objective, ties to the
+    lowest global worker id (engine.hpp:129-138 publication order); None if all infinite."""
+    best, bo, bw = None, float("inf"), None
+    for i, (o, w) in enumerate(recs):
+        if o < bo or (o == bo and bw is not None and w < bw and o != float("inf")):
+            best, bo, bw = i, o, w
+    return best
+
+
+def run_gpu(args, world, rank, local):
+    import torch
+    import paper_2311_04517_b200 as hp
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    X = make_data(rank)
+    Xd = torch.from_numpy(X).to(device)
+    stream = torch.cuda.current_stream(device)
+    ctx = hp.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    ds = hp.DeviceDataset.from_torch(Xd, ctx)
+    cfg = hp.EngineConfig(k=K, sample_size=S, n_workers=W_PER_GPU, max_samples=ROUNDS, strategy="cooperative",
+                          rng="philox", worker_base=rank * W_PER_GPU)
+    eng = hp.Engine(ds, cfg)
+    fma_tfma = ctx.fma_peak()
+
+    def step(seed):
+        eng.reset(seed)
+        for _ in range(ROUNDS):
+            eng.rounds(1)
+            if world > 1:
+                exchange_best(eng, world, device)
+        res = eng.finish()
+        return res
+
+    for i in range(args.warmup):
+        step(10_000 + i)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ctx.enable_timing(True)
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nd_total = 0
+    objs = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            res = step(20_000 + i)
+            nd_total += res.distance_evals
+            objs.append(res.full_objective)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    launches = ctx.launches - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    kt = ctx.kernel_times()
+    ctx.enable_timing(False)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+        n = torch.tensor([nd_total], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(n)
+        nd_all = float(n.item())
+    else:
+        nd_all = float(nd_total)
+    ms_step = ms_total / args.steps
+    value = nd_all / (ms_total * 1e-3)
+
+    # ---- full-data objective pass alone (f(C,X) GB/s, HBM roofline); X (640 MB) > L2
+    C_dev = torch.from_numpy(res.centroids).to(device)
+    cost = torch.zeros(1, dtype=torch.float64, device=device)
+    obj_ms = []
+    for i in range(3 + args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hp._lib.check(hp._lib.lib.hpcg_assign_dev(ctx.h, ds.h, C_dev.data_ptr(), K, None, cost.data_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            obj_ms.append(e0.elapsed_time(e1))
+    obj_bytes = M * N * 4
+    obj_gbs = obj_bytes / (np.median(obj_ms) * 1e-3) / 1e9
+
+    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # dominant kernel: the worker step (Lloyd screen = n FMA per evaluation)
+    step_cnt, step_ms = kt["step"]
+    lloyd_flops_per_launch = nd_total / max(1, step_cnt) * N * 2  # per-rank launches
+    achieved_tflops = lloyd_flops_per_launch / (step_ms / max(1, step_cnt) * 1e-3) / 1e12
+    peak_tflops = 2 * fma_tfma
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 screen + f64 accumulate/recheck", "data": "synthetic",
+        "config": {"workload": "BASELINE config 2: X 1e7x16 fp32 Gaussian mixture (10 comps, Zipf(1.1)), k=10, "
+                               "s=20000, 256 workers/GPU, cooperative, 4 lockstep rounds (1024 samples) + "
+                               "full-data f(C,X)", "m_per_gpu": M, "n": N, "k": K, "s": S,
+                   "workers_per_gpu": W_PER_GPU, "rounds": ROUNDS, "rng": "philox",
+                   "l2": "X (640 MB/GPU) exceeds L2 (126 MB); samples gathered from HBM every round",
+                   "parallelism": f"{world} GPU(s), one process per GPU, NCCL incumbent exchange per round"},
+        "distance_evals_per_step": nd_all / args.steps,
+        "objective_pass": {"gbs": obj_gbs, "ms": float(np.median(obj_ms)), "bytes": obj_bytes,
+                           "roofline": {"bound": "hbm", "achieved": obj_gbs, "peak": hbm_peak, "unit": "GB/s",
+                                        "frac": obj_gbs / hbm_peak, "traffic": None,
+                                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
+        "roofline": {"bound": "fma", "kernel": "worker_step_kernel", "achieved": achieved_tflops,
+                     "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
+                     "traffic": None,
+                     "algorithmic": "n_d (Lloyd+seeding evaluations) x n FMA x 2 flop per launch / mean launch time",
+                     "peak_source": "FFMA2 loop measured in-run on this GPU (fp32 FMA; MEASURED_PEAKS.json has "
+                                    "only hbm and bf16)",
+                     "launches": step_cnt, "mean_launch_ms": step_ms / max(1, step_cnt)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "mean_full_objective": float(np.mean(objs)),
+    }
+    return result, X, eng, ctx
+
+
+def e2e_run(X, args):
+    """hpcg_run on pinned host data: upload + rounds + final pass + readback, per step."""
+    import torch
+    import paper_2311_04517_b200 as hp
+    pinned = torch.from_numpy(X).pin_memory()
+    Xp = pinned.numpy()
+    cfg = hp.EngineConfig(k=K, sample_size=S, n_workers=W_PER_GPU, max_samples=ROUNDS, strategy="cooperative",
+                          rng="philox")
+    times, nds = [], []
+    for i in range(1 + max(1, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cfg.master_seed = 30_000 + i
+        r = hp.run(Xp, cfg)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i >= 1:
+            times.append(dt)
+            nds.append(r.distance_evals)
+    h2d = X.nbytes
+    d2h = K * N * 8 + K + 8 * 6
+    return {"value": float(np.sum(nds) / np.sum(times)), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(times) * 1e3),
+            "path": "hpcg_run (C-ABI one-call run, pinned host X) == hpclust::run"}
+
+
+def cpu_baseline(X, budget_s=10.0):
+    """The reference's own kmeans (oracle/_ref, stock code path) on config-2 samples, one
+    std::thread per worker (its competitive threading model, engine.hpp:313-332), host cores."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_py import ref
+    R = ref()
+    if R is None:
+        return None
+    P = host_cores()
+    rs = np.random.default_rng(0)
+    nd_tot, t_tot, reps = 0, 0.0, 0
+    while t_tot < budget_s and reps < 1000:
+        idx = [rs.choice(M, S, replace=False) for _ in range(P)]
+        samples = np.stack([X[i].astype(np.float64) for i in idx])
+        inits = np.stack([smp[rs.choice(S, K, replace=False)] for smp in samples])
+        t0 = time.perf_counter()
+        nd, _ = R.kmeans_threads(samples, inits)
+        t_tot += time.perf_counter() - t0
+        nd_tot += nd
+        reps += 1
+    return {"value": nd_tot / t_tot, "unit": "Lloyd evals/s", "cores": P, "kind": "reference",
+            "sample": f"{reps} batches x {P} workers: reference kmeans() (lloyd.hpp:100-164) on s=20000 x 16 "
+                      f"config-2 samples from random-row inits, {t_tot:.1f} s CPU wall",
+            "cpu_model": cpu_model()}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: hpclust::run (reference, oracle/_ref) on the config-2 data in fp64."""
+    if rank != 0:
+        return None
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_py import ref
+    R = ref()
+    if R is None:
+        return {"impl": "reference", "unavailable": "oracle/_ref/libhpclust_ref.so not built"}
+    P = host_cores()
+    X = make_data(0).astype(np.float64)
+    Wr = min(W_PER_GPU, P)
+    times, nds = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = R.run(X, k=K, sample_size=S, n_workers=Wr, max_samples=ROUNDS, strategy="cooperative", seed=40_000 + i,
+                  n_threads=P, full=True)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            nds.append(r["distance_evals"])
+    value = float(np.sum(nds) / np.sum(times))
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(times) * 1e3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config 2 data (fp64 copy), hpclust::run cooperative, {Wr} workers "
+                                   f"(host threads) x 4 lockstep rounds + full-data objective",
+                       "m": M, "n": N, "k": K, "s": S, "workers": Wr, "rounds": ROUNDS},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "reference",
+                             "sample": f"{args.steps} full reference runs with {Wr} workers (bounded sample of the "
+                                       f"256-worker workload)", "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    result, X, eng, ctx = run_gpu(args, world, rank, local)
+    if rank == 0:
+        if not args.no_e2e and world == 1:
+            result["e2e"] = e2e_run(X, args)
+        elif world > 1:
+            result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                             "note": "e2e measured at N=1"}
+        if not args.no_cpu and world == 1:
+            result["cpu_baseline"] = cpu_baseline(X)
+        print(json.dumps(result))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -71,7 +71,9 @@ int hpcg_abi_version(void);
 /* ---- context ----------------------------------------------------------------------- */
 int hpcg_ctx_create(int device, hpcg_ctx** out);
 int hpcg_ctx_destroy(hpcg_ctx* ctx);
-/* Run on a caller stream (e.g. torch.cuda.current_stream().cuda_stream); NULL = own stream. */
+/* Run on a caller stream (e.g. torch.cuda.current_stream().cuda_stream; NULL = the legacy
+ * default stream, which is what torch's default stream handle 0 denotes). A context starts on
+ * its own non-blocking stream. */
 int hpcg_ctx_set_stream(hpcg_ctx* ctx, void* cuda_stream);
 int hpcg_ctx_synchronize(hpcg_ctx* ctx);
 /* Number of kernels this library launched on the context since creation (bench evidence). */

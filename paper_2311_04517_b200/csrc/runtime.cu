@@ -393,13 +393,8 @@ int hpcg_ctx_set_stream(hpcg_ctx* ctx, void* st) {
     std::lock_guard<std::mutex> lk(ctx->mu);
     cudaSetDevice(ctx->device);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
-    if (st) {
-        ctx->stream = static_cast<cudaStream_t>(st);
-        ctx->own_stream = false;
-    } else {
-        CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-        ctx->own_stream = true;
-    }
+    ctx->stream = static_cast<cudaStream_t>(st);  // NULL: legacy default stream
+    ctx->own_stream = false;
     return HPCG_OK;
 }
 

@@ -118,7 +118,7 @@ struct Geo {
 
 struct SmemLayout {  // byte offsets into dynamic smem
     int samp, cm, cs, part, scratch, total;
-    int labels, wpart, d2;
+    int labels, pos, perm, wpart, d2, gidx;
 };
 
 template <typename T, int NP>
@@ -133,9 +133,12 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k) {
     L.part = up(L.cs + k * G::CSR * 4);
     L.scratch = up(L.part + 2 * part_d * 8);
     L.labels = L.scratch;
-    L.wpart = up(L.labels + rows_cap);
+    L.pos = up(L.labels + rows_cap);
+    L.perm = up(L.pos + rows_cap * 2);
+    L.wpart = up(L.perm + rows_cap * 2);
     const int lloyd_end = L.wpart + kStepWarps * part_d * 8;
-    L.d2 = L.scratch;
+    L.d2 = L.scratch;    // seeding only
+    L.gidx = L.scratch;  // gather only
     const int seed_end = L.d2 + rows_cap * 8;
     L.total = up(lloyd_end > seed_end ? lloyd_end : seed_end);
     return L;
@@ -155,6 +158,9 @@ struct StepShared {  // static smem: per-step scalars and exchange slots
     double wtot[kStepWarps];
     long long whit[kStepWarps][kMaxCandidates];
     float cmax;
+    int32_t wcnt[kStepWarps][kMaxK];  // per-warp label counts (counting sort)
+    int32_t woff[kStepWarps][kMaxK];  // sorted-order offset of (warp, label)
+    int32_t cstart[kMaxK + 1];        // sorted-order start of each cluster
     int32_t decision;  // 0 continue, 1 done
     int32_t err;
 };
@@ -201,6 +207,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
     float* cs = reinterpret_cast<float*>(smem + L.cs);
     double* part = reinterpret_cast<double*>(smem + L.part);
     uint8_t* labels = smem + L.labels;
+    uint16_t* pos = reinterpret_cast<uint16_t*>(smem + L.pos);
+    uint16_t* perm = reinterpret_cast<uint16_t*>(smem + L.perm);
     double* wpart = reinterpret_cast<double*>(smem + L.wpart);
     double* d2 = reinterpret_cast<double*>(smem + L.d2);
     const int part_d = k * NP + k + 1;
@@ -215,30 +223,30 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             if (p.sample_mode == 1) return (int64_t)prp((uint64_t)i);
             return (int64_t)wl * s + i;
         };
-        // every copy is issued before any is awaited (cp.async: no register staging), so a
-        // CTA keeps its whole sample chunk in flight at once
+        // (a) one sample index per row into smem; (b) every copy is issued before any is
+        // awaited (cp.async, no register staging) so the CTA's whole chunk is in flight at once
+        int64_t* gx = reinterpret_cast<int64_t*>(smem + L.gidx);
+        for (int li = tid; li < nr; li += kStepThreads) gx[li] = gidx_of(r0 + li);
+        __syncthreads();
         const int rowb = n * (int)sizeof(T);
         if ((rowb & 15) == 0) {  // 16-B chunks
             const int cpr = rowb >> 4;
             constexpr int EPC = 16 / (int)sizeof(T);
             for (int e = tid; e < nr * cpr; e += kStepThreads) {
                 const int li = e / cpr, q = e - li * cpr;
-                const int64_t g = gidx_of(r0 + li);
-                cp_async16(samp + G::elem_off(li, q * EPC), X + g * n + q * EPC);
+                cp_async16(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
             }
         } else if ((rowb & 7) == 0) {  // 8-B chunks
             const int cpr = rowb >> 3;
             constexpr int EPC = 8 / (int)sizeof(T);
             for (int e = tid; e < nr * cpr; e += kStepThreads) {
                 const int li = e / cpr, q = e - li * cpr;
-                const int64_t g = gidx_of(r0 + li);
-                cp_async8(samp + G::elem_off(li, q * EPC), X + g * n + q * EPC);
+                cp_async8(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
             }
         } else {  // 4-B elements (fp32, odd n)
             for (int e = tid; e < nr * n; e += kStepThreads) {
                 const int li = e / n, d = e - li * n;
-                const int64_t g = gidx_of(r0 + li);
-                cp_async4(samp + G::elem_off(li, d), X + g * n + d);
+                cp_async4(samp + G::elem_off(li, d), X + gx[li] * n + d);
             }
         }
         if (NP > n)
@@ -270,6 +278,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
         }
     }
     cp_async_wait_all();
+    __syncthreads();  // gx (aliases d2) fully consumed before seeding reuses the region
     cluster.sync();  // sample rows of every CTA now visible cluster-wide (DSMEM)
 
     int64_t nd = 0;  // distance evaluations (reference accounting)
@@ -527,6 +536,8 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             const float cmax = sh.cmax;
 
             // ---- assign: fp32 FFMA2 screen, exact fp64 recheck of near ties
+            if (lane < kMaxK) sh.wcnt[warp][lane] = 0;
+            __syncwarp();
             for (int g = warp; g < ngroups; g += kStepWarps) {
                 float2 x2[G::R][G::NPF / 2];
                 float xn[G::R];
@@ -590,10 +601,10 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                 }
 #pragma unroll
                 for (int r = 0; r < G::R; ++r) {
-                    if (!valid[r]) continue;
                     const int row = g * G::GROUP + r * 32 + lane;
-                    const float sc = xn[r] + cmax;
                     int lab = i1[r];
+                    if (valid[r]) {
+                    const float sc = xn[r] + cmax;
                     if (!(m2[r] - m1[r] > kappa * sc * sc)) {  // near tie (or k == 1 -> m2 = inf skips)
                         double best = __longlong_as_double(0x7ff0000000000000LL);
                         lab = 0;
@@ -610,46 +621,112 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                         }
                     }
                     labels[row] = (uint8_t)lab;
+                    }
+                    // stable counting-sort rank of this row among the warp's rows with its label
+                    const unsigned peers = __match_any_sync(0xffffffffu, valid[r] ? lab : 0xff);
+                    const int rank = __popc(peers & ((1u << lane) - 1u));
+                    const int base = valid[r] ? sh.wcnt[warp][lab] : 0;
+                    __syncwarp();
+                    if (valid[r]) {
+                        if (rank == 0) sh.wcnt[warp][lab] = base + __popc(peers);
+                        pos[row] = (uint16_t)(base + rank);
+                    }
+                    __syncwarp();
                 }
             }
             __syncthreads();
+            // cluster ranges of the sorted order and (warp, label) offsets
+            if (warp == 0) {
+                int col = 0;
+                for (int w2 = 0; w2 < kStepWarps; ++w2) col += lane < k ? sh.wcnt[w2][lane] : 0;
+                int incl = col;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int start = incl - col;
+                if (lane < k) {
+                    sh.cstart[lane] = start;
+                    int run = start;
+                    for (int w2 = 0; w2 < kStepWarps; ++w2) {
+                        sh.woff[w2][lane] = run;
+                        run += sh.wcnt[w2][lane];
+                    }
+                }
+                if (lane == k - 1) sh.cstart[k] = incl;
+            }
+            __syncthreads();
+            for (int li = tid; li < nr; li += kStepThreads) {
+                const int w2 = (li / G::GROUP) % kStepWarps;
+                perm[sh.woff[w2][labels[li]] + pos[li]] = (uint16_t)li;
+            }
+            __syncthreads();
 
-            // ---- update: per-warp partial sums / counts / cost in fixed order
+            // ---- update: sums / cost along the label-sorted order. Warp w owns sorted
+            // positions [w*L, (w+1)*L); per cluster its lanes cover ROWS_PER_STEP rows x
+            // LANES_PER_ROW units (16-B chunks or single elements) so every smem read is a
+            // vector load and no label test sits in the inner loop. Fixed order throughout.
             {
+                constexpr int U = G::VEC16 ? 16 / (int)sizeof(T) : 1;       // elements per lane unit
+                constexpr int UPR = G::VEC16 ? G::CPR : NP;                  // units per row
+                constexpr int LR = UPR <= 1 ? 1 : UPR <= 2 ? 2 : UPR <= 4 ? 4 : UPR <= 8 ? 8 : UPR <= 16 ? 16 : 32;
+                constexpr int RPS = 32 / LR;                                 // rows per step
                 double* wp = wpart + warp * part_d;
-                const int gi = lane / G::LPR, di = lane % G::LPR;
+                const int gi = lane / LR, q = lane % LR;
+                const bool active_unit = q < UPR;
+                const int Lw = (nr + kStepWarps - 1) / kStepWarps;
+                const int lo = warp * Lw < nr ? warp * Lw : nr;
+                const int hi = lo + Lw < nr ? lo + Lw : nr;
                 double cost_w = 0.0;
                 for (int j = 0; j < k; ++j) {
-                    const double cj = di < n ? Cm[j * NP + di] : 0.0;
-                    double acc = 0.0, accc = 0.0;
-                    int cnt = 0;
-                    for (int g = warp; g < ngroups; g += kStepWarps) {
-                        for (int q = 0; q < G::R; ++q) {
-                            const int rowb = g * G::GROUP + q * 32;
-                            const int row_l = rowb + lane;
-                            const bool hitj = row_l < nr && labels[row_l] == j;
-                            unsigned b = __ballot_sync(0xffffffffu, hitj);
-                            cnt += __popc(b);
-                            while (b) {
-                                unsigned bb = b;
-                                for (int t = 0; t < gi; ++t) bb &= bb - 1;  // gi-th set bit
-                                if (bb && di < n) {
-                                    const int row = rowb + __ffs(bb) - 1;
-                                    const double xv = (double)samp[G::elem_off(row, di)];
-                                    acc += xv;
-                                    const double diff = xv - cj;
+                    const int a = max(sh.cstart[j], lo), b = min(sh.cstart[j + 1], hi);
+                    double acc[U], cj[U];
+                    double accc = 0.0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        acc[u] = 0.0;
+                        const int d = q * U + u;
+                        cj[u] = (active_unit && d < NP) ? Cm[j * NP + d] : 0.0;
+                    }
+                    for (int p0 = a; p0 < b; p0 += RPS) {
+                        const int pp = p0 + gi;
+                        if (pp < b && active_unit) {
+                            const int row = perm[pp];
+                            if constexpr (G::VEC16 && sizeof(T) == 4) {
+                                const float4 v = *reinterpret_cast<const float4*>(samp + G::elem_off(row, q * 4));
+                                const double xv[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    acc[u] += xv[u];
+                                    const double diff = xv[u] - cj[u];
                                     accc = fma(diff, diff, accc);
                                 }
-#pragma unroll
-                                for (int t = 0; t < G::RPS; ++t) b &= b - 1;
+                            } else if constexpr (G::VEC16) {
+                                const double2 v = *reinterpret_cast<const double2*>(samp + G::elem_off(row, q * 2));
+                                acc[0] += v.x;
+                                acc[1] += v.y;
+                                const double d0 = v.x - cj[0], d1 = v.y - cj[1];
+                                accc = fma(d0, d0, accc);
+                                accc = fma(d1, d1, accc);
+                            } else {
+                                const double xv = (double)samp[G::elem_off(row, q)];
+                                acc[0] += xv;
+                                const double diff = xv - cj[0];
+                                accc = fma(diff, diff, accc);
                             }
                         }
                     }
-                    // fold the lane groups (fixed tree) -> lanes of group 0 hold the sums
+                    // fold the row groups (fixed tree): lanes gi == 0 hold the sums
 #pragma unroll
-                    for (int o = 16; o >= G::LPR; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-                    if (lane < NP) wp[j * NP + lane] = lane < n ? acc : 0.0;
-                    if (lane == 0) wp[k * NP + j] = (double)cnt;
+                    for (int o = 16; o >= LR; o >>= 1)
+#pragma unroll
+                        for (int u = 0; u < U; ++u) acc[u] += __shfl_down_sync(0xffffffffu, acc[u], o);
+                    if (gi == 0 && active_unit)
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (q * U + u < NP) wp[j * NP + q * U + u] = acc[u];
+                    if (lane == 0) wp[k * NP + j] = (double)(b > a ? b - a : 0);
                     cost_w += warp_sum(accc);
                 }
                 if (lane == 0) wp[k * NP + k] = cost_w;
