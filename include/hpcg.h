@@ -179,6 +179,10 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
 int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed);
 int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds);
 int64_t hpcg_engine_round_index(const hpcg_engine* e);
+/* Diagnostics: per-CTA phase timestamps (%globaltimer ns) of subsequent rounds written to
+ * trace_dev[W * cluster * 16] (NULL disables); mode 0 details the first Lloyd pass, mode 1
+ * the first K-means++ slot. */
+int hpcg_engine_set_trace(hpcg_engine* e, int64_t* trace_dev, int32_t mode);
 /* Sum of n_d over the rounds run so far (device-side exact count; synchronises). */
 int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d);
 /* Outputs as hpref/orc_run: centroids[k*n], flags[k], labels[m] (if compute_assignment),

@@ -23,7 +23,7 @@ struct StepGeometry {
 // Chooses the cluster size (smallest that fits the sample in smem, widened while the
 // occupancy API reports more SMs in use) and launches W clusters. Returns a CUDA error.
 cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeometry* geo_out, std::string* why);
-cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int W, StepGeometry* g, std::string* why);
+cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why);
 
 // *nblocks: in = capacity of p.block_cost, out = grid used (fixed per device/kernel/kv)
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st);

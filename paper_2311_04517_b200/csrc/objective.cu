@@ -6,8 +6,8 @@ namespace hpcg {
 
 cudaError_t launch_step_f32(const StepParams& p, cudaStream_t st, StepGeometry* g, std::string* why, int np);
 cudaError_t launch_step_f64(const StepParams& p, cudaStream_t st, StepGeometry* g, std::string* why, int np);
-cudaError_t geometry_f32(int np, int64_t s, int k, int W, StepGeometry* g, std::string* why);
-cudaError_t geometry_f64(int np, int64_t s, int k, int W, StepGeometry* g, std::string* why);
+cudaError_t geometry_f32(int np, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why);
+cudaError_t geometry_f64(int np, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why);
 
 int pick_np(int dtype, int n) {
     static const int f32[] = {2, 4, 8, 12, 16, 24, 32};
@@ -28,10 +28,10 @@ cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeo
     return dtype == 0 ? launch_step_f32(p, st, g, why, np) : launch_step_f64(p, st, g, why, np);
 }
 
-cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int W, StepGeometry* g, std::string* why) {
+cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why) {
     const int np = pick_np(dtype, n);
     if (np == 0) return cudaErrorInvalidValue;
-    return dtype == 0 ? geometry_f32(np, s, k, W, g, why) : geometry_f64(np, s, k, W, g, why);
+    return dtype == 0 ? geometry_f32(np, s, k, ncand, W, g, why) : geometry_f64(np, s, k, ncand, W, g, why);
 }
 
 int objective_blocks() {  // upper bound on the grid of any objective launch

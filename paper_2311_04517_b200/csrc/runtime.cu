@@ -670,7 +670,7 @@ int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_
         if (!(cfg->rel_tol > 0.0)) return fail(HPCG_EINVAL, "kmeans: rel_tol must be positive");
     }
     if (int rc = check_shape(ds->dtype, n, k)) return rc;
-    if (cfg->candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 8 K-means++ candidates");
+    if (cfg->candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 4 K-means++ candidates per centre");
     if (idx_host) {
         for (int64_t i = 0; i < W * s; ++i)
             if (idx_host[i] < 0 || idx_host[i] >= ds->m) return fail(HPCG_EINVAL, "sample index out of range");
@@ -800,6 +800,8 @@ struct hpcg_engine {
     std::vector<int64_t> h_idx, h_fr;
     std::vector<double> h_un;
     int64_t ucap = 0;
+    int64_t* trace_buf = nullptr;  // optional phase timeline (hpcg_engine_set_trace)
+    int32_t trace_mode = 0;
 };
 
 namespace {
@@ -897,6 +899,8 @@ int engine_round(hpcg_engine* e) {
     p.inc_f = e->inc_f.as<uint8_t>();
     p.inc_obj = e->inc_obj.as<double>();
     p.accepted = e->acc.as<uint8_t>();
+    p.trace = e->trace_buf;
+    p.trace_mode = e->trace_mode;
     std::string why;
     KTimer kt(ctx, 0);
     cudaError_t ce = launch_step(e->ds->dtype, p, ctx->stream, nullptr, &why);
@@ -976,11 +980,11 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     if (cfg.max_iters < 1) return fail(HPCG_EINVAL, "kmeans: max_iters must be positive");
     if (!(cfg.rel_tol > 0.0)) return fail(HPCG_EINVAL, "kmeans: rel_tol must be positive");
     if (cfg.candidates < 1) return fail(HPCG_EINVAL, "seeding: need at least one candidate");
-    if (cfg.candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 8 K-means++ candidates");
+    if (cfg.candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 4 K-means++ candidates per centre");
     if (int rc = check_shape(ds->dtype, ds->n, cfg.k)) return rc;
     StepGeometry g;
     std::string why;
-    if (step_geometry(ds->dtype, (int)ds->n, cfg.sample_size, (int)cfg.k, (int)cfg.n_workers, &g, &why) != cudaSuccess)
+    if (step_geometry(ds->dtype, (int)ds->n, cfg.sample_size, (int)cfg.k, (int)cfg.candidates, (int)cfg.n_workers, &g, &why) != cudaSuccess)
         return fail(HPCG_EUNSUPPORTED, "worker step geometry: " + why);
 
     auto* e = new hpcg_engine;
@@ -1123,6 +1127,12 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
 }
 
 int64_t hpcg_engine_round_index(const hpcg_engine* e) { return e->round; }
+
+int hpcg_engine_set_trace(hpcg_engine* e, int64_t* trace_dev, int32_t mode) {
+    e->trace_buf = trace_dev;
+    e->trace_mode = mode;
+    return HPCG_OK;
+}
 
 int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);

@@ -16,15 +16,15 @@ cudaError_t launch_step_f32(const StepParams& p, cudaStream_t st, StepGeometry* 
     return cudaErrorInvalidValue;
 }
 
-cudaError_t geometry_f32(int np, int64_t s, int k, int W, StepGeometry* g, std::string* why) {
+cudaError_t geometry_f32(int np, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why) {
     switch (np) {
-        case 2: return step_geometry_t<float, 2>(s, k, W, g, why);
-        case 4: return step_geometry_t<float, 4>(s, k, W, g, why);
-        case 8: return step_geometry_t<float, 8>(s, k, W, g, why);
-        case 12: return step_geometry_t<float, 12>(s, k, W, g, why);
-        case 16: return step_geometry_t<float, 16>(s, k, W, g, why);
-        case 24: return step_geometry_t<float, 24>(s, k, W, g, why);
-        case 32: return step_geometry_t<float, 32>(s, k, W, g, why);
+        case 2: return step_geometry_t<float, 2>(s, k, ncand, W, g, why);
+        case 4: return step_geometry_t<float, 4>(s, k, ncand, W, g, why);
+        case 8: return step_geometry_t<float, 8>(s, k, ncand, W, g, why);
+        case 12: return step_geometry_t<float, 12>(s, k, ncand, W, g, why);
+        case 16: return step_geometry_t<float, 16>(s, k, ncand, W, g, why);
+        case 24: return step_geometry_t<float, 24>(s, k, ncand, W, g, why);
+        case 32: return step_geometry_t<float, 32>(s, k, ncand, W, g, why);
     }
     return cudaErrorInvalidValue;
 }

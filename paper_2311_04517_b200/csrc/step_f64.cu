@@ -19,18 +19,18 @@ cudaError_t launch_step_f64(const StepParams& p, cudaStream_t st, StepGeometry* 
     return cudaErrorInvalidValue;
 }
 
-cudaError_t geometry_f64(int np, int64_t s, int k, int W, StepGeometry* g, std::string* why) {
+cudaError_t geometry_f64(int np, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why) {
     switch (np) {
-        case 1: return step_geometry_t<double, 1>(s, k, W, g, why);
-        case 2: return step_geometry_t<double, 2>(s, k, W, g, why);
-        case 3: return step_geometry_t<double, 3>(s, k, W, g, why);
-        case 4: return step_geometry_t<double, 4>(s, k, W, g, why);
-        case 6: return step_geometry_t<double, 6>(s, k, W, g, why);
-        case 8: return step_geometry_t<double, 8>(s, k, W, g, why);
-        case 12: return step_geometry_t<double, 12>(s, k, W, g, why);
-        case 16: return step_geometry_t<double, 16>(s, k, W, g, why);
-        case 24: return step_geometry_t<double, 24>(s, k, W, g, why);
-        case 32: return step_geometry_t<double, 32>(s, k, W, g, why);
+        case 1: return step_geometry_t<double, 1>(s, k, ncand, W, g, why);
+        case 2: return step_geometry_t<double, 2>(s, k, ncand, W, g, why);
+        case 3: return step_geometry_t<double, 3>(s, k, ncand, W, g, why);
+        case 4: return step_geometry_t<double, 4>(s, k, ncand, W, g, why);
+        case 6: return step_geometry_t<double, 6>(s, k, ncand, W, g, why);
+        case 8: return step_geometry_t<double, 8>(s, k, ncand, W, g, why);
+        case 12: return step_geometry_t<double, 12>(s, k, ncand, W, g, why);
+        case 16: return step_geometry_t<double, 16>(s, k, ncand, W, g, why);
+        case 24: return step_geometry_t<double, 24>(s, k, ncand, W, g, why);
+        case 32: return step_geometry_t<double, 32>(s, k, ncand, W, g, why);
     }
     return cudaErrorInvalidValue;
 }

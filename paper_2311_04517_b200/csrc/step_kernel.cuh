@@ -19,10 +19,10 @@
 
 namespace hpcg {
 
-constexpr int kStepThreads = 256;  // 2 CTAs per SM: one cluster gathers while another computes
+constexpr int kStepThreads = 512;  // one CTA per SM, 16 warps
 constexpr int kStepWarps = kStepThreads / 32;
 constexpr int kMaxK = 32;          // label fits u8 and the per-warp partial table fits smem
-constexpr int kMaxCandidates = 8;  // K-means++ candidates per slot evaluated in one sweep
+constexpr int kMaxCandidates = 4;  // K-means++ candidates per slot (reference default 3) in one sweep
 
 enum StepErr : int32_t { kErrNone = 0, kErrDegenerateInit = 1, kErrMonotone = 2 };
 
@@ -76,7 +76,22 @@ struct StepParams {
     uint8_t* inc_f;
     double* inc_obj;
     uint8_t* accepted;
+    // optional phase timeline (ns, %globaltimer) per CTA: [W*C][kTraceSlots]
+    int64_t* trace;
+    int32_t trace_mode;  // 0: first Lloyd pass in detail, 1: first K-means++ slot in detail
 };
+
+constexpr int kTraceSlots = 16;
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
+
+HPCG_DEV int64_t gtimer() {
+    int64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ------------------------------------------------------------- smem geometry
 template <typename T, int NP>
@@ -118,11 +133,22 @@ struct Geo {
 
 struct SmemLayout {  // byte offsets into dynamic smem
     int samp, cm, cs, part, scratch, total;
-    int labels, pos, perm, wpart, d2, gidx;
+    int labels, pos, perm, wpart, d2, gidx, xnorm, wlist;
 };
 
+// per-warp exact-work list: one 32-row chunk of (row, candidate) entries plus a carried
+// partial batch of < 32
+__host__ __device__ constexpr int list_cap(int ncand) { return 32 * (ncand + 1); }
+
+// receive slot stride (doubles) of the cluster exchange: a Lloyd partial or seeding scalars
+__host__ __device__ inline int xch_stride(int k, int NP) {
+    const int part_d = k * NP + k + 1;
+
+    return part_d > 2 * kMaxCandidates ? part_d : 2 * kMaxCandidates;
+}
+
 template <typename T, int NP>
-__host__ __device__ inline SmemLayout step_layout(int rows_cap, int k) {
+__host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand, int C) {
     using G = Geo<T, NP>;
     SmemLayout L;
     auto up = [](int v) { return (v + 15) & ~15; };
@@ -131,30 +157,38 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k) {
     L.cm = up(L.samp + rows_cap * G::RS);
     L.cs = up(L.cm + k * NP * 8);
     L.part = up(L.cs + k * G::CSR * 4);
-    L.scratch = up(L.part + 2 * part_d * 8);
+    L.scratch = up(L.part + 2 * C * xch_stride(k, NP) * 8);  // exchange receive buffers
     L.labels = L.scratch;
     L.pos = up(L.labels + rows_cap);
     L.perm = up(L.pos + rows_cap * 2);
-    L.wpart = up(L.perm + rows_cap * 2);
+    L.wpart = up(L.perm + (rows_cap + (kStepWarps + 1) * G::GROUP) * 2);
     const int lloyd_end = L.wpart + kStepWarps * part_d * 8;
     L.d2 = L.scratch;    // seeding only
     L.gidx = L.scratch;  // gather only
-    const int seed_end = L.d2 + rows_cap * 8;
+    L.xnorm = up(L.d2 + rows_cap * 8);
+    L.wlist = up(L.xnorm + rows_cap * 4);
+    const int seed_end = L.wlist + kStepWarps * list_cap(ncand) * 4;
     L.total = up(lloyd_end > seed_end ? lloyd_end : seed_end);
     return L;
 }
 
 struct StepShared {  // static smem: per-step scalars and exchange slots
+    uint64_t xbar[2];                        // exchange mbarriers (parity buffered)
     uint8_t flags[kMaxK];
     int32_t pending[kMaxK];
     int32_t n_pending, n_valid;
     double xch_total[2];                     // CTA CDF totals (parity buffered)
     long long xch_hit[2][kMaxCandidates];    // first CDF hit per candidate
     double xch_cost[2][kMaxCandidates];      // candidate cost partials
+    double xch_err[2][kMaxCandidates];       // their screen error budgets
     double cand[kMaxCandidates][32];         // candidate coordinates (fp64, n <= 32)
+    float candf[kMaxCandidates][32];         // negated fp32 copy for the screen
+    float candn[kMaxCandidates];             // |candidate| (fp32, rounded up)
     double wsum[kStepWarps][kMaxCandidates];
     double rank_val[16];
     double rank_cost[kMaxCandidates][16];
+    double rank_err[kMaxCandidates][16];
+    double werr[kStepWarps][kMaxCandidates];
     double wtot[kStepWarps];
     long long whit[kStepWarps][kMaxCandidates];
     float cmax;
@@ -164,6 +198,36 @@ struct StepShared {  // static smem: per-step scalars and exchange slots
     int32_t decision;  // 0 continue, 1 done
     int32_t err;
 };
+
+// ------------------------------------------------- cluster exchange primitives
+// Push model (no cluster barrier): every CTA st.async's its values into a slot of each peer's
+// receive buffer with mbarrier complete_tx; each CTA then waits only on its own mbarrier.
+HPCG_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+HPCG_DEV uint32_t mapa_u32(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+HPCG_DEV void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+HPCG_DEV void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+HPCG_DEV void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+HPCG_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+HPCG_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
 
 HPCG_DEV void cp_async16(void* sdst, const void* gsrc) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
@@ -184,9 +248,66 @@ HPCG_DEV void cp_async_wait_group() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------- row helpers
+// Row `row` of the smem sample as fp32 pairs (operand of the fp32 screens).
+template <typename T, int NP>
+HPCG_DEV void load_row_f32(const T* samp, int row, float2 (&x2)[Geo<T, NP>::NPF / 2]) {
+    using G = Geo<T, NP>;
+    if constexpr (G::VEC16 && sizeof(T) == 4) {
+#pragma unroll
+        for (int q = 0; q < NP / 4; ++q) {
+            const float4 v = *reinterpret_cast<const float4*>(samp + G::elem_off(row, q * 4));
+            x2[2 * q] = make_float2(v.x, v.y);
+            x2[2 * q + 1] = make_float2(v.z, v.w);
+        }
+    } else if constexpr (G::VEC16) {
+#pragma unroll
+        for (int q = 0; q < NP / 2; ++q) {
+            const double2 v = *reinterpret_cast<const double2*>(samp + G::elem_off(row, q * 2));
+            x2[q] = make_float2((float)v.x, (float)v.y);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < G::NPF / 2; ++q) {
+            const float a = (float)samp[G::elem_off(row, 2 * q)];
+            const float b = 2 * q + 1 < NP ? (float)samp[G::elem_off(row, 2 * q + 1)] : 0.f;
+            x2[q] = make_float2(a, b);
+        }
+    }
+}
+
+// fp32 direct-form squared distance to a point stored negated as fp32 pairs (FADD2+FFMA2).
+// |result - exact| <= kScreenK * (|x| + |c|)^2 with kScreenK below (covers fp64 inputs
+// rounded to fp32, the per-term rounding and the pair sums).
+template <int NPF>
+HPCG_DEV float screen_dist(const float2 (&x2)[NPF / 2], const float* negc) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NPF / 2; ++q) {
+        const float2 df = __fadd2_rn(x2[q], *reinterpret_cast<const float2*>(negc + 2 * q));
+        acc = __ffma2_rn(df, df, acc);
+    }
+    return acc.x + acc.y;
+}
+
+// The reference distance (core.hpp:100-108): ascending d, separately rounded sub/mul/add.
+template <typename T, int NP>
+HPCG_DEV double exact_dist(const T* samp, int row, const double* c, int n) {
+    using G = Geo<T, NP>;
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < NP; ++d) {
+        if (d < n) {
+            const double diff = __dsub_rn((double)samp[G::elem_off(row, d)], c[d]);
+            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+        }
+    }
+    return acc;
+}
+
 // ------------------------------------------------------------------ the kernel
 template <typename T, int NP>
-__global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const StepParams p) {
+__global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const StepParams p) {
     using G = Geo<T, NP>;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
@@ -201,7 +322,14 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
 
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ StepShared sh;
-    const SmemLayout L = step_layout<T, NP>(p.rows_cap, k);
+    int64_t* trace = p.trace ? p.trace + (int64_t)blockIdx.x * kTraceSlots : nullptr;
+    int tslot = 0;
+    auto mark = [&]() {
+        if (trace && tid == 0 && tslot < kTraceSlots) trace[tslot] = gtimer();
+        ++tslot;
+    };
+    mark();  // 0: start
+    const SmemLayout L = step_layout<T, NP>(p.rows_cap, k, p.candidates, C);
     T* samp = reinterpret_cast<T*>(smem + L.samp);
     double* Cm = reinterpret_cast<double*>(smem + L.cm);
     float* cs = reinterpret_cast<float*>(smem + L.cs);
@@ -212,6 +340,25 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
     double* wpart = reinterpret_cast<double*>(smem + L.wpart);
     double* d2 = reinterpret_cast<double*>(smem + L.d2);
     const int part_d = k * NP + k + 1;
+    const int xs = xch_stride(k, NP);
+    // one exchange: values v(e), e < nv, of this CTA land in slot [cr] of every CTA's receive
+    // buffer; returns the local buffer holding all C slots (rank order). Callers separate the
+    // reads of one exchange from the pushes of the next with a __syncthreads.
+    uint32_t xcount = 0, xph0 = 0, xph1 = 0;
+    auto exchange = [&](int nv, auto&& value_of) -> const double* {
+        const int par = (int)(xcount++ & 1);
+        double* rx = part + par * C * xs;
+        uint64_t* bar = &sh.xbar[par];
+        if (tid == 0) mbar_expect_tx(bar, (uint32_t)(C * nv * 8));
+        const uint32_t rbar_local = smem_u32(bar), slot_local = smem_u32(rx + cr * xs);
+        for (int e = tid; e < nv; e += kStepThreads) {
+            const double v = value_of(e);
+            for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(slot_local + e * 8, r), v, mapa_u32(rbar_local, r));
+        }
+        mbar_wait_cluster(bar, par ? xph1 : xph0);
+        if (par) xph1 ^= 1u; else xph0 ^= 1u;
+        return rx;
+    };
 
     // ---------------------------------------------------------------- gather
     {
@@ -229,7 +376,14 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
         for (int li = tid; li < nr; li += kStepThreads) gx[li] = gidx_of(r0 + li);
         __syncthreads();
         const int rowb = n * (int)sizeof(T);
-        if ((rowb & 15) == 0) {  // 16-B chunks
+        if (G::VEC16 && n == NP) {  // whole rows of 16-B chunks; consecutive lanes take consecutive
+            // chunks of the same row so each warp instruction touches few distinct lines
+            constexpr int EPC = 16 / (int)sizeof(T);
+            for (int e = tid; e < nr * G::CPR; e += kStepThreads) {
+                const int li = e / G::CPR, q = e % G::CPR;
+                cp_async16(samp + G::elem_off(li, q * EPC), X + gx[li] * NP + q * EPC);
+            }
+        } else if ((rowb & 15) == 0) {  // 16-B chunks
             const int cpr = rowb >> 4;
             constexpr int EPC = 16 / (int)sizeof(T);
             for (int e = tid; e < nr * cpr; e += kStepThreads) {
@@ -277,9 +431,17 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             sh.n_valid = nv;
         }
     }
+    if (tid == 0) {
+        mbar_init(&sh.xbar[0], 1);
+        mbar_init(&sh.xbar[1], 1);
+        mbar_init_fence();
+    }
+    mark();  // 1: copies issued
     cp_async_wait_all();
     __syncthreads();  // gx (aliases d2) fully consumed before seeding reuses the region
+    mark();  // 2: sample landed
     cluster.sync();  // sample rows of every CTA now visible cluster-wide (DSMEM)
+    mark();  // 3: cluster synced
 
     int64_t nd = 0;  // distance evaluations (reference accounting)
     int filled = 0;
@@ -290,19 +452,76 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
     if (sh.n_pending > 0) {
         const int np_ = sh.n_pending;
         const int ncand = p.candidates;
-        for (int li = tid; li < nr; li += kStepThreads) d2[li] = __longlong_as_double(0x7ff0000000000000LL);
+        float* xnorm = reinterpret_cast<float*>(smem + L.xnorm);
+        uint32_t* wlist = reinterpret_cast<uint32_t*>(smem + L.wlist) + warp * list_cap(ncand);
+        constexpr float kScreenK = 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
+        for (int li = tid; li < nr; li += kStepThreads) {
+            d2[li] = __longlong_as_double(0x7ff0000000000000LL);
+            float2 x2[G::NPF / 2];
+            load_row_f32<T, NP>(samp, li, x2);
+            float nn = 0.f;
+#pragma unroll
+            for (int q = 0; q < G::NPF / 2; ++q) nn = fmaf(x2[q].x, x2[q].x, fmaf(x2[q].y, x2[q].y, nn));
+            xnorm[li] = sqrtf(nn) * 1.0001f;
+        }
+        // fp32 screen record of slot c of sh.cand (negated copy + norm); caller syncs
+        auto make_candf = [&](int c) {
+            for (int d = lane; d < G::NPF; d += 32) sh.candf[c][d] = d < n ? -(float)sh.cand[c][d] : 0.f;
+            if (lane == 0) {
+                double nn = 0.0;
+                for (int d = 0; d < n; ++d) nn += sh.cand[c][d] * sh.cand[c][d];
+                sh.candn[c] = (float)sqrt(nn) * 1.0001f;
+            }
+        };
+        // d2 = min(d2, dist(., cand c)) for every local row (seeding.hpp:20-42); the exact
+        // reference distance is evaluated only where the fp32 screen cannot prove
+        // dist >= d2, and those rows are compacted so the fp64 work runs on full warps.
+        auto d2_update = [&](int c) {
+            int cnt = 0;
+            const int nchunks = (nr + 31) / 32;
+            for (int ch = warp; ch < nchunks + kStepWarps; ch += kStepWarps) {
+                if (ch < nchunks) {
+                    const int row = ch * 32 + lane;
+                    bool need = false;
+                    if (row < nr) {
+                        float2 x2[G::NPF / 2];
+                        load_row_f32<T, NP>(samp, row, x2);
+                        const float df = screen_dist<G::NPF>(x2, sh.candf[c]);
+                        const float sc = xnorm[row] + sh.candn[c];
+                        need = !(df - kScreenK * sc * sc > __double2float_ru(d2[row]));  // ru: conservative
+                    }
+                    const unsigned msk = __ballot_sync(0xffffffffu, need);
+                    if (need) wlist[cnt + __popc(msk & ((1u << lane) - 1u))] = (uint32_t)row;
+                    cnt += __popc(msk);
+                    __syncwarp();
+                }
+                const bool last = ch >= nchunks;
+                while (cnt >= 32 || (last && cnt > 0)) {
+                    const int take = cnt < 32 ? cnt : 32;
+                    if (lane < take) {
+                        const int r = (int)wlist[lane];
+                        d2[r] = fmin(d2[r], exact_dist<T, NP>(samp, r, sh.cand[c], n));
+                    }
+                    __syncwarp();
+                    for (int t = lane; t + take < cnt; t += 32) wlist[t] = wlist[t + take];
+                    __syncwarp();
+                    cnt -= take;
+                }
+                if (last) break;
+            }
+        };
         __syncthreads();
         // valid centres in slot order (seeding.hpp:60-68)
         for (int j = 0; j < k; ++j) {
             if (sh.flags[j]) continue;
-            for (int li = tid; li < nr; li += kStepThreads) {
-                double dd = 0.0;
-                for (int d = 0; d < n; ++d) {
-                    const double diff = __dsub_rn((double)samp[G::elem_off(li, d)], Cm[j * NP + d]);
-                    dd = __dadd_rn(dd, __dmul_rn(diff, diff));
-                }
-                d2[li] = fmin(d2[li], dd);
+            if (warp == 0) {
+                for (int d = lane; d < 32; d += 32) sh.cand[0][d] = d < n ? Cm[j * NP + d] : 0.0;
+                __syncwarp();
+                make_candf(0);
             }
+            __syncthreads();
+            d2_update(0);
+            __syncthreads();
             nd += s;
         }
         // fetch a sample row (global sample position) from its owner CTA into dst[n]
@@ -332,21 +551,15 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             if (warp == 0) {
                 fetch_row(row, sh.cand[0]);
                 __syncwarp();
+                make_candf(0);
                 for (int d = lane; d < NP; d += 32) Cm[j * NP + d] = d < n ? sh.cand[0][d] : 0.0;
                 if (lane == 0) sh.flags[j] = 0;
             }
             __syncthreads();
-            for (int li = tid; li < nr; li += kStepThreads) {
-                double dd = 0.0;
-                for (int d = 0; d < n; ++d) {
-                    const double diff = __dsub_rn((double)samp[G::elem_off(li, d)], Cm[j * NP + d]);
-                    dd = __dadd_rn(dd, __dmul_rn(diff, diff));
-                }
-                d2[li] = fmin(d2[li], dd);
-            }
+            d2_update(0);
             nd += s;
             ++filled;
-            __syncthreads();  // d2 written row-strided above, read per contiguous segment below
+            __syncthreads();
         }
         // per-thread contiguous segment of local rows for the CDF
         const int seg = (nr + kStepThreads - 1) / kStepThreads;
@@ -377,10 +590,12 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                 for (int li = sb; li < se; ++li) run += d2[li];
                 sh.xch_total[par] = texcl + run;
             }
+            if (it == 0 && p.trace_mode == 1) mark();  // 5: CDF local done
             cluster.sync();
-            // P = sum of lower ranks' totals (rank order); total = P_{C-1} + T_{C-1}
+            if (it == 0 && p.trace_mode == 1) mark();  // 6: CDF exchange synced
             if (warp == 0 && lane < C) sh.rank_val[lane] = *cluster.map_shared_rank(&sh.xch_total[par], lane);
             __syncthreads();
+            // P = sum of lower ranks' totals (rank order); total = P_{C-1} + T_{C-1}
             double P = 0.0, total = 0.0;
             {
                 double acc = 0.0;
@@ -396,25 +611,44 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             if (!(total > 0.0)) break;  // distinct rows exhausted (seeding.hpp:87)
             // (2) candidate draws u_c = unit * total; first global row with cum > u_c
             double u[kMaxCandidates];
-            for (int c = 0; c < ncand; ++c) {
-                const double unit = p.seed_mode == 0
-                                        ? p.units[(int64_t)wl * p.units_stride + (int64_t)it * ncand + c]
-                                        : philox_unit(p.key, p.round, (uint32_t)(p.worker_base + wl),
-                                                      (uint32_t)(0x10000 + next * kMaxCandidates + c));
-                u[c] = unit * total;
-            }
             long long hit[kMaxCandidates];
-            for (int c = 0; c < ncand; ++c) hit[c] = LLONG_MAX;
-            {
+#pragma unroll
+            for (int c = 0; c < kMaxCandidates; ++c) {
+                hit[c] = LLONG_MAX;
+                u[c] = 0.0;
+                if (c < ncand) {
+                    const double unit = p.seed_mode == 0
+                                            ? p.units[(int64_t)wl * p.units_stride + (int64_t)it * ncand + c]
+                                            : philox_unit(p.key, p.round, (uint32_t)(p.worker_base + wl),
+                                                          (uint32_t)(0x10000 + next * kMaxCandidates + c));
+                    u[c] = unit * total;
+                }
+            }
+            bool any = false;
+            if (sb < se) {  // cum is non-decreasing along a segment: scan only where a draw crosses it
+                const double seg_hi = P + (texcl + tsum), seg_lo = P + (texcl + d2[sb]);
+#pragma unroll
+                for (int c = 0; c < kMaxCandidates; ++c) {
+                    if (c >= ncand) break;
+                    if (seg_lo > u[c])
+                        hit[c] = r0 + sb;
+                    else
+                        any |= seg_hi > u[c];
+                }
+            }
+            if (any) {
                 double run = 0.0;
                 for (int li = sb; li < se; ++li) {
                     run += d2[li];
                     const double cum = P + (texcl + run);
-                    for (int c = 0; c < ncand; ++c)
-                        if (hit[c] == LLONG_MAX && cum > u[c]) hit[c] = r0 + li;
+#pragma unroll
+                    for (int c = 0; c < kMaxCandidates; ++c)
+                        if (c < ncand && hit[c] == LLONG_MAX && cum > u[c]) hit[c] = r0 + li;
                 }
             }
-            for (int c = 0; c < ncand; ++c) {
+#pragma unroll
+            for (int c = 0; c < kMaxCandidates; ++c) {
+                if (c >= ncand) break;
                 long long h = hit[c];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) h = min(h, __shfl_xor_sync(0xffffffffu, h, o));
@@ -426,7 +660,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                 for (int w2 = 0; w2 < kStepWarps; ++w2) h = min(h, sh.whit[w2][tid]);
                 sh.xch_hit[par][tid] = h;
             }
+            if (it == 0 && p.trace_mode == 1) mark();  // 7: search done
             cluster.sync();
+            if (it == 0 && p.trace_mode == 1) mark();  // 8: hit exchange synced
             // every CTA: global first hit per candidate (rank order == row order)
             for (int c = warp; c < ncand; c += kStepWarps) {
                 long long h = lane < C ? *cluster.map_shared_rank(&sh.xch_hit[par][c], lane) : LLONG_MAX;
@@ -434,68 +670,144 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                 for (int o = 16; o > 0; o >>= 1) h = min(h, __shfl_xor_sync(0xffffffffu, h, o));
                 const int64_t row = h == LLONG_MAX ? s - 1 : (int64_t)h;  // rng.hpp:87-92 fallback
                 fetch_row(row, sh.cand[c]);
+                __syncwarp();
+                make_candf(c);
             }
             __syncthreads();
-            // (3) candidate costs sum_i min(d2_i, dist(S_i, cand_c)), fixed order
-            double cost[kMaxCandidates];
-            for (int c = 0; c < ncand; ++c) cost[c] = 0.0;
-            for (int li = sb; li < se; ++li) {
-                for (int c = 0; c < ncand; ++c) {
-                    double dd = 0.0;
-                    for (int d = 0; d < n; ++d) {
-                        const double diff = __dsub_rn((double)samp[G::elem_off(li, d)], sh.cand[c][d]);
-                        dd = __dadd_rn(dd, __dmul_rn(diff, diff));
-                    }
-                    cost[c] += fmin(d2[li], dd);
-                }
-            }
-            for (int c = 0; c < ncand; ++c) {
-                const double v = warp_sum(cost[c]);
-                if (lane == 0) sh.wsum[warp][c] = v;
-            }
-            __syncthreads();
-            if (tid < ncand) {
-                double v = 0.0;
-                for (int w2 = 0; w2 < kStepWarps; ++w2) v += sh.wsum[w2][tid];
-                sh.xch_cost[par][tid] = v;
-            }
-            cluster.sync();
-            for (int e = tid; e < ncand * C; e += kStepThreads) {
-                const int c = e / C, rr = e - c * C;
-                sh.rank_cost[c][rr] = *cluster.map_shared_rank(&sh.xch_cost[par][c], rr);
-            }
-            __syncthreads();
+            if (it == 0 && p.trace_mode == 1) mark();  // 9: candidates fetched
+            // (3) candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93). First from
+            // the fp32 screen with a rigorous per-row error budget; only if two candidates are
+            // within their budgets (or tie) are the costs recomputed with exact distances.
             int best = 0;
-            {
-                double bc = __longlong_as_double(0x7ff0000000000000LL);
-                for (int c = 0; c < ncand; ++c) {
-                    double tc = 0.0;
-                    for (int rr = 0; rr < C; ++rr) tc += sh.rank_cost[c][rr];
-                    if (tc < bc) {  // strict <, first candidate wins ties (seeding.hpp:94-98)
-                        bc = tc;
+            for (int exact_pass = 0; exact_pass < 2; ++exact_pass) {
+                double cost[kMaxCandidates], err[kMaxCandidates];
+#pragma unroll
+                for (int c = 0; c < kMaxCandidates; ++c) cost[c] = err[c] = 0.0;
+                int cnt = 0;
+                const int nchunks = (nr + 31) / 32;
+                for (int ch = warp; ch < nchunks + kStepWarps; ch += kStepWarps) {
+                    if (ch < nchunks) {
+                        const int row = ch * 32 + lane;
+                        const bool valid = row < nr;
+                        float2 x2[G::NPF / 2];
+                        double d2i = 0.0;
+                        float xnr = 0.f;
+                        if (valid) {
+                            load_row_f32<T, NP>(samp, row, x2);
+                            d2i = d2[row];
+                            xnr = xnorm[row];
+                        }
+#pragma unroll
+                        for (int c = 0; c < kMaxCandidates; ++c) {
+                            if (c >= ncand) break;
+                            bool need = false;
+                            if (valid) {
+                                const float df = screen_dist<G::NPF>(x2, sh.candf[c]);
+                                const float sc = xnr + sh.candn[c];
+                                const float B = kScreenK * sc * sc;
+                                need = !(df - B > __double2float_ru(d2i));
+                                if (!need) {
+                                    cost[c] += d2i;
+                                } else if (!exact_pass) {
+                                    cost[c] += fmin(d2i, (double)df);
+                                    err[c] += (double)B;
+                                    need = false;
+                                }
+                            }
+                            const unsigned msk = __ballot_sync(0xffffffffu, need);
+                            if (need) wlist[cnt + __popc(msk & ((1u << lane) - 1u))] = (uint32_t)row | ((uint32_t)c << 16);
+                            cnt += __popc(msk);
+                        }
+                        __syncwarp();
+                    }
+                    const bool last = ch >= nchunks;
+                    while (cnt >= 32 || (last && cnt > 0)) {
+                        const int take = cnt < 32 ? cnt : 32;
+                        if (lane < take) {
+                            const uint32_t e = wlist[lane];
+                            const int r = (int)(e & 0xffffu), c = (int)(e >> 16);
+                            const double v = fmin(d2[r], exact_dist<T, NP>(samp, r, sh.cand[c], n));
+#pragma unroll
+                            for (int cc = 0; cc < kMaxCandidates; ++cc)
+                                if (cc == c) cost[cc] += v;
+                        }
+                        __syncwarp();
+                        for (int t = lane; t + take < cnt; t += 32) wlist[t] = wlist[t + take];
+                        __syncwarp();
+                        cnt -= take;
+                    }
+                    if (last) break;
+                }
+#pragma unroll
+                for (int c = 0; c < kMaxCandidates; ++c) {
+                    if (c >= ncand) break;
+                    const double v = warp_sum(cost[c]);
+                    const double e = warp_sum(err[c]);
+                    if (lane == 0) {
+                        sh.wsum[warp][c] = v;
+                        sh.werr[warp][c] = e;
+                    }
+                }
+                __syncthreads();
+                if (tid < ncand) {
+                    double v = 0.0, e = 0.0;
+                    for (int w2 = 0; w2 < kStepWarps; ++w2) {
+                        v += sh.wsum[w2][tid];
+                        e += sh.werr[w2][tid];
+                    }
+                    sh.xch_cost[par][tid] = v;
+                    sh.xch_err[par][tid] = e;
+                }
+                if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 10: costs local done
+                cluster.sync();
+                if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 11: cost exchange synced
+                for (int e = tid; e < ncand * C; e += kStepThreads) {
+                    const int c = e / C, rr = e - c * C;
+                    sh.rank_cost[c][rr] = *cluster.map_shared_rank(&sh.xch_cost[par][c], rr);
+                    sh.rank_err[c][rr] = *cluster.map_shared_rank(&sh.xch_err[par][c], rr);
+                }
+                __syncthreads();
+                double tc[kMaxCandidates], te[kMaxCandidates];
+                double bc = __longlong_as_double(0x7ff0000000000000LL), be = 0.0;
+                best = 0;
+#pragma unroll
+                for (int c = 0; c < kMaxCandidates; ++c) {
+                    tc[c] = 0.0;
+                    te[c] = 0.0;
+                    if (c >= ncand) continue;
+                    for (int rr = 0; rr < C; ++rr) {
+                        tc[c] += sh.rank_cost[c][rr];
+                        te[c] += sh.rank_err[c][rr];
+                    }
+                    te[c] += 1e-9 * fabs(tc[c]);  // summation-order slack
+                    if (tc[c] < bc) {  // strict <, first candidate wins ties (seeding.hpp:94-98)
+                        bc = tc[c];
+                        be = te[c];
                         best = c;
                     }
                 }
+                bool decided = true;
+                if (!exact_pass)
+#pragma unroll
+                    for (int c = 0; c < kMaxCandidates; ++c)
+                        if (c < ncand && c != best && !(tc[c] - te[c] > bc + be)) decided = false;
+                // every CTA evaluated the same totals: the decision is cluster-uniform
+                if (decided) break;
+                cluster.sync();  // peers may still read this CTA's xch_* of the screened pass
             }
             nd += (int64_t)ncand * s;
             const int j = sh.pending[next];
-            __syncthreads();
             for (int d = tid; d < NP; d += kStepThreads) Cm[j * NP + d] = d < n ? sh.cand[best][d] : 0.0;
             if (tid == 0) sh.flags[j] = 0;
-            for (int li = tid; li < nr; li += kStepThreads) {
-                double dd = 0.0;
-                for (int d = 0; d < n; ++d) {
-                    const double diff = __dsub_rn((double)samp[G::elem_off(li, d)], sh.cand[best][d]);
-                    dd = __dadd_rn(dd, __dmul_rn(diff, diff));
-                }
-                d2[li] = fmin(d2[li], dd);
-            }
+            d2_update(best);
             ++filled;
             __syncthreads();
+            if (it == 0 && p.trace_mode == 1) mark();  // 12: d2 updated (slot done)
         }
         __syncthreads();
     }
 
+    mark();  // 4: seeding done
     // ---------------------------------------------------------------- Lloyd
     int iters = 0, stop = 1 /*max_iters*/, hist_len = 0;
     double f_final = 0.0, f_prev = __longlong_as_double(0x7ff0000000000000LL), last = 0.0;
@@ -510,73 +822,59 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
         constexpr float kappa = 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
         bool closing = false;
         int pass = 0;
-        const int ngroups = (nr + G::GROUP - 1) / G::GROUP;
         for (;; ++pass) {
             // ---- screen prep: c' = -2c (fp32), cc = |c|^2, cmax
-            if (tid < k) {
-                const int j = tid;
-                float* rec = cs + j * G::CSR;
-                double cc = 0.0;
-                for (int d = 0; d < NP; ++d) {
-                    const double c = Cm[j * NP + d];
-                    cc += c * c;
-                    rec[d] = (float)(-2.0 * c);
-                }
-                for (int d = NP; d < G::NPF; ++d) rec[d] = 0.f;
-                rec[G::NPF] = (float)cc;
-                rec[G::NPF + 1] = 0.f;
-            }
-            __syncthreads();
-            if (tid == 0) {  // max |c_j| (k <= 32): scales the screen's error bound
+            if (warp == 0) {  // k <= 32: one lane per centroid, max |c_j| by shuffle
                 float cm = 0.f;
-                for (int j = 0; j < k; ++j) cm = fmaxf(cm, sqrtf(cs[j * G::CSR + G::NPF]) * 1.0001f);
-                sh.cmax = cm;
+                if (lane < k) {
+                    float* rec = cs + lane * G::CSR;
+                    double cc = 0.0;
+                    for (int d = 0; d < NP; ++d) {
+                        const double c = Cm[lane * NP + d];
+                        cc += c * c;
+                        rec[d] = (float)(-2.0 * c);
+                    }
+                    for (int d = NP; d < G::NPF; ++d) rec[d] = 0.f;
+                    rec[G::NPF] = (float)cc;
+                    rec[G::NPF + 1] = 0.f;
+                    cm = sqrtf((float)cc) * 1.0001f;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+                if (lane == 0) sh.cmax = cm;
             }
             __syncthreads();
             const float cmax = sh.cmax;
 
-            // ---- assign: fp32 FFMA2 screen, exact fp64 recheck of near ties
+            if (pass == 0 && p.trace_mode == 0) mark();  // 5: prep done
+            // ---- assign: fp32 FFMA2 screen, exact fp64 recheck of near ties. Rows are dealt
+            // to warps as 32-row chunks (chunk c -> warp c % NW) and each warp screens 4, 2 or 1
+            // of its chunks at a time, so warps differ by at most one chunk of work.
             if (lane < kMaxK) sh.wcnt[warp][lane] = 0;
             __syncwarp();
-            for (int g = warp; g < ngroups; g += kStepWarps) {
-                float2 x2[G::R][G::NPF / 2];
-                float xn[G::R];
-                bool valid[G::R];
+            const int nchunks = (nr + 31) / 32;
+            const int nchw = warp < nchunks ? (nchunks - warp + kStepWarps - 1) / kStepWarps : 0;
+            auto screen_chunks = [&](auto RRc, int t0) {
+                constexpr int RR = decltype(RRc)::value;
+                float2 x2[RR][G::NPF / 2];
+                float xn[RR];
+                bool valid[RR];
+                int rowr[RR];
 #pragma unroll
-                for (int r = 0; r < G::R; ++r) {
-                    const int row = g * G::GROUP + r * 32 + lane;
+                for (int r = 0; r < RR; ++r) {
+                    const int row = (warp + kStepWarps * (t0 + r)) * 32 + lane;
+                    rowr[r] = row;
                     valid[r] = row < nr;
-                    const int rowc = valid[r] ? row : 0;
-                    if constexpr (G::VEC16 && sizeof(T) == 4) {
-#pragma unroll
-                        for (int q = 0; q < NP / 4; ++q) {
-                            const float4 v = *reinterpret_cast<const float4*>(samp + G::elem_off(rowc, q * 4));
-                            x2[r][2 * q] = make_float2(v.x, v.y);
-                            x2[r][2 * q + 1] = make_float2(v.z, v.w);
-                        }
-                    } else if constexpr (G::VEC16) {  // fp64, 16-B chunks of 2 doubles
-#pragma unroll
-                        for (int q = 0; q < NP / 2; ++q) {
-                            const double2 v = *reinterpret_cast<const double2*>(samp + G::elem_off(rowc, q * 2));
-                            x2[r][q] = make_float2((float)v.x, (float)v.y);
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < G::NPF / 2; ++q) {
-                            const float a = (float)samp[G::elem_off(rowc, 2 * q)];
-                            const float b = 2 * q + 1 < NP ? (float)samp[G::elem_off(rowc, 2 * q + 1)] : 0.f;
-                            x2[r][q] = make_float2(a, b);
-                        }
-                    }
+                    load_row_f32<T, NP>(samp, valid[r] ? row : 0, x2[r]);
                     float nn = 0.f;
 #pragma unroll
                     for (int q = 0; q < G::NPF / 2; ++q) nn = fmaf(x2[r][q].x, x2[r][q].x, fmaf(x2[r][q].y, x2[r][q].y, nn));
                     xn[r] = sqrtf(nn);
                 }
-                float m1[G::R], m2[G::R];
-                int i1[G::R];
+                float m1[RR], m2[RR];
+                int i1[RR];
 #pragma unroll
-                for (int r = 0; r < G::R; ++r) {
+                for (int r = 0; r < RR; ++r) {
                     m1[r] = __int_as_float(0x7f800000);
                     m2[r] = __int_as_float(0x7f800000);
                     i1[r] = 0;
@@ -588,7 +886,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                     for (int q = 0; q < G::NPF / 2; ++q) c2[q] = *reinterpret_cast<const float2*>(rec + 2 * q);
                     const float2 init = *reinterpret_cast<const float2*>(rec + G::NPF);
 #pragma unroll
-                    for (int r = 0; r < G::R; ++r) {
+                    for (int r = 0; r < RR; ++r) {
                         float2 acc = init;
 #pragma unroll
                         for (int q = 0; q < G::NPF / 2; ++q) acc = __ffma2_rn(x2[r][q], c2[q], acc);
@@ -599,43 +897,66 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                         i1[r] = lt ? j : i1[r];
                     }
                 }
+                // near ties (k == 1 gives m2 = inf: never): exact reference argmin, warp-parallel --
+                // lane j evaluates centroid j, then a tie-aware shuffle argmin (core.hpp:146-157)
+                unsigned ties[RR];
 #pragma unroll
-                for (int r = 0; r < G::R; ++r) {
-                    const int row = g * G::GROUP + r * 32 + lane;
-                    int lab = i1[r];
-                    if (valid[r]) {
+                for (int r = 0; r < RR; ++r) {
                     const float sc = xn[r] + cmax;
-                    if (!(m2[r] - m1[r] > kappa * sc * sc)) {  // near tie (or k == 1 -> m2 = inf skips)
-                        double best = __longlong_as_double(0x7ff0000000000000LL);
-                        lab = 0;
-                        for (int j = 0; j < k; ++j) {
-                            double dd = 0.0;
-                            for (int d = 0; d < n; ++d) {
-                                const double diff = __dsub_rn((double)samp[G::elem_off(row, d)], Cm[j * NP + d]);
-                                dd = __dadd_rn(dd, __dmul_rn(diff, diff));
-                            }
-                            if (dd < best) {
-                                best = dd;
-                                lab = j;
+                    ties[r] = __ballot_sync(0xffffffffu, valid[r] && !(m2[r] - m1[r] > kappa * sc * sc));
+                }
+#pragma unroll
+                for (int r = 0; r < RR; ++r) {
+                    unsigned tie = ties[r];
+                    while (tie) {
+                        const int src = __ffs(tie) - 1;
+                        tie &= tie - 1;
+                        const int trow = rowr[r] - lane + src;
+                        double dv = __longlong_as_double(0x7ff0000000000000LL);
+                        int dj = lane;
+                        if (lane < k) dv = exact_dist<T, NP>(samp, trow, Cm + lane * NP, n);
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
+                            const int oj = __shfl_xor_sync(0xffffffffu, dj, o);
+                            if (ov < dv || (ov == dv && oj < dj)) {
+                                dv = ov;
+                                dj = oj;
                             }
                         }
+                        if (lane == src) i1[r] = dj;
                     }
-                    labels[row] = (uint8_t)lab;
-                    }
-                    // stable counting-sort rank of this row among the warp's rows with its label
+                }
+                // labels + stable counting-sort rank among this warp's rows of the same label
+#pragma unroll
+                for (int r = 0; r < RR; ++r) {
+                    const int lab = i1[r];
                     const unsigned peers = __match_any_sync(0xffffffffu, valid[r] ? lab : 0xff);
                     const int rank = __popc(peers & ((1u << lane) - 1u));
                     const int base = valid[r] ? sh.wcnt[warp][lab] : 0;
                     __syncwarp();
                     if (valid[r]) {
+                        labels[rowr[r]] = (uint8_t)lab;
                         if (rank == 0) sh.wcnt[warp][lab] = base + __popc(peers);
-                        pos[row] = (uint16_t)(base + rank);
+                        pos[rowr[r]] = (uint16_t)(base + rank);
                     }
                     __syncwarp();
                 }
+            };
+            {
+                int t = 0;
+                for (; t + G::R <= nchw; t += G::R) screen_chunks(IntC<G::R>{}, t);
+                if constexpr (G::R > 2) {
+                    if (t + 2 <= nchw) {
+                        screen_chunks(IntC<2>{}, t);
+                        t += 2;
+                    }
+                }
+                if (t < nchw) screen_chunks(IntC<1>{}, t);
             }
+            if (pass == 0 && p.trace_mode == 0) mark();  // 6: assign done
             __syncthreads();
-            // cluster ranges of the sorted order and (warp, label) offsets
+            // CTA-wide stable counting sort by label: cluster ranges + (warp, label) offsets
             if (warp == 0) {
                 int col = 0;
                 for (int w2 = 0; w2 < kStepWarps; ++w2) col += lane < k ? sh.wcnt[w2][lane] : 0;
@@ -657,14 +978,14 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                 if (lane == k - 1) sh.cstart[k] = incl;
             }
             __syncthreads();
-            for (int li = tid; li < nr; li += kStepThreads) {
-                const int w2 = (li / G::GROUP) % kStepWarps;
-                perm[sh.woff[w2][labels[li]] + pos[li]] = (uint16_t)li;
+            for (int t = 0; t < nchw; ++t) {
+                const int row = (warp + kStepWarps * t) * 32 + lane;
+                if (row < nr) perm[sh.woff[warp][labels[row]] + pos[row]] = (uint16_t)row;
             }
             __syncthreads();
-
-            // ---- update: sums / cost along the label-sorted order. Warp w owns sorted
-            // positions [w*L, (w+1)*L); per cluster its lanes cover ROWS_PER_STEP rows x
+            if (pass == 0 && p.trace_mode == 0) mark();  // 7: sort done
+            // ---- update: sums / cost of the warp's own rows, cluster by cluster along its
+            // label-sorted segment; per cluster the lanes cover ROWS_PER_STEP rows x
             // LANES_PER_ROW units (16-B chunks or single elements) so every smem read is a
             // vector load and no label test sits in the inner loop. Fixed order throughout.
             {
@@ -675,47 +996,53 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                 double* wp = wpart + warp * part_d;
                 const int gi = lane / LR, q = lane % LR;
                 const bool active_unit = q < UPR;
+                const uint16_t* wperm = perm;
+                double cost_w = 0.0;
+                // this warp's contiguous range of the label-sorted order (1-3 clusters)
                 const int Lw = (nr + kStepWarps - 1) / kStepWarps;
                 const int lo = warp * Lw < nr ? warp * Lw : nr;
                 const int hi = lo + Lw < nr ? lo + Lw : nr;
-                double cost_w = 0.0;
+                for (int e = lane; e < part_d; e += 32) wp[e] = 0.0;
+                __syncwarp();
                 for (int j = 0; j < k; ++j) {
                     const int a = max(sh.cstart[j], lo), b = min(sh.cstart[j + 1], hi);
-                    double acc[U], cj[U];
-                    double accc = 0.0;
+                    if (a >= b) continue;  // warp-uniform
+                    double acc[U], cj[U], accc[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         acc[u] = 0.0;
+                        accc[u] = 0.0;
                         const int d = q * U + u;
                         cj[u] = (active_unit && d < NP) ? Cm[j * NP + d] : 0.0;
                     }
-                    for (int p0 = a; p0 < b; p0 += RPS) {
-                        const int pp = p0 + gi;
-                        if (pp < b && active_unit) {
-                            const int row = perm[pp];
-                            if constexpr (G::VEC16 && sizeof(T) == 4) {
-                                const float4 v = *reinterpret_cast<const float4*>(samp + G::elem_off(row, q * 4));
-                                const double xv[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+                    auto add_row = [&](int row) {
+                        if constexpr (G::VEC16 && sizeof(T) == 4) {
+                            const float4 v = *reinterpret_cast<const float4*>(samp + G::elem_off(row, q * 4));
+                            const double xv[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
 #pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    acc[u] += xv[u];
-                                    const double diff = xv[u] - cj[u];
-                                    accc = fma(diff, diff, accc);
-                                }
-                            } else if constexpr (G::VEC16) {
-                                const double2 v = *reinterpret_cast<const double2*>(samp + G::elem_off(row, q * 2));
-                                acc[0] += v.x;
-                                acc[1] += v.y;
-                                const double d0 = v.x - cj[0], d1 = v.y - cj[1];
-                                accc = fma(d0, d0, accc);
-                                accc = fma(d1, d1, accc);
-                            } else {
-                                const double xv = (double)samp[G::elem_off(row, q)];
-                                acc[0] += xv;
-                                const double diff = xv - cj[0];
-                                accc = fma(diff, diff, accc);
+                            for (int u = 0; u < 4; ++u) {
+                                acc[u] += xv[u];
+                                const double diff = xv[u] - cj[u];
+                                accc[u] = fma(diff, diff, accc[u]);
                             }
+                        } else if constexpr (G::VEC16) {
+                            const double2 v = *reinterpret_cast<const double2*>(samp + G::elem_off(row, q * 2));
+                            acc[0] += v.x;
+                            acc[1] += v.y;
+                            const double d0 = v.x - cj[0], d1 = v.y - cj[1];
+                            accc[0] = fma(d0, d0, accc[0]);
+                            accc[1] = fma(d1, d1, accc[1]);
+                        } else {
+                            const double xv = (double)samp[G::elem_off(row, q)];
+                            acc[0] += xv;
+                            const double diff = xv - cj[0];
+                            accc[0] = fma(diff, diff, accc[0]);
                         }
+                    };
+                    if (active_unit) {
+                        int p0 = a + gi;
+#pragma unroll 2
+                        for (; p0 < b; p0 += RPS) add_row(wperm[p0]);
                     }
                     // fold the row groups (fixed tree): lanes gi == 0 hold the sums
 #pragma unroll
@@ -727,35 +1054,31 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
                         for (int u = 0; u < U; ++u)
                             if (q * U + u < NP) wp[j * NP + q * U + u] = acc[u];
                     if (lane == 0) wp[k * NP + j] = (double)(b > a ? b - a : 0);
-                    cost_w += warp_sum(accc);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) cost_w += accc[u];  // per lane; reduced once below
                 }
+                cost_w = warp_sum(cost_w);
                 if (lane == 0) wp[k * NP + k] = cost_w;
             }
             __syncthreads();
-            // ---- CTA partial (warps in order) -> cluster exchange
-            double* pb = part + (pass & 1) * part_d;
-            for (int e = tid; e < part_d; e += kStepThreads) {
+            if (pass == 0 && p.trace_mode == 0) mark();  // 8: update done
+            // ---- CTA partial (warps in order) pushed to every CTA; totals in rank order
+            const double* rxp = exchange(part_d, [&](int e) {
                 double v = 0.0;
                 for (int w2 = 0; w2 < kStepWarps; ++w2) v += wpart[w2 * part_d + e];
-                pb[e] = v;
-            }
-            cluster.sync();
-            // totals in rank order (identical in every CTA), new means
-            double* tot = wpart;  // reuse (warp partials consumed)
+                return v;
+            });
+            if (pass == 0 && p.trace_mode == 0) mark();  // 9: partials pushed
+            if (pass == 0 && p.trace_mode == 0) mark();  // 10: exchange complete
+            __syncthreads();  // every warp partial consumed before tot overwrites wpart
+            double* tot = wpart;
             for (int e = tid; e < part_d; e += kStepThreads) {
-                double t = 0.0;  // batches of remote loads issued before the (rank-ordered) sum
-                for (int r8 = 0; r8 < C; r8 += 8) {
-                    double v[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (r8 + q < C) v[q] = cluster.map_shared_rank(pb, r8 + q)[e];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (r8 + q < C) t = (r8 + q == 0) ? v[q] : t + v[q];
-                }
+                double t = rxp[e];
+                for (int r = 1; r < C; ++r) t += rxp[r * xs + e];
                 tot[e] = t;
             }
             __syncthreads();
+            if (pass == 0 && p.trace_mode == 0) mark();  // 11: cluster reduce done
             const double f = tot[k * NP + k];
             if (hist_len > 0 && f > last * (1.0 + 1e-12)) {  // lloyd.hpp:114-121
                 if (tid == 0) sh.err = kErrMonotone;
@@ -814,6 +1137,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             }
             closing = go_close;
             __syncthreads();
+            if (pass == 0 && p.trace_mode == 0) mark();  // 12: means done
         }
         // outputs of the last pass: labels (sample order), flags = empty clusters
         if (stop >= 0) {
@@ -864,7 +1188,9 @@ __global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const Step
             }
         }
     }
+    if (trace && tid == 0) trace[kTraceSlots - 2] = gtimer();
     cluster.sync();  // no CTA may exit while peers can still read its smem
+    if (trace && tid == 0) trace[kTraceSlots - 1] = gtimer();
 }
 
 }  // namespace hpcg

@@ -1,6 +1,8 @@
 // Launch plumbing for worker_step_kernel<T, NP>: cluster-size choice and
 // cudaLaunchKernelEx with a runtime cluster dimension. Included once per dtype TU.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -9,10 +11,10 @@
 
 namespace hpcg {
 
-constexpr int kMaxDynSmem = 232448 - 8192;  // 227 KB opt-in minus static StepShared headroom
+constexpr int kMaxDynSmem = 232448 - (int)sizeof(StepShared) - 256;  // 227 KB opt-in minus static smem
 
 template <typename T, int NP>
-cudaError_t step_geometry_uncached(int64_t s, int k, int W, StepGeometry* g, std::string* why) {
+cudaError_t step_geometry_uncached(int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why) {
     auto kern = worker_step_kernel<T, NP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e != cudaSuccess) return e;
@@ -22,7 +24,7 @@ cudaError_t step_geometry_uncached(int64_t s, int k, int W, StepGeometry* g, std
     for (int c = 1; c <= 16; ++c) {
         if (c > s) break;
         const int rows = (int)((s + c - 1) / c);
-        if (step_layout<T, NP>(rows, k).total <= kMaxDynSmem) {
+        if (step_layout<T, NP>(rows, k, ncand, c).total <= kMaxDynSmem) {
             cmin = c;
             break;
         }
@@ -37,7 +39,7 @@ cudaError_t step_geometry_uncached(int64_t s, int k, int W, StepGeometry* g, std
     for (int c = cmin; c <= 16 && c <= s; ++c) {
         const int rows = (int)((s + c - 1) / c);
         if (c > cmin && rows < 128) break;
-        const int smem = step_layout<T, NP>(rows, k).total;
+        const int smem = step_layout<T, NP>(rows, k, ncand, c).total;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(c * (W > 0 ? W : 1)));
         cfg.blockDim = dim3(kStepThreads);
@@ -70,7 +72,7 @@ cudaError_t step_geometry_uncached(int64_t s, int k, int W, StepGeometry* g, std
     }
     g->cluster = best_c;
     g->rows_cap = (int)((s + best_c - 1) / best_c);
-    g->smem = step_layout<T, NP>(g->rows_cap, k).total;
+    g->smem = step_layout<T, NP>(g->rows_cap, k, ncand, best_c).total;
     g->active_clusters = best_active;
     return cudaSuccess;
 }
@@ -78,12 +80,12 @@ cudaError_t step_geometry_uncached(int64_t s, int k, int W, StepGeometry* g, std
 // Geometry is a pure function of (device, shape): cache it (the occupancy queries cost
 // tens of microseconds each and the engine launches one step per round).
 template <typename T, int NP>
-cudaError_t step_geometry_t(int64_t s, int k, int W, StepGeometry* g, std::string* why) {
+cudaError_t step_geometry_t(int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why) {
     static std::mutex mu;
-    static std::map<std::tuple<int, int64_t, int, int>, StepGeometry> cache;
+    static std::map<std::tuple<int, int64_t, int, int, int>, StepGeometry> cache;
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_tuple(dev, s, k, W);
+    const auto key = std::make_tuple(dev, s, k, ncand, W);
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
@@ -92,7 +94,7 @@ cudaError_t step_geometry_t(int64_t s, int k, int W, StepGeometry* g, std::strin
             return cudaSuccess;
         }
     }
-    cudaError_t e = step_geometry_uncached<T, NP>(s, k, W, g, why);
+    cudaError_t e = step_geometry_uncached<T, NP>(s, k, ncand, W, g, why);
     if (e == cudaSuccess) {
         std::lock_guard<std::mutex> lk(mu);
         cache[key] = *g;
@@ -103,7 +105,7 @@ cudaError_t step_geometry_t(int64_t s, int k, int W, StepGeometry* g, std::strin
 template <typename T, int NP>
 cudaError_t launch_step_t(const StepParams& p_in, cudaStream_t st, StepGeometry* geo_out, std::string* why) {
     StepGeometry g;
-    cudaError_t e = step_geometry_t<T, NP>(p_in.s, p_in.k, p_in.W, &g, why);
+    cudaError_t e = step_geometry_t<T, NP>(p_in.s, p_in.k, p_in.candidates, p_in.W, &g, why);
     if (e != cudaSuccess) return e;
     StepParams p = p_in;
     p.rows_cap = g.rows_cap;
@@ -121,6 +123,10 @@ cudaError_t launch_step_t(const StepParams& p_in, cudaStream_t st, StepGeometry*
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, worker_step_kernel<T, NP>, p);
     if (geo_out) *geo_out = g;
+    static const bool dbg = getenv("HPCG_DEBUG") != nullptr;
+    if (dbg)
+        fprintf(stderr, "[hpcg] step NP=%d s=%lld k=%d W=%d: cluster %d rows_cap %d smem %d active_clusters %d\n", NP,
+                (long long)p.s, p.k, p.W, g.cluster, g.rows_cap, g.smem, g.active_clusters);
     return e;
 }
 
