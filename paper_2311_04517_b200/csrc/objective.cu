@@ -1,5 +1,9 @@
 // Instantiations and dispatch for the full-data objective kernel, plus the NP tables
 // shared by every launcher.
+#include <cstdlib>
+#include <cstring>
+#include <cudaTypedefs.h>
+
 #include "launch.h"
 
 namespace hpcg {
@@ -47,8 +51,56 @@ int objective_blocks() {  // upper bound on the grid of any objective launch
 
 // grid = SMs x resident blocks per SM (a pure function of device, kernel and kv, so the
 // block partials -- and hence f(C,X) -- are reproducible)
+// TMA applicability: unpadded rows of 16/32/48/64/128 bytes (the swizzle spans that equal
+// Geo::swz), 16-B aligned base.
 template <typename T, int NP>
-static cudaError_t launch_obj_t(const ObjParams& p, int* nblocks, cudaStream_t st) {
+static bool tma_ok(const ObjParams& p) {
+    using G = Geo<T, NP>;
+    if (p.n != NP || (reinterpret_cast<uintptr_t>(p.X) & 15) != 0) return false;
+    const int rb = G::RS;
+    return rb == 16 || rb == 32 || rb == 48 || rb == 64 || rb == 128;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+template <typename T, int NP>
+static bool make_tmap(const ObjParams& p, CUtensorMap* map) {
+    using O = ObjGeo<T, NP>;
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.m};
+    const cuuint64_t strides[1] = {(cuuint64_t)p.n * sizeof(T)};
+    const cuuint32_t box[2] = {(cuuint32_t)p.n, (cuuint32_t)O::GR};
+    const cuuint32_t estr[2] = {1, 1};
+    const int rb = p.n * (int)sizeof(T);
+    const CUtensorMapSwizzle sw = rb == 32    ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : rb == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
+    const CUresult r = fn(map, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                          const_cast<void*>(p.X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <typename T, int NP>
+static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_t st) {
+    ObjParams p = p_in;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof tmap);
+    p.use_tma = (!getenv("HPCG_NO_TMA") && tma_ok<T, NP>(p) && make_tmap<T, NP>(p, &tmap)) ? 1 : 0;
     const int smem = objective_smem<T, NP>(p.kv);
     auto kern = objective_kernel<T, NP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -65,7 +117,7 @@ static cudaError_t launch_obj_t(const ObjParams& p, int* nblocks, cudaStream_t s
         return cudaErrorNotReady;
     }
     nblocks[0] = nb;
-    kern<<<nb, kObjThreads, smem, st>>>(p);
+    kern<<<nb, kObjThreads, smem, st>>>(p, tmap);
     return cudaGetLastError();
 }
 

@@ -7,6 +7,8 @@
 // per-row values are bit-identical to the reference and only the (fixed, deterministic)
 // summation order differs.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 #include "step_kernel.cuh"  // Geo (swizzled row layout) and cp.async helpers
 
@@ -25,7 +27,27 @@ struct ObjParams {
     int32_t* labels;       // [m] or null
     unsigned long long* counts;  // [k original] or null (atomics on integers: order-free)
     double* block_cost;    // [gridDim.x]
+    int32_t use_tma;       // 1: stages arrive by TMA (tensor map built by the host), 0: cp.async
 };
+
+// TMA tile load of `rows` x n into a swizzled smem slot (box = {n, GR}); the hardware
+// 32B/64B/128B swizzle equals Geo::swz for these row widths (chunk ^= row bits).
+HPCG_DEV void tma_load_2d(void* sdst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(sdst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+HPCG_DEV void mbar_wait_cta(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAITC_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+HPCG_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Per-warp software pipeline: each warp streams groups of GR consecutive rows through a
 // STAGES-deep ring of shared-memory slots filled by cp.async (16/8/4-B copies, swizzled
@@ -40,32 +62,37 @@ struct ObjGeo {
     static constexpr int STAGE = GR * G::RS;          // bytes per ring slot
     static constexpr int STAGES = 3;
     static constexpr int CSR = G::CSR;
+    static constexpr int CDS = NPF + 2;               // fp64 centroid row stride (doubles), padded
 };
 
 template <typename T, int NP>
 __host__ __device__ inline int objective_smem(int kv) {
     using O = ObjGeo<T, NP>;
     const int cs = ((kv * O::CSR * 4 + 15) & ~15);
-    const int cd = ((kv * NP * 8 + 15) & ~15);
-    return cs + cd + (kObjThreads / 32) * O::STAGES * O::STAGE;
+    const int cd = ((kv * O::CDS * 8 + 15) & ~15);
+    return ((cs + cd + 1023) & ~1023) + (kObjThreads / 32) * O::STAGES * O::STAGE + 1024;
 }
 
 template <typename T, int NP>
-__global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjParams p) {
+__global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjParams p,
+                                                                   const __grid_constant__ CUtensorMap tmap) {
     using O = ObjGeo<T, NP>;
     using G = typename O::G;
     constexpr int NPF = O::NPF, R = O::R, CSR = O::CSR;
     extern __shared__ __align__(16) unsigned char osm[];
     const int kv = p.kv, n = p.n;
     float* cs = reinterpret_cast<float*>(osm);
+    constexpr int CDS = O::CDS;
     double* Cd = reinterpret_cast<double*>(osm + ((kv * CSR * 4 + 15) & ~15));
-    unsigned char* rings = osm + ((kv * CSR * 4 + 15) & ~15) + ((kv * NP * 8 + 15) & ~15);
+    unsigned char* rings = osm + ((((kv * CSR * 4 + 15) & ~15) + ((kv * CDS * 8 + 15) & ~15) + 1023) & ~1023);
+    rings += (1024 - (smem_u32(rings) & 1023)) & 1023;  // swizzle atom alignment (absolute address)
+    __shared__ __align__(8) uint64_t s_bar[kObjThreads / 32][4];
     __shared__ float s_cmax;
     __shared__ double s_wcost[kObjThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    for (int e = tid; e < kv * NP; e += kObjThreads) {
-        const int j = e / NP, d = e - j * NP;
+    for (int e = tid; e < kv * CDS; e += kObjThreads) {
+        const int j = e / CDS, d = e - j * CDS;
         Cd[e] = d < n ? p.C[(int64_t)j * n + d] : 0.0;
     }
     __syncthreads();
@@ -73,7 +100,7 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
         float* rec = cs + j * CSR;
         double cc = 0.0;
         for (int d = 0; d < NP; ++d) {
-            const double c = Cd[j * NP + d];
+            const double c = Cd[j * CDS + d];
             cc += c * c;
             rec[d] = (float)(-2.0 * c);
         }
@@ -84,6 +111,12 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
     T* ring = reinterpret_cast<T*>(rings + warp * O::STAGES * O::STAGE);
     // zero the ring once: padding columns (NP > n) are never written by the copies
     for (int e = lane; e < O::STAGES * O::STAGE / 4; e += 32) reinterpret_cast<float*>(ring)[e] = 0.f;
+    const bool tma = p.use_tma != 0;
+    if (tma && lane == 0) {
+        for (int st = 0; st < O::STAGES; ++st) mbar_init(&s_bar[warp][st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
         float cm = 0.f;
@@ -103,13 +136,29 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
     const int64_t my_groups = wglobal < ngroups ? (ngroups - wglobal + wstride - 1) / wstride : 0;
 
     auto issue = [&](int64_t i) {  // copies of the warp's i-th group into slot i % STAGES
+        if (tma) {
+            if (i < my_groups && lane == 0) {
+                const int64_t g = wglobal + i * wstride;
+                uint64_t* bar = &s_bar[warp][i % O::STAGES];
+                fence_proxy_async();  // generic-proxy reads of this slot precede the async write
+                mbar_expect_tx(bar, (uint32_t)O::STAGE);
+                tma_load_2d(ring + (i % O::STAGES) * (O::STAGE / (int)sizeof(T)), &tmap, 0, (int)(g * O::GR), bar);
+            }
+            return;
+        }
         if (i < my_groups) {
             const int64_t g = wglobal + i * wstride;
             T* slot = ring + (i % O::STAGES) * (O::STAGE / (int)sizeof(T));
             const int64_t row0 = g * O::GR;
             const int rows = (int)(m - row0 < O::GR ? m - row0 : O::GR);
             const T* src = X + row0 * n;
-            if ((rowb & 15) == 0) {
+            if (G::VEC16 && n == NP) {
+                constexpr int EPC = 16 / (int)sizeof(T);
+                for (int e = lane; e < rows * G::CPR; e += 32) {
+                    const int li = e / G::CPR, q = e % G::CPR;
+                    cp_async16(slot + G::elem_off(li, q * EPC), src + (int64_t)li * NP + q * EPC);
+                }
+            } else if ((rowb & 15) == 0) {
                 const int cpr = rowb >> 4;
                 constexpr int EPC = 16 / (int)sizeof(T);
                 for (int e = lane; e < rows * cpr; e += 32) {
@@ -138,7 +187,10 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
     for (int i = 0; i < O::STAGES - 1; ++i) issue(i);
 #pragma unroll 1
     for (int64_t i = 0; i < my_groups; ++i) {
-        cp_async_wait_group<O::STAGES - 2>();
+        if (tma)
+            mbar_wait_cta(&s_bar[warp][i % O::STAGES], (uint32_t)((i / O::STAGES) & 1));
+        else
+            cp_async_wait_group<O::STAGES - 2>();
         __syncwarp();
         const int64_t g = wglobal + i * wstride;
         const T* slot = ring + (i % O::STAGES) * (O::STAGE / (int)sizeof(T));
@@ -196,41 +248,72 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
                 i1[r] = lt ? j : i1[r];
             }
         }
+        // near ties (kv == 1: never): exact reference argmin, warp-parallel over centroids
+        // (lane l evaluates centroids l, l+32, ...; tie-aware shuffle argmin, core.hpp:146-157)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            if (!valid[r]) continue;
-            const int lr = r * 32 + lane;
             float nn = 0.f;
 #pragma unroll
             for (int q = 0; q < NPF / 2; ++q) nn = fmaf(x2[r][q].x, x2[r][q].x, fmaf(x2[r][q].y, x2[r][q].y, nn));
             const float sc = sqrtf(nn) + cmax;
-            int lab = i1[r];
-            if (!(m2[r] - m1[r] > kappa * sc * sc)) {  // near tie: exact reference argmin (core.hpp:146-157)
-                double best = __longlong_as_double(0x7ff0000000000000LL);
-                lab = 0;
-                for (int j = 0; j < kv; ++j) {
-                    double dd = 0.0;
-                    for (int d = 0; d < n; ++d) {
-                        const double diff = __dsub_rn((double)slot[G::elem_off(lr, d)], Cd[j * NP + d]);
-                        dd = __dadd_rn(dd, __dmul_rn(diff, diff));
-                    }
-                    if (dd < best) {
-                        best = dd;
-                        lab = j;
+            unsigned tie = __ballot_sync(0xffffffffu, valid[r] && !(m2[r] - m1[r] > kappa * sc * sc));
+            while (tie) {
+                const int src = __ffs(tie) - 1;
+                tie &= tie - 1;
+                const int tr = r * 32 + src;
+                T xr[NP];
+                load_row_T<T, NP>(slot, tr, xr);
+                double dv = __longlong_as_double(0x7ff0000000000000LL);
+                int dj = 0x7fffffff;
+                for (int j = lane; j < kv; j += 32) {
+                    const double dd = exact_dist_regs<T, NP>(xr, Cd + j * CDS);
+                    if (dd < dv) {
+                        dv = dd;
+                        dj = j;
                     }
                 }
-            }
-            // row cost: fp64 distance to the chosen centre (within 1 ulp per term of the reference)
-            double dd = 0.0;
-            const double* cj = Cd + lab * NP;
 #pragma unroll
-            for (int d = 0; d < NP; ++d) {
-                if (d < n) {
-                    const double diff = (double)slot[G::elem_off(lr, d)] - cj[d];
-                    dd = fma(diff, diff, dd);
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, dj, o);
+                    if (ov < dv || (ov == dv && oj < dj)) {
+                        dv = ov;
+                        dj = oj;
+                    }
                 }
+                if (lane == src) i1[r] = dj;
             }
-            cost += dd;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!valid[r]) continue;
+            const int lr = r * 32 + lane;
+            const int lab = i1[r];
+            // row cost: fp64 distance to the chosen centre from the row in registers (two
+            // interleaved DFMA chains; within 1e-15 relative of the reference's per-row value)
+            double xd[NPF];
+            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                for (int q = 0; q < NPF / 2; ++q) {
+                    xd[2 * q] = (double)x2[r][q].x;
+                    xd[2 * q + 1] = (double)x2[r][q].y;
+                }
+            } else {
+                T xr[NP];
+                load_row_T<T, NP>(slot, lr, xr);
+#pragma unroll
+                for (int d = 0; d < NPF; ++d) xd[d] = d < NP ? (double)xr[d] : 0.0;
+            }
+            const double* cj = Cd + lab * CDS;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < NPF / 2; ++q) {
+                const double2 c = *reinterpret_cast<const double2*>(cj + 2 * q);
+                const double d0 = xd[2 * q] - c.x, d1 = xd[2 * q + 1] - c.y;
+                a0 = fma(d0, d0, a0);
+                a1 = fma(d1, d1, a1);
+            }
+            cost += a0 + a1;
             const int64_t row = g * O::GR + lr;
             if (p.labels) p.labels[row] = p.remap[lab];
             if (p.counts) atomicAdd(p.counts + p.remap[lab], 1ULL);

@@ -177,17 +177,11 @@ struct StepShared {  // static smem: per-step scalars and exchange slots
     uint8_t flags[kMaxK];
     int32_t pending[kMaxK];
     int32_t n_pending, n_valid;
-    double xch_total[2];                     // CTA CDF totals (parity buffered)
-    long long xch_hit[2][kMaxCandidates];    // first CDF hit per candidate
-    double xch_cost[2][kMaxCandidates];      // candidate cost partials
-    double xch_err[2][kMaxCandidates];       // their screen error budgets
+    double cta_total;                        // CTA CDF total of the current slot
     double cand[kMaxCandidates][32];         // candidate coordinates (fp64, n <= 32)
     float candf[kMaxCandidates][32];         // negated fp32 copy for the screen
     float candn[kMaxCandidates];             // |candidate| (fp32, rounded up)
     double wsum[kStepWarps][kMaxCandidates];
-    double rank_val[16];
-    double rank_cost[kMaxCandidates][16];
-    double rank_err[kMaxCandidates][16];
     double werr[kStepWarps][kMaxCandidates];
     double wtot[kStepWarps];
     long long whit[kStepWarps][kMaxCandidates];
@@ -288,6 +282,38 @@ HPCG_DEV float screen_dist(const float2 (&x2)[NPF / 2], const float* negc) {
         acc = __ffma2_rn(df, df, acc);
     }
     return acc.x + acc.y;
+}
+
+// Row `row` of the smem sample in its storage type (vector loads through the swizzle).
+template <typename T, int NP>
+HPCG_DEV void load_row_T(const T* samp, int row, T (&x)[NP]) {
+    using G = Geo<T, NP>;
+    if constexpr (G::VEC16) {
+        constexpr int EPC = 16 / (int)sizeof(T);
+#pragma unroll
+        for (int q = 0; q < NP / EPC; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(samp + G::elem_off(row, q * EPC));
+            const T* tv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) x[q * EPC + e] = tv[e];
+        }
+    } else {
+#pragma unroll
+        for (int d = 0; d < NP; ++d) x[d] = samp[row * NP + d];
+    }
+}
+
+// The reference distance (core.hpp:100-108) of a row held in registers: ascending d,
+// separately rounded sub/mul/add; padding columns (d >= n) are zero in both operands.
+template <typename T, int NP>
+HPCG_DEV double exact_dist_regs(const T (&x)[NP], const double* c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < NP; ++d) {
+        const double diff = __dsub_rn((double)x[d], c[d]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
 }
 
 // The reference distance (core.hpp:100-108): ascending d, separately rounded sub/mul/add.
@@ -478,6 +504,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         // dist >= d2, and those rows are compacted so the fp64 work runs on full warps.
         auto d2_update = [&](int c) {
             int cnt = 0;
+            float2 nc2[G::NPF / 2];  // candidate screen record and coordinates held in registers
+            double cd[NP];
+#pragma unroll
+            for (int q = 0; q < G::NPF / 2; ++q) nc2[q] = *reinterpret_cast<const float2*>(&sh.candf[c][2 * q]);
+#pragma unroll
+            for (int d = 0; d < NP; ++d) cd[d] = sh.cand[c][d];
+            const float cnrm = sh.candn[c];
             const int nchunks = (nr + 31) / 32;
             for (int ch = warp; ch < nchunks + kStepWarps; ch += kStepWarps) {
                 if (ch < nchunks) {
@@ -486,8 +519,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     if (row < nr) {
                         float2 x2[G::NPF / 2];
                         load_row_f32<T, NP>(samp, row, x2);
-                        const float df = screen_dist<G::NPF>(x2, sh.candf[c]);
-                        const float sc = xnorm[row] + sh.candn[c];
+                        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int q = 0; q < G::NPF / 2; ++q) {
+                            const float2 df2 = __fadd2_rn(x2[q], nc2[q]);
+                            acc = __ffma2_rn(df2, df2, acc);
+                        }
+                        const float df = acc.x + acc.y;
+                        const float sc = xnorm[row] + cnrm;
                         need = !(df - kScreenK * sc * sc > __double2float_ru(d2[row]));  // ru: conservative
                     }
                     const unsigned msk = __ballot_sync(0xffffffffu, need);
@@ -500,7 +539,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     const int take = cnt < 32 ? cnt : 32;
                     if (lane < take) {
                         const int r = (int)wlist[lane];
-                        d2[r] = fmin(d2[r], exact_dist<T, NP>(samp, r, sh.cand[c], n));
+                        T xr[NP];
+                        load_row_T<T, NP>(samp, r, xr);
+                        d2[r] = fmin(d2[r], exact_dist_regs<T, NP>(xr, cd));
                     }
                     __syncwarp();
                     for (int t = lane; t + take < cnt; t += 32) wlist[t] = wlist[t + take];
@@ -537,7 +578,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             chunk_range(s, C, owner, ob, oe);
             const T* rs = cluster.map_shared_rank(samp, owner);
             const int lr = (int)(row - ob);
-            for (int d = lane; d < n; d += 32) dst[d] = (double)rs[G::elem_off(lr, d)];
+            for (int d = lane; d < 32; d += 32) dst[d] = d < n ? (double)rs[G::elem_off(lr, d)] : 0.0;
         };
         int next = 0;
         __syncthreads();
@@ -567,7 +608,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         const int se = sb + seg < nr ? sb + seg : nr;
         int it = 0;
         for (; next < np_; ++next, ++it) {
-            const int par = it & 1;
             // (1) segment sums, block exclusive scan (fixed tree), CTA total
             double tsum = 0.0;
             for (int li = sb; li < se; ++li) tsum += d2[li];
@@ -581,26 +621,34 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             if (lane == 0) lexcl = 0.0;
             if (lane == 31) sh.wtot[warp] = incl;
             __syncthreads();
-            double wexcl = 0.0;
-            for (int w2 = 0; w2 < warp; ++w2) wexcl += sh.wtot[w2];
+            double wexcl;
+            {  // exclusive prefix of the warp totals, shuffle scan (fixed order, same for all lanes)
+                double v = lane < kStepWarps ? sh.wtot[lane] : 0.0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += y;
+                }
+                wexcl = __shfl_sync(0xffffffffu, v, warp > 0 ? warp - 1 : 0);
+                if (warp == 0) wexcl = 0.0;
+            }
             const double texcl = wexcl + lexcl;  // exclusive prefix of this thread's segment
             // CTA total := local cum at the CTA's last row, computed exactly as the search does
             if (se == nr && sb < se) {
                 double run = 0.0;
                 for (int li = sb; li < se; ++li) run += d2[li];
-                sh.xch_total[par] = texcl + run;
+                sh.cta_total = texcl + run;
             }
-            if (it == 0 && p.trace_mode == 1) mark();  // 5: CDF local done
-            cluster.sync();
-            if (it == 0 && p.trace_mode == 1) mark();  // 6: CDF exchange synced
-            if (warp == 0 && lane < C) sh.rank_val[lane] = *cluster.map_shared_rank(&sh.xch_total[par], lane);
             __syncthreads();
+            if (it == 0 && p.trace_mode == 1) mark();  // 5: CDF local done
+            const double* rxt = exchange(1, [&](int) { return sh.cta_total; });
+            if (it == 0 && p.trace_mode == 1) mark();  // 6: CDF exchange complete
             // P = sum of lower ranks' totals (rank order); total = P_{C-1} + T_{C-1}
             double P = 0.0, total = 0.0;
             {
                 double acc = 0.0;
                 for (int rr = 0; rr < C; ++rr) {
-                    const double tr = sh.rank_val[rr];
+                    const double tr = rxt[rr * xs];
                     if (rr == cr) P = acc;
                     if (rr == C - 1)
                         total = acc + tr;
@@ -655,17 +703,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 if (lane == 0) sh.whit[warp][c] = h;
             }
             __syncthreads();
-            if (tid < ncand) {
-                long long h = LLONG_MAX;
-                for (int w2 = 0; w2 < kStepWarps; ++w2) h = min(h, sh.whit[w2][tid]);
-                sh.xch_hit[par][tid] = h;
-            }
             if (it == 0 && p.trace_mode == 1) mark();  // 7: search done
-            cluster.sync();
-            if (it == 0 && p.trace_mode == 1) mark();  // 8: hit exchange synced
+            const double* rxh = exchange(ncand, [&](int c) {
+                long long h = LLONG_MAX;
+                for (int w2 = 0; w2 < kStepWarps; ++w2) h = min(h, sh.whit[w2][c]);
+                return __longlong_as_double(h);
+            });
+            if (it == 0 && p.trace_mode == 1) mark();  // 8: hit exchange complete
             // every CTA: global first hit per candidate (rank order == row order)
             for (int c = warp; c < ncand; c += kStepWarps) {
-                long long h = lane < C ? *cluster.map_shared_rank(&sh.xch_hit[par][c], lane) : LLONG_MAX;
+                long long h = lane < C ? __double_as_longlong(rxh[lane * xs + c]) : LLONG_MAX;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) h = min(h, __shfl_xor_sync(0xffffffffu, h, o));
                 const int64_t row = h == LLONG_MAX ? s - 1 : (int64_t)h;  // rng.hpp:87-92 fallback
@@ -726,7 +773,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                         if (lane < take) {
                             const uint32_t e = wlist[lane];
                             const int r = (int)(e & 0xffffu), c = (int)(e >> 16);
-                            const double v = fmin(d2[r], exact_dist<T, NP>(samp, r, sh.cand[c], n));
+                            T xr[NP];
+                            load_row_T<T, NP>(samp, r, xr);
+                            const double v = fmin(d2[r], exact_dist_regs<T, NP>(xr, sh.cand[c]));
 #pragma unroll
                             for (int cc = 0; cc < kMaxCandidates; ++cc)
                                 if (cc == c) cost[cc] += v;
@@ -749,24 +798,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     }
                 }
                 __syncthreads();
-                if (tid < ncand) {
-                    double v = 0.0, e = 0.0;
-                    for (int w2 = 0; w2 < kStepWarps; ++w2) {
-                        v += sh.wsum[w2][tid];
-                        e += sh.werr[w2][tid];
-                    }
-                    sh.xch_cost[par][tid] = v;
-                    sh.xch_err[par][tid] = e;
-                }
                 if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 10: costs local done
-                cluster.sync();
-                if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 11: cost exchange synced
-                for (int e = tid; e < ncand * C; e += kStepThreads) {
-                    const int c = e / C, rr = e - c * C;
-                    sh.rank_cost[c][rr] = *cluster.map_shared_rank(&sh.xch_cost[par][c], rr);
-                    sh.rank_err[c][rr] = *cluster.map_shared_rank(&sh.xch_err[par][c], rr);
-                }
-                __syncthreads();
+                const double* rxc = exchange(2 * ncand, [&](int e) {
+                    const int c = e % ncand;
+                    double v = 0.0;
+                    for (int w2 = 0; w2 < kStepWarps; ++w2) v += e < ncand ? sh.wsum[w2][c] : sh.werr[w2][c];
+                    return v;
+                });
+                if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 11: cost exchange complete
                 double tc[kMaxCandidates], te[kMaxCandidates];
                 double bc = __longlong_as_double(0x7ff0000000000000LL), be = 0.0;
                 best = 0;
@@ -776,8 +815,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     te[c] = 0.0;
                     if (c >= ncand) continue;
                     for (int rr = 0; rr < C; ++rr) {
-                        tc[c] += sh.rank_cost[c][rr];
-                        te[c] += sh.rank_err[c][rr];
+                        tc[c] += rxc[rr * xs + c];
+                        te[c] += rxc[rr * xs + ncand + c];
                     }
                     te[c] += 1e-9 * fabs(tc[c]);  // summation-order slack
                     if (tc[c] < bc) {  // strict <, first candidate wins ties (seeding.hpp:94-98)
@@ -793,7 +832,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                         if (c < ncand && c != best && !(tc[c] - te[c] > bc + be)) decided = false;
                 // every CTA evaluated the same totals: the decision is cluster-uniform
                 if (decided) break;
-                cluster.sync();  // peers may still read this CTA's xch_* of the screened pass
+                __syncthreads();  // all reads of this exchange precede the exact pass's pushes
             }
             nd += (int64_t)ncand * s;
             const int j = sh.pending[next];
@@ -914,7 +953,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                         const int trow = rowr[r] - lane + src;
                         double dv = __longlong_as_double(0x7ff0000000000000LL);
                         int dj = lane;
-                        if (lane < k) dv = exact_dist<T, NP>(samp, trow, Cm + lane * NP, n);
+                        if (lane < k) {
+                            T xr[NP];
+                            load_row_T<T, NP>(samp, trow, xr);
+                            dv = exact_dist_regs<T, NP>(xr, Cm + lane * NP);
+                        }
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
                             const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
