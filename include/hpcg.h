@@ -191,6 +191,8 @@ int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d);
 int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels,
                        double* publications, int64_t pub_cap, double* worker_obj, double* traces,
                        int64_t trace_cap, int64_t* trace_len);
+/* Per-worker incumbents after finish/rounds: C_out[W*k*n], f_out[W*k], obj_out[W] (any may be NULL). */
+int hpcg_engine_worker_incumbents(hpcg_engine* e, double* C_out, uint8_t* f_out, double* obj_out);
 int hpcg_engine_destroy(hpcg_engine* e);
 
 /* Multi-rank exchange hooks (cooperative / hybrid across GPUs):

@@ -21,7 +21,7 @@ EXPORTS = (
     "hpcg_rng_derive", "hpcg_rng_draw", "hpcg_engine_create", "hpcg_engine_rounds", "hpcg_engine_round_index",
     "hpcg_engine_distance_evals", "hpcg_engine_finish", "hpcg_engine_destroy", "hpcg_engine_export_best",
     "hpcg_run", "hpcg_gen_mixture", "hpcg_ctx_enable_timing", "hpcg_ctx_kernel_times", "hpcg_probe_fma_peak",
-    "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace",
+    "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -130,6 +130,7 @@ def _load():
         "hpcg_engine_reset": (C.c_int, [P, U64]),
         "hpcg_engine_import_best": (C.c_int, [P, D, I64, P, P]),
         "hpcg_engine_set_trace": (C.c_int, [P, P, I32]),
+        "hpcg_engine_worker_incumbents": (C.c_int, [P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

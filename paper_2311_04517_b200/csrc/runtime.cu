@@ -1268,6 +1268,18 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     return HPCG_OK;
 }
 
+int hpcg_engine_worker_incumbents(hpcg_engine* e, double* C_out, uint8_t* f_out, double* obj_out) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    const int64_t W = e->W, k = e->k, kn = k * e->n;
+    if (C_out) CU(d2h(C_out, e->inc_c.as<double>(), (size_t)(W * kn), ctx->stream));
+    if (f_out) CU(d2h(f_out, e->inc_f.as<uint8_t>(), (size_t)(W * k), ctx->stream));
+    if (obj_out) CU(d2h(obj_out, e->inc_obj.as<double>(), (size_t)W, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return HPCG_OK;
+}
+
 int hpcg_engine_destroy(hpcg_engine* e) {
     if (e) {
         cudaSetDevice(e->ctx->device);

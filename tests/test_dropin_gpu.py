@@ -1,0 +1,52 @@
+"""GPU: the C++ drop-in (include/hpclust/hpclust.hpp over libhpcg.so) used exactly as a
+reference user would (examples/dropin_example.cpp) reproduces the reference semantics:
+same draw_sample rows, same K-means++ centres, same Lloyd outcome, same engine run."""
+import json
+import subprocess
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle_py import orc
+
+ROOT = Path(__file__).resolve().parents[1]
+EXE = ROOT / "examples" / "dropin_example"
+
+
+def test_dropin_binary_builds():
+    if not EXE.exists():
+        subprocess.run(["make", "-C", str(ROOT / "examples")], check=True)
+    assert EXE.exists()
+
+
+@pytest.mark.gpu
+def test_dropin_matches_reference_semantics():
+    rs = np.random.default_rng(4)
+    means = rs.uniform(-10, 10, (5, 2))
+    X = means[rs.integers(0, 5, 8000)] + rs.standard_normal((8000, 2))
+    with tempfile.NamedTemporaryFile(suffix=".f64", delete=False) as f:
+        X.astype(np.float64).tofile(f.name)
+        out = subprocess.run([str(EXE), f.name, "8000", "2"], capture_output=True, text=True, timeout=300)
+    r = json.loads(out.stdout)
+    assert "error" not in r, r
+    o = orc()
+    rng = o.rng(seed=7)
+    idx = o.draw_indices(8000, 500, rng)
+    S = X[idx]
+    assert r["sample0"] == S[0, 0]
+    C0, f0, nd_seed = o.reinit(S, np.zeros((5, 2)), np.ones(5, np.uint8), rng)
+    assert r["seed_c0"] == C0[0, 0]
+    e = o.kmeans(S, C0)
+    assert abs(r["lloyd_obj"] - e["objective"]) <= 1e-12 * e["objective"]
+    assert r["lloyd_iters"] == e["iterations"]
+    assert r["lloyd_stop"] == ["tolerance", "max_iters", "fixed_point"][e["stop"]]
+    assert r["nd"] == nd_seed + e["n_d"]
+    _, _, fo, _ = o.assign(X, e["centroids"])
+    assert abs(r["f_full"] - fo) <= 1e-12 * fo
+    run = o.run(X, k=5, sample_size=500, n_workers=3, max_samples=4, strategy="cooperative", seed=11)
+    assert abs(r["run_full"] - run["full_objective"]) <= 1e-12 * run["full_objective"]
+    assert r["run_best"] == run["best_worker"] and r["run_nd"] == run["distance_evals"]
+    assert abs(r["run_c0"] - run["centroids"][0, 0]) <= 1e-12 * abs(run["centroids"][0, 0])
+    assert r["pubs"] == len(run["publications"])
