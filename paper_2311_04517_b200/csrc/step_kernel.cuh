@@ -19,7 +19,7 @@
 
 namespace hpcg {
 
-constexpr int kStepThreads = 512;  // one CTA per SM, 16 warps
+constexpr int kStepThreads = 256;  // two CTAs per SM: one cluster computes while another waits
 constexpr int kStepWarps = kStepThreads / 32;
 constexpr int kMaxK = 32;          // label fits u8 and the per-warp partial table fits smem
 constexpr int kMaxCandidates = 4;  // K-means++ candidates per slot (reference default 3) in one sweep
@@ -140,11 +140,12 @@ struct SmemLayout {  // byte offsets into dynamic smem
 // partial batch of < 32
 __host__ __device__ constexpr int list_cap(int ncand) { return 32 * (ncand + 1); }
 
-// receive slot stride (doubles) of the cluster exchange: a Lloyd partial or seeding scalars
-__host__ __device__ inline int xch_stride(int k, int NP) {
-    const int part_d = k * NP + k + 1;
-
-    return part_d > 2 * kMaxCandidates ? part_d : 2 * kMaxCandidates;
+// cluster exchange buffers (doubles): all-to-all slots for the seeding scalars, and the
+// reduce-scatter / all-gather slices of the Lloyd partial (k*NP sums + k counts + cost)
+constexpr int kXchSmall = 2 * kMaxCandidates;
+__host__ __device__ inline int xch_slice(int k, int NP, int C) { return (k * NP + k + 1 + C - 1) / C; }
+__host__ __device__ inline int xch_doubles(int k, int NP, int C) {
+    return 2 * C * kXchSmall + 2 * C * xch_slice(k, NP, C) + 2 * C * xch_slice(k, NP, C);
 }
 
 template <typename T, int NP>
@@ -157,7 +158,7 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand
     L.cm = up(L.samp + rows_cap * G::RS);
     L.cs = up(L.cm + k * NP * 8);
     L.part = up(L.cs + k * G::CSR * 4);
-    L.scratch = up(L.part + 2 * C * xch_stride(k, NP) * 8);  // exchange receive buffers
+    L.scratch = up(L.part + xch_doubles(k, NP, C) * 8);  // exchange receive buffers
     L.labels = L.scratch;
     L.pos = up(L.labels + rows_cap);
     L.perm = up(L.pos + rows_cap * 2);
@@ -174,6 +175,7 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand
 
 struct StepShared {  // static smem: per-step scalars and exchange slots
     uint64_t xbar[2];                        // exchange mbarriers (parity buffered)
+    uint64_t rbar1[2], rbar2[2];             // reduce-scatter / all-gather mbarriers
     uint8_t flags[kMaxK];
     int32_t pending[kMaxK];
     int32_t n_pending, n_valid;
@@ -333,7 +335,7 @@ HPCG_DEV double exact_dist(const T* samp, int row, const double* c, int n) {
 
 // ------------------------------------------------------------------ the kernel
 template <typename T, int NP>
-__global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const StepParams p) {
+__global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const StepParams p) {
     using G = Geo<T, NP>;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
@@ -366,14 +368,19 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
     double* wpart = reinterpret_cast<double*>(smem + L.wpart);
     double* d2 = reinterpret_cast<double*>(smem + L.d2);
     const int part_d = k * NP + k + 1;
-    const int xs = xch_stride(k, NP);
-    // one exchange: values v(e), e < nv, of this CTA land in slot [cr] of every CTA's receive
-    // buffer; returns the local buffer holding all C slots (rank order). Callers separate the
-    // reads of one exchange from the pushes of the next with a __syncthreads.
-    uint32_t xcount = 0, xph0 = 0, xph1 = 0;
+    // Cluster exchanges. Push model (no cluster barrier): values are st.async'd into peers'
+    // receive slots with mbarrier complete_tx; each CTA waits only on its own mbarrier. Callers
+    // separate the reads of one exchange from the pushes of the next with a __syncthreads.
+    const int xs = kXchSmall;
+    double* rxs = part;                                // [2][C][kXchSmall]
+    const int sl = xch_slice(k, NP, C);
+    double* rx1 = part + 2 * C * kXchSmall;            // [2][C][sl]   reduce-scatter inputs
+    double* rx2 = rx1 + 2 * C * sl;                    // [2][C*sl]    all-gathered totals
+    uint32_t xcount = 0, xph[2] = {0u, 0u};
+    // all-to-all of nv <= kXchSmall scalars: returns [C][xs] slots in rank order
     auto exchange = [&](int nv, auto&& value_of) -> const double* {
         const int par = (int)(xcount++ & 1);
-        double* rx = part + par * C * xs;
+        double* rx = rxs + par * C * xs;
         uint64_t* bar = &sh.xbar[par];
         if (tid == 0) mbar_expect_tx(bar, (uint32_t)(C * nv * 8));
         const uint32_t rbar_local = smem_u32(bar), slot_local = smem_u32(rx + cr * xs);
@@ -381,9 +388,41 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             const double v = value_of(e);
             for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(slot_local + e * 8, r), v, mapa_u32(rbar_local, r));
         }
-        mbar_wait_cluster(bar, par ? xph1 : xph0);
-        if (par) xph1 ^= 1u; else xph0 ^= 1u;
+        mbar_wait_cluster(bar, xph[par]);
+        xph[par] ^= 1u;
         return rx;
+    };
+    // cluster-wide sum of nv values per CTA, reduced in rank order by the element's owner rank
+    // (reduce-scatter) and broadcast (all-gather): returns the nv totals, identical in every CTA
+    uint32_t rcount = 0, rph1[2] = {0u, 0u}, rph2[2] = {0u, 0u};
+    auto reduce_all = [&](int nv, auto&& value_of) -> const double* {
+        const int par = (int)(rcount++ & 1);
+        double* in = rx1 + par * C * sl;
+        double* tot = rx2 + par * C * sl;
+        uint64_t* b1 = &sh.rbar1[par];
+        uint64_t* b2 = &sh.rbar2[par];
+        const int mylo = cr * sl, mylen = max(0, min(sl, nv - mylo));
+        if (tid == 0) {
+            mbar_expect_tx(b1, (uint32_t)(C * mylen * 8));
+            mbar_expect_tx(b2, (uint32_t)(nv * 8));
+        }
+        const uint32_t in_l = smem_u32(in + cr * sl), b1_l = smem_u32(b1);
+        for (int e = tid; e < nv; e += kStepThreads) {
+            const double v = value_of(e);
+            const int o = e / sl;
+            st_async_f64(mapa_u32(in_l + (e - o * sl) * 8, o), v, mapa_u32(b1_l, o));
+        }
+        mbar_wait_cluster(b1, rph1[par]);
+        rph1[par] ^= 1u;
+        const uint32_t tot_l = smem_u32(tot), b2_l = smem_u32(b2);
+        for (int e = tid; e < mylen; e += kStepThreads) {
+            double t = in[e];
+            for (int r = 1; r < C; ++r) t += in[r * sl + e];
+            for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(tot_l + (mylo + e) * 8, r), t, mapa_u32(b2_l, r));
+        }
+        mbar_wait_cluster(b2, rph2[par]);
+        rph2[par] ^= 1u;
+        return tot;
     };
 
     // ---------------------------------------------------------------- gather
@@ -460,6 +499,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
     if (tid == 0) {
         mbar_init(&sh.xbar[0], 1);
         mbar_init(&sh.xbar[1], 1);
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(&sh.rbar1[q], 1);
+            mbar_init(&sh.rbar2[q], 1);
+        }
         mbar_init_fence();
     }
     mark();  // 1: copies issued
@@ -1106,7 +1149,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             __syncthreads();
             if (pass == 0 && p.trace_mode == 0) mark();  // 8: update done
             // ---- CTA partial (warps in order) pushed to every CTA; totals in rank order
-            const double* rxp = exchange(part_d, [&](int e) {
+            const double* totx = reduce_all(part_d, [&](int e) {
                 double v = 0.0;
                 for (int w2 = 0; w2 < kStepWarps; ++w2) v += wpart[w2 * part_d + e];
                 return v;
@@ -1115,11 +1158,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             if (pass == 0 && p.trace_mode == 0) mark();  // 10: exchange complete
             __syncthreads();  // every warp partial consumed before tot overwrites wpart
             double* tot = wpart;
-            for (int e = tid; e < part_d; e += kStepThreads) {
-                double t = rxp[e];
-                for (int r = 1; r < C; ++r) t += rxp[r * xs + e];
-                tot[e] = t;
-            }
+            for (int e = tid; e < part_d; e += kStepThreads) tot[e] = totx[e];
             __syncthreads();
             if (pass == 0 && p.trace_mode == 0) mark();  // 11: cluster reduce done
             const double f = tot[k * NP + k];
