@@ -19,7 +19,7 @@
 
 namespace hpcg {
 
-constexpr int kStepThreads = 256;  // two CTAs per SM: one cluster computes while another waits
+constexpr int kStepThreads = 512;  // one CTA per SM, 16 warps
 constexpr int kStepWarps = kStepThreads / 32;
 constexpr int kMaxK = 32;          // label fits u8 and the per-warp partial table fits smem
 constexpr int kMaxCandidates = 4;  // K-means++ candidates per slot (reference default 3) in one sweep
@@ -335,7 +335,7 @@ HPCG_DEV double exact_dist(const T* samp, int row, const double* c, int n) {
 
 // ------------------------------------------------------------------ the kernel
 template <typename T, int NP>
-__global__ void __launch_bounds__(kStepThreads, 2) worker_step_kernel(const StepParams p) {
+__global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const StepParams p) {
     using G = Geo<T, NP>;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
