@@ -36,7 +36,10 @@ cudaError_t step_geometry_uncached(int64_t s, int k, int ncand, int W, StepGeome
     // widen the cluster while it raises the number of SMs busy (few workers) or the
     // packing of clusters into GPCs; stop at 16 and at >= 128 rows per CTA.
     int best_c = cmin, best_used = -1, best_active = 0;
+    const char* force = getenv("HPCG_CLUSTER");  // diagnostics: pin the cluster size
+    const int fc = force ? atoi(force) : 0;
     for (int c = cmin; c <= 16 && c <= s; ++c) {
+        if (fc && c != fc) continue;
         const int rows = (int)((s + c - 1) / c);
         if (c > cmin && rows < 128) break;
         const int smem = step_layout<T, NP>(rows, k, ncand, c).total;
