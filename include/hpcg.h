@@ -137,6 +137,11 @@ int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_
 
 /* ---- sample gather (engine.hpp:165-177 draw_sample with the indices it would draw) --------- */
 int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, int64_t s, void* S_host);
+/* Device sample definition of HPCG_RNG_PHILOX rounds (replaces engine.hpp:165-177 there): the
+ * first s images of [0, m) under the keyed permutation of worker `worker` in round `round`
+ * (distinct by construction). The engine uses key = its Philox key (hpcg_engine_cfg seed). */
+int hpcg_sample_indices(hpcg_ctx* ctx, int64_t m, int64_t s, uint64_t key, uint32_t round, uint32_t worker,
+                        int64_t* idx_out);
 /* Reference-exact draw_sample indices: partial Fisher-Yates of the stream seeded `seed_state`
  * in O(s) (sparse swaps); advances the 312-word mt19937_64 state in place (rng.hpp). */
 int hpcg_reference_draw_indices(uint64_t* mt_state, int32_t* mt_pos, int64_t m, int64_t s, int64_t* idx_out);
@@ -180,7 +185,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed);
 int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds);
 int64_t hpcg_engine_round_index(const hpcg_engine* e);
 /* Diagnostics: per-CTA phase timestamps (%globaltimer ns) of subsequent rounds written to
- * trace_dev[W * cluster * 16] (NULL disables); mode 0 details the first Lloyd pass, mode 1
+ * trace_dev[W * cluster * 32] (NULL disables); mode 0 details the first Lloyd pass, mode 1
  * the first K-means++ slot. */
 int hpcg_engine_set_trace(hpcg_engine* e, int64_t* trace_dev, int32_t mode);
 /* Sum of n_d over the rounds run so far (device-side exact count; synchronises). */

@@ -17,7 +17,7 @@ EXPORTS = (
     "hpcg_last_error", "hpcg_abi_version", "hpcg_ctx_create", "hpcg_ctx_destroy", "hpcg_ctx_set_stream",
     "hpcg_ctx_synchronize", "hpcg_ctx_launch_count", "hpcg_dataset_upload", "hpcg_dataset_wrap",
     "hpcg_dataset_destroy", "hpcg_dataset_device_ptr", "hpcg_assign", "hpcg_assign_dev",
-    "hpcg_worker_step_batched", "hpcg_gather", "hpcg_reference_draw_indices", "hpcg_rng_seed",
+    "hpcg_worker_step_batched", "hpcg_gather", "hpcg_sample_indices", "hpcg_reference_draw_indices", "hpcg_rng_seed",
     "hpcg_rng_derive", "hpcg_rng_draw", "hpcg_engine_create", "hpcg_engine_rounds", "hpcg_engine_round_index",
     "hpcg_engine_distance_evals", "hpcg_engine_finish", "hpcg_engine_destroy", "hpcg_engine_export_best",
     "hpcg_run", "hpcg_gen_mixture", "hpcg_ctx_enable_timing", "hpcg_ctx_kernel_times", "hpcg_probe_fma_peak",
@@ -111,6 +111,7 @@ def _load():
         "hpcg_worker_step_batched": (C.c_int, [P, P, P, I64, I64, P, P, I64, P, P, P, I64, C.c_int, P, P, P, P,
                                                P, P, P, P, P, P, I32, P]),
         "hpcg_gather": (C.c_int, [P, P, P, I64, P]),
+        "hpcg_sample_indices": (C.c_int, [P, I64, I64, C.c_uint64, C.c_uint32, C.c_uint32, P]),
         "hpcg_reference_draw_indices": (C.c_int, [P, P, I64, I64, P]),
         "hpcg_rng_seed": (C.c_int, [U64, P, P]),
         "hpcg_rng_derive": (C.c_int, [U64, U64, U64, P, P]),

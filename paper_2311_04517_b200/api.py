@@ -452,6 +452,16 @@ def reference_draw_indices(m: int, s: int, rng: RngStream) -> np.ndarray:
     return out
 
 
+def philox_sample_indices(m: int, s: int, key: int, round_: int, worker: int, ctx=None) -> np.ndarray:
+    """The rows a philox-mode engine round samples for `worker` (device keyed permutation)."""
+    if not 1 <= s <= m:
+        raise _lib.InvalidArgument("draw_sample: sample size must be in [1, m]")
+    ctx = ctx or default_context()
+    out = np.empty(s, dtype=np.int64)
+    check(lib.hpcg_sample_indices(ctx.h, m, s, key, round_, worker, ptr(out)))
+    return out
+
+
 def draw_sample(X, s: int, rng: RngStream, ctx=None) -> np.ndarray:
     """engine.hpp:165-177: s distinct rows in draw order, gathered on the device."""
     ds = _as_dataset(X, ctx)

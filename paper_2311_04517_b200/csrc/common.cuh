@@ -1,6 +1,7 @@
 // Shared device helpers for the HPClust B200 kernels (sm_100a only).
 #pragma once
 #include <cstdint>
+#include <cmath>
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 
@@ -45,23 +46,35 @@ HPCG_DEV uint64_t philox_index(uint64_t key, uint32_t a, uint32_t b, uint32_t c,
 }
 
 // ------------------------------------------------------ sample-index permutation
-// s distinct rows of [0, m) in "draw order": a keyed pseudo-random permutation of
-// [0, 2^bits) (4-round Feistel over Philox-derived round keys) with cycle walking
-// back into [0, m). Distinctness is by construction (bijection), replacing the
-// reference's O(m) partial Fisher-Yates (engine.hpp:165-177) with O(1) per draw.
-struct FeistelPRP {
+// s distinct rows of [0, m) in "draw order": a keyed pseudo-random permutation of [0, a*b)
+// with a = ceil(sqrt(m)), b = ceil(m / a) — a 4-round Feistel network over Z_a x Z_b with
+// modular addition (the halves alternate between the two moduli, so every round is a
+// bijection) — and cycle walking back into [0, m), which a*b - m < a makes rare (< 1/b).
+// Distinctness is by construction (bijection), replacing the reference's O(m) partial
+// Fisher-Yates (engine.hpp:165-177) with O(1) work per draw and no divergent walks.
+struct SamplePRP {
     uint64_t m;
-    uint32_t half_bits, half_mask;
+    uint32_t a, b;
+    float inv_b;
     uint32_t rk[4];
 
-    HPCG_DEV static FeistelPRP make(uint64_t key, uint32_t round, uint32_t worker, uint64_t m) {
-        FeistelPRP p;
-        p.m = m;
-        int bits = 64 - __clzll((long long)(m > 1 ? m - 1 : 1));
-        bits = bits < 2 ? 2 : bits;
-        bits += bits & 1;
-        p.half_bits = (uint32_t)bits / 2;
-        p.half_mask = (1u << p.half_bits) - 1u;
+    // host side: the moduli depend on m only (StepParams carries them)
+    static inline void moduli(uint64_t m, uint32_t& a, uint32_t& b, float& inv_b) {
+        m = m > 0 ? m : 1;
+        uint64_t r = (uint64_t)sqrt((double)m);
+        while (r * r < m) ++r;
+        while (r > 1 && (r - 1) * (r - 1) >= m) --r;
+        a = (uint32_t)r;
+        b = (uint32_t)((m + r - 1) / r);
+        inv_b = 1.0f / (float)b;
+    }
+    HPCG_DEV static SamplePRP make(uint64_t key, uint32_t round, uint32_t worker, uint64_t m, uint32_t a, uint32_t b,
+                                   float inv_b) {
+        SamplePRP p;
+        p.m = m > 0 ? m : 1;
+        p.a = a;
+        p.b = b;
+        p.inv_b = inv_b;
         u32x4 r = philox4x32(u32x4{round, worker, 0x50525031u, 0x50525032u}, (uint32_t)key, (uint32_t)(key >> 32));
         p.rk[0] = r.x;
         p.rk[1] = r.y;
@@ -69,29 +82,41 @@ struct FeistelPRP {
         p.rk[3] = r.w;
         return p;
     }
-    HPCG_DEV uint64_t permute_once(uint64_t v) const {
-        uint32_t L = (uint32_t)(v >> half_bits) & half_mask, R = (uint32_t)v & half_mask;
+    HPCG_DEV uint64_t permute_once(uint64_t x) const {
+        // x = L*b + R, L in Z_a, R in Z_b (fp32 quotient estimate, exact after one correction
+        // each way: a*b <= 2^42 keeps the estimate within +-1 of floor(x/b))
+        uint64_t Lq = (uint64_t)((float)x * inv_b);
+        if (Lq * b > x) --Lq;
+        if (x - Lq * b >= b) ++Lq;
+        uint32_t L = (uint32_t)Lq, R = (uint32_t)(x - Lq * b);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+            const uint32_t mod = (i & 1) ? b : a;  // L lives in Z_mod
             uint32_t f = R * 0x9E3779B1u ^ rk[i];
             f ^= f >> 15;
             f *= 0x85EBCA77u;
             f ^= f >> 13;
-            const uint32_t nl = R;
-            R = (L ^ f) & half_mask;
-            L = nl;
+            uint32_t t = L + __umulhi(f, mod);  // F(R) in [0, mod)
+            if (t >= mod) t -= mod;
+            L = R;
+            R = t;
         }
-        return ((uint64_t)L << half_bits) | R;
+        return (uint64_t)L * b + R;  // L in Z_a, R in Z_b again after an even round count
     }
     HPCG_DEV uint64_t operator()(uint64_t i) const {
         uint64_t v = permute_once(i);
-        while (v >= m) v = permute_once(v);  // cycle walking: expected < 4 steps
+        while (v >= m) v = permute_once(v);  // cycle walking: P(step) < 1/b
         return v;
     }
 };
 
 // ------------------------------------------------------------------ reductions
 HPCG_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+HPCG_DEV float warp_sum_f(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;

@@ -606,6 +606,34 @@ int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, 
     return HPCG_OK;
 }
 
+// the device sample definition of RngMode::philox (SamplePRP), for tests and reproduction
+__global__ void sample_prp_kernel(uint64_t m, uint32_t a, uint32_t b, float inv_b, uint64_t key, uint32_t round,
+                                  uint32_t worker, int64_t s, int64_t* out) {
+    const SamplePRP prp = SamplePRP::make(key, round, worker, m, a, b, inv_b);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)prp((uint64_t)i);
+}
+
+int hpcg_sample_indices(hpcg_ctx* ctx, int64_t m, int64_t s, uint64_t key, uint32_t round, uint32_t worker,
+                        int64_t* idx_out) {
+    if (!ctx || !idx_out) return fail(HPCG_EINVAL, "sample_indices: null argument");
+    if (s < 1 || s > m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    uint32_t a, b;
+    float inv_b;
+    SamplePRP::moduli((uint64_t)m, a, b, inv_b);
+    CU(ctx->s_a.reserve((size_t)s * 8));
+    const unsigned grid = (unsigned)std::min<int64_t>((s + 255) / 256, 4096);
+    sample_prp_kernel<<<grid, 256, 0, ctx->stream>>>((uint64_t)m, a, b, inv_b, key, round, worker, s,
+                                                     ctx->s_a.as<int64_t>());
+    CU(cudaGetLastError());
+    ctx->launches += 1;
+    CU(cudaMemcpyAsync(idx_out, ctx->s_a.p, (size_t)s * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return HPCG_OK;
+}
+
 int hpcg_reference_draw_indices(uint64_t* mt_state, int32_t* mt_pos, int64_t m, int64_t s, int64_t* idx_out) {
     if (s < 1 || s > m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
     Mt64 r;
@@ -717,6 +745,7 @@ int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_
     StepParams p = {};
     p.X = ds->X;
     p.m = ds->m;
+    SamplePRP::moduli((uint64_t)p.m, p.prp_a, p.prp_b, p.prp_inv_b);
     p.n = (int)n;
     p.s = s;
     p.W = (int)W;
@@ -859,6 +888,7 @@ int engine_round(hpcg_engine* e) {
     StepParams p = {};
     p.X = e->ds->X;
     p.m = e->ds->m;
+    SamplePRP::moduli((uint64_t)p.m, p.prp_a, p.prp_b, p.prp_inv_b);
     p.n = (int)n;
     p.s = s;
     p.W = (int)W;

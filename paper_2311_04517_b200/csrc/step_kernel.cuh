@@ -36,6 +36,8 @@ struct StepParams {
     int32_t sample_mode;  // 0 explicit idx[W*s], 1 Philox PRP over [0,m), 2 contiguous (X is [W*s x n])
     const int64_t* idx;
     uint64_t key;        // Philox key (sample PRP and K-means++ draws)
+    uint32_t prp_a, prp_b;  // sample PRP moduli (SamplePRP::moduli of m)
+    float prp_inv_b;
     uint32_t round;      // Philox counter component
     int32_t worker_base;  // global id of local worker 0 (Philox stream id)
     // initial centroids
@@ -81,7 +83,7 @@ struct StepParams {
     int32_t trace_mode;  // 0: first Lloyd pass in detail, 1: first K-means++ slot in detail
 };
 
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 32;
 template <int V>
 struct IntC {
     static constexpr int value = V;
@@ -133,12 +135,12 @@ struct Geo {
 
 struct SmemLayout {  // byte offsets into dynamic smem
     int samp, cm, cs, part, scratch, total;
-    int labels, pos, perm, wpart, d2, gidx, xnorm, wlist;
+    int labels, pos, perm, wpart, d2, gidx, xnorm, wlist, nflag;
 };
 
-// per-warp exact-work list: one 32-row chunk of (row, candidate) entries plus a carried
-// partial batch of < 32
-__host__ __device__ constexpr int list_cap(int ncand) { return 32 * (ncand + 1); }
+// per-warp exact-work list: the entries one step appends (ncand per row) plus a carried
+// partial batch of < 32 (the D^2 update appends two chunks per step, hence the floor of 2)
+__host__ __device__ constexpr int list_cap(int ncand) { return 32 * ((ncand > 2 ? ncand : 2) + 1); }
 
 // cluster exchange buffers (doubles): all-to-all slots for the seeding scalars, and the
 // reduce-scatter / all-gather slices of the Lloyd partial (k*NP sums + k counts + cost)
@@ -168,7 +170,8 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand
     L.gidx = L.scratch;  // gather only
     L.xnorm = up(L.d2 + rows_cap * 8);
     L.wlist = up(L.xnorm + rows_cap * 4);
-    const int seed_end = L.wlist + kStepWarps * list_cap(ncand) * 4;
+    L.nflag = up(L.wlist + kStepWarps * list_cap(ncand) * 4);
+    const int seed_end = L.nflag + rows_cap;
     L.total = up(lloyd_end > seed_end ? lloyd_end : seed_end);
     return L;
 }
@@ -176,22 +179,27 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand
 struct StepShared {  // static smem: per-step scalars and exchange slots
     uint64_t xbar[2];                        // exchange mbarriers (parity buffered)
     uint64_t rbar1[2], rbar2[2];             // reduce-scatter / all-gather mbarriers
+    uint64_t cbar;                           // K-means++ candidate push mbarrier
     uint8_t flags[kMaxK];
     int32_t pending[kMaxK];
     int32_t n_pending, n_valid;
     double cta_total;                        // CTA CDF total of the current slot
     double cand[kMaxCandidates][32];         // candidate coordinates (fp64, n <= 32)
-    float candf[kMaxCandidates][32];         // negated fp32 copy for the screen
-    float candn[kMaxCandidates];             // |candidate| (fp32, rounded up)
+    float candf[kMaxCandidates][32];         // -2 * candidate (fp32) for the screen
+    float candn[kMaxCandidates];             // |candidate|^2 (fp32)
     double wsum[kStepWarps][kMaxCandidates];
     double werr[kStepWarps][kMaxCandidates];
     double wtot[kStepWarps];
-    long long whit[kStepWarps][kMaxCandidates];
+    uint32_t whit[kStepWarps][kMaxCandidates];
+    double units[kMaxK][kMaxCandidates];     // K-means++ draws of every slot (unit interval)
     float cmax;
     int32_t wcnt[kStepWarps][kMaxK];  // per-warp label counts (counting sort)
     int32_t woff[kStepWarps][kMaxK];  // sorted-order offset of (warp, label)
     int32_t cstart[kMaxK + 1];        // sorted-order start of each cluster
     int32_t decision;  // 0 continue, 1 done
+    int32_t exact_passes;  // K-means++ slots that needed the exact cost pass (diagnostic)
+    int32_t exact_rows;    // rows given an exact distance in the D^2 updates (diagnostic)
+    int32_t exact_rows1;   // ... in the first K-means++ slot's update (diagnostic)
     int32_t err;
 };
 
@@ -272,18 +280,39 @@ HPCG_DEV void load_row_f32(const T* samp, int row, float2 (&x2)[Geo<T, NP>::NPF 
     }
 }
 
-// fp32 direct-form squared distance to a point stored negated as fp32 pairs (FADD2+FFMA2).
-// |result - exact| <= kScreenK * (|x| + |c|)^2 with kScreenK below (covers fp64 inputs
-// rounded to fp32, the per-term rounding and the pair sums).
+// K-means++ screens, expanded form: dist ~ s + x.(-2c), s = |x|^2 + |c|^2, with the seed
+// (s, or s minus the bound) folded into the first chain; two rows per call, four independent
+// FFMA2 chains. |screen - exact| <= kScreenK (|x| + |c|)^2 <= 2 kScreenK s (the fp32 rounding
+// of x.c, of s and of c, and the chain sums are inside kScreenK's slack).
 template <int NPF>
-HPCG_DEV float screen_dist(const float2 (&x2)[NPF / 2], const float* negc) {
-    float2 acc = make_float2(0.f, 0.f);
+HPCG_DEV void screen_exp2(const float2 (&xa)[NPF / 2], const float2 (&xb)[NPF / 2], const float2* m2c, float sa,
+                          float sb, float& da, float& db) {
+    float2 a0 = make_float2(sa, 0.f), a1 = make_float2(0.f, 0.f), b0 = make_float2(sb, 0.f), b1 = a1;
 #pragma unroll
     for (int q = 0; q < NPF / 2; ++q) {
-        const float2 df = __fadd2_rn(x2[q], *reinterpret_cast<const float2*>(negc + 2 * q));
-        acc = __ffma2_rn(df, df, acc);
+        const float2 c = m2c[q];
+        if (q & 1) {
+            a1 = __ffma2_rn(xa[q], c, a1);
+            b1 = __ffma2_rn(xb[q], c, b1);
+        } else {
+            a0 = __ffma2_rn(xa[q], c, a0);
+            b0 = __ffma2_rn(xb[q], c, b0);
+        }
     }
-    return acc.x + acc.y;
+    da = (a0.x + a1.x) + (a0.y + a1.y);
+    db = (b0.x + b1.x) + (b0.y + b1.y);
+}
+template <int NPF>
+HPCG_DEV float screen_exp1(const float2 (&x)[NPF / 2], const float2* m2c, float sx) {
+    float2 a0 = make_float2(sx, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NPF / 2; ++q) {
+        if (q & 1)
+            a1 = __ffma2_rn(x[q], m2c[q], a1);
+        else
+            a0 = __ffma2_rn(x[q], m2c[q], a0);
+    }
+    return (a0.x + a1.x) + (a0.y + a1.y);
 }
 
 // Row `row` of the smem sample in its storage type (vector loads through the swizzle).
@@ -356,7 +385,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         if (trace && tid == 0 && tslot < kTraceSlots) trace[tslot] = gtimer();
         ++tslot;
     };
+    // fixed-slot diagnostic stamp (slots 16..25), warp 0's view
+    auto stamp = [&](int slot) {  // SM clock (cycles): finer than %globaltimer's 256 ns
+        if (trace && tid == 0) trace[slot] = clock64();
+    };
     mark();  // 0: start
+    if (trace && tid == 0) trace[kTraceSlots - 6] = clock64();  // SM clock rate check
     const SmemLayout L = step_layout<T, NP>(p.rows_cap, k, p.candidates, C);
     T* samp = reinterpret_cast<T*>(smem + L.samp);
     double* Cm = reinterpret_cast<double*>(smem + L.cm);
@@ -428,72 +462,93 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
     // ---------------------------------------------------------------- gather
     {
         const T* X = static_cast<const T*>(p.X);
-        FeistelPRP prp;
-        if (p.sample_mode == 1) prp = FeistelPRP::make(p.key, p.round, (uint32_t)(p.worker_base + wl), (uint64_t)p.m);
+        // initial centroids and flags: loads issued first so their latency hides under the gather
+        const int64_t v = p.shared_version ? *p.shared_version : 1;
+        const double* ic = p.init_c + (int64_t)wl * p.init_stride;
+        const uint8_t* ifl = p.init_f + (int64_t)wl * p.initf_stride;
+        constexpr int kIC = (kMaxK * 32 + kStepThreads - 1) / kStepThreads;
+        double icv[kIC];
+#pragma unroll
+        for (int u = 0; u < kIC; ++u) {
+            const int e = tid + u * kStepThreads, j = e / NP, d = e - j * NP;
+            icv[u] = (e < k * NP && d < n) ? ic[(int64_t)j * n + d] : 0.0;
+        }
+        const uint8_t fl0 = tid < k ? ifl[tid] : (uint8_t)1;
+        SamplePRP prp;
+        if (p.sample_mode == 1)
+            prp = SamplePRP::make(p.key, p.round, (uint32_t)(p.worker_base + wl), (uint64_t)p.m, p.prp_a, p.prp_b,
+                                  p.prp_inv_b);
         auto gidx_of = [&](int64_t i) -> int64_t {
             if (p.sample_mode == 0) return p.idx[(int64_t)wl * s + i];
             if (p.sample_mode == 1) return (int64_t)prp((uint64_t)i);
             return (int64_t)wl * s + i;
         };
-        // (a) one sample index per row into smem; (b) every copy is issued before any is
-        // awaited (cp.async, no register staging) so the CTA's whole chunk is in flight at once
-        int64_t* gx = reinterpret_cast<int64_t*>(smem + L.gidx);
-        for (int li = tid; li < nr; li += kStepThreads) gx[li] = gidx_of(r0 + li);
-        __syncthreads();
+        if (p.trace_mode == 0) stamp(16);
         const int rowb = n * (int)sizeof(T);
-        if (G::VEC16 && n == NP) {  // whole rows of 16-B chunks; consecutive lanes take consecutive
-            // chunks of the same row so each warp instruction touches few distinct lines
-            constexpr int EPC = 16 / (int)sizeof(T);
-            for (int e = tid; e < nr * G::CPR; e += kStepThreads) {
-                const int li = e / G::CPR, q = e % G::CPR;
-                cp_async16(samp + G::elem_off(li, q * EPC), X + gx[li] * NP + q * EPC);
-            }
-        } else if ((rowb & 15) == 0) {  // 16-B chunks
-            const int cpr = rowb >> 4;
-            constexpr int EPC = 16 / (int)sizeof(T);
-            for (int e = tid; e < nr * cpr; e += kStepThreads) {
-                const int li = e / cpr, q = e - li * cpr;
-                cp_async16(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
-            }
-        } else if ((rowb & 7) == 0) {  // 8-B chunks
-            const int cpr = rowb >> 3;
-            constexpr int EPC = 8 / (int)sizeof(T);
-            for (int e = tid; e < nr * cpr; e += kStepThreads) {
-                const int li = e / cpr, q = e - li * cpr;
-                cp_async8(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
-            }
-        } else {  // 4-B elements (fp32, odd n)
-            for (int e = tid; e < nr * n; e += kStepThreads) {
-                const int li = e / n, d = e - li * n;
-                cp_async4(samp + G::elem_off(li, d), X + gx[li] * n + d);
+        if constexpr (G::VEC16 && 32 % G::CPR == 0) {
+            if (n == NP) {  // whole rows of 16-B chunks. Per warp step: every lane computes one
+                // row's index, then the warp copies those 32 rows chunk-major (CPR consecutive
+                // lanes per row) with the indices shuffled across: no index buffer, no barrier,
+                // and the next indices are computed while these copies are in flight
+                constexpr int EPC = 16 / (int)sizeof(T), RPI = 32 / G::CPR;
+                const int q = lane % G::CPR;
+                for (int g = warp; g * 32 < nr; g += kStepWarps) {
+                    const int li = g * 32 + lane;
+                    const int64_t gi = li < nr ? gidx_of(r0 + li) : 0;
+#pragma unroll
+                    for (int j = 0; j < G::CPR; ++j) {
+                        const int rl = j * RPI + lane / G::CPR, row = g * 32 + rl;
+                        const int64_t src = __shfl_sync(0xffffffffu, gi, rl);
+                        if (row < nr) cp_async16(samp + G::elem_off(row, q * EPC), X + src * NP + q * EPC);
+                    }
+                }
             }
         }
+        if (!(G::VEC16 && 32 % G::CPR == 0 && n == NP)) {
+            // general rows: one sample index per row into smem, then the copies
+            int64_t* gx = reinterpret_cast<int64_t*>(smem + L.gidx);
+            for (int li = tid; li < nr; li += kStepThreads) gx[li] = gidx_of(r0 + li);
+            __syncthreads();
+            if ((rowb & 15) == 0) {  // 16-B chunks
+                const int cpr = rowb >> 4;
+                constexpr int EPC = 16 / (int)sizeof(T);
+                for (int e = tid; e < nr * cpr; e += kStepThreads) {
+                    const int li = e / cpr, q = e - li * cpr;
+                    cp_async16(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
+                }
+            } else if ((rowb & 7) == 0) {  // 8-B chunks
+                const int cpr = rowb >> 3;
+                constexpr int EPC = 8 / (int)sizeof(T);
+                for (int e = tid; e < nr * cpr; e += kStepThreads) {
+                    const int li = e / cpr, q = e - li * cpr;
+                    cp_async8(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
+                }
+            } else {  // 4-B elements (fp32, odd n)
+                for (int e = tid; e < nr * n; e += kStepThreads) {
+                    const int li = e / n, d = e - li * n;
+                    cp_async4(samp + G::elem_off(li, d), X + gx[li] * n + d);
+                }
+            }
+        }
+        if (p.trace_mode == 0) stamp(17);
         if (NP > n)
             for (int e = tid; e < nr * (NP - n); e += kStepThreads) {
                 const int li = e / (NP - n), d = n + (e - li * (NP - n));
                 samp[G::elem_off(li, d)] = T(0);
             }
-        // initial centroids (fp64 master, zero padded) and flags
-        const int64_t v = p.shared_version ? *p.shared_version : 1;
-        const double* ic = p.init_c + (int64_t)wl * p.init_stride;
-        const uint8_t* ifl = p.init_f + (int64_t)wl * p.initf_stride;
-        for (int e = tid; e < k * NP; e += kStepThreads) {
-            const int j = e / NP, d = e - j * NP;
-            Cm[e] = (d < n && v != 0) ? ic[(int64_t)j * n + d] : 0.0;
+        // initial centroids (fp64 master, zero padded) and flags; a zero shared version means
+        // no incumbent yet: every slot pending
+#pragma unroll
+        for (int u = 0; u < kIC; ++u) {
+            const int e = tid + u * kStepThreads;
+            if (e < k * NP) Cm[e] = v != 0 ? icv[u] : 0.0;
         }
-        if (tid < k) sh.flags[tid] = v != 0 ? ifl[tid] : (uint8_t)1;
+        if (tid < k) sh.flags[tid] = v != 0 ? fl0 : (uint8_t)1;
         if (tid == 0) {
             sh.err = kErrNone;
-            int np_ = 0, nv = 0;
-            for (int j = 0; j < k; ++j) {
-                const uint8_t f = v != 0 ? ifl[j] : (uint8_t)1;
-                if (f)
-                    sh.pending[np_++] = j;
-                else
-                    ++nv;
-            }
-            sh.n_pending = np_;
-            sh.n_valid = nv;
+            sh.exact_passes = 0;
+            sh.exact_rows = 0;
+            sh.exact_rows1 = 0;
         }
     }
     if (tid == 0) {
@@ -503,11 +558,24 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             mbar_init(&sh.rbar1[q], 1);
             mbar_init(&sh.rbar2[q], 1);
         }
+        mbar_init(&sh.cbar, 1);
         mbar_init_fence();
     }
+    if (p.trace_mode == 0) stamp(18);
     mark();  // 1: copies issued
     cp_async_wait_all();
     __syncthreads();  // gx (aliases d2) fully consumed before seeding reuses the region
+    if (tid == 0) {   // pending slots in slot order
+        int np_ = 0, nv = 0;
+        for (int j = 0; j < k; ++j) {
+            if (sh.flags[j])
+                sh.pending[np_++] = j;
+            else
+                ++nv;
+        }
+        sh.n_pending = np_;
+        sh.n_valid = nv;
+    }
     mark();  // 2: sample landed
     cluster.sync();  // sample rows of every CTA now visible cluster-wide (DSMEM)
     mark();  // 3: cluster synced
@@ -521,65 +589,45 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
     if (sh.n_pending > 0) {
         const int np_ = sh.n_pending;
         const int ncand = p.candidates;
-        float* xnorm = reinterpret_cast<float*>(smem + L.xnorm);
+        float* xsq = reinterpret_cast<float*>(smem + L.xnorm);  // |x|^2 (fp32) per local row
         uint32_t* wlist = reinterpret_cast<uint32_t*>(smem + L.wlist) + warp * list_cap(ncand);
-        constexpr float kScreenK = 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
+        uint8_t* nflag = smem + L.nflag;  // bit c: the cost screen could not settle (row, candidate c)
+        // screen bound B = kScreenK2 * s (see screen_exp2); s itself is rounded, hence the 1.001
+        constexpr float kScreenK2 = 2.002f * 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
+        constexpr float kScreenTiny = 1e-42f;  // absolute slack: fp32 denormal rounding
+        constexpr float kD2Round = 2.5e-7f;     // |ru(d2) - d2| <= 2^-23 d2, plus one fp32 subtraction
+        constexpr float kOneK2 = 1.0f - kScreenK2;  // screen - bound = (1 - K2) s + x.(-2c) - tiny
         for (int li = tid; li < nr; li += kStepThreads) {
             d2[li] = __longlong_as_double(0x7ff0000000000000LL);
             float2 x2[G::NPF / 2];
             load_row_f32<T, NP>(samp, li, x2);
-            float nn = 0.f;
+            float2 nn = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int q = 0; q < G::NPF / 2; ++q) nn = fmaf(x2[q].x, x2[q].x, fmaf(x2[q].y, x2[q].y, nn));
-            xnorm[li] = sqrtf(nn) * 1.0001f;
+            for (int q = 0; q < G::NPF / 2; ++q) nn = __ffma2_rn(x2[q], x2[q], nn);
+            xsq[li] = nn.x + nn.y;
         }
-        // fp32 screen record of slot c of sh.cand (negated copy + norm); caller syncs
+        // fp32 screen record of slot c of sh.cand (-2c and |c|^2); one warp, caller syncs
         auto make_candf = [&](int c) {
-            for (int d = lane; d < G::NPF; d += 32) sh.candf[c][d] = d < n ? -(float)sh.cand[c][d] : 0.f;
-            if (lane == 0) {
-                double nn = 0.0;
-                for (int d = 0; d < n; ++d) nn += sh.cand[c][d] * sh.cand[c][d];
-                sh.candn[c] = (float)sqrt(nn) * 1.0001f;
-            }
+            const float cf = lane < n ? (float)sh.cand[c][lane] : 0.f;
+            if (lane < G::NPF) sh.candf[c][lane] = -2.f * cf;
+            const float cc = warp_sum_f(cf * cf);
+            if (lane == 0) sh.candn[c] = cc;
         };
         // d2 = min(d2, dist(., cand c)) for every local row (seeding.hpp:20-42); the exact
         // reference distance is evaluated only where the fp32 screen cannot prove
         // dist >= d2, and those rows are compacted so the fp64 work runs on full warps.
         auto d2_update = [&](int c) {
             int cnt = 0;
-            float2 nc2[G::NPF / 2];  // candidate screen record and coordinates held in registers
-            double cd[NP];
+            float2 nc2[G::NPF / 2];  // candidate screen record held in registers
 #pragma unroll
             for (int q = 0; q < G::NPF / 2; ++q) nc2[q] = *reinterpret_cast<const float2*>(&sh.candf[c][2 * q]);
-#pragma unroll
-            for (int d = 0; d < NP; ++d) cd[d] = sh.cand[c][d];
-            const float cnrm = sh.candn[c];
-            const int nchunks = (nr + 31) / 32;
-            for (int ch = warp; ch < nchunks + kStepWarps; ch += kStepWarps) {
-                if (ch < nchunks) {
-                    const int row = ch * 32 + lane;
-                    bool need = false;
-                    if (row < nr) {
-                        float2 x2[G::NPF / 2];
-                        load_row_f32<T, NP>(samp, row, x2);
-                        float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                        for (int q = 0; q < G::NPF / 2; ++q) {
-                            const float2 df2 = __fadd2_rn(x2[q], nc2[q]);
-                            acc = __ffma2_rn(df2, df2, acc);
-                        }
-                        const float df = acc.x + acc.y;
-                        const float sc = xnorm[row] + cnrm;
-                        need = !(df - kScreenK * sc * sc > __double2float_ru(d2[row]));  // ru: conservative
-                    }
-                    const unsigned msk = __ballot_sync(0xffffffffu, need);
-                    if (need) wlist[cnt + __popc(msk & ((1u << lane) - 1u))] = (uint32_t)row;
-                    cnt += __popc(msk);
-                    __syncwarp();
-                }
-                const bool last = ch >= nchunks;
-                while (cnt >= 32 || (last && cnt > 0)) {
+            const double* cd = sh.cand[c];
+            const float cnp = fmaf(sh.candn[c], kOneK2, -kScreenTiny);
+            // exact distances for the listed rows, 32 at a time (the warp owns its rows' d2)
+            auto flush = [&](bool all) {
+                while (cnt >= 32 || (all && cnt > 0)) {
                     const int take = cnt < 32 ? cnt : 32;
+                    if (trace && lane == 0) atomicAdd(&sh.exact_rows, take);
                     if (lane < take) {
                         const int r = (int)wlist[lane];
                         T xr[NP];
@@ -591,8 +639,66 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     __syncwarp();
                     cnt -= take;
                 }
-                if (last) break;
+            };
+            const int nchunks = (nr + 31) / 32;
+            const unsigned lt = (1u << lane) - 1u;
+            for (int ch = warp; ch < nchunks; ch += 2 * kStepWarps) {  // two rows per lane per step
+                const int ra = ch * 32 + lane, rb = ra + kStepWarps * 32;
+                const bool va = ra < nr, vb = rb < nr;
+                float2 xa[G::NPF / 2], xb[G::NPF / 2];
+                load_row_f32<T, NP>(samp, va ? ra : 0, xa);
+                load_row_f32<T, NP>(samp, vb ? rb : 0, xb);
+                float dfa, dfb;  // screen - bound
+                screen_exp2<G::NPF>(xa, xb, nc2, fmaf(va ? xsq[ra] : 0.f, kOneK2, cnp),
+                                    fmaf(vb ? xsq[rb] : 0.f, kOneK2, cnp), dfa, dfb);
+                const bool na = va && !(dfa > __double2float_ru(d2[ra]));
+                const bool nb = vb && !(dfb > __double2float_ru(d2[rb]));
+                const unsigned ma = __ballot_sync(0xffffffffu, na);
+                if (na) wlist[cnt + __popc(ma & lt)] = (uint32_t)ra;
+                cnt += __popc(ma);
+                const unsigned mb = __ballot_sync(0xffffffffu, nb);
+                if (nb) wlist[cnt + __popc(mb & lt)] = (uint32_t)rb;
+                cnt += __popc(mb);
+                __syncwarp();
+                flush(false);
             }
+            flush(true);
+        };
+        // the same update for the winning candidate of a K-means++ slot: the cost pass already
+        // screened every row against it, so only its flagged rows get an exact distance
+        auto d2_update_flagged = [&](int c, bool tr) {
+            int cnt = 0;
+            const double* cd = sh.cand[c];
+            auto flush = [&](bool all) {
+                while (cnt >= 32 || (all && cnt > 0)) {
+                    const int take = cnt < 32 ? cnt : 32;
+                    if (tr && lane == 0) atomicAdd(&sh.exact_rows1, take);
+                    if (lane < take) {
+                        const int r = (int)wlist[lane];
+                        T xr[NP];
+                        load_row_T<T, NP>(samp, r, xr);
+                        d2[r] = fmin(d2[r], exact_dist_regs<T, NP>(xr, cd));
+                    }
+                    __syncwarp();
+                    for (int t = lane; t + take < cnt; t += 32) wlist[t] = wlist[t + take];
+                    __syncwarp();
+                    cnt -= take;
+                }
+            };
+            const int nchunks = (nr + 31) / 32;
+            const unsigned lt = (1u << lane) - 1u;
+            for (int ch = warp; ch < nchunks; ch += kStepWarps) {
+                const int r = ch * 32 + lane;
+                const bool nd_ = r < nr && ((nflag[r] >> c) & 1u);
+                const unsigned m = __ballot_sync(0xffffffffu, nd_);
+                if (nd_) wlist[cnt + __popc(m & lt)] = (uint32_t)r;
+                cnt += __popc(m);
+                __syncwarp();
+                flush(false);
+            }
+            if (tr) stamp(22);
+            flush(true);
+            if (tr) stamp(23);
         };
         __syncthreads();
         // valid centres in slot order (seeding.hpp:60-68)
@@ -610,17 +716,19 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         }
         // fetch a sample row (global sample position) from its owner CTA into dst[n]
         auto fetch_row = [&](int64_t row, double* dst) {
-            // owner rank: invert chunk_range
-            const int64_t base = s / C, extra = s % C;
-            int owner;
-            if (row < extra * (base + 1))
-                owner = (int)(row / (base + 1));
-            else
-                owner = (int)(extra + (row - extra * (base + 1)) / (base > 0 ? base : 1));
-            int64_t ob, oe;
-            chunk_range(s, C, owner, ob, oe);
+            // owner rank: invert chunk_range (the whole sample is cluster-resident: 32-bit)
+            const int si = (int)s, r32 = (int)row;
+            const int base = si / C, extra = si - base * C;
+            int owner, lr;
+            if (r32 < extra * (base + 1)) {
+                owner = r32 / (base + 1);
+                lr = r32 - owner * (base + 1);
+            } else {
+                const int q = r32 - extra * (base + 1);
+                owner = extra + q / base;  // base > 0 here: rows past the extras exist only then
+                lr = q - (owner - extra) * base;
+            }
             const T* rs = cluster.map_shared_rank(samp, owner);
-            const int lr = (int)(row - ob);
             for (int d = lane; d < 32; d += 32) dst[d] = d < n ? (double)rs[G::elem_off(lr, d)] : 0.0;
         };
         int next = 0;
@@ -649,7 +757,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         const int seg = (nr + kStepThreads - 1) / kStepThreads;
         const int sb = tid * seg < nr ? tid * seg : nr;
         const int se = sb + seg < nr ? sb + seg : nr;
+        // every slot's K-means++ draws up front, one per thread (read after the CDF's barriers)
+        for (int e = tid; e < (np_ - next) * ncand; e += kStepThreads) {
+            const int it_ = e / ncand, c = e - it_ * ncand;
+            sh.units[it_][c] = p.seed_mode == 0 ? p.units[(int64_t)wl * p.units_stride + (int64_t)it_ * ncand + c]
+                                                : philox_unit(p.key, p.round, (uint32_t)(p.worker_base + wl),
+                                                              (uint32_t)(0x10000 + (next + it_) * kMaxCandidates + c));
+        }
         int it = 0;
+        uint32_t cph = 0u;  // sh.cbar phase
         for (; next < np_; ++next, ++it) {
             // (1) segment sums, block exclusive scan (fixed tree), CTA total
             double tsum = 0.0;
@@ -702,18 +818,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             if (!(total > 0.0)) break;  // distinct rows exhausted (seeding.hpp:87)
             // (2) candidate draws u_c = unit * total; first global row with cum > u_c
             double u[kMaxCandidates];
-            long long hit[kMaxCandidates];
+            uint32_t hit[kMaxCandidates];  // local row of the first crossing (0xffffffff: none)
 #pragma unroll
             for (int c = 0; c < kMaxCandidates; ++c) {
-                hit[c] = LLONG_MAX;
-                u[c] = 0.0;
-                if (c < ncand) {
-                    const double unit = p.seed_mode == 0
-                                            ? p.units[(int64_t)wl * p.units_stride + (int64_t)it * ncand + c]
-                                            : philox_unit(p.key, p.round, (uint32_t)(p.worker_base + wl),
-                                                          (uint32_t)(0x10000 + next * kMaxCandidates + c));
-                    u[c] = unit * total;
-                }
+                hit[c] = 0xffffffffu;
+                u[c] = c < ncand ? sh.units[it][c] * total : 0.0;
             }
             bool any = false;
             if (sb < se) {  // cum is non-decreasing along a segment: scan only where a draw crosses it
@@ -722,7 +831,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 for (int c = 0; c < kMaxCandidates; ++c) {
                     if (c >= ncand) break;
                     if (seg_lo > u[c])
-                        hit[c] = r0 + sb;
+                        hit[c] = (uint32_t)sb;
                     else
                         any |= seg_hi > u[c];
                 }
@@ -734,84 +843,132 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     const double cum = P + (texcl + run);
 #pragma unroll
                     for (int c = 0; c < kMaxCandidates; ++c)
-                        if (c < ncand && hit[c] == LLONG_MAX && cum > u[c]) hit[c] = r0 + li;
+                        if (c < ncand && hit[c] == 0xffffffffu && cum > u[c]) hit[c] = (uint32_t)li;
                 }
             }
 #pragma unroll
             for (int c = 0; c < kMaxCandidates; ++c) {
                 if (c >= ncand) break;
-                long long h = hit[c];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) h = min(h, __shfl_xor_sync(0xffffffffu, h, o));
+                const uint32_t h = __reduce_min_sync(0xffffffffu, hit[c]);
                 if (lane == 0) sh.whit[warp][c] = h;
             }
             __syncthreads();
             if (it == 0 && p.trace_mode == 1) mark();  // 7: search done
-            const double* rxh = exchange(ncand, [&](int c) {
-                long long h = LLONG_MAX;
-                for (int w2 = 0; w2 < kStepWarps; ++w2) h = min(h, sh.whit[w2][c]);
-                return __longlong_as_double(h);
-            });
-            if (it == 0 && p.trace_mode == 1) mark();  // 8: hit exchange complete
-            // every CTA: global first hit per candidate (rank order == row order)
+            // cum is monotone across the cluster and P equals the previous rank's last cum
+            // exactly, so exactly one CTA holds the first global row with cum > u_c: the CTA with a
+            // local crossing and P <= u_c (rank 0: P = 0); if no row crosses, rank C-1 takes the
+            // fallback row s - 1 (rng.hpp:87-92). That CTA pushes the row's coordinates straight
+            // into every CTA's candidate slot c (st.async + mbarrier): draw and fetch in one step.
+            if (tid == 0) mbar_expect_tx(&sh.cbar, (uint32_t)(ncand * NP * 8));
             for (int c = warp; c < ncand; c += kStepWarps) {
-                long long h = lane < C ? __double_as_longlong(rxh[lane * xs + c]) : LLONG_MAX;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) h = min(h, __shfl_xor_sync(0xffffffffu, h, o));
-                const int64_t row = h == LLONG_MAX ? s - 1 : (int64_t)h;  // rng.hpp:87-92 fallback
-                fetch_row(row, sh.cand[c]);
-                __syncwarp();
-                make_candf(c);
+                const uint32_t h = __reduce_min_sync(0xffffffffu, lane < kStepWarps ? sh.whit[lane][c] : 0xffffffffu);
+                const double uc = sh.units[it][c] * total;
+                int own = -1;
+                if (h != 0xffffffffu && (cr == 0 || !(P > uc)))
+                    own = (int)h;
+                else if (cr == C - 1 && !(total > uc))
+                    own = nr - 1;
+                if (own >= 0) {
+                    const uint32_t dst = smem_u32(&sh.cand[c][0]), bar = smem_u32(&sh.cbar);
+                    for (int d = lane; d < NP; d += 32) {
+                        const double v = d < n ? (double)samp[G::elem_off(own, d)] : 0.0;
+                        for (int rr = 0; rr < C; ++rr) st_async_f64(mapa_u32(dst + d * 8, rr), v, mapa_u32(bar, rr));
+                    }
+                }
             }
+            mbar_wait_cluster(&sh.cbar, cph);
+            cph ^= 1u;
+            if (it == 0 && p.trace_mode == 1) mark();  // 8: candidates received
+            for (int c = warp; c < ncand; c += kStepWarps) make_candf(c);
             __syncthreads();
             if (it == 0 && p.trace_mode == 1) mark();  // 9: candidates fetched
+            if (it == 0 && p.trace_mode == 1) stamp(16);
             // (3) candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93). First from
             // the fp32 screen with a rigorous per-row error budget; only if two candidates are
             // within their budgets (or tie) are the costs recomputed with exact distances.
-            int best = 0;
-            for (int exact_pass = 0; exact_pass < 2; ++exact_pass) {
-                double cost[kMaxCandidates], err[kMaxCandidates];
+            // (a) approximate pass, templated on the candidate count so the candidates' screen
+            //     chains interleave. Per row and candidate: dfB = screen - B (one FFMA2 chain
+            //     seeded with (1 - K2) s - tiny), the cost reduction d' = max(ru(d2) - dfB, 0),
+            //     and for the rows the screen cannot settle (dfB <= ru(d2)) the error terms. The
+            //     local cost is T - sum d' + [0, E], E = sum (2B + kD2Round ru(d2)); T, the CTA's
+            //     CDF total, is common to all candidates, so only sum d' and E are exchanged.
+            auto approx_costs = [&](auto ncc) {
+                constexpr int NC = decltype(ncc)::value;
+                float red[NC], efx[NC], eff[NC], cnp[NC];
+                int efn[NC];
 #pragma unroll
-                for (int c = 0; c < kMaxCandidates; ++c) cost[c] = err[c] = 0.0;
-                int cnt = 0;
-                const int nchunks = (nr + 31) / 32;
-                for (int ch = warp; ch < nchunks + kStepWarps; ch += kStepWarps) {
-                    if (ch < nchunks) {
-                        const int row = ch * 32 + lane;
-                        const bool valid = row < nr;
-                        float2 x2[G::NPF / 2];
-                        double d2i = 0.0;
-                        float xnr = 0.f;
-                        if (valid) {
-                            load_row_f32<T, NP>(samp, row, x2);
-                            d2i = d2[row];
-                            xnr = xnorm[row];
-                        }
+                for (int c = 0; c < NC; ++c) {
+                    red[c] = efx[c] = eff[c] = 0.f;
+                    efn[c] = 0;
+                    cnp[c] = fmaf(sh.candn[c], kOneK2, -kScreenTiny);
+                }
+                auto rows = [&](auto rr, int rbase) {  // rows rbase + i * kStepThreads, i < R
+                    constexpr int R = decltype(rr)::value;
+                    float2 x[R][G::NPF / 2];
+                    float f[R], xq[R];
 #pragma unroll
-                        for (int c = 0; c < kMaxCandidates; ++c) {
-                            if (c >= ncand) break;
-                            bool need = false;
-                            if (valid) {
-                                const float df = screen_dist<G::NPF>(x2, sh.candf[c]);
-                                const float sc = xnr + sh.candn[c];
-                                const float B = kScreenK * sc * sc;
-                                need = !(df - B > __double2float_ru(d2i));
-                                if (!need) {
-                                    cost[c] += d2i;
-                                } else if (!exact_pass) {
-                                    cost[c] += fmin(d2i, (double)df);
-                                    err[c] += (double)B;
-                                    need = false;
-                                }
-                            }
-                            const unsigned msk = __ballot_sync(0xffffffffu, need);
-                            if (need) wlist[cnt + __popc(msk & ((1u << lane) - 1u))] = (uint32_t)row | ((uint32_t)c << 16);
-                            cnt += __popc(msk);
-                        }
-                        __syncwarp();
+                    for (int i = 0; i < R; ++i) {
+                        const int r = rbase + i * kStepThreads;
+                        const bool v = r < nr;
+                        load_row_f32<T, NP>(samp, v ? r : 0, x[i]);
+                        f[i] = v ? __double2float_ru(d2[r]) : 0.f;
+                        xq[i] = v ? xsq[r] : __int_as_float(0x7f800000);  // invalid rows: dfB = inf
                     }
-                    const bool last = ch >= nchunks;
-                    while (cnt >= 32 || (last && cnt > 0)) {
+                    uint32_t fl[R];
+#pragma unroll
+                    for (int i = 0; i < R; ++i) fl[i] = 0u;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        const float2* m2c = reinterpret_cast<const float2*>(sh.candf[c]);
+#pragma unroll
+                        for (int i = 0; i < R; ++i) {
+                            float2 acc = make_float2(fmaf(xq[i], kOneK2, cnp[c]), 0.f);
+#pragma unroll
+                            for (int q = 0; q < G::NPF / 2; ++q) acc = __ffma2_rn(x[i][q], m2c[q], acc);
+                            const float dfB = acc.x + acc.y;
+                            red[c] += fmaxf(f[i] - dfB, 0.f);
+                            if (!(dfB > f[i])) {  // unsettled (NaN included: its error is NaN)
+                                efx[c] += xq[i];
+                                eff[c] += f[i];
+                                ++efn[c];
+                                fl[i] |= 1u << c;
+                            }
+                        }
+                    }
+                    // the flags are the D^2 update's work list for whichever candidate wins
+#pragma unroll
+                    for (int i = 0; i < R; ++i)
+                        if (rbase + i * kStepThreads < nr) nflag[rbase + i * kStepThreads] = (uint8_t)fl[i];
+                };
+                // two rows per thread per step while any lane of the warp has a second row
+                int r = tid;
+                for (; r - lane + kStepThreads < nr; r += 2 * kStepThreads) rows(IntC<2>{}, r);
+                if (it == 0 && p.trace_mode == 1) stamp(17);
+                if (r - lane < nr) rows(IntC<1>{}, r);
+                if (it == 0 && p.trace_mode == 1) stamp(18);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const float E = fmaf(2.f * kScreenK2, fmaf((float)efn[c], sh.candn[c], efx[c]),
+                                         fmaf(kD2Round, eff[c], 4e-42f * (float)efn[c]));
+                    // midpoint and half-width; the slack covers the fp32 lane and warp sums
+                    const float v = warp_sum_f(0.5f * E - red[c]);
+                    const float e = warp_sum_f(0.5005f * E + 1e-5f * red[c]);
+                    if (lane == 0) {
+                        sh.wsum[warp][c] = (double)v;
+                        sh.werr[warp][c] = (double)e;
+                    }
+                }
+                if (it == 0 && p.trace_mode == 1) stamp(19);
+            };
+            // (b) exact pass (only when (a) cannot separate the winner): exact distances for every
+            //     row the screen cannot settle, compacted into the warp's work list
+            auto exact_costs = [&]() {
+                double cost[kMaxCandidates];
+#pragma unroll
+                for (int c = 0; c < kMaxCandidates; ++c) cost[c] = 0.0;
+                int cnt = 0;
+                auto flush = [&](bool all) {
+                    while (cnt >= 32 || (all && cnt > 0)) {
                         const int take = cnt < 32 ? cnt : 32;
                         if (lane < take) {
                             const uint32_t e = wlist[lane];
@@ -828,63 +985,103 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                         __syncwarp();
                         cnt -= take;
                     }
-                    if (last) break;
+                };
+                const int nchunks = (nr + 31) / 32;
+                const unsigned lt = (1u << lane) - 1u;
+                for (int ch = warp; ch < nchunks; ch += kStepWarps) {
+                    const int row = ch * 32 + lane;
+                    const bool valid = row < nr;
+                    float2 x2[G::NPF / 2];
+                    load_row_f32<T, NP>(samp, valid ? row : 0, x2);
+                    const double d2i = valid ? d2[row] : 0.0;
+                    const float xq = valid ? xsq[row] : 0.f;
+#pragma unroll
+                    for (int c = 0; c < kMaxCandidates; ++c) {
+                        if (c >= ncand) break;
+                        const float sc = xq + sh.candn[c];
+                        const float df = screen_exp1<G::NPF>(x2, reinterpret_cast<const float2*>(sh.candf[c]), sc);
+                        const bool need = valid && !(df - fmaf(kScreenK2, sc, kScreenTiny) > __double2float_ru(d2i));
+                        if (valid && !need) cost[c] += d2i;
+                        const unsigned msk = __ballot_sync(0xffffffffu, need);
+                        if (need) wlist[cnt + __popc(msk & lt)] = (uint32_t)row | ((uint32_t)c << 16);
+                        cnt += __popc(msk);
+                    }
+                    __syncwarp();
+                    flush(false);
                 }
+                flush(true);
 #pragma unroll
                 for (int c = 0; c < kMaxCandidates; ++c) {
                     if (c >= ncand) break;
                     const double v = warp_sum(cost[c]);
-                    const double e = warp_sum(err[c]);
                     if (lane == 0) {
                         sh.wsum[warp][c] = v;
-                        sh.werr[warp][c] = e;
+                        sh.werr[warp][c] = 0.0;
                     }
                 }
+            };
+            // cluster totals in rank order; strict <, first candidate wins ties (seeding.hpp:94-98).
+            // Every CTA evaluates the same totals, so the decision is cluster-uniform.
+            int best = 0;
+            auto exchange_decide = [&](bool exact) -> bool {
                 __syncthreads();
-                if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 10: costs local done
                 const double* rxc = exchange(2 * ncand, [&](int e) {
-                    const int c = e % ncand;
+                    const int c = e < ncand ? e : e - ncand;
                     double v = 0.0;
                     for (int w2 = 0; w2 < kStepWarps; ++w2) v += e < ncand ? sh.wsum[w2][c] : sh.werr[w2][c];
                     return v;
                 });
-                if (it == 0 && p.trace_mode == 1 && !exact_pass) mark();  // 11: cost exchange complete
+                if (it == 0 && p.trace_mode == 1 && !exact) mark();  // 11: cost exchange complete
+                if (it == 0 && p.trace_mode == 1 && !exact) stamp(20);
+                // lane e < 2*ncand sums column e over ranks (rank order), then broadcast
+                double col = 0.0;
+                if (lane < 2 * ncand)
+                    for (int rr = 0; rr < C; ++rr) col += rxc[rr * xs + lane];
                 double tc[kMaxCandidates], te[kMaxCandidates];
                 double bc = __longlong_as_double(0x7ff0000000000000LL), be = 0.0;
                 best = 0;
 #pragma unroll
                 for (int c = 0; c < kMaxCandidates; ++c) {
-                    tc[c] = 0.0;
-                    te[c] = 0.0;
+                    tc[c] = (exact ? 0.0 : total) + __shfl_sync(0xffffffffu, col, c);
+                    te[c] = __shfl_sync(0xffffffffu, col, (ncand + c) & 31);
                     if (c >= ncand) continue;
-                    for (int rr = 0; rr < C; ++rr) {
-                        tc[c] += rxc[rr * xs + c];
-                        te[c] += rxc[rr * xs + ncand + c];
-                    }
                     te[c] += 1e-9 * fabs(tc[c]);  // summation-order slack
-                    if (tc[c] < bc) {  // strict <, first candidate wins ties (seeding.hpp:94-98)
+                    if (tc[c] < bc) {
                         bc = tc[c];
                         be = te[c];
                         best = c;
                     }
                 }
                 bool decided = true;
-                if (!exact_pass)
+                if (!exact)
 #pragma unroll
                     for (int c = 0; c < kMaxCandidates; ++c)
                         if (c < ncand && c != best && !(tc[c] - te[c] > bc + be)) decided = false;
-                // every CTA evaluated the same totals: the decision is cluster-uniform
-                if (decided) break;
+                return decided;
+            };
+            switch (ncand) {
+                case 1: approx_costs(IntC<1>{}); break;
+                case 2: approx_costs(IntC<2>{}); break;
+                case 3: approx_costs(IntC<3>{}); break;
+                default: approx_costs(IntC<kMaxCandidates>{}); break;
+            }
+            if (it == 0 && p.trace_mode == 1) mark();  // 10: costs local done
+            if (!exchange_decide(false)) {
                 __syncthreads();  // all reads of this exchange precede the exact pass's pushes
+                if (tid == 0) ++sh.exact_passes;
+                exact_costs();
+                exchange_decide(true);
             }
             nd += (int64_t)ncand * s;
             const int j = sh.pending[next];
             for (int d = tid; d < NP; d += kStepThreads) Cm[j * NP + d] = d < n ? sh.cand[best][d] : 0.0;
             if (tid == 0) sh.flags[j] = 0;
-            d2_update(best);
+            if (it == 0 && p.trace_mode == 1) stamp(21);
+            d2_update_flagged(best, it == 0 && p.trace_mode == 1);
             ++filled;
             __syncthreads();
             if (it == 0 && p.trace_mode == 1) mark();  // 12: d2 updated (slot done)
+            if (it == 0 && p.trace_mode == 1) stamp(24);
         }
         __syncthreads();
     }
@@ -1270,7 +1467,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             }
         }
     }
-    if (trace && tid == 0) trace[kTraceSlots - 2] = gtimer();
+    if (trace && tid == 0) {
+        if (p.trace_mode == 1) {
+            trace[kTraceSlots - 3] = sh.exact_passes;
+            trace[kTraceSlots - 4] = sh.exact_rows;
+            trace[kTraceSlots - 7] = sh.exact_rows1;
+        }
+        trace[kTraceSlots - 5] = clock64();
+        trace[kTraceSlots - 2] = gtimer();
+    }
     cluster.sync();  // no CTA may exit while peers can still read its smem
     if (trace && tid == 0) trace[kTraceSlots - 1] = gtimer();
 }

@@ -234,3 +234,25 @@ def test_philox_engine_runs_and_is_deterministic():
     _, cost, _, _ = None, None, None, None
     lab, cnt, cost, nd = orc().assign(X.astype(np.float64), a.centroids, a.degenerate)
     assert rel(a.full_objective, cost) <= RTOL
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 97, 1000, 4096, 65537, 100003])
+def test_philox_sample_is_a_permutation(m):
+    # s = m: the device sample of a philox round is a permutation of [0, m) (distinct by
+    # construction: keyed Feistel bijection over Z_a x Z_b plus cycle walking)
+    for worker in (0, 7):
+        idx = hp.philox_sample_indices(m, m, key=0x1234567890ABCDEF, round_=3, worker=worker)
+        assert np.array_equal(np.sort(idx), np.arange(m))
+
+
+def test_philox_sample_distinct_in_range_and_keyed():
+    m, s = 10_000_000, 20000
+    a = hp.philox_sample_indices(m, s, key=5, round_=0, worker=0)
+    assert a.min() >= 0 and a.max() < m and len(np.unique(a)) == s
+    assert np.array_equal(a, hp.philox_sample_indices(m, s, key=5, round_=0, worker=0))
+    b = hp.philox_sample_indices(m, s, key=5, round_=0, worker=1)
+    c = hp.philox_sample_indices(m, s, key=5, round_=1, worker=0)
+    assert len(np.intersect1d(a, b)) < 200 and len(np.intersect1d(a, c)) < 200  # ~ s^2/m = 40 expected
+    # roughly uniform over [0, m): each decile holds ~s/10 rows
+    h = np.bincount(a * 10 // m, minlength=10)
+    assert h.min() > 0.8 * s / 10 and h.max() < 1.2 * s / 10
