@@ -192,7 +192,7 @@ struct StepShared {  // static smem: per-step scalars and exchange slots
     double wtot[kStepWarps];
     uint32_t whit[kStepWarps][kMaxCandidates];
     double units[kMaxK][kMaxCandidates];     // K-means++ draws of every slot (unit interval)
-    float cmax;
+    float cnorm[kMaxK];  // |c_j| (fp32, rounded up) of the current screen records
     int32_t wcnt[kStepWarps][kMaxK];  // per-warp label counts (counting sort)
     int32_t woff[kStepWarps][kMaxK];  // sorted-order offset of (warp, label)
     int32_t cstart[kMaxK + 1];        // sorted-order start of each cluster
@@ -1101,30 +1101,24 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         constexpr float kappa = 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
         bool closing = false;
         int pass = 0;
-        for (;; ++pass) {
-            // ---- screen prep: c' = -2c (fp32), cc = |c|^2, cmax
-            if (warp == 0) {  // k <= 32: one lane per centroid, max |c_j| by shuffle
-                float cm = 0.f;
-                if (lane < k) {
-                    float* rec = cs + lane * G::CSR;
-                    double cc = 0.0;
-                    for (int d = 0; d < NP; ++d) {
-                        const double c = Cm[lane * NP + d];
-                        cc += c * c;
-                        rec[d] = (float)(-2.0 * c);
-                    }
-                    for (int d = NP; d < G::NPF; ++d) rec[d] = 0.f;
-                    rec[G::NPF] = (float)cc;
-                    rec[G::NPF + 1] = 0.f;
-                    cm = sqrtf((float)cc) * 1.0001f;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
-                if (lane == 0) sh.cmax = cm;
+        // screen record of centroid j from its fp64 master value c (lane = dimension):
+        // c' = -2c (fp32), |c|^2 (fp32 sum of rounded squares), |c| rounded up into sh.cnorm
+        auto make_rec = [&](int j, double c) {
+            float* rec = cs + j * G::CSR;
+            if (lane < G::NPF) rec[lane] = lane < NP ? (float)(-2.0 * c) : 0.f;
+            const float cc = warp_sum_f(lane < NP ? (float)(c * c) : 0.f);
+            if (lane == 0) {
+                rec[G::NPF] = cc;
+                rec[G::NPF + 1] = 0.f;
+                sh.cnorm[j] = sqrtf(cc) * 1.0001f;
             }
-            __syncthreads();
-            const float cmax = sh.cmax;
-
+        };
+        for (int j = warp; j < k; j += kStepWarps) make_rec(j, lane < NP ? Cm[j * NP + lane] : 0.0);
+        __syncthreads();
+        for (;; ++pass) {
+            // max |c_j| over the centroids (records made by the previous means phase)
+            const float cmax =
+                __uint_as_float(__reduce_max_sync(0xffffffffu, lane < k ? __float_as_uint(sh.cnorm[lane]) : 0u));
             if (pass == 0 && p.trace_mode == 0) mark();  // 5: prep done
             // ---- assign: fp32 FFMA2 screen, exact fp64 recheck of near ties. Rows are dealt
             // to warps as 32-row chunks (chunk c -> warp c % NW) and each warp screens 4, 2 or 1
@@ -1373,28 +1367,23 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 break;
             }
             ++iters;
-            // means_from_sums (lloyd.hpp:75-89) + fixed-point test (lloyd.hpp:131)
+            // means_from_sums (lloyd.hpp:75-89) + fixed-point test (lloyd.hpp:131), one warp per
+            // centroid (lane = dimension; only that warp touches the centroid here), and the
+            // next pass's screen record from the new means
             bool same = true;
-            double nv[(kMaxK * 32 + kStepThreads - 1) / kStepThreads];
-            {
-                int q = 0;
-                for (int e = tid; e < k * NP; e += kStepThreads, ++q) {
-                    const int j = e / NP;
-                    const double cnt = tot[k * NP + j];
-                    double v = Cm[e];
-                    if (cnt > 0.0) {
-                        const double inv = 1.0 / cnt;
-                        v = tot[e] * inv;
-                    }
-                    nv[q] = v;
-                    same &= (v == Cm[e]);
+            for (int j = warp; j < k; j += kStepWarps) {
+                const double cnt = tot[k * NP + j];
+                const double old = lane < NP ? Cm[j * NP + lane] : 0.0;
+                double v = old;
+                if (lane < NP && cnt > 0.0) {
+                    const double inv = 1.0 / cnt;
+                    v = tot[j * NP + lane] * inv;
                 }
+                same &= (v == old);
+                if (lane < NP) Cm[j * NP + lane] = v;
+                make_rec(j, v);
             }
             const bool all_same = __syncthreads_and(same);
-            {
-                int q = 0;
-                for (int e = tid; e < k * NP; e += kStepThreads, ++q) Cm[e] = nv[q];
-            }
             if (all_same) {
                 stop = 2;  // fixed_point
                 f_final = f;
