@@ -1257,7 +1257,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             __syncthreads();
             for (int t = 0; t < nchw; ++t) {
                 const int row = (warp + kStepWarps * t) * 32 + lane;
-                if (row < nr) perm[sh.woff[warp][labels[row]] + pos[row]] = (uint16_t)row;
+                // VEC16 rows: the 16-B unit index of the row's chunk 0 with its swizzle folded in,
+                // (row * CPR + swz(row)); chunk q of the row is unit (entry ^ q)
+                if (row < nr)
+                    perm[sh.woff[warp][labels[row]] + pos[row]] =
+                        (uint16_t)(G::VEC16 ? row * G::CPR + G::swz(row) : row);
             }
             __syncthreads();
             if (pass == 0 && p.trace_mode == 0) mark();  // 7: sort done
@@ -1292,9 +1296,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                         const int d = q * U + u;
                         cj[u] = (active_unit && d < NP) ? Cm[j * NP + d] : 0.0;
                     }
-                    auto add_row = [&](int row) {
+                    const unsigned char* sbytes = reinterpret_cast<const unsigned char*>(samp);
+                    auto add_row = [&](int row) {  // row: perm entry (see the scatter above)
                         if constexpr (G::VEC16 && sizeof(T) == 4) {
-                            const float4 v = *reinterpret_cast<const float4*>(samp + G::elem_off(row, q * 4));
+                            const float4 v = *reinterpret_cast<const float4*>(sbytes + ((row ^ q) << 4));
                             const double xv[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
@@ -1303,7 +1308,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                                 accc[u] = fma(diff, diff, accc[u]);
                             }
                         } else if constexpr (G::VEC16) {
-                            const double2 v = *reinterpret_cast<const double2*>(samp + G::elem_off(row, q * 2));
+                            const double2 v = *reinterpret_cast<const double2*>(sbytes + ((row ^ q) << 4));
                             acc[0] += v.x;
                             acc[1] += v.y;
                             const double d0 = v.x - cj[0], d1 = v.y - cj[1];
@@ -1318,7 +1323,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     };
                     if (active_unit) {
                         int p0 = a + gi;
-#pragma unroll 2
+#pragma unroll 4
                         for (; p0 < b; p0 += RPS) add_row(wperm[p0]);
                     }
                     // fold the row groups (fixed tree): lanes gi == 0 hold the sums
