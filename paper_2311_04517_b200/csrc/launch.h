@@ -25,6 +25,13 @@ struct StepGeometry {
 cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeometry* geo_out, std::string* why);
 cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why);
 
+// Grid-wide worker step over samples materialised in HBM (wide.cu): any n, k (k*n <= kWideMaxKN),
+// any s. launch_step falls back to it when the cluster-resident kernel cannot hold the shape.
+constexpr int64_t kWideMaxKN = 24576;
+constexpr int kWideMaxN = 4096, kWideMaxK = 4096;
+cudaError_t launch_step_wide(int dtype, const StepParams& p, cudaStream_t st, std::string* why);
+cudaError_t launch_objective_wide(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st);
+
 // *nblocks: in = capacity of p.block_cost, out = grid used (fixed per device/kernel/kv)
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st);
 int objective_blocks();  // fixed grid for deterministic block partials

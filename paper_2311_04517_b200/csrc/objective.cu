@@ -27,9 +27,18 @@ int pick_np(int dtype, int n) {
 }
 
 cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeometry* g, std::string* why) {
+    // the cluster-resident kernel when the shape fits it (n <= 32, k <= 32, sample in a
+    // cluster's shared memory), the grid-wide HBM path otherwise
     const int np = pick_np(dtype, p.n);
-    if (np == 0) return cudaErrorInvalidValue;
-    return dtype == 0 ? launch_step_f32(p, st, g, why, np) : launch_step_f64(p, st, g, why, np);
+    static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
+    if (np != 0 && p.k <= kMaxK && p.candidates <= kMaxCandidates && !force_wide) {
+        StepGeometry tmp;
+        std::string w2;
+        if (step_geometry(dtype, p.n, p.s, p.k, p.candidates, p.W, &tmp, &w2) == cudaSuccess)
+            return dtype == 0 ? launch_step_f32(p, st, g, why, np) : launch_step_f64(p, st, g, why, np);
+    }
+    if (g) *g = StepGeometry{};
+    return launch_step_wide(dtype, p, st, why);
 }
 
 cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int ncand, int W, StepGeometry* g, std::string* why) {
@@ -123,6 +132,8 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
 
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {
     const int np = pick_np(dtype, p.n);
+    static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
+    if (np == 0 || p.kv > kObjMaxK || force_wide) return launch_objective_wide(dtype, p, nblocks, st);
     if (dtype == 0) {
         switch (np) {
             case 2: return launch_obj_t<float, 2>(p, nblocks, st);

@@ -212,9 +212,10 @@ size_t dsize(int dtype) { return dtype == HPCG_F32 ? 4 : 8; }
 
 int check_shape(int dtype, int64_t n, int64_t k) {
     if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
-    if (pick_np(dtype, (int)n) == 0 || n < 1)
-        return fail(HPCG_EUNSUPPORTED, "n > 32 features is not supported by this build's kernels");
-    if (k > kMaxK) return fail(HPCG_EUNSUPPORTED, "k > 32 centroids is not supported by this build's kernels");
+    if (n < 1) return fail(HPCG_EINVAL, "dataset needs at least one feature");
+    // n <= 32 and k <= 32 run cluster-resident; larger shapes take the grid-wide path (wide.cu)
+    if (n > kWideMaxN || k > kWideMaxK || n * k > kWideMaxKN)
+        return fail(HPCG_EUNSUPPORTED, "k * n beyond the grid-wide path's pass accumulator (24576)");
     return HPCG_OK;
 }
 
@@ -527,9 +528,7 @@ int hpcg_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_host, con
     }
     if (remap.empty()) return fail(HPCG_EINVAL, "assignment: every centroid is degenerate");
     const int kv = (int)remap.size();
-    if (kv > kObjMaxK) return fail(HPCG_EUNSUPPORTED, "more than 256 valid centroids");
-    if (pick_np(ds->dtype, (int)n) == 0)
-        return fail(HPCG_EUNSUPPORTED, "n > 32 features is not supported by this build's kernels");
+    if (int rc = check_shape(ds->dtype, n, kv)) return rc;
     CU(ctx->s_a.reserve(cv.size() * 8));
     CU(ctx->s_b.reserve(remap.size() * 4 + 16));
     CU(ctx->s_c.reserve(8));
@@ -567,9 +566,7 @@ int hpcg_assign_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_dev, 
     std::lock_guard<std::mutex> lk(ctx->mu);
     cudaSetDevice(ctx->device);
     if (k_valid < 1) return fail(HPCG_EINVAL, "assign: need at least one centroid");
-    if (k_valid > kObjMaxK) return fail(HPCG_EUNSUPPORTED, "more than 256 valid centroids");
-    if (pick_np(ds->dtype, (int)ds->n) == 0)
-        return fail(HPCG_EUNSUPPORTED, "n > 32 features is not supported by this build's kernels");
+    if (int rc = check_shape(ds->dtype, ds->n, k_valid)) return rc;
     if (ctx->s_b.bytes < (size_t)k_valid * 4) {
         std::vector<int32_t> remap((size_t)k_valid);
         for (int64_t j = 0; j < k_valid; ++j) remap[(size_t)j] = (int32_t)j;
@@ -1012,10 +1009,7 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     if (cfg.candidates < 1) return fail(HPCG_EINVAL, "seeding: need at least one candidate");
     if (cfg.candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 4 K-means++ candidates per centre");
     if (int rc = check_shape(ds->dtype, ds->n, cfg.k)) return rc;
-    StepGeometry g;
-    std::string why;
-    if (step_geometry(ds->dtype, (int)ds->n, cfg.sample_size, (int)cfg.k, (int)cfg.candidates, (int)cfg.n_workers, &g, &why) != cudaSuccess)
-        return fail(HPCG_EUNSUPPORTED, "worker step geometry: " + why);
+    // shapes without a cluster-resident geometry run on the grid-wide path (launch_step decides)
 
     auto* e = new hpcg_engine;
     e->ctx = ctx;

@@ -1,0 +1,748 @@
+// The HPClust worker step for shapes the cluster-resident kernel cannot hold: n > 32 features
+// (config 4: n = 128), k > 32 centres, or samples larger than a 16-CTA cluster's shared
+// memory. Same contract as worker_step_kernel (StepParams in, the same per-worker outputs,
+// acceptance and n_d accounting out), built from grid-wide kernels over samples materialised
+// in HBM:
+//
+//   gather     sample rows -> S[w][i][:]                     engine.hpp:165-177 (PRP indices)
+//   seeding    D^2 init, per pending slot: block CDF totals, draw, candidate costs, decision,
+//              D^2 update                                    seeding.hpp:47-105
+//   Lloyd      per pass: assign + per-CTA partial sums/counts/cost, fixed-order reduce, means,
+//              stop rules                                    lloyd.hpp:75-89, 100-164
+//   outputs    centroids, flags, objective, iterations, stop, n_d, keep-the-best (engine.hpp:254)
+//
+// Distances are the reference's own (core.hpp:100-108: fp64, ascending d, separately rounded
+// sub/mul/add), so labels and argmins are exact by construction. Every reduction is in a fixed
+// order (row blocks in order, CTAs in order), so results are deterministic.
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include "launch.h"
+
+namespace hpcg {
+namespace {
+
+constexpr int kWT = 256;           // threads per CTA
+constexpr int kSeedRows = 256;     // rows per seeding block (CDF and cost partials)
+constexpr int kJT = 8;             // centroids per distance tile (registers)
+
+// ---------------------------------------------------------------- per-worker state
+struct WState {
+    int32_t n_pending, n_valid, next, it, filled, seed_stop;  // seeding progress
+    int32_t best;                                             // winner of the current slot
+    int32_t iters, stop, hist_len, closing, done, err, run_lloyd;
+    int64_t nd;
+    double f_prev, last, f_final;
+};
+
+struct WideBufs {  // device scratch for one worker batch
+    void* S = nullptr;
+    double *Cm = nullptr, *d2 = nullptr, *dc = nullptr, *cand = nullptr, *btot = nullptr, *bcost = nullptr,
+           *part = nullptr, *lastcnt = nullptr;
+    uint8_t* flags = nullptr;
+    int32_t *pend = nullptr, *labels = nullptr, *active = nullptr;
+    WState* st = nullptr;
+};
+
+// the reference distance (core.hpp:100-108) of one row to JT centroids (row-major, stride n),
+// in registers; centroids past jn are skipped
+template <typename T>
+__device__ __forceinline__ void dist_tile(const T* __restrict__ x, int n, const double* __restrict__ C, int jn,
+                                          double (&acc)[kJT]) {
+#pragma unroll
+    for (int j = 0; j < kJT; ++j) acc[j] = 0.0;
+    for (int d = 0; d < n; ++d) {
+        const double xv = (double)x[d];
+#pragma unroll
+        for (int j = 0; j < kJT; ++j)
+            if (j < jn) {
+                const double diff = __dsub_rn(xv, __ldg(C + (int64_t)j * n + d));
+                acc[j] = __dadd_rn(acc[j], __dmul_rn(diff, diff));
+            }
+    }
+}
+
+// fixed-order tree sum over the CTA (kWT threads); result valid in thread 0
+__device__ double cta_sum(double v, double* red) {
+    const int tid = threadIdx.x;
+    red[tid] = v;
+    __syncthreads();
+#pragma unroll
+    for (int o = kWT / 2; o > 0; o >>= 1) {
+        if (tid < o) red[tid] = red[tid] + red[tid + o];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------- gather + init
+template <typename T>
+__global__ void wide_gather_kernel(const StepParams p, int w0, T* __restrict__ S) {
+    const int w = blockIdx.y, wl = w0 + w;
+    const int64_t s = p.s;
+    const int n = p.n;
+    SamplePRP prp;
+    if (p.sample_mode == 1)
+        prp = SamplePRP::make(p.key, p.round, (uint32_t)(p.worker_base + wl), (uint64_t)p.m, p.prp_a, p.prp_b,
+                              p.prp_inv_b);
+    const T* X = static_cast<const T*>(p.X);
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (kWT / 32);
+    for (int64_t i = (int64_t)blockIdx.x * (kWT / 32) + (threadIdx.x >> 5); i < s; i += warps) {
+        int64_t g = 0;
+        if (lane == 0) {
+            if (p.sample_mode == 0)
+                g = p.idx[(int64_t)wl * s + i];
+            else if (p.sample_mode == 1)
+                g = (int64_t)prp((uint64_t)i);
+            else
+                g = (int64_t)wl * s + i;
+        }
+        g = __shfl_sync(0xffffffffu, g, 0);
+        const T* src = X + g * n;
+        T* dst = S + ((int64_t)w * s + i) * n;
+        for (int d = lane; d < n; d += 32) dst[d] = src[d];
+    }
+}
+
+template <typename T>
+__global__ void wide_init_kernel(const StepParams p, int w0, WideBufs b) {
+    const int w = blockIdx.x, wl = w0 + w, tid = threadIdx.x;
+    const int k = p.k, n = p.n;
+    const int64_t kn = (int64_t)k * n, s = p.s;
+    const int64_t v = p.shared_version ? *p.shared_version : 1;
+    const double* ic = p.init_c + (int64_t)wl * p.init_stride;
+    const uint8_t* ifl = p.init_f + (int64_t)wl * p.initf_stride;
+    double* Cm = b.Cm + (int64_t)w * kn;
+    uint8_t* fl = b.flags + (int64_t)w * k;
+    for (int64_t e = tid; e < kn; e += kWT) Cm[e] = v != 0 ? ic[e] : 0.0;
+    for (int j = tid; j < k; j += kWT) fl[j] = v != 0 ? ifl[j] : (uint8_t)1;
+    __syncthreads();
+    __shared__ int64_t first_row;
+    if (tid == 0) {
+        WState st = {};
+        int32_t* pend = b.pend + (int64_t)w * k;
+        for (int j = 0; j < k; ++j) {
+            if (fl[j])
+                pend[st.n_pending++] = j;
+            else
+                ++st.n_valid;
+        }
+        st.stop = 1;
+        st.f_prev = __longlong_as_double(0x7ff0000000000000LL);
+        first_row = -1;
+        if (st.n_pending > 0) {
+            st.nd += s * st.n_valid;  // one D^2 pass per valid centre (seeding.hpp:60-68)
+            if (st.n_valid == 0) {    // seeding.hpp:72-79: uniform first centre
+                first_row = p.seed_mode == 0 ? p.first_row[wl]
+                                             : (int64_t)philox_index(p.key, p.round, (uint32_t)(p.worker_base + wl),
+                                                                     0xF1F1u, (uint64_t)s);
+                st.next = 1;
+                st.filled = 1;
+                st.nd += s;
+            }
+        }
+        b.st[w] = st;
+    }
+    __syncthreads();
+    if (first_row >= 0) {
+        const int j = b.pend[(int64_t)w * k];
+        const T* S = static_cast<const T*>(b.S) + ((int64_t)w * s + first_row) * n;
+        for (int d = tid; d < n; d += kWT) Cm[(int64_t)j * n + d] = (double)S[d];
+        if (tid == 0) fl[j] = 0;
+    }
+}
+
+// D^2 from every valid centre (including a first centre just drawn); min is order-free
+template <typename T>
+__global__ void wide_d2init_kernel(const StepParams p, WideBufs b) {
+    const int w = blockIdx.y, k = p.k, n = p.n;
+    const int64_t s = p.s;
+    if (b.st[w].n_pending == 0) return;
+    const int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x;
+    if (i >= s) return;
+    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
+    const double* Cm = b.Cm + (int64_t)w * k * n;
+    const uint8_t* fl = b.flags + (int64_t)w * k;
+    double d2 = __longlong_as_double(0x7ff0000000000000LL);
+    for (int j0 = 0; j0 < k; j0 += kJT) {
+        double acc[kJT];
+        const int jn = min(kJT, k - j0);
+        dist_tile<T>(x, n, Cm + (int64_t)j0 * n, jn, acc);
+#pragma unroll
+        for (int j = 0; j < kJT; ++j)
+            if (j < jn && !fl[j0 + j]) d2 = fmin(d2, acc[j]);
+    }
+    b.d2[(int64_t)w * s + i] = d2;
+}
+
+// ---------------------------------------------------------------- K-means++ slot
+__device__ __forceinline__ bool slot_live(const WState& st) {
+    return st.seed_stop == 0 && st.next < st.n_pending;
+}
+
+// block CDF totals: rows of a block summed sequentially (the order the draw re-walks)
+__global__ void wide_cdf_kernel(const StepParams p, WideBufs b, int nblk) {
+    const int w = blockIdx.y;
+    if (!slot_live(b.st[w])) return;
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk >= nblk) return;
+    const int64_t s = p.s, r0 = (int64_t)blk * kSeedRows, r1 = min(s, r0 + kSeedRows);
+    const double* d2 = b.d2 + (int64_t)w * s;
+    double run = 0.0;
+    for (int64_t i = r0; i < r1; ++i) run += d2[i];
+    b.btot[(int64_t)w * nblk + blk] = run;
+}
+
+// inverse-CDF draw of candidate c (seeding.hpp:85-92; rng.hpp:83-93): first row with cum > u,
+// cum = P_block + (sequential run within the block); no crossing -> row s-1
+template <typename T>
+__global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nblk) {
+    const int c = blockIdx.x, w = blockIdx.y, wl = w0 + w;
+    WState* stp = b.st + w;
+    if (!slot_live(*stp) || threadIdx.x != 0) return;
+    const int64_t s = p.s;
+    const int n = p.n;
+    const double* bt = b.btot + (int64_t)w * nblk;
+    double total = 0.0;
+    for (int q = 0; q < nblk; ++q) total += bt[q];
+    if (!(total > 0.0)) {  // distinct rows exhausted (seeding.hpp:87)
+        if (c == 0) stp->seed_stop = 1;
+        return;
+    }
+    const int it = stp->it, next = stp->next, ncand = p.candidates;
+    const double unit = p.seed_mode == 0 ? p.units[(int64_t)wl * p.units_stride + (int64_t)it * ncand + c]
+                                         : philox_unit(p.key, p.round, (uint32_t)(p.worker_base + wl),
+                                                       (uint32_t)(0x10000 + next * kMaxCandidates + c));
+    const double u = unit * total;
+    int64_t row = s - 1;
+    double P = 0.0;
+    for (int q = 0; q < nblk; ++q) {
+        if (P + bt[q] > u) {
+            const double* d2 = b.d2 + (int64_t)w * s;
+            const int64_t r0 = (int64_t)q * kSeedRows, r1 = min(s, r0 + kSeedRows);
+            double run = 0.0;
+            for (int64_t i = r0; i < r1; ++i) {
+                run += d2[i];
+                if (P + run > u) {
+                    row = i;
+                    break;
+                }
+            }
+            break;
+        }
+        P += bt[q];
+    }
+    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + row) * n;
+    double* cd = b.cand + ((int64_t)w * kMaxCandidates + c) * n;
+    for (int d = 0; d < n; ++d) cd[d] = (double)x[d];
+}
+
+// candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): per-row values kept for
+// the D^2 update of the winner, block partials by a fixed tree
+template <typename T>
+__global__ void wide_cost_kernel(const StepParams p, WideBufs b, int nblk) {
+    __shared__ double red[kWT];
+    const int w = blockIdx.y, blk = blockIdx.x, n = p.n, ncand = p.candidates;
+    if (!slot_live(b.st[w])) return;
+    const int64_t s = p.s, i = (int64_t)blk * kSeedRows + threadIdx.x;
+    const bool valid = i < s;
+    double acc[kJT];
+    if (valid) {
+        const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
+        dist_tile<T>(x, n, b.cand + (int64_t)w * kMaxCandidates * n, ncand, acc);
+    }
+    const double d2i = valid ? b.d2[(int64_t)w * s + i] : 0.0;
+    for (int c = 0; c < ncand; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < kMaxCandidates; ++j)
+            if (j == c) v = valid ? fmin(d2i, acc[j]) : 0.0;
+        if (valid) b.dc[((int64_t)w * kMaxCandidates + c) * s + i] = v;
+        const double tot = cta_sum(v, red);
+        if (threadIdx.x == 0) b.bcost[((int64_t)w * kMaxCandidates + c) * nblk + blk] = tot;
+    }
+}
+
+// winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot
+__global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
+    const int w = blockIdx.x, n = p.n, k = p.k, ncand = p.candidates;
+    WState* stp = b.st + w;
+    if (!slot_live(*stp)) return;
+    __shared__ int best_s;
+    if (threadIdx.x == 0) {
+        double bc = __longlong_as_double(0x7ff0000000000000LL);
+        int best = 0;
+        for (int c = 0; c < ncand; ++c) {
+            const double* bc_c = b.bcost + ((int64_t)w * kMaxCandidates + c) * nblk;
+            double t = 0.0;
+            for (int q = 0; q < nblk; ++q) t += bc_c[q];
+            if (t < bc) {
+                bc = t;
+                best = c;
+            }
+        }
+        best_s = best;
+    }
+    __syncthreads();
+    const int best = best_s;
+    const int j = b.pend[(int64_t)w * k + stp->next];
+    const double* cd = b.cand + ((int64_t)w * kMaxCandidates + best) * n;
+    for (int d = threadIdx.x; d < n; d += blockDim.x) b.Cm[((int64_t)w * k + j) * n + d] = cd[d];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        b.flags[(int64_t)w * k + j] = 0;
+        stp->best = best;
+        stp->nd += (int64_t)ncand * p.s;
+        stp->filled += 1;
+        stp->next += 1;
+        stp->it += 1;
+    }
+}
+
+__global__ void wide_d2upd_kernel(const StepParams p, WideBufs b, int it_expect) {
+    const int w = blockIdx.y;
+    const WState& st = b.st[w];
+    if (st.it != it_expect + 1 || st.seed_stop) return;  // this slot was decided for w
+    const int64_t s = p.s, i = (int64_t)blockIdx.x * kWT + threadIdx.x;
+    if (i < s) b.d2[(int64_t)w * s + i] = b.dc[((int64_t)w * kMaxCandidates + st.best) * s + i];
+}
+
+// ---------------------------------------------------------------- Lloyd
+__global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
+    const int w = blockIdx.x, k = p.k;
+    if (threadIdx.x != 0) return;
+    WState& st = b.st[w];
+    bool degenerate = false;
+    for (int j = 0; j < k; ++j) degenerate |= b.flags[(int64_t)w * k + j] != 0;
+    st.run_lloyd = p.do_lloyd && !degenerate;
+    if (p.do_lloyd && degenerate) st.err = kErrDegenerateInit;
+    st.done = st.run_lloyd ? 0 : 1;
+}
+
+// one pass for CTA g of worker w: rows chunk_range(s, G, g) in rounds of kWT; labels by exact
+// strict-< argmin (core.hpp:146-157); per-cluster sums of each round's rows (label-sorted, row
+// order) and its cost tree-sum are added to the CTA accumulators in round order
+template <typename T>
+__global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, WideBufs b, int G) {
+    extern __shared__ double wsm[];
+    const int w = blockIdx.y, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (b.st[w].done) return;
+    const int k = p.k, n = p.n;
+    const int64_t s = p.s, kn = (int64_t)k * n;
+    double* acc = wsm;                  // [k*n] sums
+    double* cnt = acc + kn;             // [k] counts
+    double* red = cnt + k;              // [kWT] tree
+    int* wcnt = reinterpret_cast<int*>(red + kWT);  // [8][k] per-warp label counts
+    int* cstart = wcnt + 8 * k;         // [k+1]
+    int* sorted = cstart + k + 1;       // [kWT] label-sorted round rows
+    for (int64_t e = tid; e < kn + k; e += kWT) acc[e] = 0.0;
+    double cost = 0.0;
+    int64_t r0, r1;
+    chunk_range(s, G, g, r0, r1);
+    const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
+    const double* Cm = b.Cm + (int64_t)w * kn;
+    int32_t* labels = b.labels + (int64_t)w * s;
+    __syncthreads();
+    for (int64_t base = r0; base < r1; base += kWT) {
+        const int64_t i = base + tid;
+        const bool valid = i < r1;
+        int lab = 0;
+        double bestd = __longlong_as_double(0x7ff0000000000000LL);
+        if (valid) {
+            const T* x = S + i * n;
+            for (int j0 = 0; j0 < k; j0 += kJT) {
+                double a[kJT];
+                const int jn = min(kJT, k - j0);
+                dist_tile<T>(x, n, Cm + (int64_t)j0 * n, jn, a);
+#pragma unroll
+                for (int j = 0; j < kJT; ++j)
+                    if (j < jn && a[j] < bestd) {
+                        bestd = a[j];
+                        lab = j0 + j;
+                    }
+            }
+            labels[i] = lab;
+        }
+        // stable counting sort of the round's rows by label
+        for (int e = tid; e < 8 * k; e += kWT) wcnt[e] = 0;
+        __syncthreads();
+        const unsigned peers = __match_any_sync(0xffffffffu, valid ? lab : -1);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && rank == 0) wcnt[warp * k + lab] = __popc(peers);
+        __syncthreads();
+        if (tid == 0) {
+            int off = 0;
+            for (int j = 0; j < k; ++j) {
+                cstart[j] = off;
+                for (int q = 0; q < 8; ++q) {
+                    const int c = wcnt[q * k + j];
+                    wcnt[q * k + j] = off;
+                    off += c;
+                }
+            }
+            cstart[k] = off;
+        }
+        __syncthreads();
+        if (valid) sorted[wcnt[warp * k + lab] + rank] = tid;
+        cost += cta_sum(valid ? bestd : 0.0, red);  // thread 0's copy is the one used
+        // per-cluster sums of this round, rows in order, added to the CTA accumulator
+        for (int64_t e = tid; e < kn; e += kWT) {
+            const int j = (int)(e / n), d = (int)(e - (int64_t)j * n);
+            double sj = 0.0;
+            for (int q = cstart[j]; q < cstart[j + 1]; ++q) sj += (double)S[(base + sorted[q]) * n + d];
+            acc[e] += sj;
+        }
+        for (int j = tid; j < k; j += kWT) cnt[j] += (double)(cstart[j + 1] - cstart[j]);
+        __syncthreads();
+    }
+    const int64_t pd = kn + k + 1;
+    double* out = b.part + ((int64_t)w * G + g) * pd;
+    for (int64_t e = tid; e < kn + k; e += kWT) out[e] = acc[e];
+    if (tid == 0) out[kn + k] = cost;
+}
+
+// partials in CTA order -> objective, monotone check, history, means, stop rules
+// (lloyd.hpp:100-164 with means_from_sums lloyd.hpp:75-89)
+__global__ void wide_lloyd_reduce_kernel(const StepParams p, WideBufs b, int G, int w0) {
+    const int w = blockIdx.x, wl = w0 + w, tid = threadIdx.x;
+    WState* stp = b.st + w;
+    if (stp->done) return;
+    const int k = p.k, n = p.n;
+    const int64_t kn = (int64_t)k * n, pd = kn + k + 1, s = p.s;
+    const double* part = b.part + (int64_t)w * G * pd;
+    double* Cm = b.Cm + (int64_t)w * kn;
+    __shared__ double f_s;
+    __shared__ int flag_s;  // 0 continue, 1 done after this pass
+    if (tid == 0) {
+        double f = 0.0;
+        for (int g = 0; g < G; ++g) f += part[(int64_t)g * pd + kn + k];
+        f_s = f;
+        WState st = *stp;
+        flag_s = 0;
+        if (st.hist_len > 0 && f > st.last * (1.0 + 1e-12)) {  // lloyd.hpp:114-121
+            st.err = kErrMonotone;
+            st.stop = -1;
+            st.done = 1;
+            flag_s = 2;
+        } else {
+            if (p.out_hist && st.hist_len < p.hist_cap) p.out_hist[(int64_t)wl * p.hist_cap + st.hist_len] = f;
+            st.last = f;
+            st.hist_len += 1;
+            st.nd += s * (int64_t)k;
+            if (st.closing) {  // lloyd.hpp:155-163
+                st.f_final = f;
+                st.done = 1;
+                flag_s = 1;
+            } else {
+                st.iters += 1;
+            }
+        }
+        *stp = st;
+    }
+    __syncthreads();
+    if (flag_s == 2) return;
+    // counts of this pass (flags / output counts if it is the last)
+    for (int j = tid; j < k; j += blockDim.x) {
+        double c = 0.0;
+        for (int g = 0; g < G; ++g) c += part[(int64_t)g * pd + kn + j];
+        b.lastcnt[(int64_t)w * k + j] = c;
+    }
+    if (flag_s == 1) return;
+    bool same = true;
+    for (int64_t e = tid; e < kn; e += blockDim.x) {
+        const int j = (int)(e / n);
+        double c = 0.0, sum = 0.0;
+        for (int g = 0; g < G; ++g) {
+            c += part[(int64_t)g * pd + kn + j];
+            sum += part[(int64_t)g * pd + e];
+        }
+        double v = Cm[e];
+        if (c > 0.0) {
+            const double inv = 1.0 / c;
+            v = sum * inv;
+        }
+        same &= (v == Cm[e]);
+        Cm[e] = v;
+    }
+    const bool all_same = __syncthreads_and(same);
+    if (tid == 0) {
+        WState st = *stp;
+        const double f = f_s;
+        if (all_same) {
+            st.stop = 2;  // fixed_point
+            st.f_final = f;
+            st.done = 1;
+        } else {
+            bool go_close = false;
+            if (isfinite(st.f_prev)) {
+                const double improvement = st.f_prev > 0.0 ? (st.f_prev - f) / st.f_prev : 0.0;
+                if (improvement < p.rel_tol) {
+                    st.stop = 0;  // tolerance
+                    go_close = true;
+                }
+            }
+            st.f_prev = f;
+            if (!go_close && st.iters == p.max_iters) {
+                st.stop = 1;
+                go_close = true;
+            }
+            st.closing = go_close ? 1 : 0;
+        }
+        *stp = st;
+    }
+}
+
+__global__ void wide_max_pending_kernel(WideBufs b, int Wb) {  // K-means++ slots still to run
+    __shared__ int c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    for (int w = threadIdx.x; w < Wb; w += blockDim.x) atomicMax(&c, b.st[w].n_pending - b.st[w].next);
+    __syncthreads();
+    if (threadIdx.x == 0) *b.active = c;
+}
+
+__global__ void wide_count_active_kernel(WideBufs b, int Wb) {
+    __shared__ int c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    for (int w = threadIdx.x; w < Wb; w += blockDim.x)
+        if (!b.st[w].done) atomicAdd(&c, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) *b.active = c;
+}
+
+// ---------------------------------------------------------------- outputs
+__global__ void wide_output_kernel(const StepParams p, WideBufs b, int w0) {
+    const int w = blockIdx.x, wl = w0 + w, tid = threadIdx.x, k = p.k, n = p.n;
+    const int64_t kn = (int64_t)k * n, s = p.s;
+    WState* stp = b.st + w;
+    uint8_t* fl = b.flags + (int64_t)w * k;
+    const double* Cm = b.Cm + (int64_t)w * kn;
+    if (stp->run_lloyd && stp->stop >= 0) {  // flags = empty clusters of the last pass
+        for (int j = tid; j < k; j += blockDim.x) fl[j] = b.lastcnt[(int64_t)w * k + j] == 0.0 ? 1 : 0;
+        if (p.out_counts)
+            for (int j = tid; j < k; j += blockDim.x)
+                p.out_counts[(int64_t)wl * k + j] = (int64_t)b.lastcnt[(int64_t)w * k + j];
+        if (p.out_labels)
+            for (int64_t i = tid; i < s; i += blockDim.x) p.out_labels[(int64_t)wl * s + i] = b.labels[(int64_t)w * s + i];
+    }
+    __syncthreads();
+    if (p.out_c)
+        for (int64_t e = tid; e < kn; e += blockDim.x) p.out_c[(int64_t)wl * kn + e] = Cm[e];
+    if (p.out_f)
+        for (int j = tid; j < k; j += blockDim.x) p.out_f[(int64_t)wl * k + j] = fl[j];
+    const WState st = *stp;
+    if (tid == 0) {
+        if (p.out_obj) p.out_obj[wl] = st.f_final;
+        if (p.out_iters) p.out_iters[wl] = st.iters;
+        if (p.out_stop) p.out_stop[wl] = st.stop;
+        if (p.out_nd) p.out_nd[wl] = st.nd;
+        if (p.out_filled) p.out_filled[wl] = st.filled;
+        if (p.out_err) p.out_err[wl] = st.err;
+        if (p.out_hist_len) p.out_hist_len[wl] = st.hist_len;
+    }
+    if (p.inc_obj) {  // keep-the-best (engine.hpp:254, strict <)
+        const bool acc = st.run_lloyd && st.err == kErrNone && st.f_final < p.inc_obj[wl];
+        __syncthreads();
+        if (acc) {
+            for (int64_t e = tid; e < kn; e += blockDim.x) p.inc_c[(int64_t)wl * kn + e] = Cm[e];
+            for (int j = tid; j < k; j += blockDim.x) p.inc_f[(int64_t)wl * k + j] = fl[j];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (acc) p.inc_obj[wl] = st.f_final;
+            p.accepted[wl] = acc ? 1 : 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- f(C, X)
+// full-data assignment/objective for n > 32 (mssc_objective core.hpp:224-233, final_assignment
+// engine.hpp:197-229): block b takes rows b*kWT + t (+ grid strides); exact distances, strict
+// argmin over the valid centres, per-block cost by thread-sequential sums and a fixed tree
+template <typename T>
+__global__ void __launch_bounds__(kWT) wide_objective_kernel(const ObjParams p) {
+    __shared__ double red[kWT];
+    const T* X = static_cast<const T*>(p.X);
+    const int n = p.n, kv = p.kv;
+    double cost = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x; i < p.m; i += (int64_t)gridDim.x * kWT) {
+        const T* x = X + i * n;
+        double bestd = __longlong_as_double(0x7ff0000000000000LL);
+        int lab = 0;
+        for (int j0 = 0; j0 < kv; j0 += kJT) {
+            double a[kJT];
+            const int jn = min(kJT, kv - j0);
+            dist_tile<T>(x, n, p.C + (int64_t)j0 * n, jn, a);
+#pragma unroll
+            for (int j = 0; j < kJT; ++j)
+                if (j < jn && a[j] < bestd) {
+                    bestd = a[j];
+                    lab = j0 + j;
+                }
+        }
+        cost += bestd;
+        const int orig = p.remap ? p.remap[lab] : lab;
+        if (p.labels) p.labels[i] = orig;
+        if (p.counts) atomicAdd(p.counts + orig, 1ull);
+    }
+    const double tot = cta_sum(cost, red);
+    if (threadIdx.x == 0) p.block_cost[blockIdx.x] = tot;
+}
+
+// ---------------------------------------------------------------- host side
+struct Arena {  // grow-only device scratch per device
+    void* p = nullptr;
+    size_t cap = 0;
+};
+std::mutex g_mu;
+std::map<int, Arena> g_arena;
+
+cudaError_t arena_get(size_t bytes, void** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    Arena& a = g_arena[dev];
+    if (a.cap < bytes) {
+        if (a.p) {
+            cudaDeviceSynchronize();
+            cudaFree(a.p);
+        }
+        a.p = nullptr;
+        a.cap = 0;
+        cudaError_t e = cudaMalloc(&a.p, bytes);
+        if (e != cudaSuccess) return e;
+        a.cap = bytes;
+    }
+    *out = a.p;
+    return cudaSuccess;
+}
+
+size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+template <typename T>
+cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std::string* why) {
+    const int k = p.k, n = p.n, ncand = p.candidates;
+    const int64_t s = p.s, kn = (int64_t)k * n;
+    const int nblk = (int)((s + kSeedRows - 1) / kSeedRows);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // CTAs per worker for the Lloyd pass: enough CTAs for the whole GPU, each at least a few rounds
+    int G = std::max(1, std::min<int>((int)((int64_t)2 * sms / Wb), (int)((s + 4 * kWT - 1) / (4 * kWT))));
+    const int64_t pd = kn + k + 1;
+    // scratch layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = up256(off + bytes);
+        return o;
+    };
+    const size_t oS = take((size_t)Wb * s * n * sizeof(T)), oC = take((size_t)Wb * kn * 8),
+                 od2 = take((size_t)Wb * s * 8), odc = take((size_t)Wb * kMaxCandidates * s * 8),
+                 ocand = take((size_t)Wb * kMaxCandidates * n * 8), obt = take((size_t)Wb * nblk * 8),
+                 obc = take((size_t)Wb * kMaxCandidates * nblk * 8), opart = take((size_t)Wb * G * pd * 8),
+                 olc = take((size_t)Wb * k * 8), ofl = take((size_t)Wb * k), opend = take((size_t)Wb * k * 4),
+                 olab = take((size_t)Wb * s * 4), oact = take(4), ost = take((size_t)Wb * sizeof(WState));
+    void* base = nullptr;
+    cudaError_t e = arena_get(off, &base);
+    if (e != cudaSuccess) {
+        if (why) *why = "wide step: scratch allocation";
+        return e;
+    }
+    char* c8 = static_cast<char*>(base);
+    WideBufs b;
+    b.S = c8 + oS;
+    b.Cm = reinterpret_cast<double*>(c8 + oC);
+    b.d2 = reinterpret_cast<double*>(c8 + od2);
+    b.dc = reinterpret_cast<double*>(c8 + odc);
+    b.cand = reinterpret_cast<double*>(c8 + ocand);
+    b.btot = reinterpret_cast<double*>(c8 + obt);
+    b.bcost = reinterpret_cast<double*>(c8 + obc);
+    b.part = reinterpret_cast<double*>(c8 + opart);
+    b.lastcnt = reinterpret_cast<double*>(c8 + olc);
+    b.flags = reinterpret_cast<uint8_t*>(c8 + ofl);
+    b.pend = reinterpret_cast<int32_t*>(c8 + opend);
+    b.labels = reinterpret_cast<int32_t*>(c8 + olab);
+    b.active = reinterpret_cast<int32_t*>(c8 + oact);
+    b.st = reinterpret_cast<WState*>(c8 + ost);
+
+    const dim3 rows_grid((unsigned)((s + kWT - 1) / kWT), (unsigned)Wb);
+    wide_gather_kernel<T><<<dim3((unsigned)std::min<int64_t>((s + 7) / 8, 4096), (unsigned)Wb), kWT, 0, st>>>(
+        p, w0, static_cast<T*>(b.S));
+    wide_init_kernel<T><<<Wb, kWT, 0, st>>>(p, w0, b);
+    wide_d2init_kernel<T><<<rows_grid, kWT, 0, st>>>(p, b);
+    // K-means++ slots: as many host iterations as the worker with the most pending slots
+    int32_t slots = 0;
+    wide_max_pending_kernel<<<1, 256, 0, st>>>(b, Wb);
+    e = cudaMemcpyAsync(&slots, b.active, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    for (int it = 0; it < slots; ++it) {
+        wide_cdf_kernel<<<dim3((unsigned)((nblk + 63) / 64), (unsigned)Wb), 64, 0, st>>>(p, b, nblk);
+        wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
+        wide_cost_kernel<T><<<dim3((unsigned)nblk, (unsigned)Wb), kWT, 0, st>>>(p, b, nblk);
+        wide_decide_kernel<<<Wb, 128, 0, st>>>(p, b, nblk);
+        wide_d2upd_kernel<<<rows_grid, kWT, 0, st>>>(p, b, it);
+    }
+    // Lloyd: passes until every worker of the batch stopped
+    wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
+    const size_t smem = (size_t)(kn + k + kWT) * 8 + (size_t)(8 * k + k + 1 + kWT) * 4;
+    e = cudaFuncSetAttribute(wide_assign_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        if (why) *why = "wide step: k*n too large for the pass accumulator";
+        return e;
+    }
+    if (p.do_lloyd) {
+        int32_t active = 0;
+        for (int pass = 0; pass <= p.max_iters + 1; ++pass) {
+            wide_assign_kernel<T><<<dim3((unsigned)G, (unsigned)Wb), kWT, smem, st>>>(p, b, G);
+            wide_lloyd_reduce_kernel<<<Wb, kWT, 0, st>>>(p, b, G, w0);
+            if ((pass & 3) == 3 || pass == p.max_iters + 1) {  // stop check every few passes
+                wide_count_active_kernel<<<1, 256, 0, st>>>(b, Wb);
+                e = cudaMemcpyAsync(&active, b.active, 4, cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) return e;
+                if (active == 0) break;
+            }
+        }
+    }
+    wide_output_kernel<<<Wb, kWT, 0, st>>>(p, b, w0);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_objective_wide(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int nb = std::max(1, std::min(nblocks[0], sms * 4));  // fixed per device: reproducible
+    nblocks[0] = nb;
+    if (dtype == 0)
+        wide_objective_kernel<float><<<nb, kWT, 0, st>>>(p);
+    else
+        wide_objective_kernel<double><<<nb, kWT, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// Wide-shape worker step: same contract as launch_step, any n and k (k*n bounded by the
+// pass accumulator in shared memory), any s; workers in batches bounded by the scratch size.
+cudaError_t launch_step_wide(int dtype, const StepParams& p, cudaStream_t st, std::string* why) {
+    const size_t row_bytes = (size_t)p.n * (dtype == 0 ? 4 : 8);
+    const size_t per_worker = (size_t)p.s * (row_bytes + 8 * (kMaxCandidates + 1) + 4) + 1024;
+    const size_t budget = (size_t)4 << 30;
+    const int Wb = (int)std::max<size_t>(1, std::min<size_t>((size_t)p.W, budget / std::max<size_t>(per_worker, 1)));
+    for (int w0 = 0; w0 < p.W; w0 += Wb) {
+        const int nb = std::min(Wb, p.W - w0);
+        StepParams q = p;
+        cudaError_t e = dtype == 0 ? run_batch<float>(q, w0, nb, st, why) : run_batch<double>(q, w0, nb, st, why);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace hpcg
