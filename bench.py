@@ -253,6 +253,16 @@ def run_gpu(args, world, rank, local):
     step_cnt, step_ms = kt["step"]
     lloyd_flops_per_launch = nd_total / max(1, step_cnt) * N * 2  # per-rank launches
     achieved_tflops = lloyd_flops_per_launch / (step_ms / max(1, step_cnt) * 1e-3) / 1e12
+    # DRAM bytes per launch from the committed ncu --set full captures (one launch each)
+    trf = {}
+    try:
+        trf = json.load(open(Path(__file__).resolve().parent / "profiles" / "r1_traffic.json"))
+    except (OSError, ValueError):
+        pass
+    step_traffic = None
+    if "worker_step_round0_bytes" in trf and "worker_step_round1_bytes" in trf:  # 1 seeding + 3 steady rounds
+        step_traffic = (trf["worker_step_round0_bytes"] + (ROUNDS - 1) * trf["worker_step_round1_bytes"]) / ROUNDS
+    obj_traffic = trf.get("objective_bytes")
     peak_tflops = 2 * fma_tfma
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -267,11 +277,13 @@ def run_gpu(args, world, rank, local):
         "distance_evals_per_step": nd_all / args.steps,
         "objective_pass": {"gbs": obj_gbs, "ms": float(np.median(obj_ms)), "bytes": obj_bytes,
                            "roofline": {"bound": "hbm", "achieved": obj_gbs, "peak": hbm_peak, "unit": "GB/s",
-                                        "frac": obj_gbs / hbm_peak, "traffic": None,
+                                        "frac": obj_gbs / hbm_peak, "traffic": obj_traffic,
+                                        "traffic_unit": "bytes/launch (ncu, profiles/r1_traffic.json)",
                                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
         "roofline": {"bound": "fma", "kernel": "worker_step_kernel", "achieved": achieved_tflops,
                      "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
-                     "traffic": None,
+                     "traffic": step_traffic,
+                     "traffic_unit": "DRAM bytes/launch (ncu; mean of 1 seeding + 3 steady rounds)",
                      "algorithmic": "n_d (Lloyd+seeding evaluations) x n FMA x 2 flop per launch / mean launch time",
                      "peak_source": "FFMA2 loop measured in-run on this GPU (fp32 FMA; MEASURED_PEAKS.json has "
                                     "only hbm and bf16)",
