@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libhpcg.so"
+LIB_PATH = Path(os.environ.get("HPCG_LIB_OVERRIDE") or (Path(__file__).resolve().parent / "libhpcg.so"))  # dev A/B
 
 # Every symbol include/hpcg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
