@@ -215,7 +215,7 @@ int check_shape(int dtype, int64_t n, int64_t k) {
     if (n < 1) return fail(HPCG_EINVAL, "dataset needs at least one feature");
     // n <= 32 and k <= 32 run cluster-resident; larger shapes take the grid-wide path (wide.cu)
     if (n > kWideMaxN || k > kWideMaxK || n * k > kWideMaxKN)
-        return fail(HPCG_EUNSUPPORTED, "k * n beyond the grid-wide path's pass accumulator (24576)");
+        return fail(HPCG_EUNSUPPORTED, "k * n beyond the grid-wide path's pass accumulator (16384)");
     return HPCG_OK;
 }
 

@@ -62,6 +62,41 @@ __device__ __forceinline__ void dist_tile(const T* __restrict__ x, int n, const 
     }
 }
 
+// the reference distance of one row to one centroid, row read in 16-B pieces (float4 /
+// double2) when aligned: same ascending-d, separately rounded arithmetic as dist_tile
+template <typename T>
+__device__ __forceinline__ double dist1(const T* __restrict__ x, int n, const double* __restrict__ c, bool vec) {
+    double acc = 0.0;
+    int d = 0;
+    if (vec) {
+        constexpr int E = 16 / (int)sizeof(T);
+        for (; d + E <= n; d += E) {
+            double xv[E];
+            if constexpr (sizeof(T) == 4) {
+                const float4 f = __ldg(reinterpret_cast<const float4*>(x + d));
+                xv[0] = f.x;
+                xv[1] = f.y;
+                xv[2] = f.z;
+                xv[3] = f.w;
+            } else {
+                const double2 f = __ldg(reinterpret_cast<const double2*>(x + d));
+                xv[0] = f.x;
+                xv[1] = f.y;
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                const double diff = __dsub_rn(xv[u], __ldg(c + d + u));
+                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            }
+        }
+    }
+    for (; d < n; ++d) {
+        const double diff = __dsub_rn((double)x[d], __ldg(c + d));
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
 // fixed-order tree sum over the CTA (kWT threads); result valid in thread 0
 __device__ double cta_sum(double v, double* red) {
     const int tid = threadIdx.x;
@@ -75,6 +110,162 @@ __device__ double cta_sum(double v, double* red) {
     const double r = red[0];
     __syncthreads();
     return r;
+}
+
+// ---------------------------------------------------------------- fp32 screen
+// d~_j = |c_j|^2 + x.(-2c_j) in fp32 (FFMA2 pairs, two chains of n/2 terms like the resident
+// kernel's screen), top-2 tracked; |d~_j - exact| <= kappa (|x| + cmax)^2 with
+// kappa = 2 (ceil(n/2) + 12) 2^-24 (covers fp64 inputs rounded to fp32). Rows whose best and
+// second-best are within the bound get the exact reference argmin. Records: rec[j][0..n) = -2c_j
+// (fp32, rows padded to kKT multiples with zeros), ccs[j] = |c_j|^2 (+inf on padding rows).
+constexpr int kKT = 16;  // centroids per screen tile
+
+template <typename T>
+__device__ __forceinline__ float4 load4(const T* __restrict__ x, int d, int n, bool vec) {
+    if constexpr (sizeof(T) == 4) {
+        if (vec) return __ldg(reinterpret_cast<const float4*>(x + d));
+    }
+    float4 v;
+    v.x = d < n ? (float)x[d] : 0.f;
+    v.y = d + 1 < n ? (float)x[d + 1] : 0.f;
+    v.z = d + 2 < n ? (float)x[d + 2] : 0.f;
+    v.w = d + 3 < n ? (float)x[d + 3] : 0.f;
+    return v;
+}
+
+// the same four elements in full precision (the sums: fp32 data widened, fp64 data as is)
+template <typename T>
+__device__ __forceinline__ void load4d(const T* __restrict__ x, int d, int n, bool vec, double (&v)[4]) {
+    if constexpr (sizeof(T) == 4) {
+        const float4 f = load4<T>(x, d, n, vec);
+        v[0] = f.x;
+        v[1] = f.y;
+        v[2] = f.z;
+        v[3] = f.w;
+    } else {
+        if (vec) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(x + d));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(x + d + 2));
+            v[0] = a.x;
+            v[1] = a.y;
+            v[2] = b.x;
+            v[3] = b.y;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = d + u < n ? (double)x[d + u] : 0.0;
+        }
+    }
+}
+
+// records of the worker's k centroids into shared memory (rec: kpad x n4 floats, ccs: kpad)
+__device__ void build_records(const double* __restrict__ Cm, int k, int kpad, int n, int n4, float* rec, float* ccs,
+                              const uint8_t* skip = nullptr) {
+    for (int e = threadIdx.x; e < kpad * n4; e += blockDim.x) {
+        const int j = e / n4, d = e - j * n4;
+        rec[e] = (j < k && d < n) ? (float)(-2.0 * Cm[(int64_t)j * n + d]) : 0.f;
+    }
+    for (int j = threadIdx.x; j < kpad; j += blockDim.x) {
+        float cc = __int_as_float(0x7f800000);
+        if (j < k && !(skip && skip[j])) {
+            double a = 0.0;
+            for (int d = 0; d < n; ++d) {
+                const double c = Cm[(int64_t)j * n + d];
+                a += c * c;
+            }
+            cc = (float)a;
+        }
+        ccs[j] = cc;
+    }
+}
+
+__device__ float records_cmax(const float* ccs, int kpad, float* red_f) {  // max |c| (rounded up), CTA-wide
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float cm = 0.f;
+        for (int j = 0; j < kpad; ++j)
+            if (ccs[j] < __int_as_float(0x7f800000)) cm = fmaxf(cm, sqrtf(ccs[j]) * 1.0001f);
+        red_f[0] = cm;
+    }
+    __syncthreads();
+    return red_f[0];
+}
+
+// screen of one row against all centroids: best index, best/second screen values, |x|^2
+template <typename T>
+__device__ __forceinline__ void screen_row(const T* __restrict__ x, int n, int n4, int kpad, const float* rec,
+                                           const float* ccs, bool vec, int& i1, float& m1, float& m2, float& xx) {
+    m1 = __int_as_float(0x7f800000);
+    m2 = m1;
+    i1 = 0;
+    float2 nn = make_float2(0.f, 0.f);
+    for (int j0 = 0; j0 < kpad; j0 += kKT) {
+        float2 a[kKT];
+#pragma unroll
+        for (int j = 0; j < kKT; ++j) a[j] = make_float2(ccs[j0 + j], 0.f);
+        for (int d = 0; d < n4; d += 4) {
+            const float4 xv = load4<T>(x, d, n, vec);
+            const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
+            if (j0 == 0) {
+                nn = __ffma2_rn(xa, xa, nn);
+                nn = __ffma2_rn(xb, xb, nn);
+            }
+#pragma unroll
+            for (int j = 0; j < kKT; ++j) {
+                const float4 c = *reinterpret_cast<const float4*>(rec + (j0 + j) * n4 + d);
+                a[j] = __ffma2_rn(xa, make_float2(c.x, c.y), a[j]);
+                a[j] = __ffma2_rn(xb, make_float2(c.z, c.w), a[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kKT; ++j) {
+            const float dj = a[j].x + a[j].y;
+            m2 = fminf(m2, fmaxf(m1, dj));
+            const bool lt = dj < m1;
+            m1 = fminf(m1, dj);
+            i1 = lt ? j0 + j : i1;
+        }
+    }
+    xx = nn.x + nn.y;
+}
+
+// exact reference argmin (core.hpp:146-157: strict <, ties -> lowest j) of row x for the lanes
+// in `tie`, warp-parallel over centroids; the winner lands in i1 of the owning lane
+template <typename T>
+__device__ void exact_ties_masked(unsigned tie, const T* __restrict__ S, int64_t row0, int n, int k,
+                                  const double* __restrict__ Cm, const uint8_t* skip, int& i1) {
+    const int lane = threadIdx.x & 31;
+    while (tie) {
+        const int src = __ffs(tie) - 1;
+        tie &= tie - 1;
+        const T* x = S + (row0 + src) * n;
+        double dv = __longlong_as_double(0x7ff0000000000000LL);
+        int dj = 0x7fffffff;
+        const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
+        for (int j = lane; j < k; j += 32) {
+            if (skip && skip[j]) continue;
+            const double a = dist1<T>(x, n, Cm + (int64_t)j * n, vecd);
+            if (a < dv) {
+                dv = a;
+                dj = j;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, dj, o);
+            if (ov < dv || (ov == dv && oj < dj)) {
+                dv = ov;
+                dj = oj;
+            }
+        }
+        if (lane == src) i1 = dj;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void exact_ties(unsigned tie, const T* __restrict__ S, int64_t row0, int n, int k,
+                                           const double* __restrict__ Cm, int& i1) {
+    exact_ties_masked<T>(tie, S, row0, n, k, Cm, nullptr, i1);
 }
 
 // ---------------------------------------------------------------- gather + init
@@ -155,27 +346,36 @@ __global__ void wide_init_kernel(const StepParams p, int w0, WideBufs b) {
     }
 }
 
-// D^2 from every valid centre (including a first centre just drawn); min is order-free
+// D^2 from every valid centre (including a first centre just drawn): the screen's argmin over
+// the valid centres (near ties exact) and the reference distance to it
 template <typename T>
-__global__ void wide_d2init_kernel(const StepParams p, WideBufs b) {
+__global__ void __launch_bounds__(kWT) wide_d2init_kernel(const StepParams p, WideBufs b) {
+    extern __shared__ __align__(16) float wrec[];
+    __shared__ float red_f[1];
     const int w = blockIdx.y, k = p.k, n = p.n;
     const int64_t s = p.s;
     if (b.st[w].n_pending == 0) return;
-    const int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x;
-    if (i >= s) return;
-    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
+    const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
+    float* rec = wrec;
+    float* ccs = rec + (int64_t)kpad * n4;
     const double* Cm = b.Cm + (int64_t)w * k * n;
     const uint8_t* fl = b.flags + (int64_t)w * k;
-    double d2 = __longlong_as_double(0x7ff0000000000000LL);
-    for (int j0 = 0; j0 < k; j0 += kJT) {
-        double acc[kJT];
-        const int jn = min(kJT, k - j0);
-        dist_tile<T>(x, n, Cm + (int64_t)j0 * n, jn, acc);
-#pragma unroll
-        for (int j = 0; j < kJT; ++j)
-            if (j < jn && !fl[j0 + j]) d2 = fmin(d2, acc[j]);
-    }
-    b.d2[(int64_t)w * s + i] = d2;
+    build_records(Cm, k, kpad, n, n4, rec, ccs, fl);
+    const float cmax = records_cmax(ccs, kpad, red_f);
+    const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
+    const bool vec = sizeof(T) == 4 && (n & 3) == 0;
+    const int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x;
+    const bool valid = i < s;
+    const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
+    int lab = 0;
+    float m1 = 0.f, m2 = 0.f, xx = 0.f;
+    if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
+    const float sc = sqrtf(xx) * 1.0001f + cmax;
+    const unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+    if (tie) exact_ties_masked<T>(tie, S, i - (threadIdx.x & 31), n, k, Cm, fl, lab);
+    if (!valid) return;
+    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
+    b.d2[(int64_t)w * s + i] = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
 }
 
 // ---------------------------------------------------------------- K-means++ slot
@@ -240,27 +440,66 @@ __global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nbl
     for (int d = 0; d < n; ++d) cd[d] = (double)x[d];
 }
 
-// candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): per-row values kept for
-// the D^2 update of the winner, block partials by a fixed tree
+// candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): an fp32 screen decides
+// the rows the candidate provably cannot improve (value d2_i, exact); the others get the
+// reference distance. Per-row values are kept for the winner's D^2 update; block partials by a
+// fixed tree, so the costs are exact sums in a fixed order.
 template <typename T>
-__global__ void wide_cost_kernel(const StepParams p, WideBufs b, int nblk) {
+__global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, WideBufs b, int nblk) {
     __shared__ double red[kWT];
+    extern __shared__ __align__(16) float crec_raw[];  // [ncand][n4] -2 * candidate (fp32)
+    __shared__ float ccn[kMaxCandidates];
     const int w = blockIdx.y, blk = blockIdx.x, n = p.n, ncand = p.candidates;
     if (!slot_live(b.st[w])) return;
+    const int n4 = (n + 3) & ~3;
+    auto crec = [&](int c) { return crec_raw + (int64_t)c * n4; };
+    const double* cand = b.cand + (int64_t)w * kMaxCandidates * n;
+    for (int e = threadIdx.x; e < ncand * n4; e += kWT) {
+        const int c = e / n4, d = e - c * n4;
+        crec(c)[d] = d < n ? (float)(-2.0 * cand[(int64_t)c * n + d]) : 0.f;
+    }
+    if (threadIdx.x < ncand) {
+        double a = 0.0;
+        for (int d = 0; d < n; ++d) a += cand[(int64_t)threadIdx.x * n + d] * cand[(int64_t)threadIdx.x * n + d];
+        ccn[threadIdx.x] = (float)a;
+    }
+    __syncthreads();
+    const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
+    const bool vec = sizeof(T) == 4 && (n & 3) == 0;
     const int64_t s = p.s, i = (int64_t)blk * kSeedRows + threadIdx.x;
     const bool valid = i < s;
-    double acc[kJT];
-    if (valid) {
-        const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
-        dist_tile<T>(x, n, b.cand + (int64_t)w * kMaxCandidates * n, ncand, acc);
-    }
+    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + (valid ? i : 0)) * n;
     const double d2i = valid ? b.d2[(int64_t)w * s + i] : 0.0;
-    for (int c = 0; c < ncand; ++c) {
-        double v = 0.0;
+    // screen: s~_c = |c|^2 + x.(-2c); dist~_c = |x|^2 + s~_c
+    float2 a[kMaxCandidates], nn = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < kMaxCandidates; ++j)
-            if (j == c) v = valid ? fmin(d2i, acc[j]) : 0.0;
-        if (valid) b.dc[((int64_t)w * kMaxCandidates + c) * s + i] = v;
+    for (int c = 0; c < kMaxCandidates; ++c) a[c] = make_float2(c < ncand ? ccn[c] : 0.f, 0.f);
+    for (int d = 0; d < n4; d += 4) {
+        const float4 xv = load4<T>(x, d, n, vec);
+        const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
+        nn = __ffma2_rn(xa, xa, nn);
+        nn = __ffma2_rn(xb, xb, nn);
+#pragma unroll
+        for (int c = 0; c < kMaxCandidates; ++c)
+            if (c < ncand) {
+                const float4 cv = *reinterpret_cast<const float4*>(crec(c) + d);
+                a[c] = __ffma2_rn(xa, make_float2(cv.x, cv.y), a[c]);
+                a[c] = __ffma2_rn(xb, make_float2(cv.z, cv.w), a[c]);
+            }
+    }
+    const float xx = nn.x + nn.y, xn = sqrtf(xx) * 1.0001f;
+    const float f2 = __double2float_ru(d2i);
+    for (int c = 0; c < ncand; ++c) {
+        double v = d2i;
+        if (valid) {
+            const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
+            const float dt = xx + (a[c].x + a[c].y);
+            if (!(dt - kappa * sc * sc > f2))  // may improve: the reference distance
+                v = fmin(d2i, dist1<T>(x, n, cand + (int64_t)c * n, sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0));
+            b.dc[((int64_t)w * kMaxCandidates + c) * s + i] = v;
+        } else {
+            v = 0.0;
+        }
         const double tot = cta_sum(v, red);
         if (threadIdx.x == 0) b.bcost[((int64_t)w * kMaxCandidates + c) * nblk + blk] = tot;
     }
@@ -332,12 +571,16 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
     if (b.st[w].done) return;
     const int k = p.k, n = p.n;
     const int64_t s = p.s, kn = (int64_t)k * n;
+    const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
     double* acc = wsm;                  // [k*n] sums
     double* cnt = acc + kn;             // [k] counts
     double* red = cnt + k;              // [kWT] tree
-    int* wcnt = reinterpret_cast<int*>(red + kWT);  // [8][k] per-warp label counts
+    float* rec = reinterpret_cast<float*>(red + kWT + ((kn + k + kWT) & 1));  // [kpad][n4], 16-B aligned
+    float* ccs = rec + (int64_t)kpad * n4;             // [kpad]
+    int* wcnt = reinterpret_cast<int*>(ccs + kpad);    // [8][k] per-warp label counts
     int* cstart = wcnt + 8 * k;         // [k+1]
     int* sorted = cstart + k + 1;       // [kWT] label-sorted round rows
+    __shared__ float cmax_s;
     for (int64_t e = tid; e < kn + k; e += kWT) acc[e] = 0.0;
     double cost = 0.0;
     int64_t r0, r1;
@@ -345,25 +588,30 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
     const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
     const double* Cm = b.Cm + (int64_t)w * kn;
     int32_t* labels = b.labels + (int64_t)w * s;
+    build_records(Cm, k, kpad, n, n4, rec, ccs);
     __syncthreads();
+    if (tid == 0) {
+        float cm = 0.f;
+        for (int j = 0; j < k; ++j) cm = fmaxf(cm, sqrtf(ccs[j]) * 1.0001f);
+        cmax_s = cm;
+    }
+    __syncthreads();
+    const float cmax = cmax_s;
+    const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
+    const bool vec = sizeof(T) == 4 && (n & 3) == 0;                           // float4 screen loads
+    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;           // 16-B sum loads
     for (int64_t base = r0; base < r1; base += kWT) {
         const int64_t i = base + tid;
         const bool valid = i < r1;
         int lab = 0;
-        double bestd = __longlong_as_double(0x7ff0000000000000LL);
-        if (valid) {
-            const T* x = S + i * n;
-            for (int j0 = 0; j0 < k; j0 += kJT) {
-                double a[kJT];
-                const int jn = min(kJT, k - j0);
-                dist_tile<T>(x, n, Cm + (int64_t)j0 * n, jn, a);
-#pragma unroll
-                for (int j = 0; j < kJT; ++j)
-                    if (j < jn && a[j] < bestd) {
-                        bestd = a[j];
-                        lab = j0 + j;
-                    }
-            }
+        double bestd = 0.0;
+        float m1 = 0.f, m2 = 0.f, xx = 0.f;
+        if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
+        const float sc = sqrtf(xx) * 1.0001f + cmax;
+        const unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+        if (tie) exact_ties<T>(tie, S, base + warp * 32, n, k, Cm, lab);
+        if (valid) {  // the row's cost: the reference distance to its centre
+            bestd = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
             labels[i] = lab;
         }
         // stable counting sort of the round's rows by label
@@ -388,12 +636,29 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         __syncthreads();
         if (valid) sorted[wcnt[warp * k + lab] + rank] = tid;
         cost += cta_sum(valid ? bestd : 0.0, red);  // thread 0's copy is the one used
-        // per-cluster sums of this round, rows in order, added to the CTA accumulator
-        for (int64_t e = tid; e < kn; e += kWT) {
-            const int j = (int)(e / n), d = (int)(e - (int64_t)j * n);
-            double sj = 0.0;
-            for (int q = cstart[j]; q < cstart[j + 1]; ++q) sj += (double)S[(base + sorted[q]) * n + d];
-            acc[e] += sj;
+        // per-cluster sums of this round: warp w takes clusters w, w+8, ..., walks the cluster's
+        // rows in order with lanes over dims (coalesced row loads), then adds to the CTA
+        // accumulator (each (j, d) owned by one lane: fixed order, no atomics)
+        for (int j = warp; j < k; j += kWT / 32) {
+            const int q0 = cstart[j], q1 = cstart[j + 1];
+            if (q0 == q1) continue;
+            for (int d0 = lane * 4; d0 < n; d0 += 128) {
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+                for (int q = q0; q < q1; ++q) {
+                    double v[4];
+                    load4d<T>(S + (base + sorted[q]) * n, d0, n, vecd, v);
+                    a0 += v[0];
+                    a1 += v[1];
+                    a2 += v[2];
+                    a3 += v[3];
+                }
+                double* aj = acc + (int64_t)j * n + d0;
+                aj[0] += a0;
+                if (d0 + 1 < n) aj[1] += a1;
+                if (d0 + 2 < n) aj[2] += a2;
+                if (d0 + 3 < n) aj[3] += a3;
+            }
         }
         for (int j = tid; j < k; j += kWT) cnt[j] += (double)(cstart[j + 1] - cstart[j]);
         __syncthreads();
@@ -565,26 +830,33 @@ __global__ void wide_output_kernel(const StepParams p, WideBufs b, int w0) {
 // argmin over the valid centres, per-block cost by thread-sequential sums and a fixed tree
 template <typename T>
 __global__ void __launch_bounds__(kWT) wide_objective_kernel(const ObjParams p) {
+    extern __shared__ __align__(16) float orec[];
     __shared__ double red[kWT];
+    __shared__ float red_f[1];
     const T* X = static_cast<const T*>(p.X);
     const int n = p.n, kv = p.kv;
+    const int kpad = (kv + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
+    float* rec = orec;
+    float* ccs = rec + (int64_t)kpad * n4;
+    build_records(p.C, kv, kpad, n, n4, rec, ccs);
+    const float cmax = records_cmax(ccs, kpad, red_f);
+    const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
+    const bool vec = sizeof(T) == 4 && (n & 3) == 0;
+    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
     double cost = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x; i < p.m; i += (int64_t)gridDim.x * kWT) {
-        const T* x = X + i * n;
-        double bestd = __longlong_as_double(0x7ff0000000000000LL);
+    const int64_t stride = (int64_t)gridDim.x * kWT;
+    const int64_t iters = (p.m + stride - 1) / stride;  // uniform trip count: warp-collective ties
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t i = it * stride + (int64_t)blockIdx.x * kWT + threadIdx.x;
+        const bool valid = i < p.m;
         int lab = 0;
-        for (int j0 = 0; j0 < kv; j0 += kJT) {
-            double a[kJT];
-            const int jn = min(kJT, kv - j0);
-            dist_tile<T>(x, n, p.C + (int64_t)j0 * n, jn, a);
-#pragma unroll
-            for (int j = 0; j < kJT; ++j)
-                if (j < jn && a[j] < bestd) {
-                    bestd = a[j];
-                    lab = j0 + j;
-                }
-        }
-        cost += bestd;
+        float m1 = 0.f, m2 = 0.f, xx = 0.f;
+        if (valid) screen_row<T>(X + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
+        const float sc = sqrtf(xx) * 1.0001f + cmax;
+        const unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+        if (tie) exact_ties<T>(tie, X, i - (threadIdx.x & 31), n, kv, p.C, lab);
+        if (!valid) continue;
+        cost += dist1<T>(X + i * n, n, p.C + (int64_t)lab * n, vecd);
         const int orig = p.remap ? p.remap[lab] : lab;
         if (p.labels) p.labels[i] = orig;
         if (p.counts) atomicAdd(p.counts + orig, 1ull);
@@ -674,23 +946,36 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     wide_gather_kernel<T><<<dim3((unsigned)std::min<int64_t>((s + 7) / 8, 4096), (unsigned)Wb), kWT, 0, st>>>(
         p, w0, static_cast<T*>(b.S));
     wide_init_kernel<T><<<Wb, kWT, 0, st>>>(p, w0, b);
-    wide_d2init_kernel<T><<<rows_grid, kWT, 0, st>>>(p, b);
+    {
+        const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
+        const size_t rs = (size_t)kpad * n4 * 4 + (size_t)kpad * 4;
+        e = cudaFuncSetAttribute(wide_d2init_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs);
+        if (e != cudaSuccess) return e;
+        wide_d2init_kernel<T><<<rows_grid, kWT, rs, st>>>(p, b);
+    }
     // K-means++ slots: as many host iterations as the worker with the most pending slots
     int32_t slots = 0;
     wide_max_pending_kernel<<<1, 256, 0, st>>>(b, Wb);
     e = cudaMemcpyAsync(&slots, b.active, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
+    const size_t cost_smem = (size_t)ncand * ((n + 3) & ~3) * 4;
+    if (slots > 0) {
+        e = cudaFuncSetAttribute(wide_cost_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem);
+        if (e != cudaSuccess) return e;
+    }
     for (int it = 0; it < slots; ++it) {
         wide_cdf_kernel<<<dim3((unsigned)((nblk + 63) / 64), (unsigned)Wb), 64, 0, st>>>(p, b, nblk);
         wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
-        wide_cost_kernel<T><<<dim3((unsigned)nblk, (unsigned)Wb), kWT, 0, st>>>(p, b, nblk);
+        wide_cost_kernel<T><<<dim3((unsigned)nblk, (unsigned)Wb), kWT, cost_smem, st>>>(p, b, nblk);
         wide_decide_kernel<<<Wb, 128, 0, st>>>(p, b, nblk);
         wide_d2upd_kernel<<<rows_grid, kWT, 0, st>>>(p, b, it);
     }
     // Lloyd: passes until every worker of the batch stopped
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
-    const size_t smem = (size_t)(kn + k + kWT) * 8 + (size_t)(8 * k + k + 1 + kWT) * 4;
+    const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
+    const size_t smem = (size_t)(kn + k + kWT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
+                        (size_t)(8 * k + k + 1 + kWT) * 4;
     e = cudaFuncSetAttribute(wide_assign_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         if (why) *why = "wide step: k*n too large for the pass accumulator";
@@ -722,10 +1007,17 @@ cudaError_t launch_objective_wide(int dtype, const ObjParams& p, int* nblocks, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nb = std::max(1, std::min(nblocks[0], sms * 4));  // fixed per device: reproducible
     nblocks[0] = nb;
+    const int kpad = (p.kv + kKT - 1) / kKT * kKT, n4 = (p.n + 3) & ~3;
+    const size_t rs = (size_t)kpad * n4 * 4 + (size_t)kpad * 4;
+    cudaError_t e = dtype == 0 ? cudaFuncSetAttribute(wide_objective_kernel<float>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs)
+                               : cudaFuncSetAttribute(wide_objective_kernel<double>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs);
+    if (e != cudaSuccess) return e;
     if (dtype == 0)
-        wide_objective_kernel<float><<<nb, kWT, 0, st>>>(p);
+        wide_objective_kernel<float><<<nb, kWT, rs, st>>>(p);
     else
-        wide_objective_kernel<double><<<nb, kWT, 0, st>>>(p);
+        wide_objective_kernel<double><<<nb, kWT, rs, st>>>(p);
     return cudaGetLastError();
 }
 
