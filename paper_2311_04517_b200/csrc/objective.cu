@@ -84,14 +84,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <typename T, int NP>
-static bool make_tmap(const ObjParams& p, CUtensorMap* map) {
-    using O = ObjGeo<T, NP>;
+template <typename T>
+static bool make_tmap(const ObjParams& p, int box_rows, CUtensorMap* map) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.m};
     const cuuint64_t strides[1] = {(cuuint64_t)p.n * sizeof(T)};
-    const cuuint32_t box[2] = {(cuuint32_t)p.n, (cuuint32_t)O::GR};
+    const cuuint32_t box[2] = {(cuuint32_t)p.n, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const int rb = p.n * (int)sizeof(T);
     const CUtensorMapSwizzle sw = rb == 32    ? CU_TENSOR_MAP_SWIZZLE_32B
@@ -104,14 +103,9 @@ static bool make_tmap(const ObjParams& p, CUtensorMap* map) {
     return r == CUDA_SUCCESS;
 }
 
-template <typename T, int NP>
-static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_t st) {
-    ObjParams p = p_in;
-    CUtensorMap tmap;
-    memset(&tmap, 0, sizeof tmap);
-    p.use_tma = (!getenv("HPCG_NO_TMA") && tma_ok<T, NP>(p) && make_tmap<T, NP>(p, &tmap)) ? 1 : 0;
-    const int smem = objective_smem<T, NP>(p.kv);
-    auto kern = objective_kernel<T, NP>;
+template <typename K>
+static cudaError_t launch_grid(K kern, int smem, const ObjParams& p, const CUtensorMap& tmap, int* nblocks,
+                               cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0, dev = 0, sms = 148;
@@ -128,6 +122,22 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
     nblocks[0] = nb;
     kern<<<nb, kObjThreads, smem, st>>>(p, tmap);
     return cudaGetLastError();
+}
+
+template <typename T, int NP>
+static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_t st) {
+    ObjParams p = p_in;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof tmap);
+    static const bool old = getenv("HPCG_OBJ_OLD") != nullptr || getenv("HPCG_NO_TMA") != nullptr;
+    if constexpr (sizeof(T) == 4 && NP % 4 == 0 && NP != 24) {  // centre-pair kernel (fp32, TMA widths)
+        if (!old && tma_ok<T, NP>(p) && make_tmap<T>(p, PairGeo<NP>::GR, &tmap)) {
+            p.use_tma = 1;
+            return launch_grid(objective_pairs_kernel<NP>, objective_pairs_smem<NP>(p.kv), p, tmap, nblocks, st);
+        }
+    }
+    p.use_tma = (!getenv("HPCG_NO_TMA") && tma_ok<T, NP>(p) && make_tmap<T>(p, ObjGeo<T, NP>::GR, &tmap)) ? 1 : 0;
+    return launch_grid(objective_kernel<T, NP>, objective_smem<T, NP>(p.kv), p, tmap, nblocks, st);
 }
 
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {

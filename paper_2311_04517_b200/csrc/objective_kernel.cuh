@@ -332,6 +332,241 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// fp32 rows, 16-B-multiple widths, TMA-fed: centre-pair screen.
+// Each FFMA2 evaluates one dimension for TWO centres (record pair (-2c_a,d, -2c_b,d)) with the
+// row value as a broadcast scalar operand, so a pair of screened distances costs NP FFMA2 and
+// no horizontal add; top-2 tracking takes the pair as a sorted (lo, hi) with a three-input min.
+// Rows are copied to registers as soon as their stage lands and the stage is refilled at once
+// (one 32R-row stage per warp keeps 8 KB per warp in flight during the compute).
+// Screen error: sequential fused chain of NP terms on a rounded record, so
+// |d~ - d| <= (NP + 2) u (|x| + |c|)^2; kPairKappa doubles that (difference of two) with slack.
+template <int NP>
+struct PairGeo {
+    using G = Geo<float, NP>;
+    static constexpr int R = NP <= 8 ? 4 : NP <= 16 ? 3 : 2;  // rows per lane
+    static constexpr int GR = 32 * R;            // rows per stage
+    static constexpr int STAGE = GR * G::RS;     // bytes per stage
+    static constexpr int STAGES = 1;             // stages per warp (refilled as soon as read; 2-3 measured slower)
+    static constexpr int RST = NP + 2;           // record stride in float2 (16-B multiple)
+    static constexpr int CDS = NP + 1;           // fp64 centre stride (doubles): odd, so the
+                                                 // 8-B loads of up to 16 distinct centres in a
+                                                 // half-warp phase hit distinct bank pairs
+    static constexpr int WARPS = kObjThreads / 32;
+    static constexpr float kappa = 2.0f * (float)(NP + 12) * 5.9604645e-8f;
+};
+
+template <int NP>
+__host__ __device__ inline int objective_pairs_smem(int kv) {
+    using PG = PairGeo<NP>;
+    const int kp = (kv + 1) / 2;
+    const int rec = kp * PG::RST * 8;
+    const int cd = ((kv * PG::CDS * 8 + 15) & ~15);
+    return ((rec + cd + 1023) & ~1023) + PG::WARPS * PG::STAGES * PG::STAGE + 1024;
+}
+
+HPCG_DEV float fmin3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const ObjParams p,
+                                                                         const __grid_constant__ CUtensorMap tmap) {
+    using PG = PairGeo<NP>;
+    using G = typename PG::G;
+    constexpr int R = PG::R, RST = PG::RST, CDS = PG::CDS, GR = PG::GR;
+    extern __shared__ __align__(16) unsigned char osm[];
+    const int kv = p.kv, kp = (kv + 1) / 2;
+    float2* rp = reinterpret_cast<float2*>(osm);
+    double* Cd = reinterpret_cast<double*>(osm + kp * RST * 8);
+    unsigned char* rings = osm + (((kp * RST * 8) + ((kv * CDS * 8 + 15) & ~15) + 1023) & ~1023);
+    rings += (1024 - (smem_u32(rings) & 1023)) & 1023;
+    __shared__ __align__(8) uint64_t s_bar[PG::WARPS][PG::STAGES];
+    __shared__ float s_cmax;
+    __shared__ double s_wcost[PG::WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int e = tid; e < kv * CDS; e += kObjThreads) {
+        const int j = e / CDS, d = e - j * CDS;
+        Cd[e] = d < NP ? p.C[(int64_t)j * NP + d] : 0.0;
+    }
+    __syncthreads();
+    // records: pair q holds centres 2q, 2q+1 interleaved; a missing odd partner screens +inf
+    for (int j = tid; j < 2 * kp; j += kObjThreads) {
+        float* rec = reinterpret_cast<float*>(rp + (j >> 1) * RST) + (j & 1);
+        if (j < kv) {
+            double cc = 0.0;
+            for (int d = 0; d < NP; ++d) {
+                const double c = Cd[j * CDS + d];
+                cc += c * c;
+                rec[2 * d] = (float)(-2.0 * c);
+            }
+            rec[2 * NP] = (float)cc;
+        } else {
+            for (int d = 0; d < NP; ++d) rec[2 * d] = 0.f;
+            rec[2 * NP] = __int_as_float(0x7f800000);
+        }
+        rec[2 * NP + 2] = 0.f;
+    }
+    if (lane == 0) {
+        for (int st = 0; st < PG::STAGES; ++st) mbar_init(&s_bar[warp][st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+        float cm = 0.f;
+        for (int j = 0; j < kv; ++j)
+            cm = fmaxf(cm, sqrtf(reinterpret_cast<const float*>(rp + (j >> 1) * RST + NP)[j & 1]) * 1.0001f);
+        s_cmax = cm;
+    }
+    __syncthreads();
+    const float cmax = s_cmax;
+
+    float* ring = reinterpret_cast<float*>(rings + warp * PG::STAGES * PG::STAGE);
+    const int64_t m = p.m;
+    const int64_t ngroups = (m + GR - 1) / GR;
+    const int64_t wglobal = (int64_t)blockIdx.x * PG::WARPS + warp;
+    const int64_t wstride = (int64_t)gridDim.x * PG::WARPS;
+    const int64_t my_groups = wglobal < ngroups ? (ngroups - wglobal + wstride - 1) / wstride : 0;
+    auto issue = [&](int64_t i) {
+        if (i < my_groups && lane == 0) {
+            uint64_t* bar = &s_bar[warp][i % PG::STAGES];
+            fence_proxy_async();  // this warp's generic reads of the stage precede the async write
+            mbar_expect_tx(bar, (uint32_t)PG::STAGE);
+            tma_load_2d(ring + (i % PG::STAGES) * (PG::STAGE / 4), &tmap, 0, (int)((wglobal + i * wstride) * GR), bar);
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < PG::STAGES; ++st) issue(st);
+
+    double cost = 0.0;
+#pragma unroll 1
+    for (int64_t i = 0; i < my_groups; ++i) {
+        mbar_wait_cta(&s_bar[warp][i % PG::STAGES], (uint32_t)((i / PG::STAGES) & 1));
+        const float* slot = ring + (i % PG::STAGES) * (PG::STAGE / 4);
+        const int64_t row0 = (wglobal + i * wstride) * GR;
+        const bool full = row0 + GR <= m;
+        float x[R][NP];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int q = 0; q < NP / 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4*>(slot + G::elem_off(r * 32 + lane, q * 4));
+                x[r][4 * q] = v.x;
+                x[r][4 * q + 1] = v.y;
+                x[r][4 * q + 2] = v.z;
+                x[r][4 * q + 3] = v.w;
+            }
+        }
+        __syncwarp();
+        issue(i + PG::STAGES);
+
+        float m1[R], m2[R];
+        int i1[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            m1[r] = __int_as_float(0x7f800000);
+            m2[r] = __int_as_float(0x7f800000);
+            i1[r] = 0;
+        }
+#pragma unroll 1
+        for (int q = 0; q < kp; ++q) {
+            const float4* rq = reinterpret_cast<const float4*>(rp + q * RST);
+            const float4 iv = rq[NP / 2];
+            float2 acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = make_float2(iv.x, iv.y);
+#pragma unroll
+            for (int h = 0; h < NP / 2; ++h) {
+                const float4 c = rq[h];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc[r] = __ffma2_rn(make_float2(x[r][2 * h], x[r][2 * h]), make_float2(c.x, c.y), acc[r]);
+                    acc[r] = __ffma2_rn(make_float2(x[r][2 * h + 1], x[r][2 * h + 1]), make_float2(c.z, c.w), acc[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float da = acc[r].x, db = acc[r].y;
+                const float lo = fminf(da, db), hi = fmaxf(da, db);
+                const int li = 2 * q + (db < da ? 1 : 0);
+                m2[r] = fmin3f(m2[r], hi, fmaxf(m1[r], lo));
+                i1[r] = lo < m1[r] ? li : i1[r];
+                m1[r] = fminf(m1[r], lo);
+            }
+        }
+        // near ties: exact reference argmin, warp-parallel over centres (core.hpp:146-157)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool valid = full || row0 + r * 32 + lane < m;
+            float2 nn2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d = 0; d < NP; d += 2) nn2 = __ffma2_rn(make_float2(x[r][d], x[r][d + 1]),
+                                                             make_float2(x[r][d], x[r][d + 1]), nn2);
+            float sx;
+            asm("sqrt.approx.f32 %0, %1;" : "=f"(sx) : "f"(nn2.x + nn2.y));
+            const float sc = fmaf(sx, 1.0001f, cmax);
+            unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2[r] - m1[r] > PG::kappa * sc * sc));
+            while (tie) {
+                const int src = __ffs(tie) - 1;
+                tie &= tie - 1;
+                float xr[NP];
+#pragma unroll
+                for (int d = 0; d < NP; ++d) xr[d] = __shfl_sync(0xffffffffu, x[r][d], src);
+                double dv = __longlong_as_double(0x7ff0000000000000LL);
+                int dj = 0x7fffffff;
+                for (int j = lane; j < kv; j += 32) {
+                    const double dd = exact_dist_regs<float, NP>(xr, Cd + j * CDS);
+                    if (dd < dv) {
+                        dv = dd;
+                        dj = j;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, dj, o);
+                    if (ov < dv || (ov == dv && oj < dj)) {
+                        dv = ov;
+                        dj = oj;
+                    }
+                }
+                if (lane == src) i1[r] = dj;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t row = row0 + r * 32 + lane;
+            if (!full && row >= m) continue;
+            const int lab = i1[r];
+            // row cost: fp64 distance to the chosen centre (two interleaved DFMA chains; within
+            // 1e-15 relative of the reference's per-row value)
+            const double* cj = Cd + lab * CDS;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int h = 0; h < NP / 2; ++h) {
+                const double d0 = (double)x[r][2 * h] - cj[2 * h], d1 = (double)x[r][2 * h + 1] - cj[2 * h + 1];
+                a0 = fma(d0, d0, a0);
+                a1 = fma(d1, d1, a1);
+            }
+            cost += a0 + a1;
+            if (p.labels) p.labels[row] = p.remap[lab];
+            if (p.counts) atomicAdd(p.counts + p.remap[lab], 1ULL);
+        }
+    }
+    cost = warp_sum(cost);
+    if (lane == 0) s_wcost[warp] = cost;
+    __syncthreads();
+    if (tid == 0) {
+        double v = 0.0;
+        for (int w = 0; w < PG::WARPS; ++w) v += s_wcost[w];
+        p.block_cost[blockIdx.x] = v;
+    }
+}
+
 // Fixed-order final sum of the block partials (deterministic f(C,X)).
 static __global__ void sum_blocks_kernel(const double* part, int nparts, double* out) {
     __shared__ double s[32];
