@@ -365,11 +365,6 @@ __host__ __device__ inline int objective_pairs_smem(int kv) {
     return ((rec + cd + 1023) & ~1023) + PG::WARPS * PG::STAGES * PG::STAGE + 1024;
 }
 
-HPCG_DEV float fmin3f(float a, float b, float c) {
-    float r;
-    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-    return r;
-}
 
 template <int NP>
 __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const ObjParams p,

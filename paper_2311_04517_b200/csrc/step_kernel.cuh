@@ -103,6 +103,7 @@ struct Geo {
     static constexpr int CPR = VEC16 ? RS / 16 : 1;            // chunks per row
     static constexpr int NPF = (NP + 1) & ~1;                  // fp32 screen dims (pairs)
     static constexpr int CSR = ((NPF + 2) + 3) & ~3;           // screen record floats (16-B mult)
+    static constexpr int RST = NPF + 2;                        // centre-pair record stride (float2)
     static constexpr int R = NP <= 16 ? 4 : 2;                 // rows per thread in the assign pass
     static constexpr int GROUP = 32 * R;                       // rows per warp group
     static constexpr int LPR = NP <= 1 ? 1 : NP <= 2 ? 2 : NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;
@@ -159,7 +160,7 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand
     L.samp = 0;
     L.cm = up(L.samp + rows_cap * G::RS);
     L.cs = up(L.cm + k * NP * 8);
-    L.part = up(L.cs + k * G::CSR * 4);
+    L.part = up(L.cs + ((k + 1) / 2) * G::RST * 8);
     L.scratch = up(L.part + xch_doubles(k, NP, C) * 8);  // exchange receive buffers
     L.labels = L.scratch;
     L.pos = up(L.labels + rows_cap);
@@ -278,6 +279,12 @@ HPCG_DEV void load_row_f32(const T* samp, int row, float2 (&x2)[Geo<T, NP>::NPF 
             x2[q] = make_float2(a, b);
         }
     }
+}
+
+HPCG_DEV float fmin3f(float a, float b, float c) {  // three-input min (sm_100 FMNMX3)
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
 }
 
 // K-means++ screens, expanded form: dist ~ s + x.(-2c), s = |x|^2 + |c|^2, with the seed
@@ -1098,22 +1105,33 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
     if (run_lloyd) {
         // error bound of the fp32 expanded-form screen vs the exact fp64 distance:
         // |screen - exact| <= kappa (|x| + max|c|)^2 per centroid; two centroids compared
-        constexpr float kappa = 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
+        // (centre-pair screen: one fused chain of NPF terms per distance)
+        constexpr float kappa = 2.0f * (float)(G::NPF + 12) * 5.9604645e-8f;
         bool closing = false;
         int pass = 0;
         // screen record of centroid j from its fp64 master value c (lane = dimension):
         // c' = -2c (fp32), |c|^2 (fp32 sum of rounded squares), |c| rounded up into sh.cnorm
+        // Records are centre PAIRS: pair q interleaves centres 2q, 2q+1 per dimension, so one
+        // FFMA2 with the row value as broadcast scalar advances both distances.
         auto make_rec = [&](int j, double c) {
-            float* rec = cs + j * G::CSR;
-            if (lane < G::NPF) rec[lane] = lane < NP ? (float)(-2.0 * c) : 0.f;
+            float* rec = cs + (j >> 1) * (2 * G::RST) + (j & 1);
+            if (lane < G::NPF) rec[2 * lane] = lane < NP ? (float)(-2.0 * c) : 0.f;
             const float cc = warp_sum_f(lane < NP ? (float)(c * c) : 0.f);
             if (lane == 0) {
-                rec[G::NPF] = cc;
-                rec[G::NPF + 1] = 0.f;
+                rec[2 * G::NPF] = cc;
+                rec[2 * G::NPF + 2] = 0.f;
                 sh.cnorm[j] = sqrtf(cc) * 1.0001f;
             }
         };
         for (int j = warp; j < k; j += kStepWarps) make_rec(j, lane < NP ? Cm[j * NP + lane] : 0.0);
+        if ((k & 1) && warp == kStepWarps - 1) {  // odd k: the missing partner never wins
+            float* rec = cs + (k >> 1) * (2 * G::RST) + 1;
+            if (lane < G::NPF) rec[2 * lane] = 0.f;
+            if (lane == 0) {
+                rec[2 * G::NPF] = 1e38f;
+                rec[2 * G::NPF + 2] = 0.f;
+            }
+        }
         __syncthreads();
         for (;; ++pass) {
             // max |c_j| over the centroids (records made by the previous means phase)
@@ -1152,22 +1170,31 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     m2[r] = __int_as_float(0x7f800000);
                     i1[r] = 0;
                 }
-                for (int j = 0; j < k; ++j) {
-                    const float* rec = cs + j * G::CSR;
-                    float2 c2[G::NPF / 2];
+                const int kp = (k + 1) >> 1;
+#pragma unroll 1
+                for (int jp = 0; jp < kp; ++jp) {
+                    const float4* rq = reinterpret_cast<const float4*>(cs + jp * (2 * G::RST));
+                    const float4 iv = rq[G::NPF / 2];
+                    float2 acc[RR];
 #pragma unroll
-                    for (int q = 0; q < G::NPF / 2; ++q) c2[q] = *reinterpret_cast<const float2*>(rec + 2 * q);
-                    const float2 init = *reinterpret_cast<const float2*>(rec + G::NPF);
+                    for (int r = 0; r < RR; ++r) acc[r] = make_float2(iv.x, iv.y);
 #pragma unroll
-                    for (int r = 0; r < RR; ++r) {
-                        float2 acc = init;
+                    for (int h = 0; h < G::NPF / 2; ++h) {
+                        const float4 c = rq[h];
 #pragma unroll
-                        for (int q = 0; q < G::NPF / 2; ++q) acc = __ffma2_rn(x2[r][q], c2[q], acc);
-                        const float dj = acc.x + acc.y;
-                        m2[r] = fminf(m2[r], fmaxf(m1[r], dj));
-                        const bool lt = dj < m1[r];
-                        m1[r] = fminf(m1[r], dj);
-                        i1[r] = lt ? j : i1[r];
+                        for (int r = 0; r < RR; ++r) {
+                            acc[r] = __ffma2_rn(make_float2(x2[r][h].x, x2[r][h].x), make_float2(c.x, c.y), acc[r]);
+                            acc[r] = __ffma2_rn(make_float2(x2[r][h].y, x2[r][h].y), make_float2(c.z, c.w), acc[r]);
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) {  // sorted pair into the top-2
+                        const float da = acc[r].x, db = acc[r].y;
+                        const float lo = fminf(da, db), hi = fmaxf(da, db);
+                        const int li = 2 * jp + (db < da ? 1 : 0);
+                        m2[r] = fmin3f(m2[r], hi, fmaxf(m1[r], lo));
+                        i1[r] = lo < m1[r] ? li : i1[r];
+                        m1[r] = fminf(m1[r], lo);
                     }
                 }
                 // near ties (k == 1 gives m2 = inf: never): exact reference argmin, warp-parallel --

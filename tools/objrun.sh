@@ -1,7 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for v in "" tools/var_U4.so tools/var_T1.so; do
-  echo "== variant ${v:-main}"
-  for a in --means "" --means; do HPCG_LIB_OVERRIDE=$v python tools/dbg_obj.py $a 2>&1 | head -1; done
+for c in "" 7 8 10 12; do
+  echo "== cluster ${c:-auto}"
+  HPCG_CLUSTER=$c HPCG_DEBUG=1 python tools/quick_time.py 2>&1 | grep -E "round [0-3]|cluster" | head -5
 done
-timeout 600 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -2
-HPCG_LIB_OVERRIDE=tools/var_U4.so timeout 600 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -2
