@@ -105,6 +105,21 @@ def test_empty_cluster_and_duplicates():
     assert centroid_close(r["centroids"][0], e["centroids"])
 
 
+def test_exact_ties_fp32_rows_pair_kernel():
+    # fp32 16-wide rows on an integer lattice, centres placed so many rows are exactly
+    # equidistant from two or more centres (ties resolved to the lowest index, core.hpp:146-157)
+    rs = np.random.default_rng(3)
+    X = rs.integers(-4, 5, (100003, 16)).astype(np.float32)
+    C_ = np.zeros((9, 16))
+    for j in range(1, 9):
+        C_[j, (j - 1) % 16] = 2.0 if j % 2 else -2.0
+    C_[5] = C_[1]  # duplicate centre: never chosen over slot 1
+    lab, cnt, cost, _ = orc().assign(X.astype(np.float64), C_)
+    a, f = hp.final_assignment(X, C_)
+    assert np.array_equal(a.labels, lab) and np.array_equal(a.counts, cnt)
+    assert f == cost  # small integers: exact
+
+
 def test_exact_ties_go_to_lowest_index():
     # X={(5)}, C={(4),(6)} -> label 0; plus many exact ties on a lattice
     a = hp.assign_nearest(np.array([[5.0]]), np.array([[4.0], [6.0]]))
@@ -119,7 +134,11 @@ def test_exact_ties_go_to_lowest_index():
 
 
 @pytest.mark.parametrize("dtype,n,k", [(np.float64, 2, 5), (np.float32, 16, 10), (np.float64, 3, 25),
-                                       (np.float32, 8, 15), (np.float32, 1, 3)])
+                                       (np.float32, 8, 15), (np.float32, 1, 3),
+                                       # centre-pair kernel widths (16/32/48/128-B rows), odd and
+                                       # large centre counts
+                                       (np.float32, 4, 7), (np.float32, 12, 33), (np.float32, 32, 64),
+                                       (np.float32, 16, 1), (np.float32, 16, 255)])
 def test_objective_vs_oracle(dtype, n, k):
     X = mixture(200003, n, k, seed=11 + n, dtype=dtype)
     C_ = mixture(k, n, k, seed=99, dtype=np.float64)
@@ -128,6 +147,8 @@ def test_objective_vs_oracle(dtype, n, k):
     assert np.array_equal(a.labels, lab)
     assert np.array_equal(a.counts, cnt)
     assert rel(f, cost) <= RTOL
+    if k == 1:
+        return  # no valid subset left to test
     # valid-subset (engine.hpp:211-229)
     deg = np.zeros(k, np.uint8)
     deg[0] = 1
