@@ -34,6 +34,7 @@ cudaError_t launch_objective_wide(int dtype, const ObjParams& p, int* nblocks, c
 
 // *nblocks: in = capacity of p.block_cost, out = grid used (fixed per device/kernel/kv)
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st);
+bool objective_device_kv(int dtype, int n, int kv);  // resident kernel (honours kv_dev)?
 int objective_blocks();  // fixed grid for deterministic block partials
 
 }  // namespace hpcg

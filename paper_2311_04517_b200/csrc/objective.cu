@@ -140,6 +140,13 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
     return launch_grid(objective_kernel<T, NP>, objective_smem<T, NP>(p.kv), p, tmap, nblocks, st);
 }
 
+// true when launch_objective takes a resident kernel for this shape, i.e. one that honours
+// ObjParams::kv_dev (the grid-wide kernel needs the exact count on the host)
+bool objective_device_kv(int dtype, int n, int kv) {
+    static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
+    return pick_np(dtype, n) != 0 && kv <= kObjMaxK && !force_wide;
+}
+
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {
     const int np = pick_np(dtype, p.n);
     static const bool force_wide = getenv("HPCG_WIDE") != nullptr;

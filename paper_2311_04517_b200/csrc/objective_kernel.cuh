@@ -28,7 +28,15 @@ struct ObjParams {
     unsigned long long* counts;  // [k original] or null (atomics on integers: order-free)
     double* block_cost;    // [gridDim.x]
     int32_t use_tma;       // 1: stages arrive by TMA (tensor map built by the host), 0: cp.async
+    const int32_t* kv_dev; // optional device-side valid count (<= kv, which then only sizes smem)
 };
+
+// valid centre count: the device value when given (the host launched with an upper bound)
+HPCG_DEV int obj_kv(const ObjParams& p) {
+    if (!p.kv_dev) return p.kv;
+    const int v = *p.kv_dev;
+    return v < p.kv ? (v > 0 ? v : 0) : p.kv;
+}
 
 // TMA tile load of `rows` x n into a swizzled smem slot (box = {n, GR}); the hardware
 // 32B/64B/128B swizzle equals Geo::swz for these row widths (chunk ^= row bits).
@@ -80,11 +88,11 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
     using G = typename O::G;
     constexpr int NPF = O::NPF, R = O::R, CSR = O::CSR;
     extern __shared__ __align__(16) unsigned char osm[];
-    const int kv = p.kv, n = p.n;
+    const int kvl = p.kv, kv = obj_kv(p), n = p.n;  // kvl: smem layout (launch bound)
     float* cs = reinterpret_cast<float*>(osm);
     constexpr int CDS = O::CDS;
-    double* Cd = reinterpret_cast<double*>(osm + ((kv * CSR * 4 + 15) & ~15));
-    unsigned char* rings = osm + ((((kv * CSR * 4 + 15) & ~15) + ((kv * CDS * 8 + 15) & ~15) + 1023) & ~1023);
+    double* Cd = reinterpret_cast<double*>(osm + ((kvl * CSR * 4 + 15) & ~15));
+    unsigned char* rings = osm + ((((kvl * CSR * 4 + 15) & ~15) + ((kvl * CDS * 8 + 15) & ~15) + 1023) & ~1023);
     rings += (1024 - (smem_u32(rings) & 1023)) & 1023;  // swizzle atom alignment (absolute address)
     __shared__ __align__(8) uint64_t s_bar[kObjThreads / 32][4];
     __shared__ float s_cmax;
@@ -373,10 +381,11 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
     using G = typename PG::G;
     constexpr int R = PG::R, RST = PG::RST, CDS = PG::CDS, GR = PG::GR;
     extern __shared__ __align__(16) unsigned char osm[];
-    const int kv = p.kv, kp = (kv + 1) / 2;
+    const int kvl = p.kv, kpl = (kvl + 1) / 2;  // smem layout (launch bound)
+    const int kv = obj_kv(p), kp = (kv + 1) / 2;
     float2* rp = reinterpret_cast<float2*>(osm);
-    double* Cd = reinterpret_cast<double*>(osm + kp * RST * 8);
-    unsigned char* rings = osm + (((kp * RST * 8) + ((kv * CDS * 8 + 15) & ~15) + 1023) & ~1023);
+    double* Cd = reinterpret_cast<double*>(osm + kpl * RST * 8);
+    unsigned char* rings = osm + (((kpl * RST * 8) + ((kvl * CDS * 8 + 15) & ~15) + 1023) & ~1023);
     rings += (1024 - (smem_u32(rings) & 1023)) & 1023;
     __shared__ __align__(8) uint64_t s_bar[PG::WARPS][PG::STAGES];
     __shared__ float s_cmax;

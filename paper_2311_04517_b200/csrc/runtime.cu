@@ -315,6 +315,68 @@ __global__ void fill_f64_kernel(double* p, int64_t n, double v) {
     if (i < n) p[i] = v;
 }
 
+// select_best (engine.hpp:180-194: strict <, worker-id order, infinite never wins) and the
+// valid-subset compaction of the winner (engine.hpp:211-229) on the device, so the final
+// objective launches without a host round trip. sel = {best worker or -1, valid count}.
+__global__ void finish_select_kernel(const double* inc_obj, const double* inc_c, const uint8_t* inc_f, int W, int k,
+                                     int n, int32_t* sel, double* best_c, uint8_t* best_f, double* cv, int32_t* remap) {
+    __shared__ double so[32];
+    __shared__ int si[32];
+    __shared__ int s_best, s_kv;
+    double bo = __longlong_as_double(0x7ff0000000000000LL);
+    int bi = -1;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        const double o = inc_obj[w];
+        if (o < bo) {
+            bo = o;
+            bi = w;
+        }
+    }
+    auto better = [](double o, int i, double bo_, int bi_) {
+        return i >= 0 && (bi_ < 0 || o < bo_ || (o == bo_ && i < bi_));
+    };
+    for (int off = 16; off > 0; off >>= 1) {
+        const double oo = __shfl_down_sync(0xffffffffu, bo, off);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (better(oo, oi, bo, bi)) {
+            bo = oo;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        so[threadIdx.x >> 5] = bo;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = __longlong_as_double(0x7ff0000000000000LL);
+        int bw = -1;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            if (better(so[w], si[w], b, bw)) {
+                b = so[w];
+                bw = si[w];
+            }
+        int kv = 0;
+        if (bw >= 0)
+            for (int j = 0; j < k; ++j)
+                if (!inc_f[(int64_t)bw * k + j]) remap[kv++] = j;
+        s_best = bw;
+        s_kv = kv;
+        sel[0] = bw;
+        sel[1] = kv;
+    }
+    __syncthreads();
+    const int bw = s_best, kv = s_kv;
+    if (bw < 0) return;
+    const int64_t kn = (int64_t)k * n;
+    for (int64_t e = threadIdx.x; e < kn; e += blockDim.x) best_c[e] = inc_c[bw * kn + e];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) best_f[j] = inc_f[(int64_t)bw * k + j];
+    for (int64_t e = threadIdx.x; e < (int64_t)kv * n; e += blockDim.x) {
+        const int64_t r = e / n;
+        cv[e] = inc_c[bw * kn + (int64_t)remap[r] * n + (e - r * n)];
+    }
+}
+
 template <typename T>
 cudaError_t h2d(T* dst, const T* src, size_t count, cudaStream_t st) {
     return cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st);
@@ -327,10 +389,12 @@ cudaError_t d2h(T* dst, const T* src, size_t count, cudaStream_t st) {
 // Full-data assignment on device: valid centres C_valid_dev [kv x n], remap [kv];
 // labels_dev may be null; counts_dev (u64 x k) may be null; cost to cost_dev.
 int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev, const int32_t* remap_dev, int kv,
-               int32_t* labels_dev, unsigned long long* counts_dev, double* cost_dev, DevBuf& blocks) {
+               int32_t* labels_dev, unsigned long long* counts_dev, double* cost_dev, DevBuf& blocks,
+               const int32_t* kv_dev = nullptr) {
     const int nb = objective_blocks();
     CU(blocks.reserve((size_t)nb * sizeof(double)));
-    ObjParams op;
+    ObjParams op = {};
+    op.kv_dev = kv_dev;
     op.X = ds->X;
     op.m = ds->m;
     op.n = (int)ds->n;
@@ -819,8 +883,13 @@ struct hpcg_engine {
     DevBuf inc_c, inc_f, inc_obj, acc, nd, err, err_first, iters, stopb, filled, objb;
     DevBuf sh_ver, sh_obj, sh_worker, sh_c, sh_f;
     DevBuf log_acc, log_obj, nd_total, pub_log, pub_count;
-    DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks;
+    DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks, fin;
     int64_t pub_cap = 0;
+    void* pin = nullptr;  // pinned staging of the finish read-back (one synchronisation)
+    size_t pin_bytes = 0;
+    ~hpcg_engine() {
+        if (pin) cudaFreeHost(pin);
+    }
     // reference-RNG replay state
     std::vector<Mt64> streams;
     std::vector<int64_t> h_idx, h_fr;
@@ -1190,35 +1259,75 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;
     const int64_t W = e->W, k = e->k, n = e->n, kn = k * n, R = e->round;
-    std::vector<double> inc_obj((size_t)W);
-    std::vector<int32_t> errf((size_t)W);
-    std::vector<uint8_t> lacc((size_t)(std::max<int64_t>(R, 1) * W));
-    std::vector<double> lobj((size_t)(std::max<int64_t>(R, 1) * W));
-    unsigned long long ndt = 0;
-    int64_t npub = 0;
-    CU(d2h(inc_obj.data(), e->inc_obj.as<double>(), (size_t)W, st));
-    CU(d2h(errf.data(), e->err_first.as<int32_t>(), (size_t)W, st));
-    if (R > 0) {
-        CU(d2h(lacc.data(), e->log_acc.as<uint8_t>(), (size_t)(R * W), st));
-        CU(d2h(lobj.data(), e->log_obj.as<double>(), (size_t)(R * W), st));
+    const int64_t Rw = std::max<int64_t>(R, 1) * W;
+    const bool want_obj = e->cfg.compute_full_objective || e->cfg.compute_assignment;
+    const bool want_labels = e->cfg.compute_assignment && labels;
+    // resident objective kernels take the valid count from the device: select_best, the
+    // valid-subset compaction and f(C,X) are queued back to back and read back once
+    const bool dev_obj = want_obj && objective_device_kv(e->ds->dtype, (int)n, (int)k);
+    CU(e->scratch_a.reserve((size_t)kn * 8));
+    CU(e->scratch_b.reserve((size_t)k * 4));
+    CU(e->scratch_c.reserve(8));
+    CU(e->fin.reserve(16 + (size_t)kn * 8 + (size_t)k));
+    int32_t* sel_d = e->fin.as<int32_t>();
+    double* bc_d = reinterpret_cast<double*>(e->fin.as<unsigned char>() + 16);
+    uint8_t* bf_d = e->fin.as<uint8_t>() + 16 + kn * 8;
+    finish_select_kernel<<<1, 256, 0, st>>>(e->inc_obj.as<double>(), e->inc_c.as<double>(), e->inc_f.as<uint8_t>(),
+                                            (int)W, (int)k, (int)n, sel_d, bc_d, bf_d, e->scratch_a.as<double>(),
+                                            e->scratch_b.as<int32_t>());
+    CU(cudaGetLastError());
+    ctx->launches += 1;
+    DevBuf lab;
+    if (dev_obj) {
+        if (want_labels) CU(lab.reserve((size_t)e->ds->m * 4));
+        int rc = run_assign(ctx, e->ds, e->scratch_a.as<double>(), e->scratch_b.as<int32_t>(), (int)k,
+                            want_labels ? lab.as<int32_t>() : nullptr, nullptr, e->scratch_c.as<double>(), e->blocks,
+                            sel_d + 1);
+        if (rc) return rc;
     }
-    CU(d2h(&ndt, e->nd_total.as<unsigned long long>(), 1, st));
-    CU(d2h(&npub, e->pub_count.as<int64_t>(), 1, st));
+    // pinned staging: [inc_obj W][lobj Rw][bc kn][f][ndt][npub][sel 2x i32][errf W][lacc Rw][bf k]
+    const size_t need = (size_t)(W + Rw + kn + 3) * 8 + 8 + (size_t)W * 4 + (size_t)Rw + (size_t)k;
+    if (need > e->pin_bytes) {
+        if (e->pin) cudaFreeHost(e->pin);
+        e->pin = nullptr;
+        e->pin_bytes = 0;
+        CU(cudaHostAlloc(&e->pin, need, cudaHostAllocDefault));
+        e->pin_bytes = need;
+    }
+    double* h_obj = static_cast<double*>(e->pin);
+    double* h_lobj = h_obj + W;
+    double* h_bc = h_lobj + Rw;
+    double* h_f = h_bc + kn;
+    unsigned long long* h_ndt = reinterpret_cast<unsigned long long*>(h_f + 1);
+    int64_t* h_npub = reinterpret_cast<int64_t*>(h_f + 2);
+    int32_t* h_sel = reinterpret_cast<int32_t*>(h_f + 3);
+    int32_t* h_errf = h_sel + 2;
+    uint8_t* h_lacc = reinterpret_cast<uint8_t*>(h_errf + W);
+    uint8_t* h_bf = h_lacc + Rw;
+    CU(d2h(h_obj, e->inc_obj.as<double>(), (size_t)W, st));
+    CU(d2h(h_errf, e->err_first.as<int32_t>(), (size_t)W, st));
+    if (R > 0) {
+        CU(d2h(h_lacc, e->log_acc.as<uint8_t>(), (size_t)(R * W), st));
+        CU(d2h(h_lobj, e->log_obj.as<double>(), (size_t)(R * W), st));
+    }
+    CU(d2h(h_ndt, e->nd_total.as<unsigned long long>(), 1, st));
+    CU(d2h(h_npub, e->pub_count.as<int64_t>(), 1, st));
+    CU(d2h(h_sel, sel_d, 2, st));
+    CU(d2h(h_bc, bc_d, (size_t)kn, st));
+    CU(d2h(h_bf, bf_d, (size_t)k, st));
+    if (dev_obj) CU(d2h(h_f, e->scratch_c.as<double>(), 1, st));
     CU(cudaStreamSynchronize(st));
+    const unsigned long long ndt = *h_ndt;
+    const int64_t npub = *h_npub;
     // worker errors are rethrown after the join, lowest worker first (engine.hpp:330-331)
     for (int64_t w = 0; w < W; ++w) {
-        if (errf[(size_t)w] == kErrDegenerateInit) return fail(HPCG_EINVAL, "kmeans: degenerate centroid in init");
-        if (errf[(size_t)w] == kErrMonotone) return fail(HPCG_ELOGIC, "kmeans: objective increased between iterations");
+        if (h_errf[w] == kErrDegenerateInit) return fail(HPCG_EINVAL, "kmeans: degenerate centroid in init");
+        if (h_errf[w] == kErrMonotone) return fail(HPCG_ELOGIC, "kmeans: objective increased between iterations");
     }
-    // select_best (engine.hpp:180-194)
-    int best = -1;
-    double best_f = kInf;
-    for (int64_t w = 0; w < W; ++w)
-        if (inc_obj[(size_t)w] < best_f) {
-            best_f = inc_obj[(size_t)w];
-            best = (int)w;
-        }
+    // select_best (engine.hpp:180-194), evaluated on the device above
+    const int best = h_sel[0];
     if (best < 0) return fail(HPCG_ENOSOL, "no solution produced: every worker incumbent is infinite");
+    const double best_f = h_obj[best];
     hpcg_run_out o = {};
     o.best_worker = e->cfg.worker_base + best;
     o.best_sample_objective = best_f;
@@ -1228,10 +1337,10 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     for (int64_t w = 0; w < W; ++w) {
         int64_t cnt = 0;
         for (int64_t r = 0; r < R; ++r) {
-            if (!lacc[(size_t)(r * W + w)]) continue;
+            if (!h_lacc[r * W + w]) continue;
             if (traces && cnt < trace_cap) {
                 traces[(w * trace_cap + cnt) * 2 + 0] = (double)(r + 1);
-                traces[(w * trace_cap + cnt) * 2 + 1] = lobj[(size_t)(r * W + w)];
+                traces[(w * trace_cap + cnt) * 2 + 1] = h_lobj[r * W + w];
             }
             last_ts[(size_t)w] = (double)(r + 1);
             ++cnt;
@@ -1242,15 +1351,22 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     o.clustering_time = min_last;  // engine.hpp:472-475
     // every worker has t_w = R in lockstep, so the first finisher is worker 0 (engine.hpp:477-481)
     o.clustering_time_first_finisher = last_ts[0] >= 0 ? last_ts[0] : 0.0;
-    std::vector<double> bc((size_t)kn);
-    std::vector<uint8_t> bf((size_t)k);
-    CU(d2h(bc.data(), e->inc_c.as<double>() + best * kn, (size_t)kn, st));
-    CU(d2h(bf.data(), e->inc_f.as<uint8_t>() + best * k, (size_t)k, st));
-    CU(cudaStreamSynchronize(st));
+    std::vector<double> bc(h_bc, h_bc + kn);
+    std::vector<uint8_t> bf(h_bf, h_bf + k);
     if (centroids) std::memcpy(centroids, bc.data(), (size_t)kn * 8);
     if (flags) std::memcpy(flags, bf.data(), (size_t)k);
     int64_t final_nd = 0;
-    if (e->cfg.compute_full_objective || e->cfg.compute_assignment) {  // engine.hpp:483-491
+    if (dev_obj) {  // engine.hpp:483-491
+        const int kv = h_sel[1];
+        if (kv == 0) return fail(HPCG_EINVAL, "assignment: every centroid is degenerate");
+        if (want_labels) {
+            CU(d2h(labels, lab.as<int32_t>(), (size_t)e->ds->m, st));
+            CU(cudaStreamSynchronize(st));
+        }
+        o.full_objective = *h_f;
+        o.has_full_objective = 1;
+        final_nd = e->ds->m * (int64_t)kv;
+    } else if (want_obj) {  // grid-wide objective: exact valid count needed on the host
         std::vector<double> cv;
         std::vector<int32_t> remap;
         for (int64_t j = 0; j < k; ++j)
@@ -1259,13 +1375,8 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
                 cv.insert(cv.end(), bc.begin() + j * n, bc.begin() + (j + 1) * n);
             }
         if (remap.empty()) return fail(HPCG_EINVAL, "assignment: every centroid is degenerate");
-        CU(e->scratch_a.reserve(cv.size() * 8));
-        CU(e->scratch_b.reserve(remap.size() * 4));
-        CU(e->scratch_c.reserve(8));
         CU(h2d(e->scratch_a.as<double>(), cv.data(), cv.size(), st));
         CU(h2d(e->scratch_b.as<int32_t>(), remap.data(), remap.size(), st));
-        DevBuf lab;
-        const bool want_labels = e->cfg.compute_assignment && labels;
         if (want_labels) CU(lab.reserve((size_t)e->ds->m * 4));
         int rc = run_assign(ctx, e->ds, e->scratch_a.as<double>(), e->scratch_b.as<int32_t>(), (int)remap.size(),
                             want_labels ? lab.as<int32_t>() : nullptr, nullptr, e->scratch_c.as<double>(), e->blocks);
@@ -1286,7 +1397,7 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
         CU(d2h(publications, e->pub_log.as<double>(), (size_t)(cnt * 4), st));
         CU(cudaStreamSynchronize(st));
     }
-    if (worker_obj) std::memcpy(worker_obj, inc_obj.data(), (size_t)W * 8);
+    if (worker_obj) std::memcpy(worker_obj, h_obj, (size_t)W * 8);
     o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
     if (out) *out = o;
     return HPCG_OK;

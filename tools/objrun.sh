@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for c in "" 7 8 10 12; do
-  echo "== cluster ${c:-auto}"
-  HPCG_CLUSTER=$c HPCG_DEBUG=1 python tools/quick_time.py 2>&1 | grep -E "round [0-3]|cluster" | head -5
-done
+timeout 900 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
+python bench.py --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['mean_launch_ms'], d['objective_pass']['ms'], d['e2e']['ms_per_step'])"
