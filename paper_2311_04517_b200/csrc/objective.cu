@@ -4,6 +4,7 @@
 #include <cstring>
 #include <cudaTypedefs.h>
 
+#define HPCG_OBJECTIVE_TU  // this TU owns the objective kernels and their constant bank
 #include "launch.h"
 
 namespace hpcg {
@@ -121,6 +122,7 @@ static cudaError_t launch_grid(K kern, int smem, const ObjParams& p, const CUten
     }
     nblocks[0] = nb;
     kern<<<nb, kObjThreads, smem, st>>>(p, tmap);
+    if (p.launched) *p.launched += 1;
     return cudaGetLastError();
 }
 
@@ -133,7 +135,23 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
     if constexpr (sizeof(T) == 4 && NP % 4 == 0 && NP != 24) {  // centre-pair kernel (fp32, TMA widths)
         if (!old && tma_ok<T, NP>(p) && make_tmap<T>(p, PairGeo<NP>::GR, &tmap)) {
             p.use_tma = 1;
-            return launch_grid(objective_pairs_kernel<NP>, objective_pairs_smem<NP>(p.kv), p, tmap, nblocks, st);
+            static const bool no_crec = getenv("HPCG_NO_CREC") != nullptr;
+            if (!no_crec && p.rec_slot >= 0 && p.rec_slot < kRecSlots && p.rec_scratch &&
+                p.kv <= 2 * kRecMaxPairs) {
+                build_pair_records_kernel<NP><<<1, 64, 0, st>>>(p);
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return e;
+                if (p.launched) *p.launched += 1;
+                const size_t bytes = (size_t)((p.kv + 1) / 2) * PairGeo<NP>::RST * sizeof(float2);
+                e = cudaMemcpyToSymbolAsync(c_pair_rec4, p.rec_scratch, bytes,
+                                            (size_t)p.rec_slot * kRecSlotF4 * sizeof(float4), cudaMemcpyDeviceToDevice,
+                                            st);
+                if (e != cudaSuccess) return e;
+                return launch_grid(objective_pairs_kernel<NP, true>, objective_pairs_smem<NP>(p.kv), p, tmap,
+                                   nblocks, st);
+            }
+            return launch_grid(objective_pairs_kernel<NP, false>, objective_pairs_smem<NP>(p.kv), p, tmap, nblocks,
+                               st);
         }
     }
     p.use_tma = (!getenv("HPCG_NO_TMA") && tma_ok<T, NP>(p) && make_tmap<T>(p, ObjGeo<T, NP>::GR, &tmap)) ? 1 : 0;
@@ -150,7 +168,11 @@ bool objective_device_kv(int dtype, int n, int kv) {
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {
     const int np = pick_np(dtype, p.n);
     static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
-    if (np == 0 || p.kv > kObjMaxK || force_wide) return launch_objective_wide(dtype, p, nblocks, st);
+    if (np == 0 || p.kv > kObjMaxK || force_wide) {
+        const cudaError_t e = launch_objective_wide(dtype, p, nblocks, st);
+        if (p.launched) *p.launched += 1;
+        return e;
+    }
     if (dtype == 0) {
         switch (np) {
             case 2: return launch_obj_t<float, 2>(p, nblocks, st);

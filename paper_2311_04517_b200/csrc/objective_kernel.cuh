@@ -29,6 +29,9 @@ struct ObjParams {
     double* block_cost;    // [gridDim.x]
     int32_t use_tma;       // 1: stages arrive by TMA (tensor map built by the host), 0: cp.async
     const int32_t* kv_dev; // optional device-side valid count (<= kv, which then only sizes smem)
+    int32_t rec_slot;      // constant-bank record slot of the calling context, or -1
+    float4* rec_scratch;   // device staging of that slot's records (kRecSlotF4 float4)
+    int* launched;         // optional: kernels launched are added here
 };
 
 // valid centre count: the device value when given (the host launched with an upper bound)
@@ -348,7 +351,10 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_kernel(const ObjPara
 // Rows are copied to registers as soon as their stage lands and the stage is refilled at once
 // (one 32R-row stage per warp keeps 8 KB per warp in flight during the compute).
 // Screen error: sequential fused chain of NP terms on a rounded record, so
-// |d~ - d| <= (NP + 2) u (|x| + |c|)^2; kPairKappa doubles that (difference of two) with slack.
+// |d~ - d| <= (NP + 2) u (|x| + |c|)^2; PairGeo::kappa doubles that (difference of two) with
+// slack. The centre index rides in the low tb = ceil(log2(2 kp)) mantissa bits of each screened
+// value, so the running min carries its own argmin (no compare/select per centre); that moves
+// a value by < 2^(tb-23) |d~|, and the tie bound grows by 2^(tb-22) (|x| + cmax)^2 to match.
 template <int NP>
 struct PairGeo {
     using G = Geo<float, NP>;
@@ -364,6 +370,16 @@ struct PairGeo {
     static constexpr float kappa = 2.0f * (float)(NP + 12) * 5.9604645e-8f;
 };
 
+// Centre-pair records in the constant bank (kv <= 2 kRecMaxPairs): FFMA2 operands come through
+// the uniform datapath and the records stop competing with the row and centre loads for
+// shared-memory bandwidth (the kernel's binding resource). One slot per context.
+constexpr int kRecSlots = 8;
+constexpr int kRecMaxPairs = 16;
+constexpr int kRecSlotF4 = kRecMaxPairs * (32 + 2) / 2;  // float4 per slot (NP <= 32)
+#ifdef HPCG_OBJECTIVE_TU
+static __constant__ float4 c_pair_rec4[kRecSlots * kRecSlotF4];
+#endif
+
 template <int NP>
 __host__ __device__ inline int objective_pairs_smem(int kv) {
     using PG = PairGeo<NP>;
@@ -374,7 +390,33 @@ __host__ __device__ inline int objective_pairs_smem(int kv) {
 }
 
 
+#ifdef HPCG_OBJECTIVE_TU
+// records of the valid centres into a slot's staging buffer (the same arithmetic as the
+// shared-memory builder in objective_pairs_kernel, so both record sets are bit-identical)
 template <int NP>
+__global__ void build_pair_records_kernel(const ObjParams p) {
+    constexpr int RST = PairGeo<NP>::RST;
+    const int kv = obj_kv(p), kpl = (p.kv + 1) / 2;
+    float* o = reinterpret_cast<float*>(p.rec_scratch);
+    for (int j = threadIdx.x; j < 2 * kpl; j += blockDim.x) {
+        float* rec = o + (j >> 1) * (2 * RST) + (j & 1);
+        if (j < kv) {
+            double cc = 0.0;
+            for (int d = 0; d < NP; ++d) {
+                const double c = p.C[(int64_t)j * NP + d];
+                cc += c * c;
+                rec[2 * d] = (float)(-2.0 * c);
+            }
+            rec[2 * NP] = (float)cc;
+        } else {
+            for (int d = 0; d < NP; ++d) rec[2 * d] = 0.f;
+            rec[2 * NP] = 1e38f;
+        }
+        rec[2 * NP + 2] = 0.f;
+    }
+}
+
+template <int NP, bool CREC>
 __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const ObjParams p,
                                                                          const __grid_constant__ CUtensorMap tmap) {
     using PG = PairGeo<NP>;
@@ -398,7 +440,16 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
     }
     __syncthreads();
     // records: pair q holds centres 2q, 2q+1 interleaved; a missing odd partner screens +inf
-    for (int j = tid; j < 2 * kp; j += kObjThreads) {
+    const int rbase = CREC ? p.rec_slot * kRecSlotF4 : 0;
+    auto rec4 = [&](int q, int h) -> float4 {
+        if constexpr (CREC)
+            return c_pair_rec4[rbase + q * (RST / 2) + h];
+        else
+            return reinterpret_cast<const float4*>(rp + q * RST)[h];
+    };
+    // the screen runs over the launch bound kpl (a uniform trip count: records stay in uniform
+    // registers); pairs past the valid count hold +inf records and never win
+    for (int j = tid; j < (CREC ? 0 : 2 * kpl); j += kObjThreads) {
         float* rec = reinterpret_cast<float*>(rp + (j >> 1) * RST) + (j & 1);
         if (j < kv) {
             double cc = 0.0;
@@ -410,7 +461,7 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
             rec[2 * NP] = (float)cc;
         } else {
             for (int d = 0; d < NP; ++d) rec[2 * d] = 0.f;
-            rec[2 * NP] = __int_as_float(0x7f800000);
+            rec[2 * NP] = 1e38f;
         }
         rec[2 * NP + 2] = 0.f;
     }
@@ -422,12 +473,17 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
     __syncthreads();
     if (tid == 0) {
         float cm = 0.f;
-        for (int j = 0; j < kv; ++j)
-            cm = fmaxf(cm, sqrtf(reinterpret_cast<const float*>(rp + (j >> 1) * RST + NP)[j & 1]) * 1.0001f);
+        for (int j = 0; j < kv; ++j) {
+            const float4 iv = rec4(j >> 1, NP / 2);
+            cm = fmaxf(cm, sqrtf((j & 1) ? iv.y : iv.x) * 1.0001f);
+        }
         s_cmax = cm;
     }
     __syncthreads();
     const float cmax = s_cmax;
+    const int tbits = 32 - __clz(2 * kpl - 1 > 0 ? 2 * kpl - 1 : 1);
+    const int tmask = (1 << tbits) - 1;
+    const float kap = PG::kappa + __int_as_float((127 + tbits - 22) << 23);  // + 2^(tb-22)
 
     float* ring = reinterpret_cast<float*>(rings + warp * PG::STAGES * PG::STAGE);
     const int64_t m = p.m;
@@ -477,15 +533,14 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
             i1[r] = 0;
         }
 #pragma unroll 1
-        for (int q = 0; q < kp; ++q) {
-            const float4* rq = reinterpret_cast<const float4*>(rp + q * RST);
-            const float4 iv = rq[NP / 2];
+        for (int q = 0; q < kpl; ++q) {
+            const float4 iv = rec4(q, NP / 2);
             float2 acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = make_float2(iv.x, iv.y);
 #pragma unroll
             for (int h = 0; h < NP / 2; ++h) {
-                const float4 c = rq[h];
+                const float4 c = rec4(q, h);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     acc[r] = __ffma2_rn(make_float2(x[r][2 * h], x[r][2 * h]), make_float2(c.x, c.y), acc[r]);
@@ -494,14 +549,15 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const float da = acc[r].x, db = acc[r].y;
+                const float da = __int_as_float((__float_as_int(acc[r].x) & ~tmask) | (2 * q));
+                const float db = __int_as_float((__float_as_int(acc[r].y) & ~tmask) | (2 * q + 1));
                 const float lo = fminf(da, db), hi = fmaxf(da, db);
-                const int li = 2 * q + (db < da ? 1 : 0);
                 m2[r] = fmin3f(m2[r], hi, fmaxf(m1[r], lo));
-                i1[r] = lo < m1[r] ? li : i1[r];
                 m1[r] = fminf(m1[r], lo);
             }
         }
+#pragma unroll
+        for (int r = 0; r < R; ++r) i1[r] = __float_as_int(m1[r]) & tmask;
         // near ties: exact reference argmin, warp-parallel over centres (core.hpp:146-157)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -513,7 +569,7 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
             float sx;
             asm("sqrt.approx.f32 %0, %1;" : "=f"(sx) : "f"(nn2.x + nn2.y));
             const float sc = fmaf(sx, 1.0001f, cmax);
-            unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2[r] - m1[r] > PG::kappa * sc * sc));
+            unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2[r] - m1[r] > kap * sc * sc));
             while (tie) {
                 const int src = __ffs(tie) - 1;
                 tie &= tie - 1;
@@ -570,6 +626,8 @@ __global__ void __launch_bounds__(kObjThreads, 2) objective_pairs_kernel(const O
         p.block_cost[blockIdx.x] = v;
     }
 }
+
+#endif  // HPCG_OBJECTIVE_TU
 
 // Fixed-order final sum of the block partials (deterministic f(C,X)).
 static __global__ void sum_blocks_kernel(const double* part, int nparts, double* out) {

@@ -145,6 +145,8 @@ struct hpcg_ctx {
     std::mutex mu;
     std::atomic<int64_t> launches{0};
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
+    int rec_slot = -1;                     // constant-bank slot of the objective records
+    DevBuf rec_scratch;
     // per-kernel-class event timing (class 0 worker step, 1 objective)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
@@ -153,6 +155,24 @@ struct hpcg_ctx {
 };
 
 namespace {
+// constant-bank record slots (objective_kernel.cuh kRecSlots), one per live context
+std::mutex g_slot_mu;
+uint32_t g_slot_used = 0;
+int acquire_rec_slot() {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    for (int i = 0; i < kRecSlots; ++i)
+        if (!(g_slot_used & (1u << i))) {
+            g_slot_used |= 1u << i;
+            return i;
+        }
+    return -1;  // more live contexts than slots: records from shared memory
+}
+void release_rec_slot(int i) {
+    if (i < 0) return;
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    g_slot_used &= ~(1u << i);
+}
+
 // Brackets one launch with events on the launching stream when timing is enabled.
 struct KTimer {
     hpcg_ctx* c;
@@ -395,6 +415,13 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
     CU(blocks.reserve((size_t)nb * sizeof(double)));
     ObjParams op = {};
     op.kv_dev = kv_dev;
+    int launched = 0;
+    op.launched = &launched;
+    op.rec_slot = -1;
+    if (ctx->rec_slot >= 0 && ctx->rec_scratch.reserve((size_t)kRecSlotF4 * sizeof(float4)) == cudaSuccess) {
+        op.rec_slot = ctx->rec_slot;
+        op.rec_scratch = ctx->rec_scratch.as<float4>();
+    }
     op.X = ds->X;
     op.m = ds->m;
     op.n = (int)ds->n;
@@ -410,7 +437,7 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
     kt.done();
     sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, cost_dev);
     CU(cudaGetLastError());
-    ctx->launches += 2;
+    ctx->launches += launched + 1;
     return HPCG_OK;
 }
 }  // namespace
@@ -442,6 +469,7 @@ int hpcg_ctx_create(int device, hpcg_ctx** out) {
         return fail(HPCG_ECUDA, cudaGetErrorString(e));
     }
     c->own_stream = true;
+    c->rec_slot = acquire_rec_slot();
     *out = c;
     return HPCG_OK;
 }
@@ -449,6 +477,10 @@ int hpcg_ctx_create(int device, hpcg_ctx** out) {
 int hpcg_ctx_destroy(hpcg_ctx* ctx) {
     if (!ctx) return HPCG_OK;
     cudaSetDevice(ctx->device);
+    if (ctx->rec_slot >= 0) {
+        cudaDeviceSynchronize();  // no launch of this context may still read its record slot
+        release_rec_slot(ctx->rec_slot);
+    }
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return HPCG_OK;
