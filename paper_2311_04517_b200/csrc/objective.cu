@@ -6,6 +6,7 @@
 
 #define HPCG_OBJECTIVE_TU  // this TU owns the objective kernels and their constant bank
 #include "launch.h"
+#include "objective_tc.cuh"
 
 namespace hpcg {
 
@@ -126,12 +127,50 @@ static cudaError_t launch_grid(K kern, int smem, const ObjParams& p, const CUten
     return cudaGetLastError();
 }
 
+// tensor-core screen kernel (objective_tc.cuh): persistent, one CTA per SM
+template <int NP, int N, int KPS>
+static cudaError_t launch_tc(const ObjParams& p, const CUtensorMap& tmap, int* nblocks, cudaStream_t st) {
+    using TG = TcGeo<NP, N>;
+    auto kern = objective_tc_kernel<NP, N, KPS>;
+    const int smem = objective_tc_smem<NP, N>(p.kv);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (nblocks[0] < sms) {
+        nblocks[0] = sms;
+        return cudaErrorNotReady;
+    }
+    nblocks[0] = sms;
+    kern<<<sms, TG::THREADS, smem, st>>>(p, tmap);
+    if (p.launched) *p.launched += 1;
+    return cudaGetLastError();
+}
+
 template <typename T, int NP>
 static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_t st) {
     ObjParams p = p_in;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof tmap);
     static const bool old = getenv("HPCG_OBJ_OLD") != nullptr || getenv("HPCG_NO_TMA") != nullptr;
+    static const bool no_tc = getenv("HPCG_OBJ_NO_TC") != nullptr;
+    if constexpr (sizeof(T) == 4 && (NP == 8 || NP == 16 || NP == 32)) {  // tensor-core screen
+        if (!old && !no_tc && p.kv >= 1 && p.kv <= 32 && tma_ok<T, NP>(p) && make_tmap<T>(p, TcGeo<NP, 16>::TM, &tmap)) {
+            p.use_tma = 1;
+            switch ((p.kv + 1) / 2) {  // screened centre pairs
+                case 1: return launch_tc<NP, 16, 1>(p, tmap, nblocks, st);
+                case 2: return launch_tc<NP, 16, 2>(p, tmap, nblocks, st);
+                case 3: return launch_tc<NP, 16, 3>(p, tmap, nblocks, st);
+                case 4: return launch_tc<NP, 16, 4>(p, tmap, nblocks, st);
+                case 5: return launch_tc<NP, 16, 5>(p, tmap, nblocks, st);
+                case 6: return launch_tc<NP, 16, 6>(p, tmap, nblocks, st);
+                case 7: return launch_tc<NP, 16, 7>(p, tmap, nblocks, st);
+                case 8: return launch_tc<NP, 16, 8>(p, tmap, nblocks, st);
+                default: return launch_tc<NP, 32, 16>(p, tmap, nblocks, st);
+            }
+        }
+    }
     if constexpr (sizeof(T) == 4 && NP % 4 == 0 && NP != 24) {  // centre-pair kernel (fp32, TMA widths)
         if (!old && tma_ok<T, NP>(p) && make_tmap<T>(p, PairGeo<NP>::GR, &tmap)) {
             p.use_tma = 1;

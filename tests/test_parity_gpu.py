@@ -138,7 +138,10 @@ def test_exact_ties_go_to_lowest_index():
                                        # centre-pair kernel widths (16/32/48/128-B rows), odd and
                                        # large centre counts
                                        (np.float32, 4, 7), (np.float32, 12, 33), (np.float32, 32, 64),
-                                       (np.float32, 16, 1), (np.float32, 16, 255)])
+                                       (np.float32, 16, 1), (np.float32, 16, 255),
+                                       # tensor-core screen kernel: N = 16 / 32 centre columns
+                                       (np.float32, 32, 20), (np.float32, 16, 17), (np.float32, 8, 32),
+                                       (np.float32, 32, 2)])
 def test_objective_vs_oracle(dtype, n, k):
     X = mixture(200003, n, k, seed=11 + n, dtype=dtype)
     C_ = mixture(k, n, k, seed=99, dtype=np.float64)
@@ -156,6 +159,20 @@ def test_objective_vs_oracle(dtype, n, k):
     a2, f2 = hp.assign_valid_subset(X, C_, deg)
     assert np.array_equal(a2.labels, lab2) and np.array_equal(a2.counts, cnt2)
     assert rel(f2, cost2) <= RTOL
+
+
+@pytest.mark.parametrize("n,k", [(16, 10), (8, 15), (32, 32)])
+def test_objective_far_offset_near_ties(n, k):
+    # rows far from the origin (|x| ~ 1e3) around centres 0.05 apart: the tensor-core screen's
+    # error bound (kappa (|x| + cmax)^2) flags most rows, which then take the exact fp64 argmin
+    rs = np.random.default_rng(n + k)
+    base = 1000.0 + rs.standard_normal(n)
+    C_ = base + 0.05 * rs.standard_normal((k, n))
+    X = (C_[rs.integers(0, k, 50001)] + 0.05 * rs.standard_normal((50001, n))).astype(np.float32)
+    lab, cnt, cost, _ = orc().assign(X.astype(np.float64), C_)
+    a, f = hp.final_assignment(X, C_)
+    assert np.array_equal(a.labels, lab) and np.array_equal(a.counts, cnt)
+    assert rel(f, cost) <= RTOL
 
 
 @pytest.mark.parametrize("dtype,n,k,s,npend", [(np.float64, 2, 5, 5000, 5), (np.float32, 16, 10, 20000, 10),
