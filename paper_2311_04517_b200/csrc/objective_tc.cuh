@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[NB], tempty[NB];
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) float s_cc[N];
+    __shared__ __align__(16) float s_rec[N][NP + 4];  // fp32 re-screen records: -2c, then |c|^2 at NP
     __shared__ double s_wcost[EW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kv = obj_kv(p);  // device-side valid count (p.kv: the launch bound, <= 2 KPS)
@@ -136,7 +137,9 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
     }
     for (int e = tid; e < N * NP; e += TG::THREADS) {
         const int j = e / NP, d = e - j * NP;
-        Bt[G::elem_off(j, d)] = j < kv ? tf32_rna((float)(-2.0 * p.C[(int64_t)j * NP + d])) : 0.f;
+        const float c2 = j < kv ? (float)(-2.0 * p.C[(int64_t)j * NP + d]) : 0.f;
+        Bt[G::elem_off(j, d)] = tf32_rna(c2);
+        s_rec[j][d] = c2;
     }
     if (tid < N) {
         float cc = 1e38f;
@@ -149,6 +152,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
             cc = (float)s;
         }
         s_cc[tid] = cc;
+        s_rec[tid][NP] = cc;
     }
     if (warp == EW + 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
@@ -309,8 +313,41 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                     nn3 = __ffma2_rn(make_float2(x[d + 2], x[d + 3]), make_float2(x[d + 2], x[d + 3]), nn3);
                 }
                 const float nn = (nn2.x + nn2.y) + (nn3.x + nn3.y);
-                // near ties: the exact reference argmin, warp-parallel over centres (core.hpp:146-157)
                 unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kap2 * (nn + cmax2)));
+                if (tie) {
+                    // second tier: rows the tf32 screen cannot settle get the fp32 FFMA2 screen
+                    // (error <= 2 (NP/2 + 12) 2^-24 (|x| + |c|)^2 per value, the bound of the centre-pair
+                    // kernel) over every valid centre, with broadcast record loads
+                    bool still = false;
+                    if (tie & (1u << lane)) {
+                        float n1 = __int_as_float(0x7f800000), n2 = n1;
+                        int l1 = 0;
+                        for (int j = 0; j < kv; ++j) {
+                            const float* rc = s_rec[j];
+                            float2 a0 = make_float2(rc[NP], 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int d = 0; d < NP; d += 4) {
+                                const float4 c4 = *reinterpret_cast<const float4*>(rc + d);
+                                a0 = __ffma2_rn(make_float2(x[d], x[d + 1]), make_float2(c4.x, c4.y), a0);
+                                a1 = __ffma2_rn(make_float2(x[d + 2], x[d + 3]), make_float2(c4.z, c4.w), a1);
+                            }
+                            const float dj = (a0.x + a0.y) + (a1.x + a1.y);
+                            if (dj < n1) {
+                                n2 = n1;
+                                n1 = dj;
+                                l1 = j;
+                            } else {
+                                n2 = fminf(n2, dj);
+                            }
+                        }
+                        lab = l1;
+                        constexpr float kap32 = 2.0f * 2.0f * (float)(NP / 2 + 12) * 5.9604645e-8f * 1.0001f;
+                        still = !(n2 - n1 > kap32 * (nn + cmax2));
+                    }
+                    tie = __ballot_sync(0xffffffffu, still);
+                }
+                // near ties of both screens: the exact reference argmin, warp-parallel over centres
+                // (core.hpp:146-157)
                 while (tie) {
                     const int src = __ffs(tie) - 1;
                     tie &= tie - 1;
