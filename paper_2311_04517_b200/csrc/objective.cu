@@ -6,7 +6,7 @@
 
 #define HPCG_OBJECTIVE_TU  // this TU owns the objective kernels and their constant bank
 #include "launch.h"
-#include "objective_tc.cuh"
+#include "objective_rows.cuh"
 
 namespace hpcg {
 
@@ -192,6 +192,12 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
             return launch_grid(objective_pairs_kernel<NP, false>, objective_pairs_smem<NP>(p.kv), p, tmap, nblocks,
                                st);
         }
+    }
+    // narrow rows (fp64 n <= 3, fp32 n = 2): bulk-copy ring + centre-pair screen
+    static const bool no_rows = getenv("HPCG_OBJ_NO_ROWS") != nullptr;
+    if constexpr ((sizeof(T) == 8 && NP <= 3) || (sizeof(T) == 4 && NP == 2)) {
+        if (!old && !no_rows && p.n == NP && (reinterpret_cast<uintptr_t>(p.X) & 15) == 0)
+            return launch_grid(objective_rows_kernel<T, NP>, objective_rows_smem<T, NP>(p.kv), p, tmap, nblocks, st);
     }
     p.use_tma = (!getenv("HPCG_NO_TMA") && tma_ok<T, NP>(p) && make_tmap<T>(p, ObjGeo<T, NP>::GR, &tmap)) ? 1 : 0;
     return launch_grid(objective_kernel<T, NP>, objective_smem<T, NP>(p.kv), p, tmap, nblocks, st);

@@ -141,7 +141,9 @@ def test_exact_ties_go_to_lowest_index():
                                        (np.float32, 16, 1), (np.float32, 16, 255),
                                        # tensor-core screen kernel: N = 16 / 32 centre columns
                                        (np.float32, 32, 20), (np.float32, 16, 17), (np.float32, 8, 32),
-                                       (np.float32, 32, 2)])
+                                       (np.float32, 32, 2),
+                                       # narrow-row kernel (bulk-copy ring): fp64 n = 1..3, fp32 n = 2
+                                       (np.float64, 1, 4), (np.float64, 2, 31), (np.float32, 2, 6)])
 def test_objective_vs_oracle(dtype, n, k):
     X = mixture(200003, n, k, seed=11 + n, dtype=dtype)
     C_ = mixture(k, n, k, seed=99, dtype=np.float64)
@@ -159,6 +161,19 @@ def test_objective_vs_oracle(dtype, n, k):
     a2, f2 = hp.assign_valid_subset(X, C_, deg)
     assert np.array_equal(a2.labels, lab2) and np.array_equal(a2.counts, cnt2)
     assert rel(f2, cost2) <= RTOL
+
+
+@pytest.mark.parametrize("m", [1, 100, 128, 640, 1000])
+@pytest.mark.parametrize("dtype,n", [(np.float64, 3), (np.float64, 2), (np.float32, 16), (np.float32, 8)])
+def test_objective_small_m(m, dtype, n):
+    # partial / single tail groups of the streaming kernels (rows read from global memory directly,
+    # TMA boxes clipped at m)
+    X = mixture(m, n, 4, seed=m + n, dtype=dtype)
+    C_ = mixture(7, n, 4, seed=5)
+    lab, cnt, cost, _ = orc().assign(X.astype(np.float64), C_)
+    a, f = hp.final_assignment(X, C_)
+    assert np.array_equal(a.labels, lab) and np.array_equal(a.counts, cnt)
+    assert rel(f, cost) <= RTOL
 
 
 @pytest.mark.parametrize("n,k", [(16, 10), (8, 15), (32, 32)])
