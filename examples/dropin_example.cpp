@@ -32,7 +32,14 @@ int main(int argc, char** argv) {
         cfg.strategy = hpclust::Strategy::cooperative();
         cfg.master_seed = 11;
         hpclust::ClusteringResult r = hpclust::run(X, cfg);
-        std::printf("{\"sample0\": %.17g, \"seed_c0\": %.17g, \"lloyd_obj\": %.17g, \"lloyd_iters\": %zu, "
+        // the reference CLI's default schedule: a wall-clock budget (engine.hpp:348-374)
+        hpclust::EngineConfig wcfg = cfg;
+        wcfg.max_samples.reset();
+        wcfg.time_limit = 0.2;
+        hpclust::ClusteringResult rw = hpclust::run(X, wcfg);
+        std::printf("{\"wall_seconds\": %.17g, \"wall_samples\": %zu, \"wall_full\": %.17g, ", rw.wall_seconds,
+                    rw.total_samples, rw.full_objective.value_or(-1.0));
+        std::printf("\"sample0\": %.17g, \"seed_c0\": %.17g, \"lloyd_obj\": %.17g, \"lloyd_iters\": %zu, "
                     "\"lloyd_stop\": \"%s\", \"nd\": %lld, \"f_full\": %.17g, \"run_full\": %.17g, "
                     "\"run_best\": %d, \"run_nd\": %lld, \"run_c0\": %.17g, \"pubs\": %zu}\n",
                     S.values[0], C0.centers[0], lo.objective, lo.iterations, hpclust::to_string(lo.converged_by),

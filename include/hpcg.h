@@ -164,6 +164,8 @@ typedef struct hpcg_engine_cfg {
     int32_t compute_full_objective, compute_assignment;
     int32_t rng_mode;     /* hpcg_rng_mode */
     int32_t worker_base;  /* global id of worker 0 on this rank (multi-GPU), else 0 */
+    double time_limit;    /* seconds; > 0: wall-clock schedule (engine.hpp:348-374) with max_samples an
+                             optional per-worker cap (0 = none); 0: lockstep over max_samples rounds */
 } hpcg_engine_cfg;
 
 typedef struct hpcg_run_out {
@@ -183,6 +185,12 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
 /* Back to round 0 with a new master seed (no allocation; stream-ordered). */
 int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed);
 int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds);
+/* The configured schedule to its end (replaces engine.hpp:459-462): lockstep max_samples rounds,
+ * or -- time_limit set -- rounds until the limit (run_wall_clock, engine.hpp:348-374, at round
+ * granularity: every worker of a round starts from the round's snapshot, accepted cooperative
+ * incumbents are published at the round end in worker-id order, the hybrid switch happens at the
+ * first round end past phase_t1 seconds, trace timestamps are seconds). */
+int hpcg_engine_run(hpcg_engine* e);
 int64_t hpcg_engine_round_index(const hpcg_engine* e);
 /* Diagnostics: per-CTA phase timestamps (%globaltimer ns) of subsequent rounds written to
  * trace_dev[W * cluster * 32] (NULL disables); mode 0 details the first Lloyd pass, mode 1

@@ -20,8 +20,8 @@
 // counts bit-exact; centroids / objectives within 1e-12 relative, the fixed-order device
 // reductions differing from the sequential host sums only in rounding). Error behaviour:
 // the same exception types and message texts. Device parallelism replaces ParallelPolicy
-// (accepted, ignored). run() supports the deterministic max_samples schedule (lockstep); the
-// reference's wall-clock schedule is not provided by this build and is rejected.
+// (accepted, ignored). run() supports both schedules: lockstep (max_samples, deterministic) and
+// the wall-clock one (time_limit; rounds until the limit, see hpcg_engine_run in hpcg.h).
 #pragma once
 
 #include <algorithm>
@@ -640,13 +640,14 @@ inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
     EngineConfig cfg = cfg_in;
     if (cfg.strategy.kind == StrategyKind::inner) cfg.n_workers = 1;
     cfg.validate(X.rows);
-    require(cfg.deterministic_mode(), "run: this build provides the max_samples (lockstep) schedule only");
-    const std::size_t W = cfg.n_workers, k = cfg.k, n = X.cols, R = *cfg.max_samples;
+    const std::size_t W = cfg.n_workers, k = cfg.k, n = X.cols;
     hpcg_engine_cfg ec{};
     ec.k = (int64_t)k;
     ec.sample_size = (int64_t)cfg.sample_size;
     ec.n_workers = (int64_t)W;
-    ec.max_samples = (int64_t)R;
+    // lockstep (deterministic_mode) or the wall-clock schedule (engine.hpp:459-462)
+    ec.max_samples = cfg.max_samples ? (int64_t)*cfg.max_samples : 0;
+    ec.time_limit = cfg.deterministic_mode() ? 0.0 : cfg.time_limit;
     ec.strategy = (int32_t)cfg.strategy.kind;
     ec.phase_t1 = cfg.strategy.phase_t1;
     ec.phase_t2 = cfg.strategy.phase_t2;
@@ -661,7 +662,8 @@ inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
     hpcg_engine* e = nullptr;
     gpu::check(hpcg_engine_create(gpu::context(), dm.ds, &ec, &e));
     std::unique_ptr<hpcg_engine, int (*)(hpcg_engine*)> guard(e, hpcg_engine_destroy);
-    gpu::check(hpcg_engine_rounds(e, (int64_t)R));
+    gpu::check(hpcg_engine_run(e));
+    const std::size_t R = (std::size_t)std::max<std::int64_t>(1, hpcg_engine_round_index(e));
     hpcg_run_out o{};
     ClusteringResult res;
     res.centroids = CentroidSet(k, n);

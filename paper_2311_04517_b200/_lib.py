@@ -18,7 +18,7 @@ EXPORTS = (
     "hpcg_ctx_synchronize", "hpcg_ctx_launch_count", "hpcg_dataset_upload", "hpcg_dataset_wrap",
     "hpcg_dataset_destroy", "hpcg_dataset_device_ptr", "hpcg_assign", "hpcg_assign_dev",
     "hpcg_worker_step_batched", "hpcg_gather", "hpcg_sample_indices", "hpcg_reference_draw_indices", "hpcg_rng_seed",
-    "hpcg_rng_derive", "hpcg_rng_draw", "hpcg_engine_create", "hpcg_engine_rounds", "hpcg_engine_round_index",
+    "hpcg_rng_derive", "hpcg_rng_draw", "hpcg_engine_create", "hpcg_engine_rounds", "hpcg_engine_run", "hpcg_engine_round_index",
     "hpcg_engine_distance_evals", "hpcg_engine_finish", "hpcg_engine_destroy", "hpcg_engine_export_best",
     "hpcg_run", "hpcg_gen_mixture", "hpcg_ctx_enable_timing", "hpcg_ctx_kernel_times", "hpcg_probe_fma_peak",
     "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
@@ -79,7 +79,8 @@ class EngineCfg(C.Structure):
                 ("max_samples", C.c_int64), ("strategy", C.c_int32), ("phase_t1", C.c_double),
                 ("phase_t2", C.c_double), ("master_seed", C.c_uint64), ("candidates", C.c_int64),
                 ("max_iters", C.c_int64), ("rel_tol", C.c_double), ("compute_full_objective", C.c_int32),
-                ("compute_assignment", C.c_int32), ("rng_mode", C.c_int32), ("worker_base", C.c_int32)]
+                ("compute_assignment", C.c_int32), ("rng_mode", C.c_int32), ("worker_base", C.c_int32),
+                ("time_limit", C.c_double)]
 
 
 class RunOut(C.Structure):
@@ -118,6 +119,7 @@ def _load():
         "hpcg_rng_draw": (C.c_int, [P, P, I32, U64, I64, P]),
         "hpcg_engine_create": (C.c_int, [P, P, P, P]),
         "hpcg_engine_rounds": (C.c_int, [P, I64]),
+        "hpcg_engine_run": (C.c_int, [P]),
         "hpcg_engine_round_index": (I64, [P]),
         "hpcg_engine_distance_evals": (C.c_int, [P, P]),
         "hpcg_engine_finish": (C.c_int, [P, P, P, P, P, P, I64, P, P, I64, P]),

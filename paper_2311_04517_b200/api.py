@@ -493,7 +493,7 @@ class EngineConfig:
     k: int = 0
     sample_size: int = 0
     n_workers: int = 1
-    max_samples: int = 1
+    max_samples: int = 0  # per worker; 0 = none (then time_limit must be set), engine.hpp:54
     strategy: str = "competitive"
     phase_t1: float = 0.0
     phase_t2: float = 0.0
@@ -505,6 +505,7 @@ class EngineConfig:
     compute_assignment: bool = False
     rng: str = "reference"  # "reference" (bit-parity streams) or "philox" (device)
     worker_base: int = 0
+    time_limit: float = 0.0  # seconds; > 0: wall-clock schedule (engine.hpp:348-374), max_samples a cap
 
     def to_c(self) -> _lib.EngineCfg:
         if self.strategy not in STRATEGIES:
@@ -513,7 +514,8 @@ class EngineConfig:
                               STRATEGIES[self.strategy], self.phase_t1, self.phase_t2, self.master_seed,
                               self.candidates, self.max_iters, self.rel_tol, int(self.compute_full_objective),
                               int(self.compute_assignment),
-                              _lib.RNG_REFERENCE if self.rng == "reference" else _lib.RNG_PHILOX, self.worker_base)
+                              _lib.RNG_REFERENCE if self.rng == "reference" else _lib.RNG_PHILOX, self.worker_base,
+                              float(self.time_limit))
 
 
 @dataclass
@@ -550,6 +552,11 @@ class Engine:
     def rounds(self, n: int = 1):
         check(lib.hpcg_engine_rounds(self.h, n))
 
+    def run(self):
+        """The configured schedule to its end: lockstep max_samples rounds, or rounds until
+        cfg.time_limit seconds (wall-clock schedule, engine.hpp:348-374)."""
+        check(lib.hpcg_engine_run(self.h))
+
     def reset(self, master_seed: int):
         check(lib.hpcg_engine_reset(self.h, C.c_uint64(master_seed)))
 
@@ -582,10 +589,11 @@ class Engine:
         cent = np.empty((k, n))
         flags = np.empty(k, dtype=np.uint8)
         labels = np.empty(m, dtype=np.int32) if self.cfg.compute_assignment else None
-        pub_cap = max(64, self.cfg.max_samples * min(W, 64))
+        rounds = max(self.round_index, self.cfg.max_samples)
+        pub_cap = max(64, rounds * min(W, 64))
         pubs = np.zeros((pub_cap, 4))
         wobj = np.empty(W)
-        tcap = max(1, self.cfg.max_samples)
+        tcap = max(1, rounds)
         traces = np.zeros((W, tcap, 2))
         tlen = np.zeros(W, dtype=np.int64)
         check(lib.hpcg_engine_finish(self.h, C.byref(out), ptr(cent), ptr(flags), ptr(labels), ptr(pubs), pub_cap,
@@ -622,6 +630,15 @@ def run(X, cfg: EngineConfig, ctx: Context | None = None) -> ClusteringResult:
     """engine.hpp:444-499 — one call on host data (upload, rounds, final pass)."""
     ctx = ctx or default_context()
     X = np.ascontiguousarray(X)
+    if cfg.time_limit > 0:  # round count unknown in advance: the stepwise engine sizes the outputs
+        ds = DeviceDataset(X, ctx=ctx)
+        eng = Engine(ds, cfg)
+        try:
+            eng.run()
+            return eng.finish()
+        finally:
+            eng.close()
+            ds.close()
     m, n = X.shape
     c = cfg.to_c()
     W = 1 if cfg.strategy == "inner" else cfg.n_workers

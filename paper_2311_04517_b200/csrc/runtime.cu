@@ -254,6 +254,7 @@ struct RoundEndParams {
     int publish;    // round was cooperative (publish accepted) ...
     int carry;      // ... or hybrid carry-over round (publish finite incumbents)
     int worker_base;
+    double ts;      // publication timestamp: round + 1 (lockstep) or seconds (wall clock)
     const uint8_t* accepted;
     const double* inc_obj;
     const double* inc_c;
@@ -307,7 +308,7 @@ __global__ void round_end_kernel(const RoundEndParams p) {
                         p.pub_log[cnt * 4 + 0] = (double)ver;
                         p.pub_log[cnt * 4 + 1] = (double)(p.worker_base + w);
                         p.pub_log[cnt * 4 + 2] = f;
-                        p.pub_log[cnt * 4 + 3] = (double)(p.round + 1);
+                        p.pub_log[cnt * 4 + 3] = p.ts;
                     }
                     ++cnt;
                 }
@@ -912,6 +913,9 @@ struct hpcg_engine {
     int64_t round = 0;
     uint64_t key = 0;
     std::chrono::steady_clock::time_point t0;
+    bool wall = false;           // wall-clock schedule (cfg.time_limit > 0)
+    std::vector<double> t_end;   // wall clock: seconds since t0 at the end of each round
+    double elapsed() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
     DevBuf inc_c, inc_f, inc_obj, acc, nd, err, err_first, iters, stopb, filled, objb;
     DevBuf sh_ver, sh_obj, sh_worker, sh_c, sh_f;
     DevBuf log_acc, log_obj, nd_total, pub_log, pub_count;
@@ -941,7 +945,8 @@ bool phase_cooperative(int strategy, double t1, double progress) {  // engine.hp
 int engine_round(hpcg_engine* e) {
     hpcg_ctx* ctx = e->ctx;
     const int64_t r = e->round, W = e->W, k = e->k, n = e->n, s = e->s, kn = k * n;
-    const bool coop = phase_cooperative(e->cfg.strategy, e->cfg.phase_t1, (double)r);
+    // phase test on the schedule's clock: samples processed (lockstep) or seconds (wall clock)
+    const bool coop = phase_cooperative(e->cfg.strategy, e->cfg.phase_t1, e->wall ? e->elapsed() : (double)r);
     const bool reference = e->cfg.rng_mode == HPCG_RNG_REFERENCE;
     const int64_t ncand = e->cfg.candidates;
     std::vector<int64_t> pending_loop, no_valid;
@@ -1043,7 +1048,17 @@ int engine_round(hpcg_engine* e) {
     q.round = r;
     q.publish = coop ? 1 : 0;  // round_was_coop (engine.hpp:393)
     const bool hybrid = e->cfg.strategy == HPCG_HYBRID;
-    q.carry = (hybrid && (r + 1) == (int64_t)(size_t)e->cfg.phase_t1) ? 1 : 0;  // engine.hpp:386,396
+    if (e->wall) {  // the round's samples are done at t_end; the hybrid switch is decided on it
+        CU(cudaStreamSynchronize(ctx->stream));
+        const double t_end = e->elapsed();
+        e->t_end.push_back(t_end);
+        q.ts = t_end;
+        // engine.hpp:359-364: entering the cooperative phase publishes each worker's incumbent
+        q.carry = (hybrid && !coop && t_end >= e->cfg.phase_t1) ? 1 : 0;
+    } else {
+        q.ts = (double)(r + 1);
+        q.carry = (hybrid && (r + 1) == (int64_t)(size_t)e->cfg.phase_t1) ? 1 : 0;  // engine.hpp:386,396
+    }
     q.worker_base = e->cfg.worker_base;
     q.accepted = e->acc.as<uint8_t>();
     q.inc_obj = e->inc_obj.as<double>();
@@ -1097,11 +1112,15 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     if (cfg.sample_size < 1 || cfg.sample_size > ds->m)
         return fail(HPCG_EINVAL, "EngineConfig: sample_size must be in [1, m]");
     if (cfg.n_workers < 1) return fail(HPCG_EINVAL, "EngineConfig: need at least one worker");
-    if (cfg.max_samples < 1) return fail(HPCG_EINVAL, "EngineConfig: need a time limit or a max_samples bound");
+    if (std::isnan(cfg.time_limit) || cfg.time_limit < 0.0)
+        return fail(HPCG_EINVAL, "EngineConfig: time limit must be positive");
+    const bool wall = cfg.time_limit > 0.0 && std::isfinite(cfg.time_limit);  // deterministic_mode() false
+    if (!wall && cfg.max_samples < 1) return fail(HPCG_EINVAL, "EngineConfig: need a time limit or a max_samples bound");
+    if (wall && cfg.max_samples < 0) return fail(HPCG_EINVAL, "EngineConfig: max_samples must be positive");
     if (cfg.strategy == HPCG_HYBRID) {
         if (!(cfg.phase_t1 >= 0.0 && cfg.phase_t2 >= 0.0))
             return fail(HPCG_EINVAL, "EngineConfig: hybrid phase durations must be nonnegative");
-        const double b = (double)cfg.max_samples;
+        const double b = wall ? cfg.time_limit : (double)cfg.max_samples;  // EngineConfig::budget()
         if (!(std::fabs(cfg.phase_t1 + cfg.phase_t2 - b) <= 1e-9 * std::max(1.0, std::fabs(b))))
             return fail(HPCG_EINVAL, "EngineConfig: hybrid phases must sum to the total budget");
     }
@@ -1120,7 +1139,10 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     e->k = cfg.k;
     e->n = ds->n;
     e->s = cfg.sample_size;
-    e->R = cfg.max_samples;
+    e->wall = wall;
+    // rounds: max_samples, or in wall-clock mode that cap (else enough for ~64 MB of round logs)
+    e->R = wall && cfg.max_samples < 1 ? std::max<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(cfg.n_workers, 1))
+                                        : cfg.max_samples;
     e->key = splitmix64(cfg.master_seed ^ 0x48504331ULL);
     e->t0 = std::chrono::steady_clock::now();
     const int64_t W = e->W, k = e->k, kn = k * e->n;
@@ -1202,6 +1224,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     e->key = splitmix64(master_seed ^ 0x48504331ULL);
     e->round = 0;
     e->t0 = std::chrono::steady_clock::now();
+    e->t_end.clear();
     if (e->cfg.rng_mode == HPCG_RNG_REFERENCE)
         for (int64_t w = 0; w < W; ++w)
             e->streams[(size_t)w] = Mt64::derive(master_seed, 1, (uint64_t)(e->cfg.worker_base + w));
@@ -1246,6 +1269,17 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
     cudaSetDevice(e->ctx->device);
     for (int64_t i = 0; i < n_rounds; ++i) {
         if (e->round >= e->R) return fail(HPCG_EINVAL, "engine: max_samples rounds already run");
+        if (int rc = engine_round(e)) return rc;
+    }
+    return HPCG_OK;
+}
+
+int hpcg_engine_run(hpcg_engine* e) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    cudaSetDevice(e->ctx->device);
+    while (e->round < e->R) {
+        // run_wall_clock (engine.hpp:355-357): stop once the time limit has passed
+        if (e->wall && e->elapsed() >= e->cfg.time_limit) break;
         if (int rc = engine_round(e)) return rc;
     }
     return HPCG_OK;
@@ -1363,7 +1397,9 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     hpcg_run_out o = {};
     o.best_worker = e->cfg.worker_base + best;
     o.best_sample_objective = best_f;
-    // traces: lockstep timestamps are samples_processed + 1 = round + 1 (engine.hpp:413)
+    // traces: lockstep timestamps are samples_processed + 1 = round + 1 (engine.hpp:413); wall
+    // clock: seconds at the end of the round (strictly increasing per worker, engine.hpp:258-262)
+    auto ts_of = [&](int64_t r) { return e->wall && r < (int64_t)e->t_end.size() ? e->t_end[(size_t)r] : (double)(r + 1); };
     double min_last = kInf;
     std::vector<double> last_ts((size_t)W, -1.0);
     for (int64_t w = 0; w < W; ++w) {
@@ -1371,10 +1407,10 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
         for (int64_t r = 0; r < R; ++r) {
             if (!h_lacc[r * W + w]) continue;
             if (traces && cnt < trace_cap) {
-                traces[(w * trace_cap + cnt) * 2 + 0] = (double)(r + 1);
+                traces[(w * trace_cap + cnt) * 2 + 0] = ts_of(r);
                 traces[(w * trace_cap + cnt) * 2 + 1] = h_lobj[r * W + w];
             }
-            last_ts[(size_t)w] = (double)(r + 1);
+            last_ts[(size_t)w] = ts_of(r);
             ++cnt;
         }
         if (trace_len) trace_len[w] = cnt;
@@ -1465,7 +1501,7 @@ int hpcg_run(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int
     int rc = hpcg_engine_create(ctx, ds, cfg, &e);
     if (!rc) {
         e->t0 = t0;
-        rc = hpcg_engine_rounds(e, cfg->max_samples);
+        rc = hpcg_engine_run(e);
     }
     if (!rc)
         rc = hpcg_engine_finish(e, out, centroids, flags, labels, publications, pub_cap, worker_obj, traces,

@@ -50,3 +50,6 @@ def test_dropin_matches_reference_semantics():
     assert r["run_best"] == run["best_worker"] and r["run_nd"] == run["distance_evals"]
     assert abs(r["run_c0"] - run["centroids"][0, 0]) <= 1e-12 * abs(run["centroids"][0, 0])
     assert r["pubs"] == len(run["publications"])
+    # wall-clock schedule through the drop-in: stops at the first round end past 0.2 s
+    assert r["wall_seconds"] >= 0.2 and r["wall_samples"] > 0 and r["wall_samples"] % 3 == 0
+    assert r["wall_full"] > 0
