@@ -309,3 +309,16 @@ def test_philox_sample_distinct_in_range_and_keyed():
     # roughly uniform over [0, m): each decile holds ~s/10 rows
     h = np.bincount(a * 10 // m, minlength=10)
     assert h.min() > 0.8 * s / 10 and h.max() < 1.2 * s / 10
+
+
+@pytest.mark.parametrize("strategy", ["competitive", "cooperative"])
+def test_run_compute_assignment_vs_oracle(strategy):
+    # the full assignment of a run (engine.hpp:60, 211-229, 490): labels of
+    # the valid subset remapped to the original slots, from the device f(C, X) pass
+    X = mixture(30000, 3, 6, seed=23)
+    e = orc().run(X, k=6, sample_size=1500, n_workers=4, max_samples=3, strategy=strategy, seed=9, assignment=True)
+    cfg = hp.EngineConfig(k=6, sample_size=1500, n_workers=4, max_samples=3, strategy=strategy, master_seed=9,
+                          rng="reference", compute_assignment=True)
+    g = hp.run(X, cfg)
+    assert np.array_equal(g.assignment, e["labels"])
+    assert rel(g.full_objective, e["full_objective"]) <= RTOL
