@@ -328,4 +328,35 @@ int hpref_kmeans_threads(const double* samples, std::size_t W, std::size_t s, st
     });
 }
 
+// baselines.hpp:29-47 forgy_kmeans / 58-147 pbk_bdc with RngStream(seed); p = 0 selects Forgy.
+// Outputs: centroids[k*n], flags[k], labels[m], full objective, n_d, total_samples.
+int hpref_baseline(const double* X, std::size_t m, std::size_t n, std::size_t k, std::size_t p,
+                   std::uint64_t seed, std::size_t max_iters, double rel_tol, double* C_out,
+                   std::uint8_t* flags_out, std::int32_t* labels_out, double* f_out, std::int64_t* nd_out,
+                   std::int64_t* samples_out) {
+    return guard([&] {
+        Dataset ds = make_ds(X, m, n);
+        RngStream rng(seed);
+        LloydConfig lc;
+        lc.max_iters = max_iters;
+        lc.rel_tol = rel_tol;
+        ClusteringResult r;
+        if (p == 0) {
+            r = forgy_kmeans(ds, k, lc, rng);
+        } else {
+            PbkConfig pc;
+            pc.segment_size = p;
+            pc.inner_lloyd = lc;
+            pc.n_threads = 1;
+            r = pbk_bdc(ds, k, pc, rng);
+        }
+        put_cs(r.centroids, C_out, flags_out);
+        if (labels_out && r.assignment)
+            for (std::size_t i = 0; i < m; ++i) labels_out[i] = r.assignment->labels[i];
+        *f_out = r.full_objective.value_or(-1.0);
+        *nd_out = r.distance_evals;
+        *samples_out = (std::int64_t)r.total_samples;
+    });
+}
+
 }  // extern "C"

@@ -203,6 +203,21 @@ class Reference(_Checker):
         L.hpref_gen_blobs.argtypes = [SZ, SZ, SZ, D, D, D, D, SZ, D, D, U64, P]
         L.hpref_brute_force.argtypes = [P, SZ, SZ, SZ, P, P, P]
         L.hpref_kmeans_threads.argtypes = [P, SZ, SZ, SZ, P, SZ, SZ, D, P, P]
+        if hasattr(L, "hpref_baseline"):
+            L.hpref_baseline.argtypes = [P, SZ, SZ, SZ, SZ, U64, SZ, D, P, P, P, P, P, P]
+
+    def baseline(self, X, k, p, seed, max_iters=300, rel_tol=1e-4):
+        """baselines.hpp forgy_kmeans (p = 0) / pbk_bdc (segment size p) with RngStream(seed)."""
+        X = np.ascontiguousarray(X, np.float64)
+        m, n = X.shape
+        Co = np.empty((k, n))
+        fo = np.empty(k, np.uint8)
+        lab = np.empty(m, np.int32)
+        f, nd, samples = D(), C.c_int64(), C.c_int64()
+        self._err(self.lib.hpref_baseline(ptr(X), m, n, k, p, seed, max_iters, rel_tol, ptr(Co), ptr(fo), ptr(lab),
+                                          C.byref(f), C.byref(nd), C.byref(samples)))
+        return dict(centroids=Co, degenerate=fo, labels=lab, full_objective=f.value, n_d=nd.value,
+                    total_samples=samples.value)
 
     def rng(self, seed=None, derive=None):
         h = self.lib.hpref_rng_derive(*derive) if derive is not None else self.lib.hpref_rng_new(seed)

@@ -53,3 +53,39 @@ def test_dropin_matches_reference_semantics():
     # wall-clock schedule through the drop-in: stops at the first round end past 0.2 s
     assert r["wall_seconds"] >= 0.2 and r["wall_samples"] > 0 and r["wall_samples"] % 3 == 0
     assert r["wall_full"] > 0
+
+
+BEXE = ROOT / "examples" / "baselines_example"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [0, 2000, 1700])  # Forgy; PBK-BDC with full segments; with a short tail
+def test_dropin_baselines_match_reference(p):
+    # hpclust/baselines.hpp on the device vs the reference's baselines.hpp (oracle/_ref): same RNG
+    # consumption, same Lloyd outcomes per segment, same repository, same final assignment
+    from oracle_py import ref
+    r_ = ref()
+    if r_ is None or not hasattr(r_.lib, "hpref_baseline"):
+        pytest.skip("reference harness not built")
+    if not BEXE.exists():
+        subprocess.run(["make", "-C", str(ROOT / "examples")], check=True)
+    rs = np.random.default_rng(8 + p)
+    means = rs.uniform(-10, 10, (6, 3))
+    X = means[rs.integers(0, 6, 10000)] + rs.standard_normal((10000, 3))
+    with tempfile.TemporaryDirectory() as d:
+        path = str(Path(d) / "X.f64")
+        X.astype(np.float64).tofile(path)
+        out = subprocess.run([str(BEXE), path, "10000", "3", "5", str(p), "77"], capture_output=True, text=True,
+                             timeout=300)
+        g = json.loads(out.stdout)
+        assert "error" not in g, g
+        C_ = np.fromfile(path + ".C").reshape(5, 3)
+        F_ = np.fromfile(path + ".F", dtype=np.uint8)
+        L_ = np.fromfile(path + ".L", dtype=np.int32)
+    e = r_.baseline(X, 5, p, 77)
+    assert g["samples"] == e["total_samples"]
+    assert g["nd"] == e["n_d"]
+    assert np.array_equal(F_, e["degenerate"])
+    assert np.array_equal(L_, e["labels"])
+    assert np.max(np.abs(C_ - e["centroids"])) <= 1e-12 * np.max(np.abs(e["centroids"]))
+    assert abs(g["f"] - e["full_objective"]) <= 1e-12 * e["full_objective"]
