@@ -276,13 +276,21 @@ struct RoundEndParams {
 };
 
 // engine.hpp:391-402 on_round_end: publications in worker-id order, strict < (engine.hpp:131)
+// The worker records are staged in shared memory by all threads first, so the sequential
+// publication scan (thread 0, worker-id order) reads shared memory instead of global memory.
 __global__ void round_end_kernel(const RoundEndParams p) {
     __shared__ int s_winner;
     __shared__ unsigned long long s_nd[256];
+    extern __shared__ double rs_obj[];  // [W] incumbent objectives, then [W] accepted flags
+    uint8_t* rs_acc = reinterpret_cast<uint8_t*>(rs_obj + p.W);
     unsigned long long nd = 0;
     for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
-        p.log_acc[p.round * p.W + w] = p.accepted[w];
-        p.log_obj[p.round * p.W + w] = p.inc_obj[w];
+        const uint8_t a = p.accepted[w];
+        const double f = p.inc_obj[w];
+        rs_acc[w] = a;
+        rs_obj[w] = f;
+        p.log_acc[p.round * p.W + w] = a;
+        p.log_obj[p.round * p.W + w] = f;
         nd += (unsigned long long)p.nd[w];
         if (p.err[w] != 0 && p.err_first[w] == 0) p.err_first[w] = p.err[w];
     }
@@ -298,8 +306,8 @@ __global__ void round_end_kernel(const RoundEndParams p) {
             int64_t ver = *p.sh_version;
             int64_t cnt = *p.pub_count;
             for (int w = 0; w < p.W; ++w) {
-                const double f = p.inc_obj[w];
-                const bool cand = (p.publish && p.accepted[w]) || (p.carry && isfinite(f));
+                const double f = rs_obj[w];
+                const bool cand = (p.publish && rs_acc[w]) || (p.carry && isfinite(f));
                 if (cand && f < best) {
                     best = f;
                     winner = w;
@@ -1078,7 +1086,13 @@ int engine_round(hpcg_engine* e) {
     q.pub_log = e->pub_log.as<double>();
     q.pub_count = e->pub_count.as<int64_t>();
     q.pub_cap = e->pub_cap;
-    round_end_kernel<<<1, 256, 0, ctx->stream>>>(q);
+    const size_t rs_bytes = (size_t)W * 9;
+    if (rs_bytes > 48 * 1024) {
+        const cudaError_t ae = cudaFuncSetAttribute(round_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)rs_bytes);
+        if (ae != cudaSuccess) return fail(HPCG_EUNSUPPORTED, "round end: too many workers for one engine");
+    }
+    round_end_kernel<<<1, 256, rs_bytes, ctx->stream>>>(q);
     CU(cudaGetLastError());
     ctx->launches += 1;
 

@@ -621,17 +621,31 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         const int rank = __popc(peers & ((1u << lane) - 1u));
         if (valid && rank == 0) wcnt[warp * k + lab] = __popc(peers);
         __syncthreads();
-        if (tid == 0) {
-            int off = 0;
-            for (int j = 0; j < k; ++j) {
-                cstart[j] = off;
-                for (int q = 0; q < 8; ++q) {
-                    const int c = wcnt[q * k + j];
-                    wcnt[q * k + j] = off;
-                    off += c;
+        if (warp == 0) {  // cluster-major, warp-minor offsets: a shuffle scan over 32 clusters at a time
+            int base = 0;
+            for (int j0 = 0; j0 < k; j0 += 32) {
+                const int j = j0 + lane;
+                int col = 0;
+                if (j < k)
+                    for (int q = 0; q < 8; ++q) col += wcnt[q * k + j];
+                int incl = col;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
                 }
+                if (j < k) {
+                    int run = base + incl - col;
+                    cstart[j] = run;
+                    for (int q = 0; q < 8; ++q) {
+                        const int c = wcnt[q * k + j];
+                        wcnt[q * k + j] = run;
+                        run += c;
+                    }
+                }
+                base += __shfl_sync(0xffffffffu, incl, 31);
             }
-            cstart[k] = off;
+            if (lane == 0) cstart[k] = base;
         }
         __syncthreads();
         if (valid) sorted[wcnt[warp * k + lab] + rank] = tid;
@@ -639,7 +653,40 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         // per-cluster sums of this round: warp w takes clusters w, w+8, ..., walks the cluster's
         // rows in order with lanes over dims (coalesced row loads), then adds to the CTA
         // accumulator (each (j, d) owned by one lane: fixed order, no atomics)
-        for (int j = warp; j < k; j += kWT / 32) {
+        // n <= 128: LR lanes cover a row's dims (4 per lane), 32/LR rows in flight per step, each
+        // lane summing rows gi, gi + RPS, ... in order, then a fixed shuffle tree over gi
+        const int LR = n <= 4 ? 1 : n <= 8 ? 2 : n <= 16 ? 4 : n <= 32 ? 8 : n <= 64 ? 16 : 32;
+        const int RPS = 32 / LR, gi = lane / LR, dq = (lane % LR) * 4;
+        for (int j = warp; j < k && n <= 128; j += kWT / 32) {
+            const int q0 = cstart[j], q1 = cstart[j + 1];
+            if (q0 == q1) continue;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (dq < n) {
+#pragma unroll 4
+                for (int q = q0 + gi; q < q1; q += RPS) {
+                    double v[4];
+                    load4d<T>(S + (base + sorted[q]) * n, dq, n, vecd, v);
+                    a0 += v[0];
+                    a1 += v[1];
+                    a2 += v[2];
+                    a3 += v[3];
+                }
+            }
+            for (int o = LR; o < 32; o <<= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+            }
+            if (gi == 0 && dq < n) {
+                double* aj = acc + (int64_t)j * n + dq;
+                aj[0] += a0;
+                if (dq + 1 < n) aj[1] += a1;
+                if (dq + 2 < n) aj[2] += a2;
+                if (dq + 3 < n) aj[3] += a3;
+            }
+        }
+        for (int j = warp; j < k && n > 128; j += kWT / 32) {
             const int q0 = cstart[j], q1 = cstart[j + 1];
             if (q0 == q1) continue;
             for (int d0 = lane * 4; d0 < n; d0 += 128) {
