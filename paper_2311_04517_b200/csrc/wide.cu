@@ -1,3 +1,4 @@
+#include <cstdlib>
 // The HPClust worker step for shapes the cluster-resident kernel cannot hold: n > 32 features
 // (config 4: n = 128), k > 32 centres, or samples larger than a 16-CTA cluster's shared
 // memory. Same contract as worker_step_kernel (StepParams in, the same per-worker outputs,
@@ -649,7 +650,8 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         }
         __syncthreads();
         if (valid) sorted[wcnt[warp * k + lab] + rank] = tid;
-        cost += cta_sum(valid ? bestd : 0.0, red);  // thread 0's copy is the one used
+        cost += valid ? bestd : 0.0;  // per-thread running sum (thread t: rows r0 + t + kWT*i, in order)
+        __syncthreads();              // sorted[] complete before the sums read it
         // per-cluster sums of this round: warp w takes clusters w, w+8, ..., walks the cluster's
         // rows in order with lanes over dims (coalesced row loads), then adds to the CTA
         // accumulator (each (j, d) owned by one lane: fixed order, no atomics)
@@ -713,6 +715,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
     const int64_t pd = kn + k + 1;
     double* out = b.part + ((int64_t)w * G + g) * pd;
     for (int64_t e = tid; e < kn + k; e += kWT) out[e] = acc[e];
+    cost = cta_sum(cost, red);  // fixed tree over the threads' running sums
     if (tid == 0) out[kn + k] = cost;
 }
 
@@ -951,7 +954,12 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // CTAs per worker for the Lloyd pass: enough CTAs for the whole GPU, each at least a few rounds
-    int G = std::max(1, std::min<int>((int)((int64_t)2 * sms / Wb), (int)((s + 4 * kWT - 1) / (4 * kWT))));
+    // (enough CTAs to fill the GPU twice, and at most ~RPC 256-row rounds per CTA: each round is a
+    // sequence of barriers, so long per-CTA row ranges serialise)
+    static const int rpc = getenv("HPCG_WIDE_RPC") ? atoi(getenv("HPCG_WIDE_RPC")) : 24;  // diagnostics
+    int G = std::max<int>(std::min<int>((int)((int64_t)2 * sms / Wb), (int)((s + 4 * kWT - 1) / (4 * kWT))),
+                          (int)((s + (int64_t)rpc * kWT - 1) / ((int64_t)rpc * kWT)));
+    G = std::max(G, 1);
     const int64_t pd = kn + k + 1;
     // scratch layout
     size_t off = 0;
