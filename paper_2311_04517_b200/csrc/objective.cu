@@ -7,6 +7,7 @@
 #define HPCG_OBJECTIVE_TU  // this TU owns the objective kernels and their constant bank
 #include "launch.h"
 #include "objective_rows.cuh"
+#include "objective_tcw.cuh"
 
 namespace hpcg {
 
@@ -210,9 +211,49 @@ bool objective_device_kv(int dtype, int n, int kv) {
     return pick_np(dtype, n) != 0 && kv <= kObjMaxK && !force_wide;
 }
 
+// wide fp32 rows (n = 64, 128) on the tensor cores (objective_tcw.cuh): TMA boxes of one
+// 128-B swizzle atom ({32 floats, 128 rows}, SWIZZLE_128B)
+template <int NA, int KPS>
+static cudaError_t launch_tcw(const ObjParams& p, int* nblocks, cudaStream_t st) {
+    using TG = TcwGeo<NA>;
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof tmap);
+    const cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.m};
+    const cuuint64_t strides[1] = {(cuuint64_t)p.n * 4};
+    const cuuint32_t box[2] = {32, (cuuint32_t)TG::M};
+    const cuuint32_t estr[2] = {1, 1};
+    if (fn(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p.X), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorNotSupported;
+    auto kern = objective_tcw_kernel<NA, KPS>;
+    const int smem = objective_tcw_smem<NA>();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (nblocks[0] < sms) {
+        nblocks[0] = sms;
+        return cudaErrorNotReady;
+    }
+    nblocks[0] = sms;
+    kern<<<sms, TG::THREADS, smem, st>>>(p, tmap);
+    if (p.launched) *p.launched += 1;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {
     const int np = pick_np(dtype, p.n);
     static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
+    static const bool no_tc = getenv("HPCG_OBJ_NO_TC") != nullptr;
+    if (dtype == 0 && (p.n == 64 || p.n == 128) && p.kv >= 1 && p.kv <= 32 && !force_wide && !no_tc &&
+        (reinterpret_cast<uintptr_t>(p.X) & 15) == 0) {
+        if (p.n == 128) return p.kv <= 16 ? launch_tcw<4, 8>(p, nblocks, st) : launch_tcw<4, 16>(p, nblocks, st);
+        return p.kv <= 16 ? launch_tcw<2, 8>(p, nblocks, st) : launch_tcw<2, 16>(p, nblocks, st);
+    }
     if (np == 0 || p.kv > kObjMaxK || force_wide) {
         const cudaError_t e = launch_objective_wide(dtype, p, nblocks, st);
         if (p.launched) *p.launched += 1;

@@ -1,0 +1,323 @@
+// Full-data objective f(C, X) (engine.hpp:197-229, core.hpp:224-233) for WIDE fp32 rows (n = 64 or
+// 128: BASELINE config 4) with the nearest-centre screen on the tensor cores -- the s x n x k
+// contraction the north star assigns to tcgen05.
+//
+// Same pipeline as objective_tc_kernel (csrc/objective_tc.cuh), adapted to rows wider than one
+// 128-B swizzle atom: a row is NA = n/32 K-atoms, so a 128-row tile lands by NA TMA box loads
+// ({32 floats, 128 rows}, SWIZZLE_128B) into NA sub-tiles [128 rows x 128 B], and the MMA warp
+// walks K in 8-float steps across the atoms (start address + 16 KB per atom + 32 B per step);
+// -2c (tf32) is the B operand in the same layout, N = 32 centre columns, D in TMEM. The epilogue
+// (8 warps, 2 groups alternating tiles, one row per thread) cannot hold a 128-float row in
+// registers: it streams the row's chunks from the stage once, accumulating |x|^2 and the fp64
+// cost to the screened nearest centre together; a row inside the tf32 bound is re-screened in
+// fp32 (FFMA2) and, if still inside that bound, given the exact fp64 argmin (warp-parallel over
+// centres), and its cost is recomputed if the label moved. The stage is released after its rows
+// have been read. fp64 centres and fp32 records are read from global memory (L1-resident).
+#pragma once
+#include "objective_tc.cuh"
+
+namespace hpcg {
+
+template <int NA>
+struct TcwGeo {
+    static constexpr int N = 32;                          // centre columns (kv <= 32)
+    static constexpr int M = 128;                         // rows per tile
+    static constexpr int NPW = 32 * NA;                   // row width (floats)
+    static constexpr int SUB = M * 128;                   // bytes per K-atom sub-tile
+    static constexpr int TILE = NA * SUB;                 // bytes per stage
+    static constexpr int STAGES = 196608 / TILE < 6 ? 196608 / TILE : 6;
+    static constexpr int BSUB = N * 128;                  // bytes per K-atom of the B tile
+    static constexpr int TCOLS = 512;
+    static constexpr int NB = TCOLS / N;                  // TMEM tile buffers
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int THREADS = (EPI_WARPS + 2) * 32;
+    static constexpr uint32_t IDESC =
+        (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    static_assert(STAGES >= 2, "stages");
+};
+
+template <int NA>
+__host__ __device__ inline int objective_tcw_smem() {
+    using TG = TcwGeo<NA>;
+    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB;
+}
+
+// byte offset of float d of row r inside a tile of NA [rows x 128 B] SWIZZLE_128B atoms
+HPCG_DEV uint32_t sw128_off(int rows, int r, int d) {
+    const int a = d >> 5, q = (d >> 2) & 7;
+    return (uint32_t)(a * rows * 128 + r * 128 + ((q ^ (r & 7)) << 4) + ((d & 3) << 2));
+}
+
+template <int NA, int KPS>
+__global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
+    objective_tcw_kernel(const ObjParams p, const __grid_constant__ CUtensorMap tmap) {
+    using TG = TcwGeo<NA>;
+    constexpr int N = TG::N, NPW = TG::NPW, STAGES = TG::STAGES, NB = TG::NB, TILE = TG::TILE, EW = TG::EPI_WARPS;
+    extern __shared__ __align__(16) unsigned char osm[];
+    unsigned char* ring = osm + ((1024 - (smem_u32(osm) & 1023)) & 1023);
+    unsigned char* Bt = ring + STAGES * TILE;
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[NB], tempty[NB];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) float s_cc[N];
+    __shared__ double s_wcost[EW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kv = obj_kv(p);
+    const double* __restrict__ Cg = p.C;  // [kv x NPW] fp64 centres (L1-resident)
+
+    for (int e = tid; e < N * NPW; e += TG::THREADS) {
+        const int j = e / NPW, d = e - j * NPW;
+        const float c2 = j < kv ? (float)(-2.0 * Cg[(int64_t)j * NPW + d]) : 0.f;
+        *reinterpret_cast<float*>(Bt + sw128_off(N, j, d)) = tf32_rna(c2);
+    }
+    if (tid < N) {
+        float cc = 1e38f;
+        if (tid < kv) {
+            double s = 0.0;
+            for (int d = 0; d < NPW; ++d) {
+                const double c = Cg[(int64_t)tid * NPW + d];
+                s += c * c;
+            }
+            cc = (float)s;
+        }
+        s_cc[tid] = cc;
+    }
+    if (warp == EW + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                     "r"(TG::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 4);  // the 4 warps of the group that read the tile's rows
+        }
+        for (int b = 0; b < NB; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        mbar_init_fence();
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = s_tmem;
+    const int64_t m = p.m;
+    const int64_t ntiles = (m + TG::M - 1) / TG::M;
+    const int my = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    double cost = 0.0;
+
+    if (warp == EW) {  // ---- TMA producer: NA box loads per tile
+        if (lane == 0) {
+            int s = 0;
+            uint32_t pl = 0;
+            for (int i = 0; i < my; ++i) {
+                if (i >= STAGES) mbar_wait_cta(&empty[s], pl ^ 1u);
+                mbar_expect_tx(&full[s], (uint32_t)TILE);
+                const int row0 = (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::M);
+#pragma unroll
+                for (int a = 0; a < NA; ++a) tma_load_2d(ring + s * TILE + a * TG::SUB, &tmap, 32 * a, row0, &full[s]);
+                if (++s == STAGES) {
+                    s = 0;
+                    pl ^= 1u;
+                }
+            }
+        }
+    } else if (warp == EW + 1) {  // ---- MMA issuer: K = NPW in 8-float steps across the atoms
+        if (lane == 0) {
+            const uint64_t a0 = umma_desc(smem_u32(ring), 1024, 2u);  // SWIZZLE_128B, SBO = 8 rows x 128 B
+            const uint64_t b0 = umma_desc(smem_u32(Bt), 1024, 2u);
+            int s = 0, b = 0;
+            uint32_t pl = 0, pb = 0;
+            for (int i = 0; i < my; ++i) {
+                mbar_wait_cta(&full[s], pl);
+                if (i >= NB) mbar_wait_cta(&tempty[b], pb ^ 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < NPW / 8; ++ks) {
+                    const uint64_t ad = a0 + (uint64_t)((s * TILE + (ks >> 2) * TG::SUB + (ks & 3) * 32) >> 4);
+                    const uint64_t bd = b0 + (uint64_t)(((ks >> 2) * TG::BSUB + (ks & 3) * 32) >> 4);
+                    asm volatile(
+                        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tm + (uint32_t)(b * N)),
+                        "l"(ad), "l"(bd), "r"(TG::IDESC), "r"(ks));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&tfull[b]))
+                             : "memory");
+                if (++s == STAGES) {
+                    s = 0;
+                    pl ^= 1u;
+                }
+                if (++b == NB) {
+                    b = 0;
+                    pb ^= 1u;
+                }
+            }
+        }
+    } else {  // ---- epilogue: group g takes local tiles g, g + 2, ...
+        const int g = warp >> 2, wq = warp & 3, r = wq * 32 + lane;
+        float cmax = 0.f;
+        for (int j = 0; j < kv; ++j) cmax = fmaxf(cmax, sqrtf(s_cc[j]) * 1.0001f);
+        const float cmax2 = cmax * cmax;
+        constexpr int TB = 5, TMASK = (1 << TB) - 1;
+        const float kap2 = 2.0f * (0.0078125f + __int_as_float((127 + TB - 22) << 23)) * 1.0001f;
+        constexpr float kap32 = 2.0f * 2.0f * (float)(NPW / 2 + 12) * 5.9604645e-8f * 1.0001f;
+        int32_t* const labels_out = p.labels;
+        unsigned long long* const counts_out = p.counts;
+        const int32_t* const remap = p.remap;
+        const float2* ccp = reinterpret_cast<const float2*>(s_cc);
+        int s = g, b = g;
+        uint32_t pb = 0;
+        for (int i = g; i < my; i += 2) {
+            mbar_wait_sleep(&tfull[b], pb);
+            tc_fence_after();
+            uint32_t v[N];
+            const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * N);
+            tmem_ld16(taddr, v);
+            tmem_ld16(taddr + 16, v + 16);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
+            const unsigned char* tile = ring + s * TILE;
+            const int64_t row = ((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::M + r;
+            const bool valid = row < m;
+            // top-2 of the screened values (column index in the low mantissa bits)
+            float p1[KPS], p2[KPS];
+#pragma unroll
+            for (int q = 0; q < KPS; ++q) {
+                const float2 d2 = __fadd2_rn(make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1])), ccp[q]);
+                const float da = __int_as_float((__float_as_int(d2.x) & ~TMASK) | (2 * q));
+                const float db = __int_as_float((__float_as_int(d2.y) & ~TMASK) | (2 * q + 1));
+                p1[q] = fminf(da, db);
+                p2[q] = fmaxf(da, db);
+            }
+#pragma unroll
+            for (int w = 1; w < KPS; w *= 2)
+#pragma unroll
+                for (int q = 0; q + w < KPS; q += 2 * w) {
+                    p2[q] = fmin3f(p2[q], p2[q + w], fmaxf(p1[q], p1[q + w]));
+                    p1[q] = fminf(p1[q], p1[q + w]);
+                }
+            int lab = __float_as_int(p1[0]) & TMASK;
+            // one pass over the row: |x|^2 (fp32) and the fp64 cost to the screened centre
+            auto row_cost = [&](int j, float* nn_out) {
+                const double* cj = Cg + (int64_t)j * NPW;
+                double a[4] = {0.0, 0.0, 0.0, 0.0};
+                float2 nn2 = make_float2(0.f, 0.f);
+#pragma unroll 4
+                for (int c = 0; c < NPW / 4; ++c) {
+                    const float4 x4 = *reinterpret_cast<const float4*>(tile + sw128_off(TG::M, r, 4 * c));
+                    nn2 = __ffma2_rn(make_float2(x4.x, x4.y), make_float2(x4.x, x4.y), nn2);
+                    nn2 = __ffma2_rn(make_float2(x4.z, x4.w), make_float2(x4.z, x4.w), nn2);
+                    const double2 c01 = __ldg(reinterpret_cast<const double2*>(cj + 4 * c));
+                    const double2 c23 = __ldg(reinterpret_cast<const double2*>(cj + 4 * c + 2));
+                    const double e0 = (double)x4.x - c01.x, e1 = (double)x4.y - c01.y;
+                    const double e2 = (double)x4.z - c23.x, e3 = (double)x4.w - c23.y;
+                    a[0] = fma(e0, e0, a[0]);
+                    a[1] = fma(e1, e1, a[1]);
+                    a[2] = fma(e2, e2, a[2]);
+                    a[3] = fma(e3, e3, a[3]);
+                }
+                if (nn_out) *nn_out = nn2.x + nn2.y;
+                return (a[0] + a[1]) + (a[2] + a[3]);
+            };
+            float nn = 0.f;
+            double rc = row_cost(valid ? lab : 0, &nn);
+            const int lab0 = lab;
+            unsigned tie = __ballot_sync(0xffffffffu, valid && !(p2[0] - p1[0] > kap2 * (nn + cmax2)));
+            if (tie) {
+                // second tier: fp32 FFMA2 re-screen of the flagged rows over every valid centre
+                bool still = false;
+                if (tie & (1u << lane)) {
+                    float n1 = __int_as_float(0x7f800000), n2 = n1;
+                    int l1 = 0;
+                    for (int j = 0; j < kv; ++j) {
+                        const double* cj = Cg + (int64_t)j * NPW;
+                        float2 acc = make_float2(s_cc[j], 0.f), acc2 = make_float2(0.f, 0.f);
+                        for (int c = 0; c < NPW / 4; ++c) {
+                            const float4 x4 = *reinterpret_cast<const float4*>(tile + sw128_off(TG::M, r, 4 * c));
+                            const double2 c01 = __ldg(reinterpret_cast<const double2*>(cj + 4 * c));
+                            const double2 c23 = __ldg(reinterpret_cast<const double2*>(cj + 4 * c + 2));
+                            acc = __ffma2_rn(make_float2(x4.x, x4.y),
+                                             make_float2((float)(-2.0 * c01.x), (float)(-2.0 * c01.y)), acc);
+                            acc2 = __ffma2_rn(make_float2(x4.z, x4.w),
+                                              make_float2((float)(-2.0 * c23.x), (float)(-2.0 * c23.y)), acc2);
+                        }
+                        const float dj = (acc.x + acc.y) + (acc2.x + acc2.y);
+                        if (dj < n1) {
+                            n2 = n1;
+                            n1 = dj;
+                            l1 = j;
+                        } else {
+                            n2 = fminf(n2, dj);
+                        }
+                    }
+                    lab = l1;
+                    still = !(n2 - n1 > kap32 * (nn + cmax2));
+                }
+                tie = __ballot_sync(0xffffffffu, still);
+                // near ties of both screens: the exact reference argmin (core.hpp:146-157), lanes over
+                // centres reading the flagged row from the stage
+                while (tie) {
+                    const int src = __ffs(tie) - 1;
+                    tie &= tie - 1;
+                    const int rs = (r & ~31) + src;
+                    double dv = __longlong_as_double(0x7ff0000000000000LL);
+                    int dj = 0x7fffffff;
+                    for (int j = lane; j < kv; j += 32) {
+                        const double* cj = Cg + (int64_t)j * NPW;
+                        double acc = 0.0;
+                        for (int d = 0; d < NPW; ++d) {
+                            const double diff =
+                                __dsub_rn((double)*reinterpret_cast<const float*>(tile + sw128_off(TG::M, rs, d)), cj[d]);
+                            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                        }
+                        if (acc < dv) {
+                            dv = acc;
+                            dj = j;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
+                        const int oj = __shfl_xor_sync(0xffffffffu, dj, o);
+                        if (ov < dv || (ov == dv && oj < dj)) {
+                            dv = ov;
+                            dj = oj;
+                        }
+                    }
+                    if (lane == src) lab = dj;
+                }
+                if (valid && lab != lab0) rc = row_cost(lab, nullptr);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are read
+            if (valid) {
+                cost += rc;
+                if (labels_out) labels_out[row] = remap[lab];
+                if (counts_out) atomicAdd(counts_out + remap[lab], 1ULL);
+            }
+            if (s += 2, s >= STAGES) s -= STAGES;
+            if (b += 2, b >= NB) {
+                b -= NB;
+                pb ^= 1u;
+            }
+        }
+        cost = warp_sum(cost);
+        if (lane == 0) s_wcost[warp] = cost;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == EW + 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TG::TCOLS));
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < EW; ++w) t += s_wcost[w];
+        p.block_cost[blockIdx.x] = t;
+    }
+}
+
+}  // namespace hpcg

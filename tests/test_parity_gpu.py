@@ -105,14 +105,15 @@ def test_empty_cluster_and_duplicates():
     assert centroid_close(r["centroids"][0], e["centroids"])
 
 
-def test_exact_ties_fp32_rows_pair_kernel():
+@pytest.mark.parametrize("n", [16, 128])
+def test_exact_ties_fp32_rows_pair_kernel(n):
     # fp32 16-wide rows on an integer lattice, centres placed so many rows are exactly
     # equidistant from two or more centres (ties resolved to the lowest index, core.hpp:146-157)
     rs = np.random.default_rng(3)
-    X = rs.integers(-4, 5, (100003, 16)).astype(np.float32)
-    C_ = np.zeros((9, 16))
+    X = rs.integers(-4, 5, (100003, n)).astype(np.float32)
+    C_ = np.zeros((9, n))
     for j in range(1, 9):
-        C_[j, (j - 1) % 16] = 2.0 if j % 2 else -2.0
+        C_[j, (j - 1) % n] = 2.0 if j % 2 else -2.0
     C_[5] = C_[1]  # duplicate centre: never chosen over slot 1
     lab, cnt, cost, _ = orc().assign(X.astype(np.float64), C_)
     a, f = hp.final_assignment(X, C_)
@@ -143,7 +144,9 @@ def test_exact_ties_go_to_lowest_index():
                                        (np.float32, 32, 20), (np.float32, 16, 17), (np.float32, 8, 32),
                                        (np.float32, 32, 2),
                                        # narrow-row kernel (bulk-copy ring): fp64 n = 1..3, fp32 n = 2
-                                       (np.float64, 1, 4), (np.float64, 2, 31), (np.float32, 2, 6)])
+                                       (np.float64, 1, 4), (np.float64, 2, 31), (np.float32, 2, 6),
+                                       # wide rows on the tensor cores (K-atom tiles): config-4 shape
+                                       (np.float32, 128, 25), (np.float32, 64, 10), (np.float32, 128, 32)])
 def test_objective_vs_oracle(dtype, n, k):
     X = mixture(200003, n, k, seed=11 + n, dtype=dtype)
     C_ = mixture(k, n, k, seed=99, dtype=np.float64)
@@ -164,7 +167,8 @@ def test_objective_vs_oracle(dtype, n, k):
 
 
 @pytest.mark.parametrize("m", [1, 100, 128, 640, 1000])
-@pytest.mark.parametrize("dtype,n", [(np.float64, 3), (np.float64, 2), (np.float32, 16), (np.float32, 8)])
+@pytest.mark.parametrize("dtype,n", [(np.float64, 3), (np.float64, 2), (np.float32, 16), (np.float32, 8),
+                                     (np.float32, 128)])
 def test_objective_small_m(m, dtype, n):
     # partial / single tail groups of the streaming kernels (rows read from global memory directly,
     # TMA boxes clipped at m)
@@ -176,7 +180,7 @@ def test_objective_small_m(m, dtype, n):
     assert rel(f, cost) <= RTOL
 
 
-@pytest.mark.parametrize("n,k", [(16, 10), (8, 15), (32, 32)])
+@pytest.mark.parametrize("n,k", [(16, 10), (8, 15), (32, 32), (128, 25), (64, 7)])
 def test_objective_far_offset_near_ties(n, k):
     # rows far from the origin (|x| ~ 1e3) around centres 0.05 apart: the tensor-core screen's
     # error bound (kappa (|x| + cmax)^2) flags most rows, which then take the exact fp64 argmin
