@@ -152,6 +152,13 @@ struct hpcg_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
     int64_t t_count[2] = {0, 0};
     double t_ms[2] = {0.0, 0.0};
+    // allocations kept across one-call runs (hpcg_run: upload, engine, finish, teardown per call):
+    // the device buffer of the last destroyed uploaded dataset and the pinned finish staging
+    std::mutex cache_mu;
+    void* spare_x = nullptr;
+    size_t spare_x_bytes = 0;
+    void* pin = nullptr;
+    size_t pin_bytes = 0;
 };
 
 namespace {
@@ -220,10 +227,20 @@ struct hpcg_dataset {
     hpcg_ctx* ctx = nullptr;
     const void* X = nullptr;
     bool owned = false;
+    size_t bytes = 0;  // owned allocation size
     int dtype = 0;
     int64_t m = 0, n = 0;
     ~hpcg_dataset() {
-        if (owned && X) cudaFree(const_cast<void*>(X));
+        if (!(owned && X)) return;
+        // keep the largest freed upload buffer for the next upload on this context
+        std::lock_guard<std::mutex> lk(ctx->cache_mu);
+        if (bytes > ctx->spare_x_bytes) {
+            if (ctx->spare_x) cudaFree(ctx->spare_x);
+            ctx->spare_x = const_cast<void*>(X);
+            ctx->spare_x_bytes = bytes;
+        } else {
+            cudaFree(const_cast<void*>(X));
+        }
     }
 };
 
@@ -491,6 +508,8 @@ int hpcg_ctx_destroy(hpcg_ctx* ctx) {
         release_rec_slot(ctx->rec_slot);
     }
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->spare_x) cudaFree(ctx->spare_x);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     delete ctx;
     return HPCG_OK;
 }
@@ -572,7 +591,20 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
     cudaSetDevice(ctx->device);
     void* d = nullptr;
     const size_t bytes = (size_t)m * (size_t)n * dsize(dtype);
-    CU(cudaMalloc(&d, bytes));
+    size_t have = 0;
+    {
+        std::lock_guard<std::mutex> lk(ctx->cache_mu);
+        if (ctx->spare_x && ctx->spare_x_bytes >= bytes) {  // reuse the last freed upload buffer
+            d = ctx->spare_x;
+            have = ctx->spare_x_bytes;
+            ctx->spare_x = nullptr;
+            ctx->spare_x_bytes = 0;
+        }
+    }
+    if (!d) {
+        CU(cudaMalloc(&d, bytes));
+        have = bytes;
+    }
     cudaError_t e = cudaMemcpyAsync(d, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
@@ -583,6 +615,7 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
     ds->ctx = ctx;
     ds->X = d;
     ds->owned = true;
+    ds->bytes = have;
     ds->dtype = dtype;
     ds->m = m;
     ds->n = n;
@@ -929,11 +962,6 @@ struct hpcg_engine {
     DevBuf log_acc, log_obj, nd_total, pub_log, pub_count;
     DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks, fin;
     int64_t pub_cap = 0;
-    void* pin = nullptr;  // pinned staging of the finish read-back (one synchronisation)
-    size_t pin_bytes = 0;
-    ~hpcg_engine() {
-        if (pin) cudaFreeHost(pin);
-    }
     // reference-RNG replay state
     std::vector<Mt64> streams;
     std::vector<int64_t> h_idx, h_fr;
@@ -1367,14 +1395,14 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     }
     // pinned staging: [inc_obj W][lobj Rw][bc kn][f][ndt][npub][sel 2x i32][errf W][lacc Rw][bf k]
     const size_t need = (size_t)(W + Rw + kn + 3) * 8 + 8 + (size_t)W * 4 + (size_t)Rw + (size_t)k;
-    if (need > e->pin_bytes) {
-        if (e->pin) cudaFreeHost(e->pin);
-        e->pin = nullptr;
-        e->pin_bytes = 0;
-        CU(cudaHostAlloc(&e->pin, need, cudaHostAllocDefault));
-        e->pin_bytes = need;
+    if (need > ctx->pin_bytes) {  // context-level: one allocation across engines / calls
+        if (ctx->pin) cudaFreeHost(ctx->pin);
+        ctx->pin = nullptr;
+        ctx->pin_bytes = 0;
+        CU(cudaHostAlloc(&ctx->pin, need, cudaHostAllocDefault));
+        ctx->pin_bytes = need;
     }
-    double* h_obj = static_cast<double*>(e->pin);
+    double* h_obj = static_cast<double*>(ctx->pin);
     double* h_lobj = h_obj + W;
     double* h_bc = h_lobj + Rw;
     double* h_f = h_bc + kn;
