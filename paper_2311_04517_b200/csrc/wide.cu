@@ -1,4 +1,5 @@
 #include <cstdlib>
+#include <cstring>
 // The HPClust worker step for shapes the cluster-resident kernel cannot hold: n > 32 features
 // (config 4: n = 128), k > 32 centres, or samples larger than a 16-CTA cluster's shared
 // memory. Same contract as worker_step_kernel (StepParams in, the same per-worker outputs,
@@ -19,6 +20,9 @@
 #include <map>
 #include <mutex>
 #include "launch.h"
+
+#include <cudaTypedefs.h>
+#include "objective_tcw.cuh"
 
 namespace hpcg {
 namespace {
@@ -566,7 +570,7 @@ __global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
 // strict-< argmin (core.hpp:146-157); per-cluster sums of each round's rows (label-sorted, row
 // order) and its cost tree-sum are added to the CTA accumulators in round order
 template <typename T>
-__global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, WideBufs b, int G) {
+__global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
     extern __shared__ double wsm[];
     const int w = blockIdx.y, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (b.st[w].done) return;
@@ -607,9 +611,16 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         int lab = 0;
         double bestd = 0.0;
         float m1 = 0.f, m2 = 0.f, xx = 0.f;
-        if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
-        const float sc = sqrtf(xx) * 1.0001f + cmax;
-        const unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+        unsigned tie;
+        if (tc_codes) {  // the tensor-core screen's code: label, bit 31 = still a near tie
+            const int32_t code = valid ? labels[i] : 0;
+            lab = code & 0x7fffffff;
+            tie = __ballot_sync(0xffffffffu, valid && code < 0);
+        } else {
+            if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
+            const float sc = sqrtf(xx) * 1.0001f + cmax;
+            tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+        }
         if (tie) exact_ties<T>(tie, S, base + warp * 32, n, k, Cm, lab);
         if (valid) {  // the row's cost: the reference distance to its centre
             bestd = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
@@ -943,6 +954,45 @@ cudaError_t arena_get(size_t bytes, void** out) {
     return cudaSuccess;
 }
 
+}  // namespace
+}  // namespace hpcg
+#include "wide_tc.cuh"
+namespace hpcg {
+namespace {
+
+// the tensor-core screen's launch: tensor map over the batch's samples, one CTA per SM
+template <int NA, int KPS>
+cudaError_t launch_wide_tc(const StepParams& p, const WideBufs& b, const float* ccw, int Wb, int sms,
+                           const CUtensorMap& tmap, cudaStream_t st) {
+    const int tpw = (int)((p.s + 127) / 128);
+    const int smem = wide_tc_smem<NA>();
+    cudaError_t e = cudaFuncSetAttribute(wide_screen_tc_kernel<NA, KPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem);
+    if (e != cudaSuccess) return e;
+    wide_screen_tc_kernel<NA, KPS><<<sms, WtcGeo<NA>::THREADS, smem, st>>>(p, b, ccw, Wb * tpw, tpw, tmap);
+    return cudaGetLastError();
+}
+
+bool wide_tmap(const void* S, int n, int64_t rows, CUtensorMap* map) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    memset(map, 0, sizeof *map);
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)n * 4};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(S), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 template <typename T>
@@ -973,7 +1023,8 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
                  ocand = take((size_t)Wb * kMaxCandidates * n * 8), obt = take((size_t)Wb * nblk * 8),
                  obc = take((size_t)Wb * kMaxCandidates * nblk * 8), opart = take((size_t)Wb * G * pd * 8),
                  olc = take((size_t)Wb * k * 8), ofl = take((size_t)Wb * k), opend = take((size_t)Wb * k * 4),
-                 olab = take((size_t)Wb * s * 4), oact = take(4), ost = take((size_t)Wb * sizeof(WState));
+                 olab = take((size_t)Wb * s * 4), oact = take(4), ost = take((size_t)Wb * sizeof(WState)),
+                 occw = take((size_t)Wb * (kTcwN + 1) * 4);
     void* base = nullptr;
     cudaError_t e = arena_get(off, &base);
     if (e != cudaSuccess) {
@@ -1036,10 +1087,24 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         if (why) *why = "wide step: k*n too large for the pass accumulator";
         return e;
     }
+    // tensor-core screen for wide fp32 samples (config 4): n = 64 / 128, k <= 32
+    static const bool no_tc = getenv("HPCG_WIDE_NO_TC") != nullptr;
+    float* ccw = reinterpret_cast<float*>(static_cast<char*>(base) + occw);
+    CUtensorMap stmap;
+    const bool tc = sizeof(T) == 4 && (n == 64 || n == 128) && k <= 32 && !no_tc &&
+                    wide_tmap(b.S, n, (int64_t)Wb * s, &stmap);
     if (p.do_lloyd) {
         int32_t active = 0;
         for (int pass = 0; pass <= p.max_iters + 1; ++pass) {
-            wide_assign_kernel<T><<<dim3((unsigned)G, (unsigned)Wb), kWT, smem, st>>>(p, b, G);
+            if (tc) {
+                wide_cc_kernel<<<Wb, 32, 0, st>>>(p, b, ccw);
+                e = n == 128 ? (k <= 16 ? launch_wide_tc<4, 8>(p, b, ccw, Wb, sms, stmap, st)
+                                        : launch_wide_tc<4, 16>(p, b, ccw, Wb, sms, stmap, st))
+                             : (k <= 16 ? launch_wide_tc<2, 8>(p, b, ccw, Wb, sms, stmap, st)
+                                        : launch_wide_tc<2, 16>(p, b, ccw, Wb, sms, stmap, st));
+                if (e != cudaSuccess) return e;
+            }
+            wide_assign_kernel<T><<<dim3((unsigned)G, (unsigned)Wb), kWT, smem, st>>>(p, b, G, tc ? 1 : 0);
             wide_lloyd_reduce_kernel<<<Wb, kWT, 0, st>>>(p, b, G, w0);
             if ((pass & 3) == 3 || pass == p.max_iters + 1) {  // stop check every few passes
                 wide_count_active_kernel<<<1, 256, 0, st>>>(b, Wb);

@@ -128,3 +128,25 @@ print("ok")
     root = str(Path(__file__).resolve().parents[1])
     out = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("n,k", [(64, 12), (128, 30)])
+def test_wide_tc_screen_near_ties_vs_oracle(n, k):
+    # config-4 widths on the tensor-core Lloyd screen with rows far from the origin around nearby
+    # centres: most rows fall inside the tf32 bound, take the fp32 re-screen and then the exact argmin
+    rs = np.random.default_rng(n + k)
+    base = 500.0 + rs.standard_normal(n)
+    C0 = base + 0.2 * rs.standard_normal((k, n))
+    m, s = 12000, 3000
+    X = (C0[rs.integers(0, k, m)] + 0.2 * rs.standard_normal((m, n))).astype(np.float32)
+    idx = np.stack([rs.choice(m, s, replace=False) for _ in range(2)])
+    inits = np.stack([X[rs.choice(m, k, replace=False)].astype(np.float64) for _ in range(2)])
+    r = hp.worker_step_batched(X, idx, inits, None, want_labels=True, want_counts=True)
+    o = orc()
+    Xw = X.astype(np.float64)
+    for w in range(2):
+        e = o.kmeans(Xw[idx[w]], inits[w])
+        assert r["iterations"][w] == e["iterations"] and r["stop"][w] == e["stop"], w
+        assert np.array_equal(r["labels"][w], e["labels"]), w
+        assert np.array_equal(r["counts"][w], e["counts"]), w
+        assert rel(r["objective"][w], e["objective"]) <= RTOL, w
