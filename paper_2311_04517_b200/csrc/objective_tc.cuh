@@ -313,16 +313,28 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                     nn3 = __ffma2_rn(make_float2(x[d + 2], x[d + 3]), make_float2(x[d + 2], x[d + 3]), nn3);
                 }
                 const float nn = (nn2.x + nn2.y) + (nn3.x + nn3.y);
-                unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kap2 * (nn + cmax2)));
+                const float btc = kap2 * (nn + cmax2);
+                unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > btc));
                 if (tie) {
                     // second tier: rows the tf32 screen cannot settle get the fp32 FFMA2 screen
                     // (error <= 2 (NP/2 + 12) 2^-24 (|x| + |c|)^2 per value, the bound of the centre-pair
-                    // kernel) over every valid centre, with broadcast record loads
+                    // kernel) over the centres whose tf32 value is within the bound of the minimum (any
+                    // other centre is provably farther than the nearest), with broadcast record loads
                     bool still = false;
                     if (tie & (1u << lane)) {
+                        const float thr = m1 + btc;
+                        uint32_t cand = 0;
+#pragma unroll
+                        for (int q = 0; q < KP; ++q) {
+                            const float2 c2 = cc[q];
+                            if (__uint_as_float(v[2 * q]) + c2.x <= thr) cand |= 1u << (2 * q);
+                            if (__uint_as_float(v[2 * q + 1]) + c2.y <= thr) cand |= 1u << (2 * q + 1);
+                        }
+                        cand &= kv >= 32 ? 0xffffffffu : ((1u << kv) - 1u);
                         float n1 = __int_as_float(0x7f800000), n2 = n1;
                         int l1 = 0;
-                        for (int j = 0; j < kv; ++j) {
+                        for (; cand; cand &= cand - 1) {  // ascending j
+                            const int j = __ffs(cand) - 1;
                             const float* rc = s_rec[j];
                             float2 a0 = make_float2(rc[NP], 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll

@@ -226,14 +226,26 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
             float nn = 0.f;
             double rc = row_cost(valid ? lab : 0, &nn);
             const int lab0 = lab;
-            unsigned tie = __ballot_sync(0xffffffffu, valid && !(p2[0] - p1[0] > kap2 * (nn + cmax2)));
+            const float btc = kap2 * (nn + cmax2);
+            unsigned tie = __ballot_sync(0xffffffffu, valid && !(p2[0] - p1[0] > btc));
             if (tie) {
-                // second tier: fp32 FFMA2 re-screen of the flagged rows over every valid centre
+                // second tier: fp32 FFMA2 re-screen of the flagged rows over the centres whose tf32
+                // value is within the bound of the minimum (the others are provably farther)
                 bool still = false;
                 if (tie & (1u << lane)) {
+                    const float thr = p1[0] + btc;
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int q = 0; q < KPS; ++q) {
+                        const float2 c2 = ccp[q];
+                        if (__uint_as_float(v[2 * q]) + c2.x <= thr) cand |= 1u << (2 * q);
+                        if (__uint_as_float(v[2 * q + 1]) + c2.y <= thr) cand |= 1u << (2 * q + 1);
+                    }
+                    cand &= kv >= 32 ? 0xffffffffu : ((1u << kv) - 1u);
                     float n1 = __int_as_float(0x7f800000), n2 = n1;
                     int l1 = 0;
-                    for (int j = 0; j < kv; ++j) {
+                    for (; cand; cand &= cand - 1) {  // ascending j
+                        const int j = __ffs(cand) - 1;
                         const double* cj = Cg + (int64_t)j * NPW;
                         float2 acc = make_float2(s_cc[j], 0.f), acc2 = make_float2(0.f, 0.f);
                         for (int c = 0; c < NPW / 4; ++c) {

@@ -447,14 +447,18 @@ __global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nbl
 
 // candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): an fp32 screen decides
 // the rows the candidate provably cannot improve (value d2_i, exact); the others get the
-// reference distance. Per-row values are kept for the winner's D^2 update; block partials by a
-// fixed tree, so the costs are exact sums in a fixed order.
+// reference distance. Per-row values are kept for the winner's D^2 update; block partials by warp
+// shuffle trees and then the warps in order, so the costs are exact sums in a fixed order. Each
+// CTA covers kCostBPC consecutive 256-row blocks (records built once).
+constexpr int kCostBPC = 8;  // 256-row blocks per CTA of the candidate-cost pass
+
 template <typename T>
 __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, WideBufs b, int nblk) {
-    __shared__ double red[kWT];
+    __shared__ double wred[kMaxCandidates][kWT / 32];
     extern __shared__ __align__(16) float crec_raw[];  // [ncand][n4] -2 * candidate (fp32)
     __shared__ float ccn[kMaxCandidates];
-    const int w = blockIdx.y, blk = blockIdx.x, n = p.n, ncand = p.candidates;
+    const int w = blockIdx.y, n = p.n, ncand = p.candidates;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (!slot_live(b.st[w])) return;
     const int n4 = (n + 3) & ~3;
     auto crec = [&](int c) { return crec_raw + (int64_t)c * n4; };
@@ -471,42 +475,52 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
     __syncthreads();
     const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
     const bool vec = sizeof(T) == 4 && (n & 3) == 0;
-    const int64_t s = p.s, i = (int64_t)blk * kSeedRows + threadIdx.x;
-    const bool valid = i < s;
-    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + (valid ? i : 0)) * n;
-    const double d2i = valid ? b.d2[(int64_t)w * s + i] : 0.0;
-    // screen: s~_c = |c|^2 + x.(-2c); dist~_c = |x|^2 + s~_c
-    float2 a[kMaxCandidates], nn = make_float2(0.f, 0.f);
+    const int64_t s = p.s;
+    const int blk0 = blockIdx.x * kCostBPC, blk1 = min(nblk, blk0 + kCostBPC);
+    for (int blk = blk0; blk < blk1; ++blk) {  // the candidate records are built once per CTA
+        const int64_t i = (int64_t)blk * kSeedRows + threadIdx.x;
+        const bool valid = i < s;
+        const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + (valid ? i : 0)) * n;
+        const double d2i = valid ? b.d2[(int64_t)w * s + i] : 0.0;
+        // screen: s~_c = |c|^2 + x.(-2c); dist~_c = |x|^2 + s~_c
+        float2 a[kMaxCandidates], nn = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int c = 0; c < kMaxCandidates; ++c) a[c] = make_float2(c < ncand ? ccn[c] : 0.f, 0.f);
-    for (int d = 0; d < n4; d += 4) {
-        const float4 xv = load4<T>(x, d, n, vec);
-        const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
-        nn = __ffma2_rn(xa, xa, nn);
-        nn = __ffma2_rn(xb, xb, nn);
+        for (int c = 0; c < kMaxCandidates; ++c) a[c] = make_float2(c < ncand ? ccn[c] : 0.f, 0.f);
+        for (int d = 0; d < n4; d += 4) {
+            const float4 xv = load4<T>(x, d, n, vec);
+            const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
+            nn = __ffma2_rn(xa, xa, nn);
+            nn = __ffma2_rn(xb, xb, nn);
 #pragma unroll
-        for (int c = 0; c < kMaxCandidates; ++c)
-            if (c < ncand) {
-                const float4 cv = *reinterpret_cast<const float4*>(crec(c) + d);
-                a[c] = __ffma2_rn(xa, make_float2(cv.x, cv.y), a[c]);
-                a[c] = __ffma2_rn(xb, make_float2(cv.z, cv.w), a[c]);
-            }
-    }
-    const float xx = nn.x + nn.y, xn = sqrtf(xx) * 1.0001f;
-    const float f2 = __double2float_ru(d2i);
-    for (int c = 0; c < ncand; ++c) {
-        double v = d2i;
-        if (valid) {
-            const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
-            const float dt = xx + (a[c].x + a[c].y);
-            if (!(dt - kappa * sc * sc > f2))  // may improve: the reference distance
-                v = fmin(d2i, dist1<T>(x, n, cand + (int64_t)c * n, sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0));
-            b.dc[((int64_t)w * kMaxCandidates + c) * s + i] = v;
-        } else {
-            v = 0.0;
+            for (int c = 0; c < kMaxCandidates; ++c)
+                if (c < ncand) {
+                    const float4 cv = *reinterpret_cast<const float4*>(crec(c) + d);
+                    a[c] = __ffma2_rn(xa, make_float2(cv.x, cv.y), a[c]);
+                    a[c] = __ffma2_rn(xb, make_float2(cv.z, cv.w), a[c]);
+                }
         }
-        const double tot = cta_sum(v, red);
-        if (threadIdx.x == 0) b.bcost[((int64_t)w * kMaxCandidates + c) * nblk + blk] = tot;
+        const float xx = nn.x + nn.y, xn = sqrtf(xx) * 1.0001f;
+        const float f2 = __double2float_ru(d2i);
+        for (int c = 0; c < ncand; ++c) {
+            double v = 0.0;
+            if (valid) {
+                v = d2i;
+                const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
+                const float dt = xx + (a[c].x + a[c].y);
+                if (!(dt - kappa * sc * sc > f2))  // may improve: the reference distance
+                    v = fmin(d2i, dist1<T>(x, n, cand + (int64_t)c * n, sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0));
+                b.dc[((int64_t)w * kMaxCandidates + c) * s + i] = v;
+            }
+            v = warp_sum(v);  // block partial: warp trees, then the warps in order (fixed order)
+            if (lane == 0) wred[c][warp] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < ncand) {
+            double tot = 0.0;
+            for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
+            b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blk] = tot;
+        }
+        __syncthreads();
     }
 }
 
@@ -1073,7 +1087,8 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     for (int it = 0; it < slots; ++it) {
         wide_cdf_kernel<<<dim3((unsigned)((nblk + 63) / 64), (unsigned)Wb), 64, 0, st>>>(p, b, nblk);
         wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
-        wide_cost_kernel<T><<<dim3((unsigned)nblk, (unsigned)Wb), kWT, cost_smem, st>>>(p, b, nblk);
+        wide_cost_kernel<T><<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, cost_smem, st>>>(
+            p, b, nblk);
         wide_decide_kernel<<<Wb, 128, 0, st>>>(p, b, nblk);
         wide_d2upd_kernel<<<rows_grid, kWT, 0, st>>>(p, b, it);
     }

@@ -242,12 +242,23 @@ __global__ void __launch_bounds__(WtcGeo<NA>::THREADS, 1)
             }
             const float nn = nn2.x + nn2.y;
             bool flag = false;
-            if (valid && !(p2[0] - p1[0] > kap2 * (nn + cmax2))) {
-                // second tier: fp32 FFMA2 re-screen over every centre of the worker
+            const float btc = kap2 * (nn + cmax2);
+            if (valid && !(p2[0] - p1[0] > btc)) {
+                // second tier: fp32 FFMA2 re-screen over the centres whose tf32 value is within the
+                // bound of the minimum (any other centre is provably farther than the nearest one)
                 const double* C = b.Cm + w * (int64_t)k * NPW;
+                const float thr = p1[0] + btc;
+                uint32_t cand = 0;  // centres within the bound (register-resident values, unrolled)
+#pragma unroll
+                for (int q = 0; q < KPS; ++q) {
+                    if (__uint_as_float(v[2 * q]) + cc[q].x <= thr) cand |= 1u << (2 * q);
+                    if (__uint_as_float(v[2 * q + 1]) + cc[q].y <= thr) cand |= 1u << (2 * q + 1);
+                }
+                cand &= k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
                 float n1 = __int_as_float(0x7f800000), n2 = n1;
                 int l1 = 0;
-                for (int j = 0; j < k; ++j) {
+                for (; cand; cand &= cand - 1) {  // ascending j, as the reference scans
+                    const int j = __ffs(cand) - 1;
                     const double* cj = C + (int64_t)j * NPW;
                     float2 acc = make_float2(__ldg(ccw + w * (kTcwN + 1) + j), 0.f), acc2 = make_float2(0.f, 0.f);
                     for (int c = 0; c < NPW / 4; ++c) {
