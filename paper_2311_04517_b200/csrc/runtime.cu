@@ -313,39 +313,63 @@ __global__ void round_end_kernel(const RoundEndParams p) {
     }
     s_nd[threadIdx.x] = nd;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        // n_d: lane sums of 8 slots, then a warp tree (integers: order-free)
+        const int lane = threadIdx.x;
         unsigned long long t = 0;
-        for (int i = 0; i < (int)blockDim.x; ++i) t += s_nd[i];
-        *p.nd_total += t;
+        for (int i = lane; i < (int)blockDim.x; i += 32) t += s_nd[i];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) *p.nd_total += t;
+        // publication in worker-id order with strict < (engine.hpp:391-402): worker w publishes iff
+        // its candidate objective is below min(shared best, every earlier candidate) -- an
+        // exclusive prefix-min, 32 workers per step
         int winner = -1;
         if (p.publish || p.carry) {
             double best = *p.sh_obj;
             int64_t ver = *p.sh_version;
             int64_t cnt = *p.pub_count;
-            for (int w = 0; w < p.W; ++w) {
-                const double f = rs_obj[w];
-                const bool cand = (p.publish && rs_acc[w]) || (p.carry && isfinite(f));
-                if (cand && f < best) {
-                    best = f;
-                    winner = w;
-                    ++ver;
-                    if (cnt < p.pub_cap) {
-                        p.pub_log[cnt * 4 + 0] = (double)ver;
-                        p.pub_log[cnt * 4 + 1] = (double)(p.worker_base + w);
-                        p.pub_log[cnt * 4 + 2] = f;
-                        p.pub_log[cnt * 4 + 3] = p.ts;
-                    }
-                    ++cnt;
+            const double inf = __longlong_as_double(0x7ff0000000000000LL);
+            for (int w0 = 0; w0 < p.W; w0 += 32) {
+                const int w = w0 + lane;
+                const double f = w < p.W ? rs_obj[w] : inf;
+                const bool cand = w < p.W && ((p.publish && rs_acc[w]) || (p.carry && isfinite(f)));
+                const double c = cand ? f : inf;
+                double incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl = fmin(incl, y);
+                }
+                double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+                if (lane == 0) excl = inf;
+                const bool pub = cand && c < fmin(best, excl);
+                const unsigned mask = __ballot_sync(0xffffffffu, pub);
+                const int rank = __popc(mask & ((1u << lane) - 1u));
+                if (pub && cnt + rank < p.pub_cap) {
+                    const int64_t at = cnt + rank;
+                    p.pub_log[at * 4 + 0] = (double)(ver + rank + 1);
+                    p.pub_log[at * 4 + 1] = (double)(p.worker_base + w);
+                    p.pub_log[at * 4 + 2] = f;
+                    p.pub_log[at * 4 + 3] = p.ts;
+                }
+                if (mask) {
+                    const int last = 31 - __clz(mask);
+                    winner = w0 + last;
+                    best = __shfl_sync(0xffffffffu, c, last);
+                    ver += __popc(mask);
+                    cnt += __popc(mask);
                 }
             }
-            *p.pub_count = cnt;
-            if (winner >= 0) {
-                *p.sh_obj = best;
-                *p.sh_version = ver;
-                *p.sh_worker = p.worker_base + winner;
+            if (lane == 0) {
+                *p.pub_count = cnt;
+                if (winner >= 0) {
+                    *p.sh_obj = best;
+                    *p.sh_version = ver;
+                    *p.sh_worker = p.worker_base + winner;
+                }
             }
         }
-        s_winner = winner;
+        if (lane == 0) s_winner = winner;
     }
     __syncthreads();
     const int wn = s_winner;
