@@ -154,6 +154,26 @@ def exchange_best(eng, world, device):
         eng.import_best(float(r[0]), int(r[1]), r[2:2 + C_.size].reshape(C_.shape), r[2 + C_.size:].astype(np.uint8))
 
 
+def finish_global(eng, ds, ctx, device):
+    """N > 1 finish: select_best over every rank's workers is the exchanged shared best (the
+    cooperative strategy publishes every strict improvement); f(C, X) = this shard's partial from
+    the device pass + all-reduce over the ranks (north star: per-shard partial sum, then allreduce).
+    n_d: the rounds' plus this shard's final pass (m_shard x valid centres)."""
+    import torch
+    import torch.distributed as dist
+    from types import SimpleNamespace
+    import paper_2311_04517_b200 as hp
+    _, _, C_, f = eng.export_best()
+    valid = f == 0
+    kv = int(valid.sum())
+    cost = torch.zeros(1, dtype=torch.float64, device=device)
+    if kv > 0:
+        Cv = torch.from_numpy(np.ascontiguousarray(C_[valid])).to(device)
+        hp._lib.check(hp._lib.lib.hpcg_assign_dev(ctx.h, ds.h, Cv.data_ptr(), kv, None, cost.data_ptr()))
+    dist.all_reduce(cost)
+    return SimpleNamespace(distance_evals=eng.distance_evals() + ds.m * kv, full_objective=float(cost.item()))
+
+
 def merge_records(recs):
     """Index of the winning (objective, worker) record: strict min objective, ties to the
     lowest global worker id (engine.hpp:129-138 publication order); None if all infinite."""
@@ -190,8 +210,7 @@ def run_gpu(args, world, rank, local):
             eng.rounds(1)
             if world > 1:
                 exchange_best(eng, world, device)
-        res = eng.finish()
-        return res
+        return eng.finish() if world == 1 else finish_global(eng, ds, ctx, device)
 
     for i in range(args.warmup):
         step(10_000 + i)
@@ -343,7 +362,7 @@ def e2e_run_multi(X, args, world, rank, ctx, device):
         for _ in range(ROUNDS):
             eng.rounds(1)
             exchange_best(eng, world, device)
-        r = eng.finish()
+        r = finish_global(eng, ds, ctx, device)
         eng.close()
         ds.close()
         torch.cuda.synchronize()
