@@ -92,6 +92,18 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
                         hpcg_dataset** out);
 int hpcg_dataset_wrap(hpcg_ctx* ctx, const void* X_dev, hpcg_dtype dtype, int64_t m, int64_t n,
                       hpcg_dataset** out); /* borrows X_dev (must outlive the handle) */
+/* Row-sharded X (multi-GPU global sampling): shard i holds shard_rows[i] rows at
+ * shard_dev[i] -- local or peer memory (hpcg_ipc_open) -- in global row order; m = the sum. Sample
+ * indices are global (engine.hpp:165-177 over all m rows), the gathers read remote rows over
+ * NVLink. Borrowed pointers (must outlive the handle); at most 8 shards. */
+int hpcg_dataset_wrap_sharded(hpcg_ctx* ctx, const void* const* shard_dev, const int64_t* shard_rows, int32_t nshards,
+                              hpcg_dtype dtype, int64_t n, hpcg_dataset** out);
+/* CUDA IPC of device memory between the processes of one node: a 72-byte handle (the
+ * allocation's cudaIpcMemHandle_t + the pointer's offset inside it). */
+#define HPCG_IPC_HANDLE_BYTES 72
+int hpcg_ipc_export(const void* dev_ptr, void* handle_out);
+int hpcg_ipc_open(hpcg_ctx* ctx, const void* handle, void** dev_ptr_out);
+int hpcg_ipc_close(hpcg_ctx* ctx, void* dev_ptr, const void* handle);
 int hpcg_dataset_destroy(hpcg_dataset* ds);
 const void* hpcg_dataset_device_ptr(const hpcg_dataset* ds);
 

@@ -7,7 +7,8 @@ from ._lib import (CudaError, HpcgError, InvalidArgument, LogicError, NoSolution
 from .api import (Assignment, ClusteringResult, Context, DeviceDataset, DistCounter, Engine,  # noqa: F401
                   EngineConfig, LloydConfig, LloydOutcome, RngStream, SeedConfig, assign_nearest,
                   assign_valid_subset, default_context, draw_sample, final_assignment, gen_mixture, kmeans,
-                  kmeanspp_seed, mssc_objective, philox_sample_indices, reference_draw_indices, reinit_degenerate, run, select_best,
+                  ipc_close, ipc_export, ipc_open, kmeanspp_seed, mssc_objective, philox_sample_indices,
+                  reference_draw_indices, reinit_degenerate, run, select_best,
                   worker_step_batched)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -16,6 +16,7 @@ LIB_PATH = Path(os.environ.get("HPCG_LIB_OVERRIDE") or (Path(__file__).resolve()
 EXPORTS = (
     "hpcg_last_error", "hpcg_abi_version", "hpcg_ctx_create", "hpcg_ctx_destroy", "hpcg_ctx_set_stream",
     "hpcg_ctx_synchronize", "hpcg_ctx_launch_count", "hpcg_dataset_upload", "hpcg_dataset_wrap",
+    "hpcg_dataset_wrap_sharded", "hpcg_ipc_export", "hpcg_ipc_open", "hpcg_ipc_close",
     "hpcg_dataset_destroy", "hpcg_dataset_device_ptr", "hpcg_assign", "hpcg_assign_dev",
     "hpcg_worker_step_batched", "hpcg_gather", "hpcg_sample_indices", "hpcg_reference_draw_indices", "hpcg_rng_seed",
     "hpcg_rng_derive", "hpcg_rng_draw", "hpcg_engine_create", "hpcg_engine_rounds", "hpcg_engine_run", "hpcg_engine_round_index",
@@ -104,6 +105,10 @@ def _load():
         "hpcg_ctx_synchronize": (C.c_int, [P]),
         "hpcg_ctx_launch_count": (I64, [P]),
         "hpcg_dataset_upload": (C.c_int, [P, P, C.c_int, I64, I64, P]),
+        "hpcg_dataset_wrap_sharded": (C.c_int, [P, P, P, C.c_int32, C.c_int, I64, P]),
+        "hpcg_ipc_export": (C.c_int, [P, P]),
+        "hpcg_ipc_open": (C.c_int, [P, P, P]),
+        "hpcg_ipc_close": (C.c_int, [P, P, P]),
         "hpcg_dataset_wrap": (C.c_int, [P, P, C.c_int, I64, I64, P]),
         "hpcg_dataset_destroy": (C.c_int, [P]),
         "hpcg_dataset_device_ptr": (P, [P]),

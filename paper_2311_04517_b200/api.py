@@ -119,6 +119,36 @@ class DeviceDataset:
         self.dtype = np.float32 if code == _lib.F32 else np.float64
 
     @classmethod
+    def from_shards(cls, shards, ctx: Context | None = None, keepalive=None):
+        """Row-sharded X (global row order): shards = [(device_ptr, rows), ...] or CUDA tensors,
+        local or peer-mapped (ipc_open). Samples are drawn over all rows (multi-GPU global sampling)."""
+        import torch
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        ptrs, rows, n, dt = [], [], None, None
+        for sh in shards:
+            if isinstance(sh, torch.Tensor):
+                assert sh.is_cuda and sh.is_contiguous() and sh.dim() == 2
+                ptrs.append(sh.data_ptr())
+                rows.append(sh.shape[0])
+                n = sh.shape[1]
+                dt = np.float32 if sh.dtype == torch.float32 else np.float64
+            else:
+                ptrs.append(int(sh[0]))
+                rows.append(int(sh[1]))
+                n, dt = int(sh[2]), np.dtype(sh[3]).type
+        pa = (C.c_void_p * len(ptrs))(*ptrs)
+        ra = (C.c_int64 * len(rows))(*rows)
+        h = C.c_void_p()
+        code = _lib.F32 if dt == np.float32 else _lib.F64
+        check(lib.hpcg_dataset_wrap_sharded(self.ctx.h, pa, ra, len(ptrs), code, n, C.byref(h)))
+        self.h = h
+        self.m, self.n = int(sum(rows)), int(n)
+        self.dtype = dt
+        self._keep = (list(shards), keepalive)
+        return self
+
+    @classmethod
     def from_torch(cls, t, ctx: Context | None = None):
         assert t.is_cuda and t.is_contiguous() and t.dim() == 2
         import torch
@@ -135,6 +165,29 @@ class DeviceDataset:
             self.close()
         except Exception:
             pass
+
+
+IPC_HANDLE_BYTES = 72
+
+
+def ipc_export(device_ptr: int) -> bytes:
+    """CUDA IPC handle of device memory (allocation handle + offset), for another process."""
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    check(lib.hpcg_ipc_export(C.c_void_p(device_ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes, ctx: Context | None = None) -> int:
+    """Map another process's memory (peer access over NVLink when it lives on another GPU)."""
+    ctx = ctx or default_context()
+    p = C.c_void_p()
+    check(lib.hpcg_ipc_open(ctx.h, C.create_string_buffer(handle, IPC_HANDLE_BYTES), C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(device_ptr: int, handle: bytes, ctx: Context | None = None):
+    ctx = ctx or default_context()
+    check(lib.hpcg_ipc_close(ctx.h, C.c_void_p(device_ptr), C.create_string_buffer(handle, IPC_HANDLE_BYTES)))
 
 
 def _as_dataset(X, ctx=None) -> DeviceDataset:

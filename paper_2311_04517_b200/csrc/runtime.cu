@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cuda.h>
 #include <limits>
 #include <mutex>
 #include <string>
@@ -225,7 +226,10 @@ __global__ void fma_probe_kernel(float* out, float a, float b, int iters) {
 
 struct hpcg_dataset {
     hpcg_ctx* ctx = nullptr;
-    const void* X = nullptr;
+    const void* X = nullptr;  // shard 0 (the whole X when unsharded)
+    int nshards = 1;          // row shards (hpcg_dataset_wrap_sharded); shard s holds rows
+    const void* shard_ptr[kMaxShards] = {};   // [shard_end[s-1], shard_end[s])
+    int64_t shard_end[kMaxShards] = {};
     bool owned = false;
     size_t bytes = 0;  // owned allocation size
     int dtype = 0;
@@ -247,6 +251,14 @@ struct hpcg_dataset {
 namespace {
 size_t dsize(int dtype) { return dtype == HPCG_F32 ? 4 : 8; }
 
+void set_shards(StepParams& p, const hpcg_dataset* ds) {
+    p.nshards = ds->nshards;
+    for (int i = 0; i < ds->nshards && i < kMaxShards; ++i) {
+        p.shard_ptr[i] = ds->shard_ptr[i];
+        p.shard_end[i] = ds->shard_end[i];
+    }
+}
+
 int check_shape(int dtype, int64_t n, int64_t k) {
     if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
     if (n < 1) return fail(HPCG_EINVAL, "dataset needs at least one feature");
@@ -257,12 +269,21 @@ int check_shape(int dtype, int64_t n, int64_t k) {
 }
 
 // ------------------------------------------------------------ small kernels
-__global__ void gather_kernel(const unsigned char* X, int64_t rowb, const int64_t* idx, int64_t s,
-                              unsigned char* out) {
+struct ShardTable {
+    int n = 1;
+    const unsigned char* ptr[kMaxShards] = {};
+    int64_t end[kMaxShards] = {};
+};
+
+__global__ void gather_kernel(const ShardTable t, int64_t rowb, const int64_t* idx, int64_t s, unsigned char* out) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= s * rowb) return;
     const int64_t i = e / rowb, b = e - i * rowb;
-    out[e] = X[idx[i] * rowb + b];
+    int64_t g = idx[i];
+    int sh = 0;
+    while (sh + 1 < t.n && g >= t.end[sh]) ++sh;
+    if (sh) g -= t.end[sh - 1];
+    out[e] = t.ptr[sh][g * rowb + b];
 }
 
 struct RoundEndParams {
@@ -472,20 +493,42 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
         op.rec_slot = ctx->rec_slot;
         op.rec_scratch = ctx->rec_scratch.as<float4>();
     }
-    op.X = ds->X;
-    op.m = ds->m;
     op.n = (int)ds->n;
     op.kv = kv;
     op.C = C_valid_dev;
     op.remap = remap_dev;
-    op.labels = labels_dev;
     op.counts = counts_dev;
     op.block_cost = blocks.as<double>();
-    int used = nb;
-    KTimer kt(ctx, 1);
-    CU(launch_objective(ds->dtype, op, &used, ctx->stream));
-    kt.done();
-    sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, cost_dev);
+    if (ds->nshards <= 1) {
+        op.X = ds->X;
+        op.m = ds->m;
+        op.labels = labels_dev;
+        int used = nb;
+        KTimer kt(ctx, 1);
+        CU(launch_objective(ds->dtype, op, &used, ctx->stream));
+        kt.done();
+        sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, cost_dev);
+        CU(cudaGetLastError());
+        ctx->launches += launched + 1;
+        return HPCG_OK;
+    }
+    // row-sharded X: one pass per shard (labels at the shard's global offset), the shard sums in
+    // shard order (fixed), then their sum
+    CU(blocks.reserve((size_t)(nb + kMaxShards) * sizeof(double)));
+    double* shard_cost = blocks.as<double>() + nb;
+    op.block_cost = blocks.as<double>();
+    for (int sh = 0; sh < ds->nshards; ++sh) {
+        const int64_t b0 = sh ? ds->shard_end[sh - 1] : 0;
+        op.X = ds->shard_ptr[sh];
+        op.m = ds->shard_end[sh] - b0;
+        op.labels = labels_dev ? labels_dev + b0 : nullptr;
+        int used = nb;
+        CU(launch_objective(ds->dtype, op, &used, ctx->stream));
+        sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, shard_cost + sh);
+        CU(cudaGetLastError());
+        ctx->launches += 1;
+    }
+    sum_blocks_kernel<<<1, 32, 0, ctx->stream>>>(shard_cost, ds->nshards, cost_dev);
     CU(cudaGetLastError());
     ctx->launches += launched + 1;
     return HPCG_OK;
@@ -638,6 +681,8 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
     auto* ds = new hpcg_dataset;
     ds->ctx = ctx;
     ds->X = d;
+    ds->shard_ptr[0] = d;
+    ds->shard_end[0] = m;
     ds->owned = true;
     ds->bytes = have;
     ds->dtype = dtype;
@@ -653,11 +698,86 @@ int hpcg_dataset_wrap(hpcg_ctx* ctx, const void* X_dev, hpcg_dtype dtype, int64_
     auto* ds = new hpcg_dataset;
     ds->ctx = ctx;
     ds->X = X_dev;
+    ds->shard_ptr[0] = X_dev;
+    ds->shard_end[0] = m;
     ds->owned = false;
     ds->dtype = dtype;
     ds->m = m;
     ds->n = n;
     *out = ds;
+    return HPCG_OK;
+}
+
+int hpcg_dataset_wrap_sharded(hpcg_ctx* ctx, const void* const* shard_dev, const int64_t* shard_rows, int32_t nshards,
+                              hpcg_dtype dtype, int64_t n, hpcg_dataset** out) {
+    if (nshards < 1 || nshards > kMaxShards) return fail(HPCG_EINVAL, "Dataset: 1 to 8 row shards");
+    if (n < 1) return fail(HPCG_EINVAL, "Dataset: needs at least one row and one column");
+    if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
+    int64_t m = 0;
+    for (int i = 0; i < nshards; ++i) {
+        if (shard_rows[i] < 1 || !shard_dev[i]) return fail(HPCG_EINVAL, "Dataset: empty shard");
+        m += shard_rows[i];
+    }
+    auto* ds = new hpcg_dataset;
+    ds->ctx = ctx;
+    ds->X = shard_dev[0];
+    ds->nshards = nshards;
+    int64_t end = 0;
+    for (int i = 0; i < nshards; ++i) {
+        end += shard_rows[i];
+        ds->shard_ptr[i] = shard_dev[i];
+        ds->shard_end[i] = end;
+    }
+    ds->owned = false;
+    ds->dtype = dtype;
+    ds->m = m;
+    ds->n = n;
+    *out = ds;
+    return HPCG_OK;
+}
+
+// the IPC handle names the whole allocation: the pointer's offset inside it travels along
+// (allocators such as torch's sub-allocate), found with the driver's cuMemGetAddressRange
+int hpcg_ipc_export(const void* dev_ptr, void* handle_out) {
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range = nullptr;
+    if (!range) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return fail(HPCG_ECUDA, "ipc: cuMemGetAddressRange unavailable");
+        range = reinterpret_cast<RangeFn>(f);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return fail(HPCG_EINVAL, "ipc: not a device allocation");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    const uint64_t off = (uint64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+    std::memcpy(handle_out, &h, sizeof h);
+    std::memcpy(static_cast<char*>(handle_out) + sizeof h, &off, 8);
+    return HPCG_OK;
+}
+
+int hpcg_ipc_open(hpcg_ctx* ctx, const void* handle, void** dev_ptr_out) {
+    cudaSetDevice(ctx->device);
+    cudaIpcMemHandle_t h;
+    uint64_t off = 0;
+    std::memcpy(&h, handle, sizeof h);
+    std::memcpy(&off, static_cast<const char*>(handle) + sizeof h, 8);
+    void* base = nullptr;
+    CU(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr_out = static_cast<char*>(base) + off;
+    return HPCG_OK;
+}
+
+int hpcg_ipc_close(hpcg_ctx* ctx, void* dev_ptr, const void* handle) {
+    cudaSetDevice(ctx->device);
+    uint64_t off = 0;
+    std::memcpy(&off, static_cast<const char*>(handle) + sizeof(cudaIpcMemHandle_t), 8);
+    CU(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - off));
     return HPCG_OK;
 }
 
@@ -756,8 +876,14 @@ int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, 
     CU(ctx->s_b.reserve((size_t)(s * rowb)));
     CU(h2d(ctx->s_a.as<int64_t>(), idx_host, (size_t)s, ctx->stream));
     const int64_t tot = s * rowb;
-    gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(
-        static_cast<const unsigned char*>(ds->X), rowb, ctx->s_a.as<int64_t>(), s, ctx->s_b.as<unsigned char>());
+    ShardTable tab;
+    tab.n = ds->nshards;
+    for (int i = 0; i < ds->nshards; ++i) {
+        tab.ptr[i] = static_cast<const unsigned char*>(ds->shard_ptr[i]);
+        tab.end[i] = ds->shard_end[i];
+    }
+    gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(tab, rowb, ctx->s_a.as<int64_t>(), s,
+                                                                        ctx->s_b.as<unsigned char>());
     CU(cudaGetLastError());
     ctx->launches += 1;
     CU(cudaMemcpyAsync(S_host, ctx->s_b.p, (size_t)tot, cudaMemcpyDeviceToHost, ctx->stream));
@@ -903,6 +1029,7 @@ int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_
 
     StepParams p = {};
     p.X = ds->X;
+    set_shards(p, ds);
     p.m = ds->m;
     SamplePRP::moduli((uint64_t)p.m, p.prp_a, p.prp_b, p.prp_inv_b);
     p.n = (int)n;
@@ -1050,6 +1177,7 @@ int engine_round(hpcg_engine* e) {
     }
     StepParams p = {};
     p.X = e->ds->X;
+    set_shards(p, e->ds);
     p.m = e->ds->m;
     SamplePRP::moduli((uint64_t)p.m, p.prp_a, p.prp_b, p.prp_inv_b);
     p.n = (int)n;

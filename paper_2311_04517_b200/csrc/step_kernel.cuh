@@ -24,6 +24,8 @@ constexpr int kStepWarps = kStepThreads / 32;
 constexpr int kMaxK = 32;          // label fits u8 and the per-warp partial table fits smem
 constexpr int kMaxCandidates = 4;  // K-means++ candidates per slot (reference default 3) in one sweep
 
+constexpr int kMaxShards = 8;      // row shards of a dataset (one per GPU of a node)
+
 enum StepErr : int32_t { kErrNone = 0, kErrDegenerateInit = 1, kErrMonotone = 2 };
 
 struct StepParams {
@@ -57,6 +59,11 @@ struct StepParams {
     int32_t max_iters;
     double rel_tol;
     int32_t do_lloyd;
+    // row-sharded X (multi-GPU global sampling: remote shards peer-mapped): nshards > 1 selects
+    // the shard of global row g by the cumulative row ends; nshards <= 1: X holds every row
+    int32_t nshards;
+    const void* shard_ptr[kMaxShards];
+    int64_t shard_end[kMaxShards];
     // geometry chosen by the host
     int32_t rows_cap;  // max rows per CTA (smem layout)
     // outputs (indexed by local worker)
@@ -84,6 +91,16 @@ struct StepParams {
 };
 
 constexpr int kTraceSlots = 32;
+
+// address of global row g (n elements of T) through the shard table
+template <typename T>
+HPCG_DEV const T* row_ptr(const StepParams& p, int64_t g) {
+    if (p.nshards <= 1) return static_cast<const T*>(p.X) + g * p.n;
+    int sh = 0;
+    while (sh + 1 < p.nshards && g >= p.shard_end[sh]) ++sh;
+    const int64_t base = sh ? p.shard_end[sh - 1] : 0;
+    return static_cast<const T*>(p.shard_ptr[sh]) + (g - base) * p.n;
+}
 template <int V>
 struct IntC {
     static constexpr int value = V;
@@ -506,7 +523,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                     for (int j = 0; j < G::CPR; ++j) {
                         const int rl = j * RPI + lane / G::CPR, row = g * 32 + rl;
                         const int64_t src = __shfl_sync(0xffffffffu, gi, rl);
-                        if (row < nr) cp_async16(samp + G::elem_off(row, q * EPC), X + src * NP + q * EPC);
+                        if (row < nr) cp_async16(samp + G::elem_off(row, q * EPC), row_ptr<T>(p, src) + q * EPC);
                     }
                 }
             }
@@ -521,19 +538,19 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 constexpr int EPC = 16 / (int)sizeof(T);
                 for (int e = tid; e < nr * cpr; e += kStepThreads) {
                     const int li = e / cpr, q = e - li * cpr;
-                    cp_async16(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
+                    cp_async16(samp + G::elem_off(li, q * EPC), row_ptr<T>(p, gx[li]) + q * EPC);
                 }
             } else if ((rowb & 7) == 0) {  // 8-B chunks
                 const int cpr = rowb >> 3;
                 constexpr int EPC = 8 / (int)sizeof(T);
                 for (int e = tid; e < nr * cpr; e += kStepThreads) {
                     const int li = e / cpr, q = e - li * cpr;
-                    cp_async8(samp + G::elem_off(li, q * EPC), X + gx[li] * n + q * EPC);
+                    cp_async8(samp + G::elem_off(li, q * EPC), row_ptr<T>(p, gx[li]) + q * EPC);
                 }
             } else {  // 4-B elements (fp32, odd n)
                 for (int e = tid; e < nr * n; e += kStepThreads) {
                     const int li = e / n, d = e - li * n;
-                    cp_async4(samp + G::elem_off(li, d), X + gx[li] * n + d);
+                    cp_async4(samp + G::elem_off(li, d), row_ptr<T>(p, gx[li]) + d);
                 }
             }
         }

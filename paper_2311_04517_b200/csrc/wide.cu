@@ -297,7 +297,7 @@ __global__ void wide_gather_kernel(const StepParams p, int w0, T* __restrict__ S
                 g = (int64_t)wl * s + i;
         }
         g = __shfl_sync(0xffffffffu, g, 0);
-        const T* src = X + g * n;
+        const T* src = p.nshards > 1 ? row_ptr<T>(p, g) : X + g * n;
         T* dst = S + ((int64_t)w * s + i) * n;
         for (int d = lane; d < n; d += 32) dst[d] = src[d];
     }
