@@ -201,7 +201,31 @@ def run_gpu(args, world, rank, local):
     ds = hp.DeviceDataset.from_torch(Xd, ctx)
     cfg = hp.EngineConfig(k=K, sample_size=S, n_workers=W_PER_GPU, max_samples=ROUNDS, strategy="cooperative",
                           rng="philox", worker_base=rank * W_PER_GPU)
-    eng = hp.Engine(ds, cfg)
+    sampling = "local shard" if world > 1 else "all rows"
+    ds_eng, peers = ds, []
+    if world > 1 and args.global_sampling:
+        # samples over all ranks' rows (engine.hpp:165-177 semantics): every rank maps the other
+        # ranks' shards by CUDA IPC (NVLink peer access) and the gathers read remote rows directly
+        try:
+            import torch.distributed as dist
+            h = torch.tensor(list(hp.ipc_export(Xd.data_ptr())), dtype=torch.uint8, device=device)
+            hs = [torch.empty_like(h) for _ in range(world)]
+            dist.all_gather(hs, h)
+            shards = []
+            for r in range(world):
+                if r == rank:
+                    shards.append((Xd.data_ptr(), M, N, np.float32))
+                else:
+                    hb = bytes(hs[r].cpu().tolist())
+                    p = hp.ipc_open(hb, ctx)
+                    peers.append((p, hb))
+                    shards.append((p, M, N, np.float32))
+            ds_eng = hp.DeviceDataset.from_shards(shards, ctx=ctx, keepalive=Xd)
+            sampling = f"global over {world} shards (NVLink P2P gathers)"
+        except Exception as ex:  # keep the run: local-shard sampling, say why
+            ds_eng = ds
+            sampling = f"local shard (global sampling unavailable: {type(ex).__name__}: {ex})"[:160]
+    eng = hp.Engine(ds_eng, cfg)
     fma_tfma = ctx.fma_peak()
 
     def step(seed):
@@ -292,7 +316,8 @@ def run_gpu(args, world, rank, local):
                                "full-data f(C,X)", "m_per_gpu": M, "n": N, "k": K, "s": S,
                    "workers_per_gpu": W_PER_GPU, "rounds": ROUNDS, "rng": "philox",
                    "l2": "X (640 MB/GPU) exceeds L2 (126 MB); samples gathered from HBM every round",
-                   "parallelism": f"{world} GPU(s), one process per GPU, NCCL incumbent exchange per round"},
+                   "parallelism": f"{world} GPU(s), one process per GPU, NCCL incumbent exchange per round",
+                   "sampling": sampling},
         "distance_evals_per_step": nd_all / args.steps,
         "objective_pass": {"gbs": obj_gbs, "ms": float(np.median(obj_ms)), "bytes": obj_bytes,
                            "roofline": {"bound": "hbm", "achieved": obj_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -449,6 +474,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--global-sampling", action="store_true",
+                    help="N > 1: sample over all ranks' rows (peer-mapped shards) instead of the local shard")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
