@@ -315,12 +315,16 @@ def test_philox_sample_distinct_in_range_and_keyed():
     assert h.min() > 0.8 * s / 10 and h.max() < 1.2 * s / 10
 
 
-@pytest.mark.parametrize("strategy", ["competitive", "cooperative"])
-def test_run_compute_assignment_vs_oracle(strategy):
+@pytest.mark.parametrize("strategy,dtype,n", [("competitive", np.float64, 3), ("cooperative", np.float64, 3),
+                                              # the tensor-core f(C,X) kernels in the engine's finish:
+                                              # device-side valid count (n = 16), host-side (n = 128)
+                                              ("cooperative", np.float32, 16), ("competitive", np.float32, 128)])
+def test_run_compute_assignment_vs_oracle(strategy, dtype, n):
     # the full assignment of a run (engine.hpp:60, 211-229, 490): labels of
     # the valid subset remapped to the original slots, from the device f(C, X) pass
-    X = mixture(30000, 3, 6, seed=23)
-    e = orc().run(X, k=6, sample_size=1500, n_workers=4, max_samples=3, strategy=strategy, seed=9, assignment=True)
+    X = mixture(30000, n, 6, seed=23, dtype=dtype)
+    e = orc().run(X.astype(np.float64), k=6, sample_size=1500, n_workers=4, max_samples=3, strategy=strategy, seed=9,
+                  assignment=True)
     cfg = hp.EngineConfig(k=6, sample_size=1500, n_workers=4, max_samples=3, strategy=strategy, master_seed=9,
                           rng="reference", compute_assignment=True)
     g = hp.run(X, cfg)
