@@ -189,6 +189,7 @@ typedef struct hpcg_run_out {
     uint64_t total_samples;
     int64_t distance_evals;
     int64_t n_publications;
+    double last_timestamp; /* every worker's t_w: rounds run (lockstep) or seconds at the last round end */
 } hpcg_run_out;
 
 /* Stepwise engine: create (validates like engine.hpp:70-86, allocates device state),
@@ -216,6 +217,9 @@ int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d);
 int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels,
                        double* publications, int64_t pub_cap, double* worker_obj, double* traces,
                        int64_t trace_cap, int64_t* trace_len);
+/* The publication log (SharedBest::publication_log, engine.hpp:149-152): up to cap records of
+ * (version, worker, objective, timestamp); *n_out = the number published so far. */
+int hpcg_engine_publications(hpcg_engine* e, double* publications, int64_t cap, int64_t* n_out);
 /* Per-worker incumbents after finish/rounds: C_out[W*k*n], f_out[W*k], obj_out[W] (any may be NULL). */
 int hpcg_engine_worker_incumbents(hpcg_engine* e, double* C_out, uint8_t* f_out, double* obj_out);
 int hpcg_engine_destroy(hpcg_engine* e);

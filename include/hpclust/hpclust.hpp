@@ -668,12 +668,14 @@ inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
     ClusteringResult res;
     res.centroids = CentroidSet(k, n);
     std::vector<std::int32_t> labels(cfg.compute_assignment ? X.rows : 0);
-    const std::int64_t pub_cap = (std::int64_t)std::max<std::size_t>(64, R * std::min<std::size_t>(W, 64));
-    std::vector<double> pubs((std::size_t)pub_cap * 4), wobj(W), traces(W * R * 2);
+    std::vector<double> wobj(W), traces(W * R * 2);
     std::vector<std::int64_t> tlen(W);
     gpu::check(hpcg_engine_finish(e, &o, res.centroids.centers.data(), res.centroids.degenerate.data(),
-                                  cfg.compute_assignment ? labels.data() : nullptr, pubs.data(), pub_cap, wobj.data(),
+                                  cfg.compute_assignment ? labels.data() : nullptr, nullptr, 0, wobj.data(),
                                   traces.data(), (int64_t)R, tlen.data()));
+    const std::int64_t pub_cap = o.n_publications;
+    std::vector<double> pubs((std::size_t)std::max<std::int64_t>(pub_cap, 1) * 4);
+    gpu::check(hpcg_engine_publications(e, pubs.data(), pub_cap, nullptr));
     std::vector<double> incC(W * k * n);
     std::vector<std::uint8_t> incF(W * k);
     gpu::check(hpcg_engine_worker_incumbents(e, incC.data(), incF.data(), nullptr));
@@ -703,7 +705,7 @@ inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
         std::copy_n(incF.data() + w * k, k, ws.incumbent.degenerate.data());
         ws.incumbent_objective = wobj[w];
         ws.samples_processed = R;
-        ws.t_w = (double)R;
+        ws.t_w = o.last_timestamp;  // the clock read after the worker's last step (engine.hpp:250)
         for (std::int64_t t = 0; t < tlen[w]; ++t)
             ws.update_trace.push_back({traces[(w * R + (std::size_t)t) * 2], traces[(w * R + (std::size_t)t) * 2 + 1]});
     }

@@ -23,6 +23,7 @@ EXPORTS = (
     "hpcg_engine_distance_evals", "hpcg_engine_finish", "hpcg_engine_destroy", "hpcg_engine_export_best",
     "hpcg_run", "hpcg_gen_mixture", "hpcg_ctx_enable_timing", "hpcg_ctx_kernel_times", "hpcg_probe_fma_peak",
     "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
+    "hpcg_engine_publications",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -88,7 +89,8 @@ class RunOut(C.Structure):
     _fields_ = [("full_objective", C.c_double), ("has_full_objective", C.c_int32), ("best_worker", C.c_int32),
                 ("best_sample_objective", C.c_double), ("clustering_time", C.c_double),
                 ("clustering_time_first_finisher", C.c_double), ("wall_seconds", C.c_double),
-                ("total_samples", C.c_uint64), ("distance_evals", C.c_int64), ("n_publications", C.c_int64)]
+                ("total_samples", C.c_uint64), ("distance_evals", C.c_int64), ("n_publications", C.c_int64),
+                ("last_timestamp", C.c_double)]
 
 
 def _load():
@@ -139,6 +141,7 @@ def _load():
         "hpcg_engine_import_best": (C.c_int, [P, D, I64, P, P]),
         "hpcg_engine_set_trace": (C.c_int, [P, P, I32]),
         "hpcg_engine_worker_incumbents": (C.c_int, [P, P, P, P]),
+        "hpcg_engine_publications": (C.c_int, [P, P, I64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

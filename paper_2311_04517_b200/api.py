@@ -643,15 +643,22 @@ class Engine:
         flags = np.empty(k, dtype=np.uint8)
         labels = np.empty(m, dtype=np.int32) if self.cfg.compute_assignment else None
         rounds = max(self.round_index, self.cfg.max_samples)
-        pub_cap = max(64, rounds * min(W, 64))
-        pubs = np.zeros((pub_cap, 4))
         wobj = np.empty(W)
         tcap = max(1, rounds)
         traces = np.zeros((W, tcap, 2))
         tlen = np.zeros(W, dtype=np.int64)
-        check(lib.hpcg_engine_finish(self.h, C.byref(out), ptr(cent), ptr(flags), ptr(labels), ptr(pubs), pub_cap,
+        check(lib.hpcg_engine_finish(self.h, C.byref(out), ptr(cent), ptr(flags), ptr(labels), None, 0,
                                      ptr(wobj), ptr(traces), tcap, ptr(tlen)))
+        pubs = self.publications()
         return _result(out, cent, flags, labels, pubs, wobj, traces, tlen)
+
+    def publications(self) -> np.ndarray:
+        """SharedBest::publication_log (engine.hpp:149-152): rows (version, worker, objective, timestamp)."""
+        n = C.c_int64()
+        check(lib.hpcg_engine_publications(self.h, None, 0, C.byref(n)))
+        pubs = np.zeros((max(1, n.value), 4))
+        check(lib.hpcg_engine_publications(self.h, ptr(pubs), n.value, None))
+        return pubs[: n.value]
 
     def close(self):
         if getattr(self, "h", None):
@@ -699,7 +706,7 @@ def run(X, cfg: EngineConfig, ctx: Context | None = None) -> ClusteringResult:
     cent = np.empty((cfg.k, n))
     flags = np.empty(cfg.k, dtype=np.uint8)
     labels = np.empty(m, dtype=np.int32) if cfg.compute_assignment else None
-    pub_cap = max(64, cfg.max_samples * min(W, 64))
+    pub_cap = (cfg.max_samples + 1) * W  # at most W publications per round (+ the hybrid carry-over)
     pubs = np.zeros((pub_cap, 4))
     wobj = np.empty(W)
     tcap = max(1, cfg.max_samples)

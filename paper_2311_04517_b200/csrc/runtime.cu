@@ -62,6 +62,23 @@ struct DevBuf {
         if (e == cudaSuccess) bytes = b;
         return e;
     }
+    // grow to b bytes keeping the first `keep` bytes (stream-ordered copy; the old block is freed
+    // after the copy completes because cudaFree synchronises the device)
+    cudaError_t grow(size_t b, size_t keep, cudaStream_t st) {
+        if (b <= bytes) return cudaSuccess;
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, b);
+        if (e != cudaSuccess) return e;
+        if (p && keep) e = cudaMemcpyAsync(q, p, std::min(keep, bytes), cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) {
+            cudaFree(q);
+            return e;
+        }
+        if (p) cudaFree(p);
+        p = q;
+        bytes = b;
+        return cudaSuccess;
+    }
     template <typename T>
     T* as() const {
         return static_cast<T*>(p);
@@ -291,6 +308,7 @@ struct RoundEndParams {
     int64_t round;  // 0-based round just finished
     int publish;    // round was cooperative (publish accepted) ...
     int carry;      // ... or hybrid carry-over round (publish finite incumbents)
+    int log;        // record the round (accept/objective logs, n_d, errors); 0 = publication only
     int worker_base;
     double ts;      // publication timestamp: round + 1 (lockstep) or seconds (wall clock)
     const uint8_t* accepted;
@@ -323,14 +341,16 @@ __global__ void round_end_kernel(const RoundEndParams p) {
     uint8_t* rs_acc = reinterpret_cast<uint8_t*>(rs_obj + p.W);
     unsigned long long nd = 0;
     for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
-        const uint8_t a = p.accepted[w];
+        const uint8_t a = p.log ? p.accepted[w] : (uint8_t)0;
         const double f = p.inc_obj[w];
         rs_acc[w] = a;
         rs_obj[w] = f;
-        p.log_acc[p.round * p.W + w] = a;
-        p.log_obj[p.round * p.W + w] = f;
-        nd += (unsigned long long)p.nd[w];
-        if (p.err[w] != 0 && p.err_first[w] == 0) p.err_first[w] = p.err[w];
+        if (p.log) {
+            p.log_acc[p.round * p.W + w] = a;
+            p.log_obj[p.round * p.W + w] = f;
+            nd += (unsigned long long)p.nd[w];
+            if (p.err[w] != 0 && p.err_first[w] == 0) p.err_first[w] = p.err[w];
+        }
     }
     s_nd[threadIdx.x] = nd;
     __syncthreads();
@@ -340,7 +360,7 @@ __global__ void round_end_kernel(const RoundEndParams p) {
         unsigned long long t = 0;
         for (int i = lane; i < (int)blockDim.x; i += 32) t += s_nd[i];
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) *p.nd_total += t;
+        if (lane == 0 && p.log) *p.nd_total += t;
         // publication in worker-id order with strict < (engine.hpp:391-402): worker w publishes iff
         // its candidate objective is below min(shared best, every earlier candidate) -- an
         // exclusive prefix-min, 32 workers per step
@@ -1112,7 +1132,10 @@ struct hpcg_engine {
     DevBuf sh_ver, sh_obj, sh_worker, sh_c, sh_f;
     DevBuf log_acc, log_obj, nd_total, pub_log, pub_count;
     DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks, fin;
-    int64_t pub_cap = 0;
+    int64_t pub_cap = 0;   // publication-log entries allocated (grown on demand)
+    int64_t pub_ub = 0;    // upper bound of the entries written so far (<= W per publishing launch)
+    int64_t log_rounds = 0;  // rounds the per-round accept/objective logs can hold (grown on demand)
+    bool entered_coop = false;  // wall clock, hybrid: the phase-1 incumbents were carried over
     // reference-RNG replay state
     std::vector<Mt64> streams;
     std::vector<int64_t> h_idx, h_fr;
@@ -1129,11 +1152,89 @@ bool phase_cooperative(int strategy, double t1, double progress) {  // engine.hp
     return false;
 }
 
-int engine_round(hpcg_engine* e) {
+// Room for one more round in the logs and for `extra` more publications (doubling growth; the
+// device copies are stream-ordered, so nothing is read back).
+int engine_reserve(hpcg_engine* e, int64_t extra_pubs) {
+    hpcg_ctx* ctx = e->ctx;
+    const int64_t W = e->W;
+    if (e->round >= e->log_rounds) {
+        const int64_t nr = std::max<int64_t>(2 * e->log_rounds, e->round + 1);
+        CU(e->log_acc.grow((size_t)(nr * W), (size_t)(e->log_rounds * W), ctx->stream));
+        CU(e->log_obj.grow((size_t)(nr * W * 8), (size_t)(e->log_rounds * W * 8), ctx->stream));
+        e->log_rounds = nr;
+    }
+    if (e->pub_ub + extra_pubs > e->pub_cap) {
+        const int64_t nc = std::max<int64_t>(2 * e->pub_cap, e->pub_ub + extra_pubs);
+        CU(e->pub_log.grow((size_t)(nc * 4 * 8), (size_t)(e->pub_cap * 4 * 8), ctx->stream));
+        e->pub_cap = nc;
+    }
+    return HPCG_OK;
+}
+
+RoundEndParams round_end_params(hpcg_engine* e) {
+    RoundEndParams q = {};
+    q.W = (int)e->W;
+    q.k = (int)e->k;
+    q.n = (int)e->n;
+    q.round = e->round;
+    q.log = 1;
+    q.worker_base = e->cfg.worker_base;
+    q.accepted = e->acc.as<uint8_t>();
+    q.inc_obj = e->inc_obj.as<double>();
+    q.inc_c = e->inc_c.as<double>();
+    q.inc_f = e->inc_f.as<uint8_t>();
+    q.nd = e->nd.as<int64_t>();
+    q.err = e->err.as<int32_t>();
+    q.log_acc = e->log_acc.as<uint8_t>();
+    q.log_obj = e->log_obj.as<double>();
+    q.err_first = e->err_first.as<int32_t>();
+    q.nd_total = e->nd_total.as<unsigned long long>();
+    q.sh_version = e->sh_ver.as<int64_t>();
+    q.sh_obj = e->sh_obj.as<double>();
+    q.sh_worker = e->sh_worker.as<int32_t>();
+    q.sh_c = e->sh_c.as<double>();
+    q.sh_f = e->sh_f.as<uint8_t>();
+    q.pub_log = e->pub_log.as<double>();
+    q.pub_count = e->pub_count.as<int64_t>();
+    q.pub_cap = e->pub_cap;
+    return q;
+}
+
+int launch_round_end(hpcg_engine* e, const RoundEndParams& q) {
+    const size_t rs_bytes = (size_t)e->W * 9;
+    if (rs_bytes > 48 * 1024) {
+        const cudaError_t ae = cudaFuncSetAttribute(round_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)rs_bytes);
+        if (ae != cudaSuccess) return fail(HPCG_EUNSUPPORTED, "round end: too many workers for one engine");
+    }
+    round_end_kernel<<<1, 256, rs_bytes, e->ctx->stream>>>(q);
+    CU(cudaGetLastError());
+    e->ctx->launches += 1;
+    return HPCG_OK;
+}
+
+// One round of the schedule. `now`: seconds since the run start read ONCE by the caller (wall
+// clock: the stop test, the phase test and the hybrid carry-over all use this one reading, as a
+// reference worker does at the top of its loop, engine.hpp:353-364); ignored in lockstep.
+int engine_round(hpcg_engine* e, double now) {
     hpcg_ctx* ctx = e->ctx;
     const int64_t r = e->round, W = e->W, k = e->k, n = e->n, s = e->s, kn = k * n;
     // phase test on the schedule's clock: samples processed (lockstep) or seconds (wall clock)
-    const bool coop = phase_cooperative(e->cfg.strategy, e->cfg.phase_t1, e->wall ? e->elapsed() : (double)r);
+    const bool coop = phase_cooperative(e->cfg.strategy, e->cfg.phase_t1, e->wall ? now : (double)r);
+    const bool hybrid = e->cfg.strategy == HPCG_HYBRID;
+    if (int rc = engine_reserve(e, 2 * W)) return rc;
+    if (e->wall && hybrid && coop && !e->entered_coop) {
+        // engine.hpp:359-364: entering the cooperative phase publishes each worker's finite
+        // incumbent (worker-id order, strict <) before the step draws its init from the snapshot
+        e->entered_coop = true;
+        RoundEndParams q = round_end_params(e);
+        q.log = 0;
+        q.publish = 0;
+        q.carry = 1;
+        q.ts = now;
+        if (int rc = launch_round_end(e, q)) return rc;
+        e->pub_ub += W;
+    }
     const bool reference = e->cfg.rng_mode == HPCG_RNG_REFERENCE;
     const int64_t ncand = e->cfg.candidates;
     std::vector<int64_t> pending_loop, no_valid;
@@ -1229,52 +1330,20 @@ int engine_round(hpcg_engine* e) {
     if (ce != cudaSuccess) return fail(HPCG_ECUDA, std::string("worker step launch: ") + cudaGetErrorString(ce) + " " + why);
     ctx->launches += 1;
 
-    RoundEndParams q = {};
-    q.W = (int)W;
-    q.k = (int)k;
-    q.n = (int)n;
-    q.round = r;
+    RoundEndParams q = round_end_params(e);
     q.publish = coop ? 1 : 0;  // round_was_coop (engine.hpp:393)
-    const bool hybrid = e->cfg.strategy == HPCG_HYBRID;
-    if (e->wall) {  // the round's samples are done at t_end; the hybrid switch is decided on it
+    if (e->wall) {  // the round's samples are done at t_end (trace / publication timestamp)
         CU(cudaStreamSynchronize(ctx->stream));
         const double t_end = e->elapsed();
         e->t_end.push_back(t_end);
         q.ts = t_end;
-        // engine.hpp:359-364: entering the cooperative phase publishes each worker's incumbent
-        q.carry = (hybrid && !coop && t_end >= e->cfg.phase_t1) ? 1 : 0;
+        q.carry = 0;  // wall clock: carried over at the start of the first cooperative round
     } else {
         q.ts = (double)(r + 1);
         q.carry = (hybrid && (r + 1) == (int64_t)(size_t)e->cfg.phase_t1) ? 1 : 0;  // engine.hpp:386,396
     }
-    q.worker_base = e->cfg.worker_base;
-    q.accepted = e->acc.as<uint8_t>();
-    q.inc_obj = e->inc_obj.as<double>();
-    q.inc_c = e->inc_c.as<double>();
-    q.inc_f = e->inc_f.as<uint8_t>();
-    q.nd = e->nd.as<int64_t>();
-    q.err = e->err.as<int32_t>();
-    q.log_acc = e->log_acc.as<uint8_t>();
-    q.log_obj = e->log_obj.as<double>();
-    q.err_first = e->err_first.as<int32_t>();
-    q.nd_total = e->nd_total.as<unsigned long long>();
-    q.sh_version = e->sh_ver.as<int64_t>();
-    q.sh_obj = e->sh_obj.as<double>();
-    q.sh_worker = e->sh_worker.as<int32_t>();
-    q.sh_c = e->sh_c.as<double>();
-    q.sh_f = e->sh_f.as<uint8_t>();
-    q.pub_log = e->pub_log.as<double>();
-    q.pub_count = e->pub_count.as<int64_t>();
-    q.pub_cap = e->pub_cap;
-    const size_t rs_bytes = (size_t)W * 9;
-    if (rs_bytes > 48 * 1024) {
-        const cudaError_t ae = cudaFuncSetAttribute(round_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    (int)rs_bytes);
-        if (ae != cudaSuccess) return fail(HPCG_EUNSUPPORTED, "round end: too many workers for one engine");
-    }
-    round_end_kernel<<<1, 256, rs_bytes, ctx->stream>>>(q);
-    CU(cudaGetLastError());
-    ctx->launches += 1;
+    if (q.publish || q.carry) e->pub_ub += W;
+    if (int rc = launch_round_end(e, q)) return rc;
 
     if (reference) {  // rewind streams of workers whose seeding stopped early (seeding.hpp:87)
         std::vector<int32_t> fl((size_t)W);
@@ -1334,9 +1403,9 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     e->n = ds->n;
     e->s = cfg.sample_size;
     e->wall = wall;
-    // rounds: max_samples, or in wall-clock mode that cap (else enough for ~64 MB of round logs)
-    e->R = wall && cfg.max_samples < 1 ? std::max<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(cfg.n_workers, 1))
-                                        : cfg.max_samples;
+    // rounds: max_samples, or in wall-clock mode that cap (none: until the time limit); the
+    // per-round logs and the publication log grow on demand (engine_reserve)
+    e->R = wall && cfg.max_samples < 1 ? INT64_MAX : cfg.max_samples;
     e->key = splitmix64(cfg.master_seed ^ 0x48504331ULL);
     e->t0 = std::chrono::steady_clock::now();
     const int64_t W = e->W, k = e->k, kn = k * e->n;
@@ -1365,10 +1434,11 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     ALLOC(sh_worker, 4);
     ALLOC(sh_c, kn * 8);
     ALLOC(sh_f, k);
-    ALLOC(log_acc, e->R * W);
-    ALLOC(log_obj, e->R * W * 8);
+    e->log_rounds = std::min<int64_t>(e->R, 64);
+    ALLOC(log_acc, e->log_rounds * W);
+    ALLOC(log_obj, e->log_rounds * W * 8);
     ALLOC(nd_total, 8);
-    e->pub_cap = std::max<int64_t>(64, e->R * std::min<int64_t>(W, 64));
+    e->pub_cap = std::max<int64_t>(256, 4 * W);
     ALLOC(pub_log, e->pub_cap * 4 * 8);
     ALLOC(pub_count, 8);
     const bool reference = cfg.rng_mode == HPCG_RNG_REFERENCE;
@@ -1400,7 +1470,7 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     chk(cudaMemsetAsync(e->err_first.p, 0, (size_t)(W * 4), st));
     chk(cudaMemsetAsync(e->nd_total.p, 0, 8, st));
     chk(cudaMemsetAsync(e->pub_count.p, 0, 8, st));
-    chk(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->R * W), st));
+    chk(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->log_rounds * W), st));
     chk(cudaGetLastError());
     ctx->launches += 2;
     if (ce != cudaSuccess) return bad(ce);
@@ -1435,7 +1505,9 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     CU(cudaMemsetAsync(e->err_first.p, 0, (size_t)(W * 4), st));
     CU(cudaMemsetAsync(e->nd_total.p, 0, 8, st));
     CU(cudaMemsetAsync(e->pub_count.p, 0, 8, st));
-    CU(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->R * W), st));
+    CU(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->log_rounds * W), st));
+    e->pub_ub = 0;
+    e->entered_coop = false;
     return HPCG_OK;
 }
 
@@ -1463,7 +1535,7 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
     cudaSetDevice(e->ctx->device);
     for (int64_t i = 0; i < n_rounds; ++i) {
         if (e->round >= e->R) return fail(HPCG_EINVAL, "engine: max_samples rounds already run");
-        if (int rc = engine_round(e)) return rc;
+        if (int rc = engine_round(e, e->wall ? e->elapsed() : 0.0)) return rc;
     }
     return HPCG_OK;
 }
@@ -1472,9 +1544,11 @@ int hpcg_engine_run(hpcg_engine* e) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     cudaSetDevice(e->ctx->device);
     while (e->round < e->R) {
-        // run_wall_clock (engine.hpp:355-357): stop once the time limit has passed
-        if (e->wall && e->elapsed() >= e->cfg.time_limit) break;
-        if (int rc = engine_round(e)) return rc;
+        // run_wall_clock (engine.hpp:353-357): one clock reading per round decides the stop,
+        // the phase and the carry-over
+        const double now = e->wall ? e->elapsed() : 0.0;
+        if (e->wall && now >= e->cfg.time_limit) break;
+        if (int rc = engine_round(e, now)) return rc;
     }
     return HPCG_OK;
 }
@@ -1651,6 +1725,7 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
         o.has_full_objective = 1;
         final_nd = e->ds->m * (int64_t)remap.size();
     }
+    o.last_timestamp = R > 0 ? ts_of(R - 1) : 0.0;  // every worker's t_w (engine.hpp:250)
     o.total_samples = (uint64_t)(W * R);
     o.distance_evals = (int64_t)ndt + final_nd;
     o.n_publications = npub;
@@ -1662,6 +1737,22 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     if (worker_obj) std::memcpy(worker_obj, h_obj, (size_t)W * 8);
     o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
     if (out) *out = o;
+    return HPCG_OK;
+}
+
+int hpcg_engine_publications(hpcg_engine* e, double* publications, int64_t cap, int64_t* n_out) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    int64_t npub = 0;
+    CU(d2h(&npub, e->pub_count.as<int64_t>(), 1, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const int64_t cnt = std::min(npub, std::min(cap, e->pub_cap));
+    if (publications && cnt > 0) {
+        CU(d2h(publications, e->pub_log.as<double>(), (size_t)(cnt * 4), ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    if (n_out) *n_out = npub;
     return HPCG_OK;
 }
 

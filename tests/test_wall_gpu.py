@@ -82,6 +82,35 @@ def test_wall_hybrid_switches_after_t1_seconds():
     assert np.all(np.diff(pubs[:, 0]) > 0) and np.all(np.diff(pubs[:, 2]) < 0)  # versions up, objective down
 
 
+def test_wall_hybrid_carry_over_publishes_phase1_incumbents():
+    """engine.hpp:353-364: one clock reading at the top of the first cooperative round both flips the
+    phase and publishes every finite phase-1 incumbent (worker-id order, strict <) before the round
+    draws its inits; so the carry-over records share that reading as timestamp and the last of them
+    is the minimum over the workers' phase-1 incumbents."""
+    X = mixture(20000, 4, 6, seed=7)
+    cfg = hp.EngineConfig(k=6, sample_size=2000, n_workers=6, strategy="hybrid", phase_t1=0.12, phase_t2=0.18,
+                          time_limit=0.3, rng="philox")
+    r = hp.run(X, cfg)
+    pubs = r.publications
+    assert len(pubs) >= 1
+    t_c = pubs[0, 3]
+    carry = pubs[pubs[:, 3] == t_c]
+    phase1 = [tr[tr[:, 0] < t_c][-1, 1] for tr in r.traces if len(tr) and np.any(tr[:, 0] < t_c)]
+    assert len(phase1) == 6  # every worker finished a competitive round before the switch
+    assert carry[-1, 2] == min(phase1)
+    # the carried records are the strict prefix minima in worker-id order
+    run_min, expect = np.inf, []
+    for w, tr in enumerate(r.traces):
+        f = tr[tr[:, 0] < t_c][-1, 1]
+        if f < run_min:
+            run_min = f
+            expect.append((w, f))
+    assert [(int(a), b) for a, b in carry[:, [1, 2]]] == expect
+    # versions 1..len(carry) and later publications strictly improve on the carried best
+    assert np.array_equal(carry[:, 0], np.arange(1, len(carry) + 1))
+    assert np.all(pubs[len(carry):, 2] < carry[-1, 2])
+
+
 def test_wall_schedule_validation():
     X = mixture(2000, 2, 3, seed=1)
     with pytest.raises(hp.InvalidArgument, match="time limit must be positive"):
