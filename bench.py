@@ -20,8 +20,9 @@ best (objective, global worker id, centroids) over NCCL and install the global w
 (cooperative exchange).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, built from the
-reference headers) runs hpclust::run on the same data (fp64), n_workers = host threads,
-max_samples=4, cooperative, on all host cores; rank 0 only.
+reference headers) runs hpclust::run on the same rows (fp64 copy; the data generator is numpy
+so this arm never loads libhpcg), n_workers = 256 (its thread-per-worker model), max_samples=4,
+cooperative, on all host cores; rank 0 only.
 """
 from __future__ import annotations
 
@@ -52,10 +53,16 @@ def mixture_params(seed=2311):
     return means, sig, w / w.sum()
 
 
-def make_data(rank: int):
-    import paper_2311_04517_b200 as hp
+def make_data(rank: int, m: int = M):
+    """Config-2 rows of rank `rank` (numpy only, so the reference arm never loads libhpcg): component
+    drawn from the Zipf(1.1) weights, then mean + sigma_c * N(0, I), fp32. Both arms call this."""
     means, sig, w = mixture_params()
-    return hp.gen_mixture(M, N, means, sig, w, seed=1000 + rank, dtype=np.float32)
+    g = np.random.default_rng(1000 + rank)
+    comp = g.choice(len(w), size=m, p=w)
+    X = g.standard_normal((m, N), dtype=np.float32)
+    X *= sig.astype(np.float32)[comp, None]
+    X += means.astype(np.float32)[comp]
+    return X
 
 
 def host_cores() -> int:
@@ -171,7 +178,8 @@ def finish_global(eng, ds, ctx, device):
         Cv = torch.from_numpy(np.ascontiguousarray(C_[valid])).to(device)
         hp._lib.check(hp._lib.lib.hpcg_assign_dev(ctx.h, ds.h, Cv.data_ptr(), kv, None, cost.data_ptr()))
     dist.all_reduce(cost)
-    return SimpleNamespace(distance_evals=eng.distance_evals() + ds.m * kv, full_objective=float(cost.item()))
+    return SimpleNamespace(distance_evals=eng.distance_evals() + ds.m * kv, full_objective=float(cost.item()),
+                           degenerate=f, centroids=C_)
 
 
 def merge_records(recs):
@@ -182,6 +190,31 @@ def merge_records(recs):
         if o < bo or (o == bo and bw is not None and w < bw and o != float("inf")):
             best, bo, bw = i, o, w
     return best
+
+
+def gather_rate(hp, ctx, ds, stream, key, reps=8):
+    """The sample gather alone: hpcg_sample_gather_dev (the worker step's PRP indices + 16-B row
+    chunks) materialising W x s x n fp32 rows; GB/s of rows read (algorithmic) vs HBM."""
+    import torch
+    Sd = torch.empty(W_PER_GPU * S * N, dtype=torch.float32, device=stream.device)
+    ms = []
+    for i in range(3 + reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hp._lib.check(hp._lib.lib.hpcg_sample_gather_dev(ctx.h, ds.h, W_PER_GPU, S, key, 100 + i, 0, Sd.data_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            ms.append(e0.elapsed_time(e1))
+    t = float(np.median(ms))
+    rd = W_PER_GPU * S * N * 4
+    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    del Sd
+    return {"kernel": "sample_gather_kernel<16>", "ms": t, "bytes_read": rd, "gbs_read": rd / (t * 1e-3) / 1e9,
+            "gbs_read_plus_write": 2 * rd / (t * 1e-3) / 1e9, "peak": hbm,
+            "frac": 2 * rd / (t * 1e-3) / 1e9 / hbm,
+            "note": "random 64-B rows (W=256 x s=20000 per round); frac counts read + write against the copy peak"}
 
 
 def run_gpu(args, world, rank, local):
@@ -245,6 +278,7 @@ def run_gpu(args, world, rank, local):
     launches0 = ctx.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nd_total = 0
+    nd_rounds = 0  # the worker-step launches' own evaluations (the final pass's m x k_valid excluded)
     objs = []
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -254,6 +288,7 @@ def run_gpu(args, world, rank, local):
         for i in range(args.steps):
             res = step(20_000 + i)
             nd_total += res.distance_evals
+            nd_rounds += res.distance_evals - M * int((res.degenerate == 0).sum())
             objs.append(res.full_objective)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -292,14 +327,23 @@ def run_gpu(args, world, rank, local):
 
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    # dominant kernel: the worker step (Lloyd screen = n FMA per evaluation)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
+    # dominant kernel: the worker step. Algorithmic work = its own n_d (Lloyd + seeding evaluations,
+    # core.hpp:205 / seeding.hpp:38; the final f(C,X) pass's m x k_valid is NOT charged to it) x n FMA.
     step_cnt, step_ms = kt["step"]
-    lloyd_flops_per_launch = nd_total / max(1, step_cnt) * N * 2  # per-rank launches
-    achieved_tflops = lloyd_flops_per_launch / (step_ms / max(1, step_cnt) * 1e-3) / 1e12
-    # DRAM bytes per launch from the committed ncu --set full captures (one launch each)
+    step_flops_per_launch = nd_rounds / max(1, step_cnt) * N * 2
+    mean_launch_ms = step_ms / max(1, step_cnt)
+    achieved_tflops = step_flops_per_launch / (mean_launch_ms * 1e-3) / 1e12
+    # the sample gather on its own (the worker step's gather phase as a dense kernel): GB/s vs HBM
+    gat = gather_rate(hp, ctx, ds, stream, eng.philox_key)
+    # what bounds a worker-step launch: its gather bytes at HBM peak plus its FMA work at the FMA peak
+    gather_bytes_launch = W_PER_GPU * S * N * 4
+    t_gather_ms = gather_bytes_launch / (hbm_peak * 1e9) * 1e3
+    t_fma_ms = step_flops_per_launch / 2 / (fma_tfma * 1e12) * 1e3
+    # DRAM bytes per launch from the committed ncu --set full captures of the current kernels
     trf = {}
     try:
-        trf = json.load(open(Path(__file__).resolve().parent / "profiles" / "r1_traffic.json"))
+        trf = json.load(open(ROOT / "profiles" / "traffic.json"))
     except (OSError, ValueError):
         pass
     step_traffic = None
@@ -322,16 +366,22 @@ def run_gpu(args, world, rank, local):
         "objective_pass": {"gbs": obj_gbs, "ms": float(np.median(obj_ms)), "bytes": obj_bytes,
                            "roofline": {"bound": "hbm", "achieved": obj_gbs, "peak": hbm_peak, "unit": "GB/s",
                                         "frac": obj_gbs / hbm_peak, "traffic": obj_traffic,
-                                        "traffic_unit": "bytes/launch (ncu, profiles/r1_traffic.json)",
-                                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
+                                        "traffic_unit": "bytes/launch (ncu, profiles/traffic.json)",
+                                        "peak_source": hbm_src}},
         "roofline": {"bound": "fma", "kernel": "worker_step_kernel", "achieved": achieved_tflops,
                      "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
                      "traffic": step_traffic,
                      "traffic_unit": "DRAM bytes/launch (ncu; mean of 1 seeding + 3 steady rounds)",
-                     "algorithmic": "n_d (Lloyd+seeding evaluations) x n FMA x 2 flop per launch / mean launch time",
+                     "algorithmic": "worker-step n_d (Lloyd + K-means++ evaluations of the rounds; the final "
+                                    "f(C,X) pass excluded) x n FMA x 2 flop per launch / mean launch time",
+                     "evals_per_launch": nd_rounds / max(1, step_cnt),
                      "peak_source": "FFMA2 loop measured in-run on this GPU (fp32 FMA; MEASURED_PEAKS.json has "
                                     "only hbm and bf16)",
-                     "launches": step_cnt, "mean_launch_ms": step_ms / max(1, step_cnt)},
+                     "launches": step_cnt, "mean_launch_ms": mean_launch_ms,
+                     "launch_bound_ms": {"gather_at_hbm": t_gather_ms, "fma_at_peak": t_fma_ms,
+                                         "serial": t_gather_ms + t_fma_ms, "overlapped": max(t_gather_ms, t_fma_ms)},
+                     "frac_of_combined_bound": (t_gather_ms + t_fma_ms) / mean_launch_ms},
+        "gather": gat,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "mean_full_objective": float(np.mean(objs)),
@@ -406,6 +456,124 @@ def e2e_run_multi(X, args, world, rank, ctx, device):
             "path": "DeviceDataset upload + Engine rounds with the NCCL exchange + finish, per rank (max over ranks)"}
 
 
+# ----------------------------------------------------------------------------- other configs
+# BASELINE.json configs 3, 4 and a config-5 shard on this GPU (extra keys of the bench line; the
+# headline is config 2). Seeded synthetic data with each config's shapes and distributions.
+CFG_SETUP = {  # k, s, workers, rounds (max_samples), strategy, t1, t2, objective after every round
+    3: (25, 50_000, 64, 20, "hybrid", 10.0, 10.0, True),
+    4: (25, 100_000, 16, 10, "collective", 0.0, 0.0, False),
+    5: (15, 200_000, 256, 4, "cooperative", 0.0, 0.0, False),
+}
+CFG_NOTE = {
+    3: "1e8 x 3 fp64, 25 Gaussians U[0,255]^3 sigma 8 + 1% uniform noise; 64 workers, 20 rounds, hybrid "
+       "t1=t2=10, f(C,X) of the shared best after every round (BASELINE.json) timed in the run",
+    4: "5e6 x 128 fp32, 25 Gaussians N(0,4I) sigma 1; 16 workers, 10 rounds, collective (= cooperative); "
+       "grid-wide path with the tcgen05 tf32 screen",
+    5: "one GPU's shard of the 8-GPU job: 2.5e8 x 8 fp32 (of 2e9), 15 Gaussians U[-20,20]^8 sigma U[0.5,3], "
+       "Dirichlet(1) weights; 256 of the 2,048 workers, 4 rounds, cooperative",
+}
+
+
+def cfg_data(hp, c):
+    rs = np.random.default_rng(2311 + c)
+    if c == 3:
+        return hp.gen_mixture(100_000_000, 3, rs.uniform(0, 255, (25, 3)), np.full(25, 8.0), np.ones(25) / 25,
+                              noise_frac=0.01, noise_box=(0.0, 255.0), seed=3, dtype=np.float64)
+    if c == 4:
+        return hp.gen_mixture(5_000_000, 128, rs.normal(0.0, 2.0, (25, 128)), np.ones(25), np.ones(25) / 25,
+                              seed=4, dtype=np.float32)
+    return hp.gen_mixture(250_000_000, 8, rs.uniform(-20, 20, (15, 8)), rs.uniform(0.5, 3.0, 15),
+                          rs.dirichlet(np.ones(15)), seed=5, dtype=np.float32)
+
+
+def config_extra(c, fma_tfma, device=0):
+    """One BASELINE config on this GPU through the engine: whole run on the device-resident X
+    (rounds + select + f(C,X)), per-round times (CUDA events), worker-step FMA fraction, f(C,X) GB/s
+    against HBM, clocks sampled during the timed region."""
+    import torch
+    import paper_2311_04517_b200 as hp
+    k, s, W, R, strat, t1, t2, obj_each = CFG_SETUP[c]
+    X = cfg_data(hp, c)
+    m, n = X.shape
+    st = torch.cuda.current_stream(device)
+    ctx = hp.Context(device)
+    ctx.set_stream(st.cuda_stream)
+    Xd = torch.from_numpy(X).to(f"cuda:{device}")
+    del X
+    ds = hp.DeviceDataset.from_torch(Xd, ctx)
+    eng = hp.Engine(ds, hp.EngineConfig(k=k, sample_size=s, n_workers=W, max_samples=R, strategy=strat,
+                                        phase_t1=t1, phase_t2=t2, rng="philox"))
+    cost = torch.zeros(1, dtype=torch.float64, device=Xd.device)
+
+    def one_run(seed, times=None):
+        eng.reset(seed)
+        for r in range(R):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            eng.rounds(1)
+            if obj_each:
+                b = eng.export_best()
+                if np.isfinite(b[0]):
+                    C_ = torch.from_numpy(b[2][b[3] == 0]).to(Xd.device)
+                    hp._lib.check(hp._lib.lib.hpcg_assign_dev(ctx.h, ds.h, C_.data_ptr(), C_.shape[0], None,
+                                                              cost.data_ptr()))
+            e1.record(st)
+            if times is not None:
+                times.append((e0, e1))
+        return eng.finish()
+
+    one_run(1)
+    one_run(2)
+    torch.cuda.synchronize()
+    ctx.enable_timing(True)
+    ev = []
+    with ClockSampler(device) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        res = one_run(3, ev)
+        e1.record(st)
+        torch.cuda.synchronize()
+    kt = ctx.kernel_times()
+    ctx.enable_timing(False)
+    ms = e0.elapsed_time(e1)
+    rounds_ms = [a.elapsed_time(b) for a, b in ev]
+    kv = int((res.degenerate == 0).sum())
+    nd_rounds = res.distance_evals - m * kv
+    step_cnt, step_ms = kt["step"]
+    step_tflops = nd_rounds * n * 2 / (step_ms * 1e-3) / 1e12 if step_ms > 0 else None
+    C_ = torch.from_numpy(res.centroids[res.degenerate == 0]).to(Xd.device)
+    ts = []
+    for i in range(8):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        hp._lib.check(hp._lib.lib.hpcg_assign_dev(ctx.h, ds.h, C_.data_ptr(), C_.shape[0], None, cost.data_ptr()))
+        b.record(st)
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(a.elapsed_time(b))
+    obj_ms = float(np.median(ts))
+    nbytes = m * n * Xd.element_size()
+    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    out = {"config": c, "workload": CFG_NOTE[c], "m": m, "n": n, "k": k, "s": s, "workers": W, "rounds": R,
+           "strategy": strat, "dtype": str(Xd.dtype).replace("torch.", ""), "run_ms": ms,
+           "distance_evals": res.distance_evals, "evals_per_s": res.distance_evals / (ms * 1e-3),
+           "round0_ms": rounds_ms[0], "steady_round_ms": float(np.median(rounds_ms[1:])) if R > 1 else None,
+           "worker_step": {"launches": step_cnt, "ms": step_ms, "evals": nd_rounds, "achieved_tflops": step_tflops,
+                           "peak_tflops": 2 * fma_tfma,
+                           "frac": step_tflops / (2 * fma_tfma) if step_tflops else None,
+                           "peak_source": "in-run FFMA2 (fp32 FMA) peak; the screen runs in fp32 for fp64 data too"},
+           "objective_pass": {"ms": obj_ms, "bytes": nbytes, "gbs": nbytes / (obj_ms * 1e-3) / 1e9, "peak": hbm,
+                              "frac": nbytes / (obj_ms * 1e-3) / 1e9 / hbm},
+           "full_objective": res.full_objective, "clocks": clk.summary()}
+    eng.close()
+    ds.close()
+    ctx.close()
+    del Xd, C_, cost
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline(X, budget_s=10.0):
     """The reference's own kmeans (oracle/_ref, stock code path) on config-2 samples, one
     std::thread per worker (its competitive threading model, engine.hpp:313-332), host cores."""
@@ -442,8 +610,8 @@ def run_reference(args, world, rank):
     if R is None:
         return {"impl": "reference", "unavailable": "oracle/_ref/libhpclust_ref.so not built"}
     P = host_cores()
-    X = make_data(0).astype(np.float64)
-    Wr = min(W_PER_GPU, P)
+    X = make_data(0).astype(np.float64)  # the same rows as the GPU arm (numpy; libhpcg never loaded)
+    Wr = W_PER_GPU  # the reference's own thread-per-worker model (engine.hpp:313-332) at the GPU arm's W
     times, nds = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -457,12 +625,16 @@ def run_reference(args, world, rank):
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(times) * 1e3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE config 2 data (fp64 copy), hpclust::run cooperative, {Wr} workers "
-                                   f"(host threads) x 4 lockstep rounds + full-data objective",
-                       "m": M, "n": N, "k": K, "s": S, "workers": Wr, "rounds": ROUNDS},
+            "config": {"workload": "BASELINE config 2: X 1e7x16 Gaussian mixture (10 comps, Zipf(1.1)), k=10, "
+                                   "s=20000, 256 workers/GPU, cooperative, 4 lockstep rounds (1024 samples) + "
+                                   "full-data f(C,X)", "m_per_gpu": M, "n": N, "k": K, "s": S,
+                       "workers_per_gpu": Wr, "rounds": ROUNDS,
+                       "reference_path": "hpclust::run (engine.hpp:444-499), oracle/_ref built from the unmodified "
+                                         "headers; fp64 copy of the same rows; one std::thread per worker",
+                       "same_config": True},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "reference",
-                             "sample": f"{args.steps} full reference runs with {Wr} workers (bounded sample of the "
-                                       f"256-worker workload)", "cpu_model": cpu_model()},
+                             "sample": f"{args.steps} full reference runs of the workload ({Wr} workers x {ROUNDS} "
+                                       f"rounds + final objective), each a timed step", "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -474,10 +646,18 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config 3/4/5 extra keys")
+    ap.add_argument("--configs-only", default="", help="e.g. 3,4,5: print one JSON line per config and exit")
     ap.add_argument("--global-sampling", action="store_true",
                     help="N > 1: sample over all ranks' rows (peer-mapped shards) instead of the local shard")
     args = ap.parse_args()
     world, rank, local = dist_setup()
+    if args.configs_only:
+        import paper_2311_04517_b200 as hp
+        fma = hp.Context(local).fma_peak()
+        for c in args.configs_only.split(","):
+            print(json.dumps(config_extra(int(c), fma, local)), flush=True)
+        return
     if args.impl == "reference":
         out = run_reference(args, world, rank)
         if out is not None:
@@ -501,6 +681,16 @@ def main():
                                           "d2h_bytes_per_step": 0, "note": "--no-e2e"}
         if not args.no_cpu and world == 1:
             result["cpu_baseline"] = cpu_baseline(X)
+        if not args.no_configs and world == 1:
+            del eng, X
+            fma = result["roofline"]["peak"] / 2
+            extras = []
+            for c in (3, 4, 5):
+                try:
+                    extras.append(config_extra(c, fma, local))
+                except Exception as ex:  # keep the bench line; say which config failed and why
+                    extras.append({"config": c, "error": f"{type(ex).__name__}: {ex}"[:200]})
+            result["configs"] = extras
         print(json.dumps(result))
     if world > 1:
         import torch.distributed as dist

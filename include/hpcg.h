@@ -154,6 +154,17 @@ int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, 
  * (distinct by construction). The engine uses key = its Philox key (hpcg_engine_cfg seed). */
 int hpcg_sample_indices(hpcg_ctx* ctx, int64_t m, int64_t s, uint64_t key, uint32_t round, uint32_t worker,
                         int64_t* idx_out);
+/* The same samples materialised: S_dev[w][i][:] = row prp_w(i) of ds for w < W (W*s*n elements of
+ * ds's dtype, caller-owned device memory); worker w uses the stream of global worker worker_base + w.
+ * The gather phase of the worker step on its own (bench.py measures its GB/s against HBM). */
+int hpcg_sample_gather_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, int64_t W, int64_t s, uint64_t key,
+                           uint32_t round, int32_t worker_base, void* S_dev);
+/* The K-means++ draws an HPCG_RNG_PHILOX round gives worker `worker` (seeding.hpp:72-99 consumption
+ * order): *first_row = the uniform first-centre row when no_valid != 0 (the sample had no valid
+ * centre), units[t*candidates + c] = the c-th unit draw of the t-th D^2-sampled slot, t < loops.
+ * Host-side; lets a parity test replay a PHILOX run through the reference with the same draws. */
+int hpcg_philox_seed_draws(uint64_t key, uint32_t round, uint32_t worker, int64_t s, int32_t no_valid,
+                           int64_t loops, int64_t candidates, int64_t* first_row, double* units);
 /* Reference-exact draw_sample indices: partial Fisher-Yates of the stream seeded `seed_state`
  * in O(s) (sparse swaps); advances the 312-word mt19937_64 state in place (rng.hpp). */
 int hpcg_reference_draw_indices(uint64_t* mt_state, int32_t* mt_pos, int64_t m, int64_t s, int64_t* idx_out);
@@ -217,12 +228,20 @@ int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d);
 int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels,
                        double* publications, int64_t pub_cap, double* worker_obj, double* traces,
                        int64_t trace_cap, int64_t* trace_len);
+/* Per-worker outcome of the last round run (worker_step, engine.hpp:238-267): the sample objective
+ * and Lloyd iterations / stop reason of this round's kmeans, its n_d, whether keep-the-best
+ * accepted it, and how many degenerate slots K-means++ refilled. Any array may be NULL. */
+int hpcg_engine_round_outcome(hpcg_engine* e, double* objective, int32_t* iterations, int32_t* stop, int64_t* n_d,
+                              uint8_t* accepted, int32_t* filled);
 /* The publication log (SharedBest::publication_log, engine.hpp:149-152): up to cap records of
  * (version, worker, objective, timestamp); *n_out = the number published so far. */
 int hpcg_engine_publications(hpcg_engine* e, double* publications, int64_t cap, int64_t* n_out);
 /* Per-worker incumbents after finish/rounds: C_out[W*k*n], f_out[W*k], obj_out[W] (any may be NULL). */
 int hpcg_engine_worker_incumbents(hpcg_engine* e, double* C_out, uint8_t* f_out, double* obj_out);
 int hpcg_engine_destroy(hpcg_engine* e);
+
+/* The engine's Philox key (HPCG_RNG_PHILOX streams derive from it; see hpcg_sample_indices). */
+uint64_t hpcg_engine_philox_key(const hpcg_engine* e);
 
 /* Multi-rank exchange hooks (cooperative / hybrid across GPUs):
  * export this rank's round candidates, import the merged shared best. */

@@ -23,7 +23,8 @@ EXPORTS = (
     "hpcg_engine_distance_evals", "hpcg_engine_finish", "hpcg_engine_destroy", "hpcg_engine_export_best",
     "hpcg_run", "hpcg_gen_mixture", "hpcg_ctx_enable_timing", "hpcg_ctx_kernel_times", "hpcg_probe_fma_peak",
     "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
-    "hpcg_engine_publications",
+    "hpcg_engine_publications", "hpcg_sample_gather_dev", "hpcg_philox_seed_draws", "hpcg_engine_round_outcome",
+    "hpcg_engine_philox_key",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -142,6 +143,10 @@ def _load():
         "hpcg_engine_set_trace": (C.c_int, [P, P, I32]),
         "hpcg_engine_worker_incumbents": (C.c_int, [P, P, P, P]),
         "hpcg_engine_publications": (C.c_int, [P, P, I64, P]),
+        "hpcg_sample_gather_dev": (C.c_int, [P, P, I64, I64, U64, C.c_uint32, I32, P]),
+        "hpcg_philox_seed_draws": (C.c_int, [U64, C.c_uint32, C.c_uint32, I64, I32, I64, I64, P, P]),
+        "hpcg_engine_round_outcome": (C.c_int, [P, P, P, P, P, P, P]),
+        "hpcg_engine_philox_key": (U64, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -627,6 +627,24 @@ class Engine:
         check(lib.hpcg_engine_distance_evals(self.h, C.byref(v)))
         return v.value
 
+    @property
+    def philox_key(self) -> int:
+        return int(lib.hpcg_engine_philox_key(self.h))
+
+    def round_outcome(self) -> dict:
+        """Per-worker outcome of the last round (worker_step, engine.hpp:238-267)."""
+        W = self.W
+        obj, it, st = np.empty(W), np.empty(W, np.int32), np.empty(W, np.int32)
+        nd, acc, fl = np.empty(W, np.int64), np.empty(W, np.uint8), np.empty(W, np.int32)
+        check(lib.hpcg_engine_round_outcome(self.h, ptr(obj), ptr(it), ptr(st), ptr(nd), ptr(acc), ptr(fl)))
+        return dict(objective=obj, iterations=it, stop=st, n_d=nd, accepted=acc.astype(bool), filled=fl)
+
+    def worker_incumbents(self):
+        k, n, W = self.cfg.k, self.ds.n, self.W
+        Cw, fw, ow = np.empty((W, k, n)), np.empty((W, k), np.uint8), np.empty(W)
+        check(lib.hpcg_engine_worker_incumbents(self.h, ptr(Cw), ptr(fw), ptr(ow)))
+        return Cw, fw, ow
+
     def export_best(self):
         k, n = self.cfg.k, self.ds.n
         obj = C.c_double()
@@ -715,6 +733,15 @@ def run(X, cfg: EngineConfig, ctx: Context | None = None) -> ClusteringResult:
     check(lib.hpcg_run(ctx.h, ptr(X), _dtype_code(X), m, n, C.byref(c), C.byref(out), ptr(cent), ptr(flags),
                        ptr(labels), ptr(pubs), pub_cap, ptr(wobj), ptr(traces), tcap, ptr(tlen)))
     return _result(out, cent, flags, labels, pubs, wobj, traces, tlen)
+
+
+def philox_seed_draws(key: int, round_: int, worker: int, s: int, no_valid: bool, loops: int, candidates: int = 3):
+    """The K-means++ draws an rng="philox" round gives a worker (hpcg_philox_seed_draws)."""
+    fr = C.c_int64()
+    units = np.empty(max(1, loops * candidates))
+    check(lib.hpcg_philox_seed_draws(C.c_uint64(key), round_, worker, s, int(no_valid), loops, candidates,
+                                     C.byref(fr), ptr(units)))
+    return fr.value, units[: loops * candidates]
 
 
 def gen_mixture(m, n, means, sigmas, weights=None, noise_frac=0.0, noise_box=(0.0, 1.0), seed=0,

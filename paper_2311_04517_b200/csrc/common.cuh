@@ -19,11 +19,28 @@ struct u32x4 {
     uint32_t x, y, z, w;
 };
 
-HPCG_DEV u32x4 philox4x32(u32x4 c, uint32_t k0, uint32_t k1) {
+#define HPCG_HD __host__ __device__ __forceinline__
+HPCG_HD uint32_t hd_umulhi(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __umulhi(a, b);
+#else
+    return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+HPCG_HD uint64_t hd_umul64hi(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// Host and device: the host replays a PHILOX round's draws for parity tests (hpcg_philox_seed_draws).
+HPCG_HD u32x4 philox4x32(u32x4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = hd_umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = hd_umulhi(0xCD9E8D57u, c.z);
         c = u32x4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
         k0 += 0x9E3779B9u;
         k1 += 0xBB67AE85u;
@@ -32,17 +49,17 @@ HPCG_DEV u32x4 philox4x32(u32x4 c, uint32_t k0, uint32_t k1) {
 }
 
 // 53-bit unit double in [0,1) from a counter, like rng.hpp:38-40 but Philox-keyed.
-HPCG_DEV double philox_unit(uint64_t key, uint32_t a, uint32_t b, uint32_t c) {
+HPCG_HD double philox_unit(uint64_t key, uint32_t a, uint32_t b, uint32_t c) {
     u32x4 r = philox4x32(u32x4{a, b, c, 0x68706367u}, (uint32_t)key, (uint32_t)(key >> 32));
     const uint64_t v = ((uint64_t)r.x << 32) | r.y;
     return (double)(v >> 11) * 0x1.0p-53;
 }
 
 // Uniform integer in [0, n) (n <= 2^40 in practice): 64x64 high product.
-HPCG_DEV uint64_t philox_index(uint64_t key, uint32_t a, uint32_t b, uint32_t c, uint64_t n) {
+HPCG_HD uint64_t philox_index(uint64_t key, uint32_t a, uint32_t b, uint32_t c, uint64_t n) {
     u32x4 r = philox4x32(u32x4{a, b, c, 0x69647831u}, (uint32_t)key, (uint32_t)(key >> 32));
     const uint64_t v = ((uint64_t)r.x << 32) | r.y;
-    return __umul64hi(v, n);
+    return hd_umul64hi(v, n);
 }
 
 // ------------------------------------------------------ sample-index permutation

@@ -18,6 +18,7 @@
 #include <thread>
 #include <unordered_map>
 #include <vector>
+#include <type_traits>
 
 #include "../../include/hpcg.h"
 #include "launch.h"
@@ -301,6 +302,46 @@ __global__ void gather_kernel(const ShardTable t, int64_t rowb, const int64_t* i
     while (sh + 1 < t.n && g >= t.end[sh]) ++sh;
     if (sh) g -= t.end[sh - 1];
     out[e] = t.ptr[sh][g * rowb + b];
+}
+
+// Dense sample gather S[w][i][:] = X[prp_w(i)][:] for W workers (the worker step's gather phase on
+// its own, for measuring the gather at HBM rate): per warp 32 rows, one PRP index per lane, then
+// the rows' V-byte chunks chunk-major across the warp with the indices shuffled across; all of a
+// lane's loads are issued before its stores.
+template <int V>
+__global__ void __launch_bounds__(256) sample_gather_kernel(const ShardTable t, int64_t m, int64_t rowb, int64_t s,
+                                                            uint64_t key, uint32_t round, int32_t worker_base,
+                                                            uint32_t pa, uint32_t pb, float pinv,
+                                                            unsigned char* __restrict__ S) {
+    using VT = typename std::conditional<V == 16, uint4, typename std::conditional<V == 8, uint2, uint32_t>::type>::type;
+    const int w = blockIdx.y, lane = threadIdx.x & 31;
+    const SamplePRP prp = SamplePRP::make(key, round, (uint32_t)(worker_base + w), (uint64_t)m, pa, pb, pinv);
+    const int cpr = (int)(rowb / V);
+    const int64_t i0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    if (i0 >= s) return;
+    const int64_t i = i0 + lane;
+    const int64_t g = i < s ? (int64_t)prp((uint64_t)i) : 0;
+    int sh = 0;
+    while (sh + 1 < t.n && g >= t.end[sh]) ++sh;
+    const unsigned char* src = t.ptr[sh] + (g - (sh ? t.end[sh - 1] : 0)) * rowb;
+    unsigned char* dst = S + ((int64_t)w * s + i0) * rowb;
+    const int total = 32 * cpr;
+    constexpr int U = 8;
+    for (int e0 = 0; e0 < total; e0 += 32 * U) {
+        VT v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * 32 + lane, r = e / cpr, q = e - r * cpr;
+            const unsigned char* sp = reinterpret_cast<const unsigned char*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), r & 31));
+            if (e < total && i0 + r < s) v[u] = __ldg(reinterpret_cast<const VT*>(sp + (int64_t)q * V));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * 32 + lane, r = e / cpr;
+            if (e < total && i0 + r < s) reinterpret_cast<VT*>(dst)[e] = v[u];
+        }
+    }
 }
 
 struct RoundEndParams {
@@ -939,6 +980,48 @@ int hpcg_sample_indices(hpcg_ctx* ctx, int64_t m, int64_t s, uint64_t key, uint3
     return HPCG_OK;
 }
 
+int hpcg_sample_gather_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, int64_t W, int64_t s, uint64_t key,
+                           uint32_t round, int32_t worker_base, void* S_dev) {
+    if (!ctx || !ds || !S_dev) return fail(HPCG_EINVAL, "sample_gather: null argument");
+    if (s < 1 || s > ds->m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
+    if (W < 1 || W > 65535) return fail(HPCG_EINVAL, "sample_gather: worker count must be in [1, 65535]");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    ShardTable t;
+    t.n = ds->nshards;
+    for (int i = 0; i < ds->nshards; ++i) {
+        t.ptr[i] = static_cast<const unsigned char*>(ds->shard_ptr[i]);
+        t.end[i] = ds->shard_end[i];
+    }
+    uint32_t a, b;
+    float inv_b;
+    SamplePRP::moduli((uint64_t)ds->m, a, b, inv_b);
+    const int64_t rowb = ds->n * (int64_t)dsize(ds->dtype);
+    const dim3 grid((unsigned)((s + 255) / 256), (unsigned)W);
+    unsigned char* S = static_cast<unsigned char*>(S_dev);
+    if (rowb % 16 == 0)
+        sample_gather_kernel<16><<<grid, 256, 0, ctx->stream>>>(t, ds->m, rowb, s, key, round, worker_base, a, b, inv_b, S);
+    else if (rowb % 8 == 0)
+        sample_gather_kernel<8><<<grid, 256, 0, ctx->stream>>>(t, ds->m, rowb, s, key, round, worker_base, a, b, inv_b, S);
+    else
+        sample_gather_kernel<4><<<grid, 256, 0, ctx->stream>>>(t, ds->m, rowb, s, key, round, worker_base, a, b, inv_b, S);
+    CU(cudaGetLastError());
+    ctx->launches += 1;
+    return HPCG_OK;
+}
+
+int hpcg_philox_seed_draws(uint64_t key, uint32_t round, uint32_t worker, int64_t s, int32_t no_valid,
+                           int64_t loops, int64_t candidates, int64_t* first_row, double* units) {
+    if (candidates < 1 || candidates > kMaxCandidates) return fail(HPCG_EINVAL, "seeding: candidates out of range");
+    if (first_row) *first_row = no_valid ? (int64_t)philox_index(key, round, worker, 0xF1F1u, (uint64_t)s) : 0;
+    if (units)
+        for (int64_t t = 0; t < loops; ++t)
+            for (int64_t c = 0; c < candidates; ++c)  // pending-slot index p = t + no_valid (step_kernel.cuh)
+                units[t * candidates + c] = philox_unit(
+                    key, round, worker, (uint32_t)(0x10000 + (t + (no_valid ? 1 : 0)) * kMaxCandidates + c));
+    return HPCG_OK;
+}
+
 int hpcg_reference_draw_indices(uint64_t* mt_state, int32_t* mt_pos, int64_t m, int64_t s, int64_t* idx_out) {
     if (s < 1 || s > m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
     Mt64 r;
@@ -1554,6 +1637,7 @@ int hpcg_engine_run(hpcg_engine* e) {
 }
 
 int64_t hpcg_engine_round_index(const hpcg_engine* e) { return e->round; }
+uint64_t hpcg_engine_philox_key(const hpcg_engine* e) { return e->key; }
 
 int hpcg_engine_set_trace(hpcg_engine* e, int64_t* trace_dev, int32_t mode) {
     e->trace_buf = trace_dev;
@@ -1737,6 +1821,22 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     if (worker_obj) std::memcpy(worker_obj, h_obj, (size_t)W * 8);
     o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
     if (out) *out = o;
+    return HPCG_OK;
+}
+
+int hpcg_engine_round_outcome(hpcg_engine* e, double* objective, int32_t* iterations, int32_t* stop, int64_t* n_d,
+                              uint8_t* accepted, int32_t* filled) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    const size_t W = (size_t)e->W;
+    if (objective) CU(d2h(objective, e->objb.as<double>(), W, ctx->stream));
+    if (iterations) CU(d2h(iterations, e->iters.as<int32_t>(), W, ctx->stream));
+    if (stop) CU(d2h(stop, e->stopb.as<int32_t>(), W, ctx->stream));
+    if (n_d) CU(d2h(n_d, e->nd.as<int64_t>(), W, ctx->stream));
+    if (accepted) CU(d2h(accepted, e->acc.as<uint8_t>(), W, ctx->stream));
+    if (filled) CU(d2h(filled, e->filled.as<int32_t>(), W, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return HPCG_OK;
 }
 

@@ -363,7 +363,52 @@ def _run(chk, fname, X, *, k, sample_size, n_workers, max_samples, strategy="com
                 traces=[traces[w, : tlen[w]].copy() for w in range(W)])
 
 
-_ORC = _REF = None
+class RefInject:
+    """oracle/_ref/libhpclust_ref_inject.so: the reference's own worker step (reinit_degenerate +
+    kmeans, engine.hpp:238-267) with injected 64-bit random draws (oracle/ref_inject.cpp)."""
+
+    def __init__(self, path):
+        self.lib = L = C.CDLL(str(path))
+        P, SZ, I64, D = C.c_void_p, C.c_size_t, C.c_int64, C.c_double
+        L.hpref_inject_last_error.restype = C.c_char_p
+        L.hpref_inject_step.argtypes = [P, SZ, SZ, P, P, SZ, SZ, SZ, D, P, I64, P, P, P, P, P, P, P, P, P]
+
+    @staticmethod
+    def philox_draws(first_row, units, no_valid):
+        """The u64 draws that make the reference consume first_row (uniform_index, rng.hpp:43-53:
+        x < limit, x % s) and the given units (next_unit, rng.hpp:38-40: (v >> 11) * 2^-53)."""
+        v = [int(first_row)] if no_valid else []
+        v += [int(round(u * 2.0 ** 53)) << 11 for u in np.asarray(units, np.float64)]
+        return np.array(v, dtype=np.uint64)
+
+    def step(self, S, C0, flags, draws, candidates=3, max_iters=300, rel_tol=1e-4, labels=False):
+        S = np.ascontiguousarray(S, np.float64)
+        s, n = S.shape
+        C0 = np.ascontiguousarray(C0, np.float64)
+        k = C0.shape[0]
+        fl = np.ascontiguousarray(flags, np.uint8)
+        draws = np.ascontiguousarray(draws, np.uint64)
+        Cs, Co, fo = np.empty((k, n)), np.empty((k, n)), np.empty(k, np.uint8)
+        f, it, st, nd, used = C.c_double(), C.c_int64(), C.c_int32(), C.c_int64(), C.c_int64()
+        lab = np.empty(s, np.int32) if labels else None
+        rc = self.lib.hpref_inject_step(ptr(S), s, n, ptr(C0), ptr(fl), k, candidates, max_iters, rel_tol,
+                                        ptr(draws), len(draws), ptr(Cs), ptr(Co), ptr(fo), C.byref(f), C.byref(it),
+                                        C.byref(st), C.byref(nd), C.byref(used), ptr(lab))
+        if rc != 0:
+            raise RuntimeError(self.lib.hpref_inject_last_error().decode())
+        return dict(seeded=Cs, centroids=Co, degenerate=fo, objective=f.value, iterations=it.value, stop=st.value,
+                    n_d=nd.value, consumed=used.value, labels=lab)
+
+
+_ORC = _REF = _INJ = None
+
+
+def ref_inject() -> RefInject | None:
+    global _INJ
+    p = ROOT / "oracle" / "_ref" / "libhpclust_ref_inject.so"
+    if _INJ is None and p.exists():
+        _INJ = RefInject(p)
+    return _INJ
 
 
 def orc() -> Oracle:

@@ -206,3 +206,47 @@ def test_oracle_vs_live_reference_random():
         Cb, fb, nb = R.reinit(S, C0 * (1 - fl[:, None]), fl, rb)
         assert np.array_equal(Ca, Cb) and np.array_equal(fa, fb) and na == nb
         assert o.next_u64(ra) == rb.next_u64()
+
+
+# ----------------------------------------- injected draws (PHILOX-round replay harness)
+def test_injected_draws_replay_the_stock_reference():
+    """oracle/ref_inject.cpp feeds queued 64-bit values to the reference's unmodified RngStream. Fed
+    the very values a stock stream would produce, the reference's worker step (reinit_degenerate +
+    kmeans) must come out bit-identical to the stock build's, consuming exactly the same count."""
+    from oracle_py import ref_inject
+    R, J = ref(), ref_inject()
+    if R is None or J is None:
+        pytest.skip("oracle/_ref not built")
+    rs = np.random.default_rng(11)
+    for case in range(12):
+        s, n, k = int(rs.integers(50, 400)), int(rs.integers(1, 6)), int(rs.integers(2, 8))
+        S = rs.standard_normal((s, n)) * 3 + rs.integers(0, 3, (s, 1))
+        C0 = S[rs.choice(s, k, replace=False)]
+        fl = np.ones(k, np.uint8) if case % 3 == 0 else (rs.random(k) < 0.5).astype(np.uint8)
+        seed = int(rs.integers(1 << 30))
+        probe = R.rng(seed=seed)
+        draws = np.array([probe.next_u64() for _ in range(200)], dtype=np.uint64)
+        stock = R.rng(seed=seed)
+        Cb, fb, nb = R.reinit(S, C0 * (1 - fl[:, None]), fl, stock)
+        b = R.kmeans(S, Cb)
+        a = J.step(S, C0 * (1 - fl[:, None]), fl, draws)
+        assert np.array_equal(a["seeded"], Cb)
+        assert np.array_equal(a["centroids"], b["centroids"]) and a["objective"] == b["objective"]
+        assert a["iterations"] == b["iterations"] and a["stop"] == b["stop"]
+        # the stock stream after reinit sits exactly `consumed` draws in
+        assert stock.next_u64() == int(draws[a["consumed"]])
+
+
+def test_injected_philox_draw_encoding():
+    """RefInject.philox_draws: the reference turns the injected values back into the given first
+    row (uniform_index) and units (next_unit) exactly."""
+    from oracle_py import ref_inject
+    J = ref_inject()
+    if J is None:
+        pytest.skip("oracle/_ref not built")
+    rs = np.random.default_rng(3)
+    units = np.floor(rs.random(9) * 2.0 ** 53) / 2.0 ** 53
+    d = J.philox_draws(17, units, True)
+    assert int(d[0]) == 17
+    back = (d[1:] >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    assert np.array_equal(back, units)
