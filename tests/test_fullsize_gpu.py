@@ -47,7 +47,7 @@ def test_config3_full_objective_1e8_rows():
     C_ = means + rs.normal(0, 2.0, means.shape)  # centroids near the components (realistic margins)
     deg = np.zeros(25, np.uint8)
     deg[[4, 17]] = 1  # two degenerate slots: the valid-subset remap (engine.hpp:211-229)
-    a, f = hp.final_assignment(X, C_ * (1 - deg[:, None]), deg)
+    a, f = hp.assign_valid_subset(X, C_ * (1 - deg[:, None]), deg)
     lab, cnt, cost, nd = R.assign(X, C_ * (1 - deg[:, None]), deg, n_chunks=_cores())
     assert np.array_equal(a.counts, cnt)
     assert np.array_equal(a.labels, lab)
