@@ -141,55 +141,34 @@ def dist_setup():
     return world, rank, local
 
 
-def exchange_best(eng, world, device):
-    """Cooperative exchange across ranks: all-gather (objective, global worker, centroids,
-    flags) and install the global winner (min objective, ties -> lowest worker id)."""
+def map_global_shards(hp, ctx, Xd, world, rank, device):
+    """Every rank's X shard mapped into this process (CUDA IPC; NVLink peer access on a multi-GPU
+    box): the engine samples over all ranks' rows (engine.hpp:165-177), its f(C,X) covers this rank's
+    shard. Returns (shards, peers) for DeviceDataset.from_shards and the later ipc_close."""
     import torch
     import torch.distributed as dist
-    obj, wk, C_, f = eng.export_best()
-    rec = torch.zeros(2 + C_.size + f.size, dtype=torch.float64, device=device)
-    rec[0] = obj
-    rec[1] = float(wk)
-    rec[2:2 + C_.size] = torch.from_numpy(C_.ravel())
-    rec[2 + C_.size:] = torch.from_numpy(f.astype(np.float64))
-    out = [torch.empty_like(rec) for _ in range(world)]
-    dist.all_gather(out, rec)
-    recs = [o.cpu().numpy() for o in out]
-    best = merge_records([(r[0], int(r[1])) for r in recs])
-    if best is not None and (recs[best][0] < obj or int(recs[best][1]) != wk):
-        r = recs[best]
-        eng.import_best(float(r[0]), int(r[1]), r[2:2 + C_.size].reshape(C_.shape), r[2 + C_.size:].astype(np.uint8))
+    h = torch.tensor(list(hp.ipc_export(Xd.data_ptr())), dtype=torch.uint8, device=device)
+    hs = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(hs, h)
+    shards, peers = [], []
+    for r in range(world):
+        if r == rank:
+            shards.append((Xd.data_ptr(), Xd.shape[0], N, np.float32))
+        else:
+            hb = bytes(hs[r].cpu().tolist())
+            p = hp.ipc_open(hb, ctx)
+            peers.append((p, hb))
+            shards.append((p, Xd.shape[0], N, np.float32))
+    return shards, peers
 
 
-def finish_global(eng, ds, ctx, device):
-    """N > 1 finish: select_best over every rank's workers is the exchanged shared best (the
-    cooperative strategy publishes every strict improvement); f(C, X) = this shard's partial from
-    the device pass + all-reduce over the ranks (north star: per-shard partial sum, then allreduce).
-    n_d: the rounds' plus this shard's final pass (m_shard x valid centres)."""
+def attach_nccl(hp, ctx, world, rank, device):
+    """The library's own NCCL communicator (ncclCommInitRank; unique id broadcast by torch)."""
     import torch
     import torch.distributed as dist
-    from types import SimpleNamespace
-    import paper_2311_04517_b200 as hp
-    _, _, C_, f = eng.export_best()
-    valid = f == 0
-    kv = int(valid.sum())
-    cost = torch.zeros(1, dtype=torch.float64, device=device)
-    if kv > 0:
-        Cv = torch.from_numpy(np.ascontiguousarray(C_[valid])).to(device)
-        hp._lib.check(hp._lib.lib.hpcg_assign_dev(ctx.h, ds.h, Cv.data_ptr(), kv, None, cost.data_ptr()))
-    dist.all_reduce(cost)
-    return SimpleNamespace(distance_evals=eng.distance_evals() + ds.m * kv, full_objective=float(cost.item()),
-                           degenerate=f, centroids=C_)
-
-
-def merge_records(recs):
-    """Index of the winning (objective, worker) record: strict min objective, ties to the
-    lowest global worker id (engine.hpp:129-138 publication order); None if all infinite."""
-    best, bo, bw = None, float("inf"), None
-    for i, (o, w) in enumerate(recs):
-        if o < bo or (o == bo and bw is not None and w < bw and o != float("inf")):
-            best, bo, bw = i, o, w
-    return best
+    uid = torch.tensor(list(hp.comm_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=device)
+    dist.broadcast(uid, 0)
+    ctx.attach_comm(world, rank, bytes(uid.cpu().tolist()))
 
 
 def gather_rate(hp, ctx, ds, stream, key, reps=8):
@@ -234,40 +213,28 @@ def run_gpu(args, world, rank, local):
     ds = hp.DeviceDataset.from_torch(Xd, ctx)
     cfg = hp.EngineConfig(k=K, sample_size=S, n_workers=W_PER_GPU, max_samples=ROUNDS, strategy="cooperative",
                           rng="philox", worker_base=rank * W_PER_GPU)
-    sampling = "local shard" if world > 1 else "all rows"
+    sampling = "all rows"
     ds_eng, peers = ds, []
-    if world > 1 and args.global_sampling:
-        # samples over all ranks' rows (engine.hpp:165-177 semantics): every rank maps the other
-        # ranks' shards by CUDA IPC (NVLink peer access) and the gathers read remote rows directly
-        try:
-            import torch.distributed as dist
-            h = torch.tensor(list(hp.ipc_export(Xd.data_ptr())), dtype=torch.uint8, device=device)
-            hs = [torch.empty_like(h) for _ in range(world)]
-            dist.all_gather(hs, h)
-            shards = []
-            for r in range(world):
-                if r == rank:
-                    shards.append((Xd.data_ptr(), M, N, np.float32))
-                else:
-                    hb = bytes(hs[r].cpu().tolist())
-                    p = hp.ipc_open(hb, ctx)
-                    peers.append((p, hb))
-                    shards.append((p, M, N, np.float32))
-            ds_eng = hp.DeviceDataset.from_shards(shards, ctx=ctx, keepalive=Xd)
-            sampling = f"global over {world} shards (NVLink P2P gathers)"
-        except Exception as ex:  # keep the run: local-shard sampling, say why
-            ds_eng = ds
-            sampling = f"local shard (global sampling unavailable: {type(ex).__name__}: {ex})"[:160]
+    if world > 1:
+        attach_nccl(hp, ctx, world, rank, device)
+        sampling = "local shard"
+        if not args.local_sampling:
+            try:  # global sampling over every rank's rows (the reference semantics), the default
+                shards, peers = map_global_shards(hp, ctx, Xd, world, rank, device)
+                ds_eng = hp.DeviceDataset.from_shards(shards, ctx=ctx, keepalive=Xd)
+                sampling = f"global over {world} shards (NVLink P2P gathers)"
+            except Exception as ex:  # keep the run: local-shard sampling, say why
+                ds_eng = ds
+                sampling = f"local shard (global sampling unavailable: {type(ex).__name__}: {ex})"[:160]
     eng = hp.Engine(ds_eng, cfg)
+    if world > 1:  # every round publishes over all ranks' workers through the library (NCCL all-gather)
+        eng.set_exchange(world, rank)
     fma_tfma = ctx.fma_peak()
 
     def step(seed):
         eng.reset(seed)
-        for _ in range(ROUNDS):
-            eng.rounds(1)
-            if world > 1:
-                exchange_best(eng, world, device)
-        return eng.finish() if world == 1 else finish_global(eng, ds, ctx, device)
+        eng.rounds(ROUNDS)
+        return eng.finish()
 
     for i in range(args.warmup):
         step(10_000 + i)
@@ -287,8 +254,8 @@ def run_gpu(args, world, rank, local):
         ev0.record(stream)
         for i in range(args.steps):
             res = step(20_000 + i)
-            nd_total += res.distance_evals
-            nd_rounds += res.distance_evals - M * int((res.degenerate == 0).sum())
+            nd_total += res.distance_evals  # all ranks' evaluations (the multi-rank finish sums them)
+            nd_rounds += eng.distance_evals()  # this rank's worker-step evaluations (no final pass)
             objs.append(res.full_objective)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -302,11 +269,7 @@ def run_gpu(args, world, rank, local):
         t = torch.tensor([ms_total], dtype=torch.float64, device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
-        n = torch.tensor([nd_total], dtype=torch.float64, device=device)
-        torch.distributed.all_reduce(n)
-        nd_all = float(n.item())
-    else:
-        nd_all = float(nd_total)
+    nd_all = float(nd_total)
     ms_step = ms_total / args.steps
     value = nd_all / (ms_total * 1e-3)
 
@@ -360,7 +323,9 @@ def run_gpu(args, world, rank, local):
                                "full-data f(C,X)", "m_per_gpu": M, "n": N, "k": K, "s": S,
                    "workers_per_gpu": W_PER_GPU, "rounds": ROUNDS, "rng": "philox",
                    "l2": "X (640 MB/GPU) exceeds L2 (126 MB); samples gathered from HBM every round",
-                   "parallelism": f"{world} GPU(s), one process per GPU, NCCL incumbent exchange per round",
+                   "parallelism": f"{world} GPU(s), one process per GPU; library NCCL all-gather of the round "
+                                  f"candidates + device publication scan every round, select_best and f(C,X) "
+                                  f"shard partials over all ranks",
                    "sampling": sampling},
         "distance_evals_per_step": nd_all / args.steps,
         "objective_pass": {"gbs": obj_gbs, "ms": float(np.median(obj_ms)), "bytes": obj_bytes,
@@ -417,8 +382,9 @@ def e2e_run(X, args):
 
 def e2e_run_multi(X, args, world, rank, ctx, device):
     """N > 1: the same run through the public API on every rank's pinned host shard -- upload
-    (DeviceDataset), engine rounds with the NCCL shared-best exchange, finish (result read-back)
-    -- timed on the host per step with a barrier on both sides, max over ranks."""
+    (DeviceDataset), the shards mapped across ranks (CUDA IPC), an Engine with the library's NCCL
+    exchange, run, finish (result read-back) -- timed on the host per step with a barrier on both
+    sides, max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2311_04517_b200 as hp
@@ -432,28 +398,40 @@ def e2e_run_multi(X, args, world, rank, ctx, device):
         dist.barrier()
         t0 = time.perf_counter()
         ds = hp.DeviceDataset(Xp, ctx=ctx)
-        eng = hp.Engine(ds, cfg)
+        mine = torch.empty(0)  # the shard buffer is ds's own allocation
+        peers = []
+        ds_eng = ds
+        if not args.local_sampling:
+            base = hp._lib.lib.hpcg_dataset_device_ptr(ds.h)
+            view = type("V", (), {"data_ptr": lambda self, b=base: b, "shape": (M, N)})()
+            shards, peers = map_global_shards(hp, ctx, view, world, rank, device)
+            ds_eng = hp.DeviceDataset.from_shards(shards, ctx=ctx, keepalive=ds)
+        eng = hp.Engine(ds_eng, cfg)
+        eng.set_exchange(world, rank)
         eng.reset(30_000 + i)
-        for _ in range(ROUNDS):
-            eng.rounds(1)
-            exchange_best(eng, world, device)
-        r = finish_global(eng, ds, ctx, device)
+        eng.run()
+        r = eng.finish()
         eng.close()
+        dist.barrier()  # no rank may free its shard while a peer still maps it
+        for p, hb in peers:
+            hp.ipc_close(p, hb, ctx)
+        if ds_eng is not ds:
+            ds_eng.close()
         ds.close()
+        del mine
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        t = torch.tensor([dt, float(r.distance_evals)], dtype=torch.float64, device=device)
-        tm = t.clone()
-        dist.all_reduce(tm[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:])
+        t = torch.tensor([dt], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if i >= 1:
-            times.append(float(tm[0].item()))
-            nds.append(float(t[1].item()))
+            times.append(float(t.item()))
+            nds.append(float(r.distance_evals))  # already the all-rank total (engine finish)
     h2d = X.nbytes * world
     d2h = (K * N * 8 + K + 8 * 6) * world
     return {"value": float(np.sum(nds) / np.sum(times)), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(times) * 1e3),
-            "path": "DeviceDataset upload + Engine rounds with the NCCL exchange + finish, per rank (max over ranks)"}
+            "path": "DeviceDataset upload + IPC-mapped shards + Engine with the library's NCCL exchange + finish, "
+                    "per rank (max over ranks)"}
 
 
 # ----------------------------------------------------------------------------- other configs
@@ -653,8 +631,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the config 3/4/5 extra keys")
     ap.add_argument("--configs-only", default="", help="e.g. 3,4,5: print one JSON line per config and exit")
-    ap.add_argument("--global-sampling", action="store_true",
-                    help="N > 1: sample over all ranks' rows (peer-mapped shards) instead of the local shard")
+    ap.add_argument("--local-sampling", action="store_true",
+                    help="N > 1: sample each rank's own shard instead of all ranks' rows (peer-mapped shards)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.configs_only:

@@ -78,6 +78,8 @@ int hpcg_ctx_set_stream(hpcg_ctx* ctx, void* cuda_stream);
 int hpcg_ctx_synchronize(hpcg_ctx* ctx);
 /* Number of kernels this library launched on the context since creation (bench evidence). */
 int64_t hpcg_ctx_launch_count(const hpcg_ctx* ctx);
+/* Host -> device bytes this context's dataset uploads moved (hpcg_dataset_upload / hpcg_run). */
+int64_t hpcg_ctx_upload_bytes(const hpcg_ctx* ctx);
 /* Per-kernel device timing: when enabled, every worker-step / objective launch is bracketed
  * by CUDA events on the launching stream; hpcg_ctx_kernel_times synchronises and returns
  * (launch count, summed milliseconds) per kernel class: 0 worker step, 1 objective. */
@@ -242,6 +244,31 @@ int hpcg_engine_destroy(hpcg_engine* e);
 
 /* The engine's Philox key (HPCG_RNG_PHILOX streams derive from it; see hpcg_sample_indices). */
 uint64_t hpcg_engine_philox_key(const hpcg_engine* e);
+
+/* ---- multi-GPU: one rank per GPU ------------------------------------------
+ * Ranks own row shards of X (hpcg_dataset_wrap_sharded with peer-mapped shards gives every rank
+ * global sampling, engine.hpp:165-177) and the contiguous worker ids [worker_base, worker_base + W).
+ * With an exchange set, every round of a cooperative / hybrid engine publishes over ALL ranks'
+ * workers exactly as one engine with every worker would (engine.hpp:391-402: global worker-id order,
+ * strict <; the hybrid carry-over at engine.hpp:386,396): each rank all-gathers its round candidates
+ * and its local best's centroids (one record of 4 + W + k*n + k doubles), and a device kernel on
+ * every rank replays the publication scan, so the shared best and the publication log are
+ * replicated bit-identically. hpcg_engine_finish then runs select_best over every rank's workers
+ * (engine.hpp:180-194), f(C, X) as this rank's shard partial, and sums partials, n_d and sample
+ * counts in rank order (labels, if requested, are this rank's rows). The collective is NCCL
+ * (ncclAllGather on the context's stream over NVLink; libnccl.so.2 is loaded at run time) or, for
+ * callers with their own transport, a host all-gather callback. */
+/* NCCL unique id (128 bytes) created on one rank and shared with the others by the caller. */
+int hpcg_comm_unique_id(void* id_out);
+/* Collective over the ranks: attach an NCCL communicator (nranks, rank) to the context. */
+int hpcg_ctx_attach_comm(hpcg_ctx* ctx, int32_t nranks, int32_t rank, const void* id);
+int hpcg_ctx_comm_info(const hpcg_ctx* ctx, int32_t* nranks, int32_t* rank);
+/* Host all-gather: copy bytes_per_rank from send into recv[rank * bytes_per_rank] on every rank
+ * (rank order); return 0 on success. */
+typedef int (*hpcg_allgather_fn)(const void* send_host, void* recv_host, size_t bytes_per_rank, void* user);
+/* Make e one rank of a multi-rank engine (before its first round; collective over the ranks).
+ * fn == NULL: the context's NCCL communicator (must match nranks / rank). */
+int hpcg_engine_set_exchange(hpcg_engine* e, int32_t nranks, int32_t rank, hpcg_allgather_fn fn, void* user);
 
 /* Multi-rank exchange hooks (cooperative / hybrid across GPUs):
  * export this rank's round candidates, import the merged shared best. */

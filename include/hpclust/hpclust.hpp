@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <barrier>
+#include <exception>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -37,11 +39,14 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
 #include "../hpcg.h"
+#include "parallel.hpp"
 
 namespace hpclust {
 
@@ -237,39 +242,107 @@ private:
 };
 
 // ----------------------------------------------------------- assignment / objective
+// ------------------------------------------------------- device-resident datasets
+enum class Precision { f64, f32 };
+
+// X resident in HBM (ADDITIVE to the reference API): upload once -- in fp64, or
+// rounded to fp32 (the north star's fp32 mode) -- or borrow device memory, then pass it to the
+// overloads of draw_sample, worker_step, assign_nearest, mssc_objective, final_assignment,
+// detail::assign_valid_subset and run below, which read it in place (no per-call upload of X; a
+// 64 GB X need not live in a host std::vector<double>).
+class DeviceDataset {
+public:
+    explicit DeviceDataset(const Dataset& X, Precision p = Precision::f64) : rows(X.rows), cols(X.cols), precision(p) {
+        X.validate();
+        if (p == Precision::f64) {
+            gpu::check(hpcg_dataset_upload(gpu::context(), X.values.data(), HPCG_F64, (int64_t)rows, (int64_t)cols, &ds_));
+        } else {
+            std::vector<float> v(X.values.begin(), X.values.end());
+            gpu::check(hpcg_dataset_upload(gpu::context(), v.data(), HPCG_F32, (int64_t)rows, (int64_t)cols, &ds_));
+        }
+    }
+    // borrow row-major m x n device memory of the default context's device (must outlive this)
+    static DeviceDataset borrow(const void* dev, std::size_t m, std::size_t n, Precision p) {
+        DeviceDataset d;
+        d.rows = m;
+        d.cols = n;
+        d.precision = p;
+        gpu::check(hpcg_dataset_wrap(gpu::context(), dev, p == Precision::f64 ? HPCG_F64 : HPCG_F32, (int64_t)m,
+                                     (int64_t)n, &d.ds_));
+        return d;
+    }
+    DeviceDataset(DeviceDataset&& o) noexcept : rows(o.rows), cols(o.cols), precision(o.precision), ds_(o.ds_) {
+        o.ds_ = nullptr;
+    }
+    DeviceDataset& operator=(DeviceDataset&& o) noexcept {
+        std::swap(ds_, o.ds_);
+        rows = o.rows;
+        cols = o.cols;
+        precision = o.precision;
+        return *this;
+    }
+    DeviceDataset(const DeviceDataset&) = delete;
+    DeviceDataset& operator=(const DeviceDataset&) = delete;
+    ~DeviceDataset() {
+        if (ds_) hpcg_dataset_destroy(ds_);
+    }
+    hpcg_dataset* handle() const { return ds_; }
+    std::size_t rows = 0, cols = 0;
+    Precision precision = Precision::f64;
+
+private:
+    DeviceDataset() = default;
+    hpcg_dataset* ds_ = nullptr;
+};
+
 namespace gpu {
-inline std::pair<Assignment, double> assign(const Dataset& X, const CentroidSet& C, bool strict, bool want_labels,
-                                            DistCounter* counter) {
-    DeviceMatrix dm(X.values.data(), X.rows, X.cols);
+inline std::pair<Assignment, double> assign_ds(hpcg_dataset* ds, std::size_t rows, const CentroidSet& C, bool strict,
+                                               bool want_labels, DistCounter* counter) {
     Assignment a;
-    if (want_labels) a.labels.resize(X.rows);
+    if (want_labels) a.labels.resize(rows);
     a.counts.assign(C.k, 0);
     double cost = 0.0;
     std::int64_t nd = 0;
-    check(hpcg_assign(context(), dm.ds, C.centers.data(), C.degenerate.data(), (int64_t)C.k, strict ? 1 : 0,
+    check(hpcg_assign(context(), ds, C.centers.data(), C.degenerate.data(), (int64_t)C.k, strict ? 1 : 0,
                       want_labels ? a.labels.data() : nullptr, a.counts.data(), &cost, &nd));
     count_distances(counter, nd);
     return {std::move(a), cost};
 }
+inline std::pair<Assignment, double> assign(const Dataset& X, const CentroidSet& C, bool strict, bool want_labels,
+                                            DistCounter* counter) {
+    DeviceMatrix dm(X.values.data(), X.rows, X.cols);
+    return assign_ds(dm.ds, X.rows, C, strict, want_labels, counter);
+}
+inline std::pair<Assignment, double> assign(const DeviceDataset& X, const CentroidSet& C, bool strict, bool want_labels,
+                                            DistCounter* counter) {
+    return assign_ds(X.handle(), X.rows, C, strict, want_labels, counter);
+}
 }  // namespace gpu
 
-inline Assignment assign_nearest(const Dataset& X, const CentroidSet& C,
-                                 const ParallelPolicy& = ParallelPolicy::sequential(), DistCounter* counter = nullptr) {
+// XS: Dataset (the reference signature; uploaded per call) or DeviceDataset (resident, additive)
+template <typename XS>
+concept AnyDataset = std::is_same_v<XS, Dataset> || std::is_same_v<XS, DeviceDataset>;
+
+template <AnyDataset XS>
+inline Assignment assign_nearest(const XS& X, const CentroidSet& C, const ParallelPolicy& = ParallelPolicy::sequential(),
+                                 DistCounter* counter = nullptr) {
     require(C.k >= 1, "assign_nearest: need at least one centroid");
     require(C.cols == X.cols, "assign_nearest: dimension mismatch");
     require(!C.any_degenerate(), "assign_nearest: degenerate centroid present");
     return gpu::assign(X, C, true, true, counter).first;
 }
 
-inline double mssc_objective(const CentroidSet& C, const Dataset& X,
-                             const ParallelPolicy& = ParallelPolicy::sequential(), DistCounter* counter = nullptr) {
+template <AnyDataset XS>
+inline double mssc_objective(const CentroidSet& C, const XS& X, const ParallelPolicy& = ParallelPolicy::sequential(),
+                             DistCounter* counter = nullptr) {
     require(C.k >= 1, "mssc_objective: need at least one centroid");
     require(C.cols == X.cols, "mssc_objective: dimension mismatch");
     require(!C.any_degenerate(), "mssc_objective: degenerate centroid present");
     return gpu::assign(X, C, true, false, counter).second;
 }
 
-inline std::pair<Assignment, double> final_assignment(const Dataset& X, const CentroidSet& C,
+template <AnyDataset XS>
+inline std::pair<Assignment, double> final_assignment(const XS& X, const CentroidSet& C,
                                                       const ParallelPolicy& = ParallelPolicy::sequential(),
                                                       DistCounter* counter = nullptr) {
     require(!C.any_degenerate(), "final_assignment: degenerate centroid present");
@@ -278,7 +351,8 @@ inline std::pair<Assignment, double> final_assignment(const Dataset& X, const Ce
 }
 
 namespace detail {
-inline std::pair<Assignment, double> assign_valid_subset(const Dataset& X, const CentroidSet& C, const ParallelPolicy&,
+template <AnyDataset XS>
+inline std::pair<Assignment, double> assign_valid_subset(const XS& X, const CentroidSet& C, const ParallelPolicy&,
                                                          DistCounter* counter) {
     if (!C.any_degenerate()) return final_assignment(X, C, ParallelPolicy::sequential(), counter);
     require(C.degenerate_count() < C.k, "assignment: every centroid is degenerate");
@@ -292,7 +366,10 @@ struct LloydConfig {
     double rel_tol = 1e-4;
     bool parallel_rows = false;
     std::size_t n_threads = 0;
-    ParallelPolicy policy() const { return parallel_rows ? ParallelPolicy::threads(n_threads) : ParallelPolicy::sequential(); }
+    ParallelPolicy policy() const {  // lloyd.hpp:16-19
+        if (!parallel_rows) return ParallelPolicy::sequential();
+        return ParallelPolicy::threads(n_threads == 0 ? ThreadPool::default_threads() : n_threads);
+    }
 };
 
 enum class LloydStop { tolerance, max_iters, fixed_point };
@@ -349,9 +426,17 @@ struct StepOut {
 // One (sample, init) problem on the device: reseed degenerate slots with the draws the
 // reference would take from `rng`, then (optionally) Lloyd. rng is left exactly where the
 // reference leaves it (draws not consumed because seeding stopped early are rewound).
+inline StepOut step_ds(hpcg_dataset* ds, const std::int64_t* idx, std::size_t s, std::size_t n, const CentroidSet& init,
+                       const LloydConfig& lc, std::size_t candidates, RngStream* rng, bool do_lloyd);
 inline StepOut step(const Dataset& S, const CentroidSet& init, const LloydConfig& lc, std::size_t candidates,
                     RngStream* rng, bool do_lloyd) {
-    const std::size_t s = S.rows, k = init.k;
+    DeviceMatrix dm(S.values.data(), S.rows, S.cols);
+    return step_ds(dm.ds, nullptr, S.rows, S.cols, init, lc, candidates, rng, do_lloyd);
+}
+// The worker step on rows idx[0..s) of a device dataset (idx == nullptr: ds is the sample itself).
+inline StepOut step_ds(hpcg_dataset* ds, const std::int64_t* idx, std::size_t s, std::size_t n, const CentroidSet& init,
+                       const LloydConfig& lc, std::size_t candidates, RngStream* rng, bool do_lloyd) {
+    const std::size_t k = init.k;
     std::size_t pend = 0;
     for (auto f : init.degenerate) pend += f ? 1 : 0;
     const bool no_valid = pend > 0 && pend == k;
@@ -365,10 +450,9 @@ inline StepOut step(const Dataset& S, const CentroidSet& init, const LloydConfig
         loops = pend - (no_valid ? 1 : 0);
         for (std::size_t t = 0; t < loops * candidates; ++t) units[t] = rng->next_unit();
     }
-    DeviceMatrix dm(S.values.data(), s, S.cols);
     const hpcg_lloyd_cfg cfg{(int64_t)lc.max_iters, lc.rel_tol, (int64_t)candidates};
     StepOut o;
-    o.C.resize(k * S.cols);
+    o.C.resize(k * n);
     o.f.resize(k);
     o.labels.resize(s);
     o.counts.resize(k);
@@ -376,7 +460,7 @@ inline StepOut step(const Dataset& S, const CentroidSet& init, const LloydConfig
     o.history.resize((std::size_t)cap);
     int32_t hl = 0;
     const int rc = hpcg_worker_step_batched(
-        context(), dm.ds, nullptr, 1, (int64_t)s, init.centers.data(), init.degenerate.data(), (int64_t)k, &cfg,
+        context(), ds, idx, 1, (int64_t)s, init.centers.data(), init.degenerate.data(), (int64_t)k, &cfg,
         &first, units.data(), (int64_t)units.size(), do_lloyd ? 1 : 0, o.C.data(), o.f.data(), &o.obj, &o.iters,
         &o.stop, &o.nd, &o.filled, do_lloyd ? o.labels.data() : nullptr, do_lloyd ? o.counts.data() : nullptr,
         do_lloyd ? o.history.data() : nullptr, do_lloyd ? cap : 0, &hl);
@@ -565,8 +649,9 @@ private:
 
 // s distinct rows in the reference's draw order: the partial Fisher-Yates replayed in O(s)
 // (only displaced slots stored), rows gathered by the device.
-inline Dataset draw_sample(const Dataset& X, std::size_t s, RngStream& rng) {
-    require(s >= 1 && s <= X.rows, "draw_sample: sample size must be in [1, m]");
+namespace detail {
+inline std::vector<std::int64_t> draw_indices(std::size_t m, std::size_t s, RngStream& rng) {
+    require(s >= 1 && s <= m, "draw_sample: sample size must be in [1, m]");
     std::vector<std::int64_t> idx(s);
     std::unordered_map<std::size_t, std::size_t> moved;
     moved.reserve(2 * s);
@@ -575,15 +660,35 @@ inline Dataset draw_sample(const Dataset& X, std::size_t s, RngStream& rng) {
         return it == moved.end() ? i : it->second;
     };
     for (std::size_t i = 0; i < s; ++i) {
-        const std::size_t j = i + rng.uniform_index(X.rows - i);
+        const std::size_t j = i + rng.uniform_index(m - i);
         const std::size_t a = at(i), b = at(j);
         moved[i] = b;
         moved[j] = a;
         idx[i] = (std::int64_t)b;
     }
+    return idx;
+}
+}  // namespace detail
+
+inline Dataset draw_sample(const Dataset& X, std::size_t s, RngStream& rng) {
+    std::vector<std::int64_t> idx = detail::draw_indices(X.rows, s, rng);
     gpu::DeviceMatrix dm(X.values.data(), X.rows, X.cols);
     Dataset out(s, X.cols);
     gpu::check(hpcg_gather(gpu::context(), dm.ds, idx.data(), (int64_t)s, out.values.data()));
+    return out;
+}
+
+// device-resident X: only the s sample rows cross PCIe (back to the host Dataset)
+inline Dataset draw_sample(const DeviceDataset& X, std::size_t s, RngStream& rng) {
+    std::vector<std::int64_t> idx = detail::draw_indices(X.rows, s, rng);
+    Dataset out(s, X.cols);
+    if (X.precision == Precision::f64) {
+        gpu::check(hpcg_gather(gpu::context(), X.handle(), idx.data(), (int64_t)s, out.values.data()));
+    } else {
+        std::vector<float> f(s * X.cols);
+        gpu::check(hpcg_gather(gpu::context(), X.handle(), idx.data(), (int64_t)s, f.data()));
+        std::copy(f.begin(), f.end(), out.values.begin());
+    }
     return out;
 }
 
@@ -619,6 +724,37 @@ inline bool worker_step(WorkerState& w, RngStream& rng, const Dataset& X, const 
     return true;
 }
 
+// device-resident X: gather, reseed and Lloyd in ONE device call on the resident rows (the same
+// draws, in the same order, as draw_sample + reinit_degenerate + kmeans take from rng)
+template <typename Clock>
+inline bool worker_step(WorkerState& w, RngStream& rng, const DeviceDataset& X, const CentroidSet& init_source,
+                        const EngineConfig& cfg, Clock&& clock, DistCounter* counter = nullptr) {
+    std::vector<std::int64_t> idx = detail::draw_indices(X.rows, cfg.sample_size, rng);
+    require(init_source.cols == X.cols, "seeding: dimension mismatch");
+    require(cfg.seed.candidates_per_center >= 1, "seeding: need at least one candidate");
+    require(cfg.lloyd.max_iters >= 1, "kmeans: max_iters must be positive");
+    require(cfg.lloyd.rel_tol > 0.0, "kmeans: rel_tol must be positive");
+    auto o = gpu::step_ds(X.handle(), idx.data(), cfg.sample_size, X.cols, init_source, cfg.lloyd,
+                          cfg.seed.candidates_per_center, &rng, true);
+    count_distances(counter, o.nd);
+    ++w.samples_processed;
+    double ts = clock();
+    w.t_w = ts;
+    if (!(o.obj < w.incumbent_objective)) return false;
+    if (!w.update_trace.empty()) {
+        if (!(o.obj < w.update_trace.back().sample_objective))
+            throw std::logic_error("worker_step: non-decreasing incumbent accepted");
+        if (!(ts > w.update_trace.back().timestamp))
+            ts = std::nextafter(w.update_trace.back().timestamp, std::numeric_limits<double>::infinity());
+    }
+    w.incumbent = CentroidSet(init_source.k, X.cols);
+    w.incumbent.centers = std::move(o.C);
+    w.incumbent.degenerate = std::move(o.f);
+    w.incumbent_objective = o.obj;
+    w.update_trace.push_back({ts, o.obj});
+    return true;
+}
+
 struct ClusteringResult {
     CentroidSet centroids;
     std::optional<double> full_objective;
@@ -636,11 +772,22 @@ struct ClusteringResult {
 
 // The whole HPClust run on the device: lockstep rounds of gather -> reseed -> Lloyd ->
 // keep-the-best -> publication for all workers, select_best, final full-data objective.
+namespace detail {
+inline ClusteringResult run_ds(hpcg_dataset* ds, std::size_t rows, std::size_t n, const EngineConfig& cfg_in);
+}
 inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
+    gpu::DeviceMatrix dm(X.values.data(), X.rows, X.cols);
+    return detail::run_ds(dm.ds, X.rows, X.cols, cfg_in);
+}
+// device-resident X (additive overload): no upload
+inline ClusteringResult run(const DeviceDataset& X, const EngineConfig& cfg_in) {
+    return detail::run_ds(X.handle(), X.rows, X.cols, cfg_in);
+}
+inline ClusteringResult detail::run_ds(hpcg_dataset* ds, std::size_t rows, std::size_t n, const EngineConfig& cfg_in) {
     EngineConfig cfg = cfg_in;
     if (cfg.strategy.kind == StrategyKind::inner) cfg.n_workers = 1;
-    cfg.validate(X.rows);
-    const std::size_t W = cfg.n_workers, k = cfg.k, n = X.cols;
+    cfg.validate(rows);
+    const std::size_t W = cfg.n_workers, k = cfg.k;
     hpcg_engine_cfg ec{};
     ec.k = (int64_t)k;
     ec.sample_size = (int64_t)cfg.sample_size;
@@ -658,16 +805,15 @@ inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
     ec.compute_full_objective = cfg.compute_full_objective ? 1 : 0;
     ec.compute_assignment = cfg.compute_assignment ? 1 : 0;
     ec.rng_mode = cfg.rng_mode == RngMode::reference ? HPCG_RNG_REFERENCE : HPCG_RNG_PHILOX;
-    gpu::DeviceMatrix dm(X.values.data(), X.rows, n);
     hpcg_engine* e = nullptr;
-    gpu::check(hpcg_engine_create(gpu::context(), dm.ds, &ec, &e));
+    gpu::check(hpcg_engine_create(gpu::context(), ds, &ec, &e));
     std::unique_ptr<hpcg_engine, int (*)(hpcg_engine*)> guard(e, hpcg_engine_destroy);
     gpu::check(hpcg_engine_run(e));
     const std::size_t R = (std::size_t)std::max<std::int64_t>(1, hpcg_engine_round_index(e));
     hpcg_run_out o{};
     ClusteringResult res;
     res.centroids = CentroidSet(k, n);
-    std::vector<std::int32_t> labels(cfg.compute_assignment ? X.rows : 0);
+    std::vector<std::int32_t> labels(cfg.compute_assignment ? rows : 0);
     std::vector<double> wobj(W), traces(W * R * 2);
     std::vector<std::int64_t> tlen(W);
     gpu::check(hpcg_engine_finish(e, &o, res.centroids.centers.data(), res.centroids.degenerate.data(),
@@ -708,6 +854,149 @@ inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in) {
         ws.t_w = o.last_timestamp;  // the clock read after the worker's last step (engine.hpp:250)
         for (std::int64_t t = 0; t < tlen[w]; ++t)
             ws.update_trace.push_back({traces[(w * R + (std::size_t)t) * 2], traces[(w * R + (std::size_t)t) * 2 + 1]});
+    }
+    return res;
+}
+
+// The same run over several GPUs of this node (additive overload): X is row-sharded
+// over `devices` (chunk_range, parallel.hpp:106-112), every rank samples over ALL rows through the
+// peer-mapped shards (engine.hpp:165-177), the workers are split contiguously over the ranks, and each
+// round publishes over every rank's workers through the library's NCCL exchange -- so the result
+// equals run(X, cfg) on one GPU (centroids, n_d, best worker, publications; f(C,X) is a sum of shard
+// partials). One host thread per device drives its rank.
+inline ClusteringResult run(const Dataset& X, const EngineConfig& cfg_in, const std::vector<int>& devices) {
+    EngineConfig cfg = cfg_in;
+    if (cfg.strategy.kind == StrategyKind::inner) cfg.n_workers = 1;
+    cfg.validate(X.rows);
+    const std::size_t G = std::min<std::size_t>(devices.size(), cfg.n_workers);
+    require(G >= 1, "run: need at least one device");
+    if (G == 1 && devices.front() == 0) return run(X, cfg);
+    const std::size_t W = cfg.n_workers, k = cfg.k, n = X.cols;
+    unsigned char uid[128] = {};
+    if (G > 1) gpu::check(hpcg_comm_unique_id(uid));
+    std::vector<const void*> shard_ptr(G);
+    std::vector<std::int64_t> shard_rows(G);
+    std::vector<ClusteringResult> part(G);
+    std::vector<std::size_t> w_lo(G), w_hi(G);
+    std::vector<std::exception_ptr> errs(G);
+    std::barrier sync((std::ptrdiff_t)G);
+    auto rank_main = [&](std::size_t g) {
+        hpcg_ctx* ctx = nullptr;
+        hpcg_dataset *mine = nullptr, *all = nullptr;
+        hpcg_engine* e = nullptr;
+        bool arrived = false;
+        try {
+            gpu::check(hpcg_ctx_create(devices[g], &ctx));
+            if (G > 1) gpu::check(hpcg_ctx_attach_comm(ctx, (int32_t)G, (int32_t)g, uid));
+            const std::size_t base = X.rows / G, extra = X.rows % G;
+            const std::size_t r0 = g * base + std::min(g, extra), r1 = r0 + base + (g < extra ? 1 : 0);
+            gpu::check(hpcg_dataset_upload(ctx, X.values.data() + r0 * n, HPCG_F64, (int64_t)(r1 - r0), (int64_t)n, &mine));
+            shard_ptr[g] = hpcg_dataset_device_ptr(mine);
+            shard_rows[g] = (std::int64_t)(r1 - r0);
+            sync.arrive_and_wait();  // every shard uploaded
+            arrived = true;
+            gpu::check(hpcg_dataset_wrap_sharded(ctx, shard_ptr.data(), shard_rows.data(), (int32_t)G, HPCG_F64,
+                                                 (int64_t)n, &all));
+            const std::size_t wb = W / G, wx = W % G;
+            w_lo[g] = g * wb + std::min(g, wx);
+            w_hi[g] = w_lo[g] + wb + (g < wx ? 1 : 0);
+            hpcg_engine_cfg ec{};
+            ec.k = (int64_t)k;
+            ec.sample_size = (int64_t)cfg.sample_size;
+            ec.n_workers = (int64_t)(w_hi[g] - w_lo[g]);
+            ec.max_samples = cfg.max_samples ? (int64_t)*cfg.max_samples : 0;
+            ec.time_limit = cfg.deterministic_mode() ? 0.0 : cfg.time_limit;
+            ec.strategy = (int32_t)cfg.strategy.kind;
+            ec.phase_t1 = cfg.strategy.phase_t1;
+            ec.phase_t2 = cfg.strategy.phase_t2;
+            ec.master_seed = cfg.master_seed;
+            ec.candidates = (int64_t)cfg.seed.candidates_per_center;
+            ec.max_iters = (int64_t)cfg.lloyd.max_iters;
+            ec.rel_tol = cfg.lloyd.rel_tol;
+            ec.compute_full_objective = cfg.compute_full_objective ? 1 : 0;
+            ec.compute_assignment = cfg.compute_assignment ? 1 : 0;
+            ec.rng_mode = cfg.rng_mode == RngMode::reference ? HPCG_RNG_REFERENCE : HPCG_RNG_PHILOX;
+            ec.worker_base = (int32_t)w_lo[g];
+            gpu::check(hpcg_engine_create(ctx, all, &ec, &e));
+            if (G > 1) gpu::check(hpcg_engine_set_exchange(e, (int32_t)G, (int32_t)g, nullptr, nullptr));
+            gpu::check(hpcg_engine_run(e));
+            const std::size_t R = (std::size_t)std::max<std::int64_t>(1, hpcg_engine_round_index(e));
+            const std::size_t Wg = w_hi[g] - w_lo[g];
+            hpcg_run_out o{};
+            ClusteringResult& res = part[g];
+            res.centroids = CentroidSet(k, n);
+            std::vector<std::int32_t> labels(cfg.compute_assignment ? (std::size_t)shard_rows[g] : 0);
+            std::vector<double> wobj(Wg), traces(Wg * R * 2);
+            std::vector<std::int64_t> tlen(Wg);
+            gpu::check(hpcg_engine_finish(e, &o, res.centroids.centers.data(), res.centroids.degenerate.data(),
+                                          cfg.compute_assignment ? labels.data() : nullptr, nullptr, 0, wobj.data(),
+                                          traces.data(), (int64_t)R, tlen.data()));
+            if (g == 0) {
+                std::vector<double> pubs((std::size_t)std::max<std::int64_t>(o.n_publications, 1) * 4);
+                gpu::check(hpcg_engine_publications(e, pubs.data(), o.n_publications, nullptr));
+                for (std::int64_t i = 0; i < o.n_publications; ++i)
+                    res.publications.push_back(
+                        {(std::int64_t)pubs[4 * i], (int)pubs[4 * i + 1], pubs[4 * i + 2], pubs[4 * i + 3]});
+            }
+            std::vector<double> incC(Wg * k * n);
+            std::vector<std::uint8_t> incF(Wg * k);
+            gpu::check(hpcg_engine_worker_incumbents(e, incC.data(), incF.data(), nullptr));
+            if (o.has_full_objective) res.full_objective = o.full_objective;
+            if (cfg.compute_assignment) {
+                Assignment a;
+                a.labels = std::move(labels);
+                res.assignment = std::move(a);
+            }
+            res.best_worker = o.best_worker;
+            res.best_sample_objective = o.best_sample_objective;
+            res.clustering_time = o.clustering_time;
+            res.clustering_time_first_finisher = o.clustering_time_first_finisher;
+            res.wall_seconds = o.wall_seconds;
+            res.total_samples = (std::size_t)o.total_samples;
+            res.distance_evals = o.distance_evals;
+            res.per_worker.resize(Wg);
+            for (std::size_t w = 0; w < Wg; ++w) {
+                WorkerState& ws = res.per_worker[w];
+                ws.worker_id = (int)(w_lo[g] + w);
+                ws.incumbent = CentroidSet(k, n);
+                std::copy_n(incC.data() + w * k * n, k * n, ws.incumbent.centers.data());
+                std::copy_n(incF.data() + w * k, k, ws.incumbent.degenerate.data());
+                ws.incumbent_objective = wobj[w];
+                ws.samples_processed = R;
+                ws.t_w = o.last_timestamp;
+                for (std::int64_t t = 0; t < tlen[w]; ++t)
+                    ws.update_trace.push_back(
+                        {traces[(w * R + (std::size_t)t) * 2], traces[(w * R + (std::size_t)t) * 2 + 1]});
+            }
+        } catch (...) {
+            errs[g] = std::current_exception();
+        }
+        if (e) hpcg_engine_destroy(e);
+        if (ctx) hpcg_ctx_synchronize(ctx);
+        if (arrived)
+            sync.arrive_and_wait();  // no rank frees its shard while a peer may still read it
+        else
+            sync.arrive_and_drop();  // failed before its shard was published: leave both phases
+        if (all) hpcg_dataset_destroy(all);
+        if (mine) hpcg_dataset_destroy(mine);
+        if (ctx) hpcg_ctx_destroy(ctx);
+    };
+    std::vector<std::thread> th;
+    for (std::size_t g = 0; g < G; ++g) th.emplace_back(rank_main, g);
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    // every rank holds the global fields; the per-worker states and labels are per rank
+    ClusteringResult res = std::move(part[0]);
+    for (std::size_t g = 1; g < G; ++g) {
+        for (auto& ws : part[g].per_worker) res.per_worker.push_back(std::move(ws));
+        if (cfg.compute_assignment && res.assignment && part[g].assignment)
+            res.assignment->labels.insert(res.assignment->labels.end(), part[g].assignment->labels.begin(),
+                                          part[g].assignment->labels.end());
+    }
+    if (cfg.compute_assignment && res.assignment) {
+        res.assignment->counts.assign(k, 0);
+        for (auto l : res.assignment->labels) ++res.assignment->counts[(std::size_t)l];
     }
     return res;
 }

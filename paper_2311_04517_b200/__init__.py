@@ -8,7 +8,7 @@ from .api import (Assignment, ClusteringResult, Context, DeviceDataset, DistCoun
                   EngineConfig, LloydConfig, LloydOutcome, RngStream, SeedConfig, assign_nearest,
                   assign_valid_subset, default_context, draw_sample, final_assignment, gen_mixture, kmeans,
                   ipc_close, ipc_export, ipc_open, kmeanspp_seed, mssc_objective, philox_sample_indices,
-                  philox_seed_draws,
+                  philox_seed_draws, comm_unique_id, allgather_callback, gloo_allgather,
                   reference_draw_indices, reinit_degenerate, run, select_best,
                   worker_step_batched)
 

@@ -24,7 +24,8 @@ EXPORTS = (
     "hpcg_run", "hpcg_gen_mixture", "hpcg_ctx_enable_timing", "hpcg_ctx_kernel_times", "hpcg_probe_fma_peak",
     "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
     "hpcg_engine_publications", "hpcg_sample_gather_dev", "hpcg_philox_seed_draws", "hpcg_engine_round_outcome",
-    "hpcg_engine_philox_key",
+    "hpcg_engine_philox_key", "hpcg_comm_unique_id", "hpcg_ctx_attach_comm", "hpcg_ctx_comm_info",
+    "hpcg_engine_set_exchange", "hpcg_ctx_upload_bytes",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -94,6 +95,10 @@ class RunOut(C.Structure):
                 ("last_timestamp", C.c_double)]
 
 
+# host all-gather callback of a multi-rank engine (include/hpcg.h hpcg_allgather_fn)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(f"{LIB_PATH} is not built (run __graft_entry__.build()); there is no CPU fallback")
@@ -107,6 +112,7 @@ def _load():
         "hpcg_ctx_set_stream": (C.c_int, [P, P]),
         "hpcg_ctx_synchronize": (C.c_int, [P]),
         "hpcg_ctx_launch_count": (I64, [P]),
+        "hpcg_ctx_upload_bytes": (I64, [P]),
         "hpcg_dataset_upload": (C.c_int, [P, P, C.c_int, I64, I64, P]),
         "hpcg_dataset_wrap_sharded": (C.c_int, [P, P, P, C.c_int32, C.c_int, I64, P]),
         "hpcg_ipc_export": (C.c_int, [P, P]),
@@ -147,6 +153,10 @@ def _load():
         "hpcg_philox_seed_draws": (C.c_int, [U64, C.c_uint32, C.c_uint32, I64, I32, I64, I64, P, P]),
         "hpcg_engine_round_outcome": (C.c_int, [P, P, P, P, P, P, P]),
         "hpcg_engine_philox_key": (U64, [P]),
+        "hpcg_comm_unique_id": (C.c_int, [P]),
+        "hpcg_ctx_attach_comm": (C.c_int, [P, I32, I32, P]),
+        "hpcg_ctx_comm_info": (C.c_int, [P, P, P]),
+        "hpcg_engine_set_exchange": (C.c_int, [P, I32, I32, ALLGATHER_FN, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -43,6 +43,11 @@ class Context:
     def synchronize(self):
         check(lib.hpcg_ctx_synchronize(self.h))
 
+    def attach_comm(self, nranks: int, rank: int, uid: bytes):
+        """Collective over the ranks: NCCL communicator for multi-rank engines (one rank per GPU)."""
+        buf = C.create_string_buffer(bytes(uid), 128)
+        check(lib.hpcg_ctx_attach_comm(self.h, nranks, rank, buf))
+
     @property
     def launches(self) -> int:
         return int(lib.hpcg_ctx_launch_count(self.h))
@@ -602,6 +607,15 @@ class Engine:
         self.h = h
         self.W = 1 if cfg.strategy == "inner" else cfg.n_workers
 
+    def set_exchange(self, nranks: int, rank: int, allgather=None):
+        """Make this engine rank `rank` of `nranks` (cooperative / hybrid publication over every
+        rank's workers, select_best and f(C, X) over all ranks; include/hpcg.h multi-GPU). allgather:
+        None -> the context's NCCL communicator; else a callable(bytes) -> bytes returning every
+        rank's bytes concatenated in rank order (the caller's own collective, e.g. gloo)."""
+        fn = _lib.ALLGATHER_FN() if allgather is None else allgather_callback(allgather, nranks)
+        self._xfn = fn  # keep the callback alive as long as the engine
+        check(lib.hpcg_engine_set_exchange(self.h, nranks, rank, fn, None))
+
     def rounds(self, n: int = 1):
         check(lib.hpcg_engine_rounds(self.h, n))
 
@@ -733,6 +747,40 @@ def run(X, cfg: EngineConfig, ctx: Context | None = None) -> ClusteringResult:
     check(lib.hpcg_run(ctx.h, ptr(X), _dtype_code(X), m, n, C.byref(c), C.byref(out), ptr(cent), ptr(flags),
                        ptr(labels), ptr(pubs), pub_cap, ptr(wobj), ptr(traces), tcap, ptr(tlen)))
     return _result(out, cent, flags, labels, pubs, wobj, traces, tlen)
+
+
+def allgather_callback(allgather, nranks: int):
+    """hpcg_allgather_fn over a Python collective: allgather(bytes) -> every rank's bytes in rank order."""
+    def _cb(send, recv, nbytes, user):
+        try:
+            out = allgather(C.string_at(send, nbytes))
+            if len(out) != nbytes * nranks:
+                return 1
+            C.memmove(recv, out, len(out))
+            return 0
+        except Exception:
+            return 1
+    return _lib.ALLGATHER_FN(_cb)
+
+
+def gloo_allgather(group=None):
+    """allgather(bytes) -> bytes over torch.distributed (any backend that gathers CPU uint8 tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    def ag(b: bytes) -> bytes:
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        outs = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(outs, t, group=group)
+        return b"".join(bytes(o.numpy()) for o in outs)
+    return ag
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id (128 bytes) for Context.attach_comm; created on one rank, shared by the caller."""
+    buf = C.create_string_buffer(128)
+    check(lib.hpcg_comm_unique_id(buf))
+    return buf.raw
 
 
 def philox_seed_draws(key: int, round_: int, worker: int, s: int, no_valid: bool, loops: int, candidates: int = 3):

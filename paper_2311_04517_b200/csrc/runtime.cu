@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cuda.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <limits>
 #include <mutex>
 #include <string>
@@ -156,6 +158,39 @@ void sparse_fisher_yates(Mt64& rng, int64_t m, int64_t s, int64_t* out) {
 }
 }  // namespace
 
+// ------------------------------------------------------------ NCCL (loaded at run time)
+// The library links no NCCL: the communicator entry points are resolved from libnccl.so.2 when a
+// multi-rank exchange is first set up, so a process that already loaded torch's NCCL shares it.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return a;
+        }
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_gather && a.error_string;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required entry point";
+        return a;
+    }();
+    return api;
+}
+
 // ============================================================== handles
 struct hpcg_ctx {
     int device = 0;
@@ -163,6 +198,7 @@ struct hpcg_ctx {
     bool own_stream = false;
     std::mutex mu;
     std::atomic<int64_t> launches{0};
+    std::atomic<int64_t> upload_bytes{0};  // host -> device bytes of dataset uploads (hpcg_dataset_upload)
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
     int rec_slot = -1;                     // constant-bank slot of the objective records
     DevBuf rec_scratch;
@@ -178,6 +214,9 @@ struct hpcg_ctx {
     size_t spare_x_bytes = 0;
     void* pin = nullptr;
     size_t pin_bytes = 0;
+    // NCCL communicator of the multi-rank exchange (hpcg_ctx_attach_comm); one rank per GPU
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
 };
 
 namespace {
@@ -462,6 +501,230 @@ __global__ void round_end_kernel(const RoundEndParams p) {
     }
 }
 
+// ---------------------------------------------------------------- multi-rank exchange
+// A round of a multi-rank engine (one rank per GPU, workers [base_r, base_r + W_r) on rank r,
+// bases contiguous in rank order) publishes exactly as ONE engine with all ranks' workers would:
+// every rank packs its round candidates (the objective of each local worker that would publish --
+// accepted in a cooperative round, or a finite incumbent at the hybrid carry-over -- else +inf) and
+// the centroids of its local minimum; the records are all-gathered (NCCL over NVLink, or a caller
+// collective); every rank then replays the reference's publication scan over the global worker
+// order (engine.hpp:391-402: worker-id order, strict < against the shared best) on the device. The
+// scan's last publisher is necessarily its rank's first local minimum, whose centroids travelled
+// in the record, so every rank installs the identical shared best and logs identical publications.
+//   round record (doubles): [W_r, base_r, clock, local argmin | cand[Wmax] | C[k*n] | flags[k]]
+__host__ __device__ inline int64_t xch_round_len(int64_t Wmax, int64_t kn, int64_t k) { return 4 + Wmax + kn + k; }
+
+struct XPackParams {
+    int W, Wmax, k, n, base;
+    int publish, carry;
+    double now;
+    const uint8_t* accepted;
+    const double* inc_obj;
+    const double* inc_c;
+    const uint8_t* inc_f;
+    double* rec;
+};
+
+__global__ void xch_pack_round_kernel(const XPackParams p) {
+    __shared__ double so[32];
+    __shared__ int si[32];
+    __shared__ int s_best;
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    double bo = inf;
+    int bi = -1;
+    for (int w = threadIdx.x; w < p.Wmax; w += blockDim.x) {
+        double c = inf;
+        if (w < p.W) {
+            const double f = p.inc_obj[w];
+            const bool cand = (p.publish && p.accepted[w]) || (p.carry && isfinite(f));
+            c = cand ? f : inf;
+        }
+        p.rec[4 + w] = c;
+        if (c < bo) {  // per-thread strided scan: ids increase, strict < keeps the first
+            bo = c;
+            bi = w;
+        }
+    }
+    auto better = [](double o, int i, double bo_, int bi_) {
+        return i >= 0 && (bi_ < 0 || o < bo_ || (o == bo_ && i < bi_));
+    };
+    for (int off = 16; off > 0; off >>= 1) {
+        const double oo = __shfl_down_sync(0xffffffffu, bo, off);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (better(oo, oi, bo, bi)) {
+            bo = oo;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        so[threadIdx.x >> 5] = bo;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = inf;
+        int bw = -1;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            if (better(so[w], si[w], b, bw)) {
+                b = so[w];
+                bw = si[w];
+            }
+        s_best = bw;
+        p.rec[0] = (double)p.W;
+        p.rec[1] = (double)p.base;
+        p.rec[2] = p.now;
+        p.rec[3] = (double)bw;
+    }
+    __syncthreads();
+    const int bw = s_best;
+    const int64_t kn = (int64_t)p.k * p.n;
+    double* rc = p.rec + 4 + p.Wmax;
+    for (int64_t e = threadIdx.x; e < kn; e += blockDim.x) rc[e] = bw >= 0 ? p.inc_c[(int64_t)bw * kn + e] : 0.0;
+    for (int j = threadIdx.x; j < p.k; j += blockDim.x) rc[kn + j] = bw >= 0 ? (double)p.inc_f[(int64_t)bw * p.k + j] : 1.0;
+}
+
+struct XMergeParams {
+    int G, Wmax, k, n;
+    int ts_from_clock;  // wall clock: the publication timestamp is the latest clock among the ranks
+    double ts;
+    const double* recv;  // [G][round record]
+    int64_t* sh_version;
+    double* sh_obj;
+    int32_t* sh_worker;
+    double* sh_c;
+    uint8_t* sh_f;
+    double* pub_log;
+    int64_t* pub_count;
+    int64_t pub_cap;
+    int32_t* err;  // set when the scan's winner is not its rank's packed minimum (cannot happen)
+};
+
+__global__ void xch_merge_round_kernel(const XMergeParams p) {
+    __shared__ int s_wr, s_ww;
+    const int lane = threadIdx.x & 31;
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    const int64_t L = xch_round_len(p.Wmax, (int64_t)p.k * p.n, p.k);
+    if (threadIdx.x < 32) {
+        double ts = p.ts;
+        if (p.ts_from_clock) {
+            ts = 0.0;
+            for (int r = 0; r < p.G; ++r) ts = fmax(ts, p.recv[r * L + 2]);
+        }
+        double best = *p.sh_obj;
+        int64_t ver = *p.sh_version, cnt = *p.pub_count;
+        int wr = -1, ww = -1;
+        for (int r = 0; r < p.G; ++r) {
+            const double* rec = p.recv + r * L;
+            const int Wr = (int)rec[0];
+            const int64_t base = (int64_t)rec[1];
+            for (int w0 = 0; w0 < Wr; w0 += 32) {  // the round_end_kernel scan, in global worker order
+                const int w = w0 + lane;
+                const double c = w < Wr ? rec[4 + w] : inf;
+                double incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl = fmin(incl, y);
+                }
+                double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+                if (lane == 0) excl = inf;
+                const bool pub = c < fmin(best, excl);
+                const unsigned mask = __ballot_sync(0xffffffffu, pub);
+                const int rank = __popc(mask & ((1u << lane) - 1u));
+                if (pub && cnt + rank < p.pub_cap) {
+                    const int64_t at = cnt + rank;
+                    p.pub_log[at * 4 + 0] = (double)(ver + rank + 1);
+                    p.pub_log[at * 4 + 1] = (double)(base + w);
+                    p.pub_log[at * 4 + 2] = c;
+                    p.pub_log[at * 4 + 3] = ts;
+                }
+                if (mask) {
+                    const int last = 31 - __clz(mask);
+                    wr = r;
+                    ww = w0 + last;
+                    best = __shfl_sync(0xffffffffu, c, last);
+                    ver += __popc(mask);
+                    cnt += __popc(mask);
+                }
+            }
+        }
+        if (lane == 0) {
+            *p.pub_count = cnt;
+            if (wr >= 0) {
+                const double* rec = p.recv + (int64_t)wr * L;
+                *p.sh_obj = best;
+                *p.sh_version = ver;
+                *p.sh_worker = (int32_t)((int64_t)rec[1] + ww);
+                if ((int)rec[3] != ww && p.err) *p.err = 1;
+            }
+            s_wr = wr;
+            s_ww = ww;
+        }
+    }
+    __syncthreads();
+    if (s_wr >= 0) {
+        const double* rc = p.recv + (int64_t)s_wr * L + 4 + p.Wmax;
+        const int64_t kn = (int64_t)p.k * p.n;
+        for (int64_t e = threadIdx.x; e < kn; e += blockDim.x) p.sh_c[e] = rc[e];
+        for (int j = threadIdx.x; j < p.k; j += blockDim.x) p.sh_f[j] = (uint8_t)rc[kn + j];
+    }
+}
+
+// select_best across ranks (engine.hpp:180-194: lowest objective, ties to the lowest global worker
+// id; an all-infinite field is NoSolutionError): each rank packs its local select_best
+// [objective, global id, C, flags]; every rank picks the same global winner and compacts its valid
+// centres (engine.hpp:211-229). out: sel = {winner found ? 1 : -1, k_valid}; gobj / ggid.
+__global__ void xch_pack_select_kernel(const int32_t* sel, const double* inc_obj, const double* best_c,
+                                       const uint8_t* best_f, int k, int n, int base, double* rec) {
+    const int b = sel[0];
+    const int64_t kn = (int64_t)k * n;
+    if (threadIdx.x == 0) {
+        rec[0] = b >= 0 ? inc_obj[b] : __longlong_as_double(0x7ff0000000000000LL);
+        rec[1] = b >= 0 ? (double)(base + b) : -1.0;
+    }
+    for (int64_t e = threadIdx.x; e < kn; e += blockDim.x) rec[2 + e] = b >= 0 ? best_c[e] : 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) rec[2 + kn + j] = b >= 0 ? (double)best_f[j] : 1.0;
+}
+
+__global__ void xch_merge_select_kernel(const double* recv, int G, int k, int n, int32_t* sel, double* best_c,
+                                        uint8_t* best_f, double* cv, int32_t* remap, double* gobj, int64_t* ggid) {
+    __shared__ int s_r, s_kv;
+    const int64_t kn = (int64_t)k * n, L = 2 + kn + k;
+    if (threadIdx.x == 0) {
+        int br = -1;
+        double bo = 0.0, bg = 0.0;
+        for (int r = 0; r < G; ++r) {
+            const double o = recv[r * L], g = recv[r * L + 1];
+            if (g < 0.0 || !(o < __longlong_as_double(0x7ff0000000000000LL))) continue;
+            if (br < 0 || o < bo || (o == bo && g < bg)) {
+                br = r;
+                bo = o;
+                bg = g;
+            }
+        }
+        int kv = 0;
+        if (br >= 0)
+            for (int j = 0; j < k; ++j)
+                if (recv[br * L + 2 + kn + j] == 0.0) remap[kv++] = j;
+        s_r = br;
+        s_kv = kv;
+        sel[0] = br >= 0 ? 1 : -1;
+        sel[1] = kv;
+        *gobj = bo;
+        *ggid = (int64_t)bg;
+    }
+    __syncthreads();
+    const int br = s_r, kv = s_kv;
+    if (br < 0) return;
+    const double* rc = recv + br * L + 2;
+    for (int64_t e = threadIdx.x; e < kn; e += blockDim.x) best_c[e] = rc[e];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) best_f[j] = (uint8_t)rc[kn + j];
+    for (int64_t e = threadIdx.x; e < (int64_t)kv * n; e += blockDim.x) {
+        const int64_t r = e / n;
+        cv[e] = rc[(int64_t)remap[r] * n + (e - r * n)];
+    }
+}
+
 __global__ void fill_f64_kernel(double* p, int64_t n, double v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -635,6 +898,7 @@ int hpcg_ctx_destroy(hpcg_ctx* ctx) {
         cudaDeviceSynchronize();  // no launch of this context may still read its record slot
         release_rec_slot(ctx->rec_slot);
     }
+    if (ctx->comm && nccl_api().ok) nccl_api().comm_destroy(ctx->comm);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->spare_x) cudaFree(ctx->spare_x);
     if (ctx->pin) cudaFreeHost(ctx->pin);
@@ -658,6 +922,7 @@ int hpcg_ctx_synchronize(hpcg_ctx* ctx) {
 }
 
 int64_t hpcg_ctx_launch_count(const hpcg_ctx* ctx) { return ctx->launches.load(); }
+int64_t hpcg_ctx_upload_bytes(const hpcg_ctx* ctx) { return ctx->upload_bytes.load(); }
 
 int hpcg_ctx_enable_timing(hpcg_ctx* ctx, int enable) {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -734,6 +999,7 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
         have = bytes;
     }
     cudaError_t e = cudaMemcpyAsync(d, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    ctx->upload_bytes += (int64_t)bytes;
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
         cudaFree(d);
@@ -778,6 +1044,22 @@ int hpcg_dataset_wrap_sharded(hpcg_ctx* ctx, const void* const* shard_dev, const
     for (int i = 0; i < nshards; ++i) {
         if (shard_rows[i] < 1 || !shard_dev[i]) return fail(HPCG_EINVAL, "Dataset: empty shard");
         m += shard_rows[i];
+    }
+    // shards resident on other devices of this process: the gathers read them over NVLink (peer
+    // access; IPC-opened shards of other processes are already mapped)
+    cudaSetDevice(ctx->device);
+    for (int i = 0; i < nshards; ++i) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, shard_dev[i]) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (at.type == cudaMemoryTypeDevice && at.device != ctx->device) {
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(at.device, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(HPCG_ECUDA, std::string("peer access to a shard's device: ") + cudaGetErrorString(pe));
+            cudaGetLastError();
+        }
     }
     auto* ds = new hpcg_dataset;
     ds->ctx = ctx;
@@ -1219,6 +1501,15 @@ struct hpcg_engine {
     int64_t pub_ub = 0;    // upper bound of the entries written so far (<= W per publishing launch)
     int64_t log_rounds = 0;  // rounds the per-round accept/objective logs can hold (grown on demand)
     bool entered_coop = false;  // wall clock, hybrid: the phase-1 incumbents were carried over
+    // multi-rank exchange (hpcg_engine_set_exchange): nranks, this rank, the collective, the
+    // workers of every rank (global ids contiguous in rank order) and the exchange buffers
+    int xr = 1, xrank = 0;
+    hpcg_allgather_fn xfn = nullptr;
+    void* xuser = nullptr;
+    int64_t xWmax = 0, xWtot = 0;
+    DevBuf xsend, xrecv, xerr;
+    std::vector<unsigned char> xhost;  // host staging of a caller collective
+    double common_now = 0.0;           // wall clock, multi-rank: the latest clock of the last exchange
     // reference-RNG replay state
     std::vector<Mt64> streams;
     std::vector<int64_t> h_idx, h_fr;
@@ -1296,6 +1587,73 @@ int launch_round_end(hpcg_engine* e, const RoundEndParams& q) {
     return HPCG_OK;
 }
 
+// all-gather of `bytes` per rank from e->xsend into e->xrecv (rank order): NCCL on the context's
+// stream, or the caller's host collective (staged through host memory)
+int engine_allgather(hpcg_engine* e, size_t bytes) {
+    hpcg_ctx* ctx = e->ctx;
+    if (e->xfn) {
+        e->xhost.resize(bytes * (size_t)(e->xr + 1));
+        unsigned char* hs = e->xhost.data();
+        unsigned char* hr = hs + bytes;
+        CU(cudaMemcpyAsync(hs, e->xsend.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (e->xfn(hs, hr, bytes, e->xuser) != 0) return fail(HPCG_ENCCL, "exchange: the caller's all-gather failed");
+        CU(cudaMemcpyAsync(e->xrecv.p, hr, bytes * (size_t)e->xr, cudaMemcpyHostToDevice, ctx->stream));
+        return HPCG_OK;
+    }
+    const NcclApi& a = nccl_api();
+    if (!a.ok || !ctx->comm) return fail(HPCG_ENCCL, "exchange: no NCCL communicator attached to the context");
+    const ncclResult_t r = a.all_gather(e->xsend.p, e->xrecv.p, bytes, ncclChar, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(HPCG_ENCCL, std::string("ncclAllGather: ") + a.error_string(r));
+    return HPCG_OK;
+}
+
+// Multi-rank publication of one round (or of the hybrid carry-over): pack -> all-gather -> the
+// global publication scan on every rank (xch_*_round_kernel). ts < 0: the latest rank clock.
+int engine_publish_global(hpcg_engine* e, int publish, int carry, double clock, double ts) {
+    hpcg_ctx* ctx = e->ctx;
+    const int64_t kn = e->k * e->n, L = xch_round_len(e->xWmax, kn, e->k);
+    XPackParams pk;
+    pk.W = (int)e->W;
+    pk.Wmax = (int)e->xWmax;
+    pk.k = (int)e->k;
+    pk.n = (int)e->n;
+    pk.base = e->cfg.worker_base;
+    pk.publish = publish;
+    pk.carry = carry;
+    pk.now = clock;
+    pk.accepted = e->acc.as<uint8_t>();
+    pk.inc_obj = e->inc_obj.as<double>();
+    pk.inc_c = e->inc_c.as<double>();
+    pk.inc_f = e->inc_f.as<uint8_t>();
+    pk.rec = e->xsend.as<double>();
+    xch_pack_round_kernel<<<1, 256, 0, ctx->stream>>>(pk);
+    CU(cudaGetLastError());
+    if (int rc = engine_allgather(e, (size_t)L * 8)) return rc;
+    XMergeParams mp;
+    mp.G = e->xr;
+    mp.Wmax = (int)e->xWmax;
+    mp.k = (int)e->k;
+    mp.n = (int)e->n;
+    mp.ts_from_clock = ts < 0.0 ? 1 : 0;
+    mp.ts = ts;
+    mp.recv = e->xrecv.as<double>();
+    mp.sh_version = e->sh_ver.as<int64_t>();
+    mp.sh_obj = e->sh_obj.as<double>();
+    mp.sh_worker = e->sh_worker.as<int32_t>();
+    mp.sh_c = e->sh_c.as<double>();
+    mp.sh_f = e->sh_f.as<uint8_t>();
+    mp.pub_log = e->pub_log.as<double>();
+    mp.pub_count = e->pub_count.as<int64_t>();
+    mp.pub_cap = e->pub_cap;
+    mp.err = e->xerr.as<int32_t>();
+    xch_merge_round_kernel<<<1, 256, 0, ctx->stream>>>(mp);
+    CU(cudaGetLastError());
+    ctx->launches += 2;
+    e->pub_ub += e->xWtot;
+    return HPCG_OK;
+}
+
 // One round of the schedule. `now`: seconds since the run start read ONCE by the caller (wall
 // clock: the stop test, the phase test and the hybrid carry-over all use this one reading, as a
 // reference worker does at the top of its loop, engine.hpp:353-364); ignored in lockstep.
@@ -1305,18 +1663,23 @@ int engine_round(hpcg_engine* e, double now) {
     // phase test on the schedule's clock: samples processed (lockstep) or seconds (wall clock)
     const bool coop = phase_cooperative(e->cfg.strategy, e->cfg.phase_t1, e->wall ? now : (double)r);
     const bool hybrid = e->cfg.strategy == HPCG_HYBRID;
-    if (int rc = engine_reserve(e, 2 * W)) return rc;
+    const bool multi = e->xr > 1;
+    if (int rc = engine_reserve(e, 2 * std::max(W, e->xWtot))) return rc;
     if (e->wall && hybrid && coop && !e->entered_coop) {
         // engine.hpp:359-364: entering the cooperative phase publishes each worker's finite
         // incumbent (worker-id order, strict <) before the step draws its init from the snapshot
         e->entered_coop = true;
-        RoundEndParams q = round_end_params(e);
-        q.log = 0;
-        q.publish = 0;
-        q.carry = 1;
-        q.ts = now;
-        if (int rc = launch_round_end(e, q)) return rc;
-        e->pub_ub += W;
+        if (multi) {
+            if (int rc = engine_publish_global(e, 0, 1, now, now)) return rc;
+        } else {
+            RoundEndParams q = round_end_params(e);
+            q.log = 0;
+            q.publish = 0;
+            q.carry = 1;
+            q.ts = now;
+            if (int rc = launch_round_end(e, q)) return rc;
+            e->pub_ub += W;
+        }
     }
     const bool reference = e->cfg.rng_mode == HPCG_RNG_REFERENCE;
     const int64_t ncand = e->cfg.candidates;
@@ -1415,18 +1778,35 @@ int engine_round(hpcg_engine* e, double now) {
 
     RoundEndParams q = round_end_params(e);
     q.publish = coop ? 1 : 0;  // round_was_coop (engine.hpp:393)
+    double t_end = 0.0;
     if (e->wall) {  // the round's samples are done at t_end (trace / publication timestamp)
         CU(cudaStreamSynchronize(ctx->stream));
-        const double t_end = e->elapsed();
-        e->t_end.push_back(t_end);
+        t_end = e->elapsed();
         q.ts = t_end;
         q.carry = 0;  // wall clock: carried over at the start of the first cooperative round
     } else {
         q.ts = (double)(r + 1);
         q.carry = (hybrid && (r + 1) == (int64_t)(size_t)e->cfg.phase_t1) ? 1 : 0;  // engine.hpp:386,396
     }
-    if (q.publish || q.carry) e->pub_ub += W;
-    if (int rc = launch_round_end(e, q)) return rc;
+    if (multi) {  // log the round locally, publish over every rank's workers
+        const int pub = q.publish, car = q.carry;
+        q.publish = 0;
+        q.carry = 0;
+        if (int rc = launch_round_end(e, q)) return rc;
+        if (int rc = engine_publish_global(e, pub, car, t_end, e->wall ? -1.0 : q.ts)) return rc;
+        if (e->wall) {  // the common clock of the ranks: the latest end of this round
+            const int64_t L = xch_round_len(e->xWmax, kn, k);
+            std::vector<double> clk((size_t)e->xr);
+            for (int g = 0; g < e->xr; ++g) CU(d2h(&clk[(size_t)g], e->xrecv.as<double>() + g * L + 2, 1, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            t_end = *std::max_element(clk.begin(), clk.end());
+            e->common_now = t_end;
+        }
+    } else {
+        if (q.publish || q.carry) e->pub_ub += W;
+        if (int rc = launch_round_end(e, q)) return rc;
+    }
+    if (e->wall) e->t_end.push_back(t_end);
 
     if (reference) {  // rewind streams of workers whose seeding stopped early (seeding.hpp:87)
         std::vector<int32_t> fl((size_t)W);
@@ -1447,6 +1827,44 @@ int engine_round(hpcg_engine* e, double now) {
 }  // namespace
 
 extern "C" {
+
+int hpcg_comm_unique_id(void* id_out) {
+    const NcclApi& a = nccl_api();
+    if (!a.ok) return fail(HPCG_ENCCL, a.why);
+    ncclUniqueId id;
+    const ncclResult_t r = a.get_unique_id(&id);
+    if (r != ncclSuccess) return fail(HPCG_ENCCL, std::string("ncclGetUniqueId: ") + a.error_string(r));
+    std::memcpy(id_out, &id, sizeof(id));
+    return HPCG_OK;
+}
+
+int hpcg_ctx_attach_comm(hpcg_ctx* ctx, int32_t nranks, int32_t rank, const void* id) {
+    if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(HPCG_EINVAL, "attach_comm: bad rank layout");
+    const NcclApi& a = nccl_api();
+    if (!a.ok) return fail(HPCG_ENCCL, a.why);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (ctx->comm) {
+        a.comm_destroy(ctx->comm);
+        ctx->comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    const ncclResult_t r = a.comm_init_rank(&ctx->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        ctx->comm = nullptr;
+        return fail(HPCG_ENCCL, std::string("ncclCommInitRank: ") + a.error_string(r));
+    }
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return HPCG_OK;
+}
+
+int hpcg_ctx_comm_info(const hpcg_ctx* ctx, int32_t* nranks, int32_t* rank) {
+    if (nranks) *nranks = ctx->comm ? ctx->nranks : 1;
+    if (rank) *rank = ctx->comm ? ctx->rank : 0;
+    return HPCG_OK;
+}
 
 int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_cfg* c, hpcg_engine** out) {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1561,6 +1979,49 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     return HPCG_OK;
 }
 
+int hpcg_engine_set_exchange(hpcg_engine* e, int32_t nranks, int32_t rank, hpcg_allgather_fn fn, void* user) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    hpcg_ctx* ctx = e->ctx;
+    cudaSetDevice(ctx->device);
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HPCG_EINVAL, "set_exchange: bad rank layout");
+    if (e->round > 0) return fail(HPCG_EINVAL, "set_exchange: rounds already run");
+    if (!fn && nranks > 1 && (!ctx->comm || ctx->nranks != nranks || ctx->rank != rank))
+        return fail(HPCG_ENCCL, "set_exchange: no matching NCCL communicator attached to the context");
+    if (e->cfg.strategy == HPCG_INNER && nranks > 1)
+        return fail(HPCG_EUNSUPPORTED, "the inner strategy runs one worker: no multi-rank exchange");
+    e->xr = nranks;
+    e->xrank = rank;
+    e->xfn = fn;
+    e->xuser = user;
+    e->xWmax = e->xWtot = e->W;
+    if (nranks == 1) return HPCG_OK;
+    // every rank's worker count and base; global ids must be contiguous in rank order
+    CU(e->xsend.reserve(16));
+    CU(e->xrecv.reserve((size_t)nranks * 16));
+    const double wb[2] = {(double)e->W, (double)e->cfg.worker_base};
+    CU(cudaMemcpyAsync(e->xsend.p, wb, 16, cudaMemcpyHostToDevice, ctx->stream));
+    if (int rc = engine_allgather(e, 16)) return rc;
+    std::vector<double> all((size_t)(2 * nranks));
+    CU(d2h(all.data(), e->xrecv.as<double>(), all.size(), ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    int64_t expect = 0, wmax = 0;
+    for (int g = 0; g < nranks; ++g) {
+        const int64_t wg = (int64_t)all[(size_t)(2 * g)], bg = (int64_t)all[(size_t)(2 * g + 1)];
+        if (bg != expect) return fail(HPCG_EINVAL, "set_exchange: worker ids must be contiguous in rank order");
+        expect += wg;
+        wmax = std::max(wmax, wg);
+    }
+    e->xWmax = wmax;
+    e->xWtot = expect;
+    const int64_t kn = e->k * e->n;
+    const int64_t L = std::max<int64_t>(xch_round_len(wmax, kn, e->k), 4 + kn + e->k) + 8;
+    CU(e->xsend.reserve((size_t)L * 8));
+    CU(e->xrecv.reserve((size_t)(L * nranks) * 8));
+    CU(e->xerr.reserve(16));
+    CU(cudaMemsetAsync(e->xerr.p, 0, 16, ctx->stream));
+    return HPCG_OK;
+}
+
 int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
@@ -1591,6 +2052,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     CU(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->log_rounds * W), st));
     e->pub_ub = 0;
     e->entered_coop = false;
+    e->common_now = 0.0;
     return HPCG_OK;
 }
 
@@ -1618,7 +2080,8 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
     cudaSetDevice(e->ctx->device);
     for (int64_t i = 0; i < n_rounds; ++i) {
         if (e->round >= e->R) return fail(HPCG_EINVAL, "engine: max_samples rounds already run");
-        if (int rc = engine_round(e, e->wall ? e->elapsed() : 0.0)) return rc;
+        const double now = !e->wall ? 0.0 : e->xr > 1 ? (e->round ? e->common_now : 0.0) : e->elapsed();
+        if (int rc = engine_round(e, now)) return rc;
     }
     return HPCG_OK;
 }
@@ -1629,7 +2092,8 @@ int hpcg_engine_run(hpcg_engine* e) {
     while (e->round < e->R) {
         // run_wall_clock (engine.hpp:353-357): one clock reading per round decides the stop,
         // the phase and the carry-over
-        const double now = e->wall ? e->elapsed() : 0.0;
+        // multi-rank: the ranks' common clock (latest round end) so every rank decides alike
+        const double now = !e->wall ? 0.0 : e->xr > 1 ? (e->round ? e->common_now : 0.0) : e->elapsed();
         if (e->wall && now >= e->cfg.time_limit) break;
         if (int rc = engine_round(e, now)) return rc;
     }
@@ -1669,12 +2133,178 @@ int hpcg_engine_export_best(hpcg_engine* e, double* obj_out, int64_t* worker_out
     return HPCG_OK;
 }
 
+// finish of a multi-rank engine (all ranks call it): local select_best -> all-gather of the
+// rank winners (+ the rank's first worker error) -> the global winner on every rank -> f(C, X) over
+// this rank's rows -> all-gather of the shard partials, n_d and clocks, summed in rank order.
+static int engine_finish_multi(hpcg_engine* e, hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels,
+                               double* worker_obj, double* traces, int64_t trace_cap, int64_t* trace_len) {
+    hpcg_ctx* ctx = e->ctx;
+    cudaStream_t st = ctx->stream;
+    const int64_t W = e->W, k = e->k, n = e->n, kn = k * n, R = e->round, G = e->xr;
+    const bool want_obj = e->cfg.compute_full_objective || e->cfg.compute_assignment;
+    const bool want_labels = e->cfg.compute_assignment && labels;
+    CU(e->scratch_a.reserve((size_t)kn * 8));
+    CU(e->scratch_b.reserve((size_t)k * 4));
+    CU(e->scratch_c.reserve(8));
+    CU(e->fin.reserve(16 + (size_t)kn * 8 + (size_t)k + 8 + 16));
+    int32_t* sel_d = e->fin.as<int32_t>();
+    double* bc_d = reinterpret_cast<double*>(e->fin.as<unsigned char>() + 16);
+    uint8_t* bf_d = e->fin.as<uint8_t>() + 16 + kn * 8;
+    double* gobj_d = reinterpret_cast<double*>(e->fin.as<unsigned char>() + ((16 + kn * 8 + k + 7) & ~7LL));
+    int64_t* ggid_d = reinterpret_cast<int64_t*>(gobj_d + 1);
+    finish_select_kernel<<<1, 256, 0, st>>>(e->inc_obj.as<double>(), e->inc_c.as<double>(), e->inc_f.as<uint8_t>(),
+                                            (int)W, (int)k, (int)n, sel_d, bc_d, bf_d, e->scratch_a.as<double>(),
+                                            e->scratch_b.as<int32_t>());
+    // the rank's first worker error travels with its winner (worker errors are rethrown before
+    // select_best, lowest worker first: engine.hpp:330-331)
+    std::vector<int32_t> errf((size_t)W);
+    CU(d2h(errf.data(), e->err_first.as<int32_t>(), (size_t)W, st));
+    CU(cudaStreamSynchronize(st));
+    double err_code = 0.0, err_gid = -1.0;
+    for (int64_t w = 0; w < W; ++w)
+        if (errf[(size_t)w]) {
+            err_code = errf[(size_t)w];
+            err_gid = (double)(e->cfg.worker_base + w);
+            break;
+        }
+    const int64_t L1 = 4 + kn + k;  // [obj, gid, err, err gid | C | f]
+    double* snd = e->xsend.as<double>();
+    xch_pack_select_kernel<<<1, 256, 0, st>>>(sel_d, e->inc_obj.as<double>(), bc_d, bf_d, (int)k, (int)n,
+                                               e->cfg.worker_base, snd + 2);  // [obj, gid, C, f] at +2
+    // shift: the select record is [err, err gid, obj, gid, C, f]
+    const double eh[2] = {err_code, err_gid};
+    CU(cudaMemcpyAsync(snd, eh, 16, cudaMemcpyHostToDevice, st));
+    CU(cudaGetLastError());
+    if (int rc = engine_allgather(e, (size_t)L1 * 8)) return rc;
+    std::vector<double> errs((size_t)(2 * G));
+    for (int64_t g = 0; g < G; ++g) CU(d2h(&errs[(size_t)(2 * g)], e->xrecv.as<double>() + g * L1, 2, st));
+    CU(cudaStreamSynchronize(st));
+    for (int64_t g = 0; g < G; ++g) {  // rank order = global worker order
+        const int code = (int)errs[(size_t)(2 * g)];
+        if (code == kErrDegenerateInit) return fail(HPCG_EINVAL, "kmeans: degenerate centroid in init");
+        if (code == kErrMonotone) return fail(HPCG_ELOGIC, "kmeans: objective increased between iterations");
+    }
+    // the gathered records without their 2-double error header: repack contiguously for the merge
+    CU(e->xerr.reserve(std::max<size_t>((size_t)(G * (L1 - 2)) * 8, 16)));
+    for (int64_t g = 0; g < G; ++g)
+        CU(cudaMemcpyAsync(e->xerr.as<double>() + g * (L1 - 2), e->xrecv.as<double>() + g * L1 + 2,
+                           (size_t)(L1 - 2) * 8, cudaMemcpyDeviceToDevice, st));
+    xch_merge_select_kernel<<<1, 256, 0, st>>>(e->xerr.as<double>(), (int)G, (int)k, (int)n, sel_d, bc_d, bf_d,
+                                                e->scratch_a.as<double>(), e->scratch_b.as<int32_t>(), gobj_d, ggid_d);
+    CU(cudaGetLastError());
+    ctx->launches += 3;
+    int32_t hsel[2];
+    double gobj = 0.0;
+    int64_t ggid = -1;
+    CU(d2h(hsel, sel_d, 2, st));
+    CU(d2h(&gobj, gobj_d, 1, st));
+    CU(d2h(&ggid, ggid_d, 1, st));
+    CU(cudaStreamSynchronize(st));
+    if (hsel[0] < 0) return fail(HPCG_ENOSOL, "no solution produced: every worker incumbent is infinite");
+    const int kv = hsel[1];
+    // this rank's rows: shard `rank` of a dataset sharded over the ranks (global sampling), else all of it
+    hpcg_dataset local;
+    const hpcg_dataset* dsl = e->ds;
+    if (e->ds->nshards == e->xr) {
+        local.ctx = ctx;
+        local.X = e->ds->shard_ptr[e->xrank];
+        local.shard_ptr[0] = local.X;
+        local.m = e->ds->shard_end[e->xrank] - (e->xrank ? e->ds->shard_end[e->xrank - 1] : 0);
+        local.shard_end[0] = local.m;
+        local.n = e->ds->n;
+        local.dtype = e->ds->dtype;
+        dsl = &local;
+    }
+    DevBuf lab;
+    double part = 0.0;
+    if (want_obj) {
+        if (kv == 0) return fail(HPCG_EINVAL, "assignment: every centroid is degenerate");
+        if (want_labels) CU(lab.reserve((size_t)dsl->m * 4));
+        if (int rc = run_assign(ctx, dsl, e->scratch_a.as<double>(), e->scratch_b.as<int32_t>(), kv,
+                                want_labels ? lab.as<int32_t>() : nullptr, nullptr, e->scratch_c.as<double>(), e->blocks))
+            return rc;
+        CU(d2h(&part, e->scratch_c.as<double>(), 1, st));
+    }
+    // local per-worker outputs (traces, objectives) and this rank's share of the totals
+    const int64_t Rw = std::max<int64_t>(R, 1) * W;
+    std::vector<uint8_t> lacc((size_t)Rw);
+    std::vector<double> lobj((size_t)Rw), hobj((size_t)W);
+    unsigned long long ndt = 0;
+    int64_t npub = 0;
+    if (R > 0) {
+        CU(d2h(lacc.data(), e->log_acc.as<uint8_t>(), (size_t)(R * W), st));
+        CU(d2h(lobj.data(), e->log_obj.as<double>(), (size_t)(R * W), st));
+    }
+    CU(d2h(hobj.data(), e->inc_obj.as<double>(), (size_t)W, st));
+    CU(d2h(&ndt, e->nd_total.as<unsigned long long>(), 1, st));
+    CU(d2h(&npub, e->pub_count.as<int64_t>(), 1, st));
+    if (centroids) CU(d2h(centroids, bc_d, (size_t)kn, st));
+    if (flags) CU(d2h(flags, bf_d, (size_t)k, st));
+    CU(cudaStreamSynchronize(st));
+    auto ts_of = [&](int64_t r) { return e->wall && r < (int64_t)e->t_end.size() ? e->t_end[(size_t)r] : (double)(r + 1); };
+    double min_last = kInf, last0 = -1.0;
+    for (int64_t w = 0; w < W; ++w) {
+        int64_t cnt = 0;
+        double last = -1.0;
+        for (int64_t r = 0; r < R; ++r) {
+            if (!lacc[(size_t)(r * W + w)]) continue;
+            if (traces && cnt < trace_cap) {
+                traces[(w * trace_cap + cnt) * 2 + 0] = ts_of(r);
+                traces[(w * trace_cap + cnt) * 2 + 1] = lobj[(size_t)(r * W + w)];
+            }
+            last = ts_of(r);
+            ++cnt;
+        }
+        if (trace_len) trace_len[w] = cnt;
+        if (cnt > 0) min_last = std::min(min_last, last);
+        if (w == 0) last0 = last;
+    }
+    const double nd_local = (double)ndt + (want_obj ? (double)dsl->m * kv : 0.0);
+    const double tail[6] = {part, nd_local, min_last, last0, (double)(W * R), 0.0};
+    CU(cudaMemcpyAsync(e->xsend.p, tail, sizeof(tail), cudaMemcpyHostToDevice, st));
+    if (int rc = engine_allgather(e, sizeof(tail))) return rc;
+    std::vector<double> tails((size_t)(6 * G));
+    CU(d2h(tails.data(), e->xrecv.as<double>(), (size_t)(6 * G), st));
+    if (want_labels) CU(d2h(labels, lab.as<int32_t>(), (size_t)dsl->m, st));
+    CU(cudaStreamSynchronize(st));
+    hpcg_run_out o = {};
+    double f = 0.0, nd = 0.0, ml = kInf, tot = 0.0;
+    for (int64_t g = 0; g < G; ++g) {  // rank order: the sum is reproducible
+        f += tails[(size_t)(6 * g)];
+        nd += tails[(size_t)(6 * g + 1)];
+        ml = std::min(ml, tails[(size_t)(6 * g + 2)]);
+        tot += tails[(size_t)(6 * g + 4)];
+    }
+    o.best_worker = (int32_t)ggid;
+    o.best_sample_objective = gobj;
+    o.clustering_time = ml;  // engine.hpp:472-475 over every rank's workers
+    // lockstep: every t_w equals R, so the first finisher is global worker 0 (rank 0's worker 0)
+    o.clustering_time_first_finisher = tails[3] >= 0 ? tails[3] : 0.0;
+    if (want_obj) {
+        o.full_objective = f;
+        o.has_full_objective = 1;
+    }
+    o.last_timestamp = R > 0 ? ts_of(R - 1) : 0.0;
+    o.total_samples = (uint64_t)tot;
+    o.distance_evals = (int64_t)nd;
+    o.n_publications = npub;
+    if (worker_obj) std::memcpy(worker_obj, hobj.data(), (size_t)W * 8);
+    o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
+    if (out) *out = o;
+    return HPCG_OK;
+}
+
 int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uint8_t* flags, int32_t* labels,
                        double* publications, int64_t pub_cap, double* worker_obj, double* traces, int64_t trace_cap,
                        int64_t* trace_len) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
     cudaSetDevice(ctx->device);
+    if (e->xr > 1) {
+        (void)publications;
+        (void)pub_cap;  // multi-rank: read the (replicated) log with hpcg_engine_publications
+        return engine_finish_multi(e, out, centroids, flags, labels, worker_obj, traces, trace_cap, trace_len);
+    }
     cudaStream_t st = ctx->stream;
     const int64_t W = e->W, k = e->k, n = e->n, kn = k * n, R = e->round;
     const int64_t Rw = std::max<int64_t>(R, 1) * W;

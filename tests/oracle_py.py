@@ -424,3 +424,11 @@ def ref() -> Reference | None:
     if _REF is None and p.exists():
         _REF = Reference(p)
     return _REF
+
+
+def chunk_range_py(rows: int, n_chunks: int, chunk: int):
+    """parallel.hpp:106-112 chunk_range: the rows of part `chunk` of `n_chunks` (the first rows % n_chunks
+    parts get one extra row) -- the row shard of rank `chunk` in a multi-GPU run."""
+    base, extra = divmod(rows, n_chunks)
+    b = chunk * base + min(chunk, extra)
+    return b, b + base + (1 if chunk < extra else 0)

@@ -89,3 +89,50 @@ def test_dropin_baselines_match_reference(p):
     assert np.array_equal(L_, e["labels"])
     assert np.max(np.abs(C_ - e["centroids"])) <= 1e-12 * np.max(np.abs(e["centroids"]))
     assert abs(g["f"] - e["full_objective"]) <= 1e-12 * e["full_objective"]
+
+
+@pytest.mark.gpu
+def test_device_dataset_overloads_no_per_call_upload():
+    """hpclust::DeviceDataset (additive overloads, SURVEY.md §8(b)): 100 draw_sample calls on a resident
+    X move no dataset bytes host -> device; the resident draw_sample / worker_step / run / mssc_objective
+    equal the reference-signature (per-call upload) versions draw for draw; parallel.hpp's ThreadPool,
+    RowRange and chunk_range and LloydConfig::policy() behave as the reference's (parallel.hpp:16-112,
+    lloyd.hpp:16-19)."""
+    import os
+    exe = ROOT / "examples" / "device_dataset_example"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(ROOT / "examples")], check=True)
+    rs = np.random.default_rng(8)
+    m, n = 200_000, 4
+    X = rs.uniform(-10, 10, (6, n))[rs.integers(0, 6, m)] + rs.standard_normal((m, n))
+    with tempfile.NamedTemporaryFile(suffix=".f64", delete=False) as f:
+        X.astype(np.float64).tofile(f.name)
+        out = subprocess.run([str(exe), f.name, str(m), str(n)], capture_output=True, text=True, timeout=300)
+    r = json.loads(out.stdout)
+    assert "error" not in r, r
+    assert r["upload_bytes_100_draws"] == 0
+    assert r["draw_same"] == 1 and r["run_same"] == 1 and r["ws_same"] == 1
+    assert r["f_dev"] == r["f_host"]
+    assert r["policy_chunks"] == (os.cpu_count() or 1)
+    base, extra = divmod(m, 4)
+    assert r["rr"] == [3 * base + min(3, extra), 3 * base + min(3, extra) + base + (1 if 3 < extra else 0)]
+    assert abs(r["pool_sum"] - X[:, 0].sum()) <= 1e-9 * np.abs(X[:, 0]).sum()
+
+
+@pytest.mark.gpu
+def test_multigpu_run_equals_single_gpu():
+    """hpclust::run(X, cfg, devices): every GPU of the node as one rank (NCCL exchange) equals run(X, cfg)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU in this pool: the multi-rank engine is covered by test_multirank_gpu.py")
+    exe = ROOT / "examples" / "multigpu_example"
+    rs = np.random.default_rng(9)
+    m, n = 100_000, 5
+    X = rs.uniform(-10, 10, (6, n))[rs.integers(0, 6, m)] + rs.standard_normal((m, n))
+    with tempfile.NamedTemporaryFile(suffix=".f64", delete=False) as f:
+        X.astype(np.float64).tofile(f.name)
+        out = subprocess.run([str(exe), f.name, str(m), str(n)], capture_output=True, text=True, timeout=600)
+    r = json.loads(out.stdout)
+    assert "error" not in r, r
+    assert r["same_centroids"] == 1 and r["nd_multi"] == r["nd_single"] and r["best_multi"] == r["best_single"]
+    assert abs(r["f_multi"] - r["f_single"]) <= 1e-12 * r["f_single"]

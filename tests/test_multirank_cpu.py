@@ -1,17 +1,19 @@
-"""CPU, world_size 2 over gloo: the cross-rank incumbent exchange used by bench.py / the
-multi-GPU cooperative engine. Each rank holds the best publication of its own workers; after
-the all-gather every rank must install the same record, equal to what the reference's
-sequential publication in worker-id order (engine.hpp:391-402, strict <) would leave."""
+"""CPU, world_size 2 over gloo: the host plumbing of the library's multi-rank exchange
+(include/hpcg.h hpcg_allgather_fn). A multi-rank engine hands its round records to the caller's
+collective through this C callback; here two processes drive the callback exactly as libhpcg does
+(ctypes call with host send / receive buffers) and check that every rank receives every rank's
+record in rank order, byte-exact -- the input of the device publication scan, which then replays
+engine.hpp:391-402 over the global worker order (tests/test_multirank_gpu.py runs the whole engine).
+Also the rank layout bench.py and the C++ multi-device run use: contiguous row shards
+(parallel.hpp:106-112 chunk_range) and contiguous worker ids per rank."""
+import ctypes as C
 import os
 import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
-
-import bench
 
 
 def _free_port():
@@ -22,54 +24,48 @@ def _free_port():
     return p
 
 
-def sequential_publish(objs):
-    """Reference semantics: publish in worker order when strictly better."""
-    best, wid = float("inf"), -1
-    for w, f in enumerate(objs):
-        if f < best:
-            best, wid = f, w
-    return best, wid
-
-
-def _worker(rank, world, port, objs_per_rank, q):
+def _worker(rank, world, port, nbytes, q):
+    import paper_2311_04517_b200 as hp
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    local = objs_per_rank[rank]
-    W = len(local)
-    o, w_local = sequential_publish(local)
-    wid = rank * W + w_local if w_local >= 0 else -1
-    C = np.full((2, 3), float(rank))
-    rec = torch.zeros(2 + C.size, dtype=torch.float64)
-    rec[0], rec[1] = o, wid
-    rec[2:] = torch.from_numpy(C.ravel())
-    out = [torch.empty_like(rec) for _ in range(world)]
-    dist.all_gather(out, rec)
-    recs = [x.numpy() for x in out]
-    win = bench.merge_records([(r[0], int(r[1])) for r in recs])
-    q.put((rank, None if win is None else (float(recs[win][0]), int(recs[win][1]), recs[win][2:].tolist())))
+    fn = hp.allgather_callback(hp.gloo_allgather(), world)
+    rs = np.random.default_rng(rank)
+    send = rs.integers(0, 256, nbytes, dtype=np.uint8)
+    recv = np.zeros(nbytes * world, np.uint8)
+    rc = fn(send.ctypes.data, recv.ctypes.data, nbytes, None)  # as libhpcg calls it
+    q.put((rank, rc, recv.tobytes()))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("objs", [
-    [[5.0, 3.0, 7.0], [4.0, 2.0, 9.0]],
-    [[1.0, 1.0, 2.0], [1.0, 0.5, 0.5]],
-    [[3.0, 2.0, 2.0], [2.0, 8.0, 1.0]],
-    [[float("inf")] * 3, [float("inf")] * 3],
-])
-def test_two_rank_exchange_matches_sequential_publication(objs):
+@pytest.mark.parametrize("nbytes", [16, 8 * (4 + 256 + 160 + 10)])  # set-up record, a config-2 round record
+def test_allgather_callback_two_ranks_gloo(nbytes):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, objs, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, nbytes, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in procs)
+    res = {r: (rc, b) for r, rc, b in (q.get(timeout=120) for _ in procs)}
     for p in procs:
         p.join(timeout=60)
-    flat = [f for r in objs for f in r]
-    best, wid = sequential_publish(flat)
-    if wid < 0:
-        assert res[0] is None and res[1] is None
-        return
-    assert res[0] == res[1]  # identical on every rank
-    assert res[0][0] == best and res[0][1] == wid
+    expect = b"".join(np.random.default_rng(r).integers(0, 256, nbytes, dtype=np.uint8).tobytes() for r in range(2))
+    for r in range(2):
+        assert res[r][0] == 0
+        assert res[r][1] == expect
+
+
+def test_allgather_callback_rejects_short_gather():
+    import paper_2311_04517_b200 as hp
+    fn = hp.allgather_callback(lambda b: b, 2)  # a broken collective returns only this rank's bytes
+    send = np.zeros(8, np.uint8)
+    recv = np.zeros(16, np.uint8)
+    assert fn(send.ctypes.data, recv.ctypes.data, 8, None) == 1
+
+
+@pytest.mark.parametrize("m,G", [(10_000_000, 8), (100_000_003, 3), (7, 4)])
+def test_rank_row_shards_are_chunk_range(m, G):
+    from oracle_py import chunk_range_py
+    ends = [chunk_range_py(m, G, g) for g in range(G)]
+    assert ends[0][0] == 0 and ends[-1][1] == m
+    assert all(ends[g][1] == ends[g + 1][0] for g in range(G - 1))
+    assert max(e - b for b, e in ends) - min(e - b for b, e in ends) <= 1
