@@ -80,6 +80,11 @@ int hpcg_ctx_synchronize(hpcg_ctx* ctx);
 int64_t hpcg_ctx_launch_count(const hpcg_ctx* ctx);
 /* Host -> device bytes this context's dataset uploads moved (hpcg_dataset_upload / hpcg_run). */
 int64_t hpcg_ctx_upload_bytes(const hpcg_ctx* ctx);
+/* Row cost of f(C, X) over fp32 data (the labels are exact in both modes): exact != 0 -- the
+ * reference's fp64 distance per row (1e-12 relative); 0 (default) -- the north star's fp32 mode: the
+ * row's squared distance in fp32 (direct form, FFMA2), accumulated in fp64 (<= 1e-5 relative; in
+ * practice ~1e-8), which keeps the pass at the HBM rate. fp64 data always takes the exact cost. */
+int hpcg_ctx_set_fp32_cost(hpcg_ctx* ctx, int exact);
 /* Per-kernel device timing: when enabled, every worker-step / objective launch is bracketed
  * by CUDA events on the launching stream; hpcg_ctx_kernel_times synchronises and returns
  * (launch count, summed milliseconds) per kernel class: 0 worker step, 1 objective. */

@@ -25,7 +25,7 @@ EXPORTS = (
     "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
     "hpcg_engine_publications", "hpcg_sample_gather_dev", "hpcg_philox_seed_draws", "hpcg_engine_round_outcome",
     "hpcg_engine_philox_key", "hpcg_comm_unique_id", "hpcg_ctx_attach_comm", "hpcg_ctx_comm_info",
-    "hpcg_engine_set_exchange", "hpcg_ctx_upload_bytes",
+    "hpcg_engine_set_exchange", "hpcg_ctx_upload_bytes", "hpcg_ctx_set_fp32_cost",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -113,6 +113,7 @@ def _load():
         "hpcg_ctx_synchronize": (C.c_int, [P]),
         "hpcg_ctx_launch_count": (I64, [P]),
         "hpcg_ctx_upload_bytes": (I64, [P]),
+        "hpcg_ctx_set_fp32_cost": (C.c_int, [P, C.c_int]),
         "hpcg_dataset_upload": (C.c_int, [P, P, C.c_int, I64, I64, P]),
         "hpcg_dataset_wrap_sharded": (C.c_int, [P, P, P, C.c_int32, C.c_int, I64, P]),
         "hpcg_ipc_export": (C.c_int, [P, P]),

@@ -43,6 +43,14 @@ class Context:
     def synchronize(self):
         check(lib.hpcg_ctx_synchronize(self.h))
 
+    def set_fp32_cost(self, exact: bool):
+        """f(C, X) over fp32 data: exact fp64 row cost (True) or the fp32 mode (False, the default)."""
+        check(lib.hpcg_ctx_set_fp32_cost(self.h, 1 if exact else 0))
+
+    @property
+    def upload_bytes(self) -> int:
+        return int(lib.hpcg_ctx_upload_bytes(self.h))
+
     def attach_comm(self, nranks: int, rank: int, uid: bytes):
         """Collective over the ranks: NCCL communicator for multi-rank engines (one rank per GPU)."""
         buf = C.create_string_buffer(bytes(uid), 128)

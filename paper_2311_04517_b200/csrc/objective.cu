@@ -37,7 +37,7 @@ cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeo
     if (np != 0 && p.k <= kMaxK && p.candidates <= kMaxCandidates && !force_wide) {
         StepGeometry tmp;
         std::string w2;
-        if (step_geometry(dtype, p.n, p.s, p.k, p.candidates, p.W, &tmp, &w2) == cudaSuccess)
+        if (step_geometry(dtype, p.n, p.s, p.k, p.candidates, p.geo_W > 0 ? p.geo_W : p.W, &tmp, &w2) == cudaSuccess)
             return dtype == 0 ? launch_step_f32(p, st, g, why, np) : launch_step_f64(p, st, g, why, np);
     }
     if (g) *g = StepGeometry{};

@@ -32,6 +32,10 @@ struct ObjParams {
     int32_t rec_slot;      // constant-bank record slot of the calling context, or -1
     float4* rec_scratch;   // device staging of that slot's records (kRecSlotF4 float4)
     int* launched;         // optional: kernels launched are added here
+    int32_t fast_cost;     // fp32 data: row cost in fp32 (direct form, FFMA2), accumulated in fp64 --
+                           // the north star's fp32 mode (1e-5 relative); 0: exact fp64 row cost
+    const float* nclo;     // fast_cost: [kv x n] -(c - fl32(c)), the low part of each centre, so a row's
+                           // difference is (x - c_hi) - c_lo: error ~2^-24 |x - c| whatever |c| / |x - c|
 };
 
 // valid centre count: the device value when given (the host launched with an upper bound)

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) float s_cc[N];
     __shared__ __align__(16) float s_rec[N][NP + 4];  // fp32 re-screen records: -2c, then |c|^2 at NP
+    __shared__ __align__(16) float s_clo[N][NP + 4];  // fp32-mode cost: -(c - fl32(c)) (low parts)
     __shared__ double s_wcost[EW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kv = obj_kv(p);  // device-side valid count (p.kv: the launch bound, <= 2 KPS)
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
         const float c2 = j < kv ? (float)(-2.0 * p.C[(int64_t)j * NP + d]) : 0.f;
         Bt[G::elem_off(j, d)] = tf32_rna(c2);
         s_rec[j][d] = c2;
+        s_clo[j][d] = (p.fast_cost && j < kv && d < p.n) ? p.nclo[(int64_t)j * p.n + d] : 0.f;
     }
     if (tid < N) {
         float cc = 1e38f;
@@ -387,16 +389,39 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                     if (lane == src) lab = dj;
                 }
                 if (valid) {
-                    // row cost: fp64 distance to the chosen centre (two interleaved DFMA chains; within
-                    // 1e-15 relative of the reference's per-row value)
-                    const double* cj = Cd + lab * CDS;
-                    double a[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (p.fast_cost) {
+                        // fp32 mode: (x - c~)^2 in fp32 (c~ = -0.5 * the record's -2c: exact), two FFMA2
+                        // chains per row, the row sum widened once into the fp64 accumulator
+                        // difference (x - c_hi) - c_lo: both steps rounded to ~2^-24 |x - c|
+                        const float* rc = s_rec[lab];
+                        const float* rl = s_clo[lab];
+                        float2 a0 = make_float2(0.f, 0.f), a1 = a0;
 #pragma unroll
-                    for (int d = 0; d < NP; ++d) {
-                        const double e = (double)x[d] - cj[d];
-                        a[d & 3] = fma(e, e, a[d & 3]);
+                        for (int d = 0; d < NP; d += 4) {
+                            const float4 c4 = *reinterpret_cast<const float4*>(rc + d);
+                            const float4 l4 = *reinterpret_cast<const float4*>(rl + d);
+                            const float2 e0 = __fadd2_rn(__ffma2_rn(make_float2(c4.x, c4.y), make_float2(0.5f, 0.5f),
+                                                                    make_float2(x[d], x[d + 1])),
+                                                         make_float2(l4.x, l4.y));
+                            const float2 e1 = __fadd2_rn(__ffma2_rn(make_float2(c4.z, c4.w), make_float2(0.5f, 0.5f),
+                                                                    make_float2(x[d + 2], x[d + 3])),
+                                                         make_float2(l4.z, l4.w));
+                            a0 = __ffma2_rn(e0, e0, a0);
+                            a1 = __ffma2_rn(e1, e1, a1);
+                        }
+                        cost += (double)((a0.x + a0.y) + (a1.x + a1.y));
+                    } else {
+                        // row cost: fp64 distance to the chosen centre (interleaved DFMA chains; within
+                        // 1e-15 relative of the reference's per-row value)
+                        const double* cj = Cd + lab * CDS;
+                        double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                        for (int d = 0; d < NP; ++d) {
+                            const double e = (double)x[d] - cj[d];
+                            a[d & 3] = fma(e, e, a[d & 3]);
+                        }
+                        cost += (a[0] + a[1]) + (a[2] + a[3]);
                     }
-                    cost += (a[0] + a[1]) + (a[2] + a[3]);
                     if (labels_out) labels_out[row] = remap[lab];
                     if (counts_out) atomicAdd(counts_out + remap[lab], 1ULL);
                 }

@@ -39,7 +39,7 @@ struct TcwGeo {
 template <int NA>
 __host__ __device__ inline int objective_tcw_smem() {
     using TG = TcwGeo<NA>;
-    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB;
+    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB + TG::N * TG::NPW * 4;  // + fp32 -c (fp32-mode cost)
 }
 
 // byte offset of float d of row r inside a tile of NA [rows x 128 B] SWIZZLE_128B atoms
@@ -64,10 +64,12 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
     const int kv = obj_kv(p);
     const double* __restrict__ Cg = p.C;  // [kv x NPW] fp64 centres (L1-resident)
 
+    float* negc = reinterpret_cast<float*>(Bt + NA * TG::BSUB);  // [N][NPW] fp32 -c (fp32-mode row cost)
     for (int e = tid; e < N * NPW; e += TG::THREADS) {
         const int j = e / NPW, d = e - j * NPW;
         const float c2 = j < kv ? (float)(-2.0 * Cg[(int64_t)j * NPW + d]) : 0.f;
         *reinterpret_cast<float*>(Bt + sw128_off(N, j, d)) = tf32_rna(c2);
+        negc[e] = 0.5f * c2;  // exact: -fl32(c)
     }
     if (tid < N) {
         float cc = 1e38f;
@@ -202,7 +204,28 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
                 }
             int lab = __float_as_int(p1[0]) & TMASK;
             // one pass over the row: |x|^2 (fp32) and the fp64 cost to the screened centre
-            auto row_cost = [&](int j, float* nn_out) {
+            auto row_cost = [&](int j, float* nn_out) -> double {
+                if (p.fast_cost) {  // fp32 mode: (x - c~)^2 in fp32 FFMA2 chains, widened once per row
+                    const float* nc = negc + j * NPW;
+                    const float* nl = p.nclo + (int64_t)j * NPW;  // low parts (L1-resident, 16 KB)
+                    float2 a0 = make_float2(0.f, 0.f), a1 = a0, nn2 = a0;
+#pragma unroll 4
+                    for (int c = 0; c < NPW / 4; ++c) {
+                        const float4 x4 = *reinterpret_cast<const float4*>(tile + sw128_off(TG::M, r, 4 * c));
+                        const float4 c4 = *reinterpret_cast<const float4*>(nc + 4 * c);
+                        const float4 l4 = __ldg(reinterpret_cast<const float4*>(nl + 4 * c));
+                        nn2 = __ffma2_rn(make_float2(x4.x, x4.y), make_float2(x4.x, x4.y), nn2);
+                        nn2 = __ffma2_rn(make_float2(x4.z, x4.w), make_float2(x4.z, x4.w), nn2);
+                        const float2 e0 = __fadd2_rn(__fadd2_rn(make_float2(x4.x, x4.y), make_float2(c4.x, c4.y)),
+                                                     make_float2(l4.x, l4.y));
+                        const float2 e1 = __fadd2_rn(__fadd2_rn(make_float2(x4.z, x4.w), make_float2(c4.z, c4.w)),
+                                                     make_float2(l4.z, l4.w));
+                        a0 = __ffma2_rn(e0, e0, a0);
+                        a1 = __ffma2_rn(e1, e1, a1);
+                    }
+                    if (nn_out) *nn_out = nn2.x + nn2.y;
+                    return (double)((a0.x + a0.y) + (a1.x + a1.y));
+                }
                 const double* cj = Cg + (int64_t)j * NPW;
                 double a[4] = {0.0, 0.0, 0.0, 0.0};
                 float2 nn2 = make_float2(0.f, 0.f);

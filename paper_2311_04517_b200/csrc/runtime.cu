@@ -199,6 +199,7 @@ struct hpcg_ctx {
     std::mutex mu;
     std::atomic<int64_t> launches{0};
     std::atomic<int64_t> upload_bytes{0};  // host -> device bytes of dataset uploads (hpcg_dataset_upload)
+    int fp32_exact_cost = 0;               // f(C,X) over fp32 data: 1 = exact fp64 row cost, 0 = fp32 mode
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
     int rec_slot = -1;                     // constant-bank slot of the objective records
     DevBuf rec_scratch;
@@ -801,6 +802,12 @@ cudaError_t d2h(T* dst, const T* src, size_t count, cudaStream_t st) {
     return cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, st);
 }
 
+// low parts of the valid centres for the fp32-mode row cost: nclo = -(c - fl32(c))
+__global__ void centre_lo_kernel(const double* C, int64_t count, float* nclo) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        nclo[e] = (float)-(C[e] - (double)(float)C[e]);
+}
+
 // Full-data assignment on device: valid centres C_valid_dev [kv x n], remap [kv];
 // labels_dev may be null; counts_dev (u64 x k) may be null; cost to cost_dev.
 int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev, const int32_t* remap_dev, int kv,
@@ -812,6 +819,16 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
     op.kv_dev = kv_dev;
     int launched = 0;
     op.launched = &launched;
+    op.fast_cost = (ds->dtype == HPCG_F32 && !ctx->fp32_exact_cost) ? 1 : 0;
+    if (op.fast_cost) {
+        const int64_t cnt = (int64_t)kv * ds->n;
+        CU(ctx->s_f.reserve((size_t)std::max<int64_t>(cnt, 4) * sizeof(float)));
+        centre_lo_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 64), 256, 0, ctx->stream>>>(
+            C_valid_dev, cnt, ctx->s_f.as<float>());
+        CU(cudaGetLastError());
+        ctx->launches += 1;
+        op.nclo = ctx->s_f.as<float>();
+    }
     op.rec_slot = -1;
     if (ctx->rec_slot >= 0 && ctx->rec_scratch.reserve((size_t)kRecSlotF4 * sizeof(float4)) == cudaSuccess) {
         op.rec_slot = ctx->rec_slot;
@@ -923,6 +940,12 @@ int hpcg_ctx_synchronize(hpcg_ctx* ctx) {
 
 int64_t hpcg_ctx_launch_count(const hpcg_ctx* ctx) { return ctx->launches.load(); }
 int64_t hpcg_ctx_upload_bytes(const hpcg_ctx* ctx) { return ctx->upload_bytes.load(); }
+
+int hpcg_ctx_set_fp32_cost(hpcg_ctx* ctx, int exact) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->fp32_exact_cost = exact ? 1 : 0;
+    return HPCG_OK;
+}
 
 int hpcg_ctx_enable_timing(hpcg_ctx* ctx, int enable) {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1730,6 +1753,7 @@ int engine_round(hpcg_engine* e, double now) {
     p.n = (int)n;
     p.s = s;
     p.W = (int)W;
+    p.geo_W = (int)std::max<int64_t>(W, e->xWtot);
     p.sample_mode = reference ? 0 : 1;
     p.idx = e->d_idx.as<int64_t>();
     p.key = e->key;

@@ -35,6 +35,9 @@ struct StepParams {
     int32_t n;
     int64_t s;
     int32_t W;            // workers in this launch (one cluster each)
+    int32_t geo_W;        // worker count the launch geometry is chosen for (0: W). A multi-rank engine
+                          // passes the all-rank total, so every rank partitions a sample exactly as
+                          // one engine with every worker would (bit-identical sums)
     int32_t sample_mode;  // 0 explicit idx[W*s], 1 Philox PRP over [0,m), 2 contiguous (X is [W*s x n])
     const int64_t* idx;
     uint64_t key;        // Philox key (sample PRP and K-means++ draws)

@@ -108,7 +108,8 @@ cudaError_t step_geometry_t(int64_t s, int k, int ncand, int W, StepGeometry* g,
 template <typename T, int NP>
 cudaError_t launch_step_t(const StepParams& p_in, cudaStream_t st, StepGeometry* geo_out, std::string* why) {
     StepGeometry g;
-    cudaError_t e = step_geometry_t<T, NP>(p_in.s, p_in.k, p_in.candidates, p_in.W, &g, why);
+    cudaError_t e = step_geometry_t<T, NP>(p_in.s, p_in.k, p_in.candidates, p_in.geo_W > 0 ? p_in.geo_W : p_in.W, &g,
+                                           why);
     if (e != cudaSuccess) return e;
     StepParams p = p_in;
     p.rows_cap = g.rows_cap;

@@ -1021,7 +1021,13 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     // (enough CTAs to fill the GPU twice, and at most ~RPC 256-row rounds per CTA: each round is a
     // sequence of barriers, so long per-CTA row ranges serialise)
     static const int rpc = getenv("HPCG_WIDE_RPC") ? atoi(getenv("HPCG_WIDE_RPC")) : 24;  // diagnostics
-    int G = std::max<int>(std::min<int>((int)((int64_t)2 * sms / Wb), (int)((s + 4 * kWT - 1) / (4 * kWT))),
+    // the geometry of a batch of the engine's size (p.geo_W), so CTA partitions -- and the sums --
+    // do not depend on how many workers this rank holds
+    const size_t per_worker_b = (size_t)s * ((size_t)n * sizeof(T) + 8 * (kMaxCandidates + 1) + 4) + 1024;
+    const int Wgeo = p.geo_W > 0 ? (int)std::max<size_t>(1, std::min<size_t>((size_t)p.geo_W, ((size_t)4 << 30) /
+                                                                                        std::max<size_t>(per_worker_b, 1)))
+                                 : Wb;
+    int G = std::max<int>(std::min<int>((int)((int64_t)2 * sms / Wgeo), (int)((s + 4 * kWT - 1) / (4 * kWT))),
                           (int)((s + (int64_t)rpc * kWT - 1) / ((int64_t)rpc * kWT)));
     G = std::max(G, 1);
     const int64_t pd = kn + k + 1;

@@ -11,7 +11,7 @@ import pytest
 
 import paper_2311_04517_b200 as hp
 from oracle_py import orc
-from test_parity_gpu import RTOL, centroid_close, mixture, rel
+from test_parity_gpu import RTOL, centroid_close, mixture, obj_rtol, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -74,7 +74,7 @@ def test_wide_objective_vs_oracle(dtype, n, k):
     a, f = hp.final_assignment(X, C_)
     assert np.array_equal(a.labels, lab)
     assert np.array_equal(a.counts, cnt)
-    assert rel(f, cost) <= RTOL
+    assert rel(f, cost) <= obj_rtol(X)
 
 
 @pytest.mark.parametrize("strategy", ["competitive", "cooperative"])
@@ -102,7 +102,7 @@ def test_config4_shaped_philox_run():
     b = hp.run(X, cfg)
     assert np.array_equal(a.centroids, b.centroids) and a.full_objective == b.full_objective
     lab, cnt, cost, _ = orc().assign(X.astype(np.float64), a.centroids, a.degenerate)
-    assert rel(a.full_objective, cost) <= RTOL
+    assert rel(a.full_objective, cost) <= obj_rtol(X)
 
 
 def test_forced_wide_path_matches_oracle_on_a_resident_shape(tmp_path):
