@@ -201,6 +201,7 @@ struct hpcg_ctx {
     std::atomic<int64_t> upload_bytes{0};  // host -> device bytes of dataset uploads (hpcg_dataset_upload)
     int fp32_exact_cost = 0;               // f(C,X) over fp32 data: 1 = exact fp64 row cost, 0 = fp32 mode
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
+    DevBuf clo;                           // low parts of the centres of the fp32-mode f(C,X) cost
     int rec_slot = -1;                     // constant-bank slot of the objective records
     DevBuf rec_scratch;
     // per-kernel-class event timing (class 0 worker step, 1 objective)
@@ -822,12 +823,12 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
     op.fast_cost = (ds->dtype == HPCG_F32 && !ctx->fp32_exact_cost) ? 1 : 0;
     if (op.fast_cost) {
         const int64_t cnt = (int64_t)kv * ds->n;
-        CU(ctx->s_f.reserve((size_t)std::max<int64_t>(cnt, 4) * sizeof(float)));
+        CU(ctx->clo.reserve((size_t)std::max<int64_t>(cnt, 4) * sizeof(float)));
         centre_lo_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 64), 256, 0, ctx->stream>>>(
-            C_valid_dev, cnt, ctx->s_f.as<float>());
+            C_valid_dev, cnt, ctx->clo.as<float>());
         CU(cudaGetLastError());
         ctx->launches += 1;
-        op.nclo = ctx->s_f.as<float>();
+        op.nclo = ctx->clo.as<float>();
     }
     op.rec_slot = -1;
     if (ctx->rec_slot >= 0 && ctx->rec_scratch.reserve((size_t)kRecSlotF4 * sizeof(float4)) == cudaSuccess) {

@@ -691,6 +691,35 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             }
             flush(true);
         };
+        // the first D^2 update of a step (every d2 still +inf): every row takes the exact distance
+        // (seeding.hpp:20-42 with d2 = inf), so no screen and no work list -- two rows per thread
+        // with interleaved fp64 chains
+        auto d2_first = [&](int c) {
+            const double* cd = sh.cand[c];
+            int li = tid;
+            constexpr bool kTwo = NP * sizeof(T) <= 64;  // two rows in registers (wider rows: one)
+            for (; kTwo && li + kStepThreads < nr; li += 2 * kStepThreads) {
+                T xa[NP], xb[NP];
+                load_row_T<T, NP>(samp, li, xa);
+                load_row_T<T, NP>(samp, li + kStepThreads, xb);
+                double a = 0.0, b = 0.0;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    const double cv = cd[d];
+                    const double ea = __dsub_rn((double)xa[d], cv), eb = __dsub_rn((double)xb[d], cv);
+                    a = __dadd_rn(a, __dmul_rn(ea, ea));
+                    b = __dadd_rn(b, __dmul_rn(eb, eb));
+                }
+                d2[li] = a;
+                d2[li + kStepThreads] = b;
+            }
+            for (; li < nr; li += kStepThreads) {
+                T xr[NP];
+                load_row_T<T, NP>(samp, li, xr);
+                d2[li] = exact_dist_regs<T, NP>(xr, cd);
+            }
+        };
+        bool d2_fresh = true;
         // the same update for the winning candidate of a K-means++ slot: the cost pass already
         // screened every row against it, so only its flagged rows get an exact distance
         auto d2_update_flagged = [&](int c, bool tr) {
@@ -737,7 +766,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 make_candf(0);
             }
             __syncthreads();
-            d2_update(0);
+            if (d2_fresh)
+                d2_first(0);
+            else
+                d2_update(0);
+            d2_fresh = false;
             __syncthreads();
             nd += s;
         }
@@ -775,7 +808,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 if (lane == 0) sh.flags[j] = 0;
             }
             __syncthreads();
-            d2_update(0);
+            if (d2_fresh)
+                d2_first(0);
+            else
+                d2_update(0);
+            d2_fresh = false;
             nd += s;
             ++filled;
             __syncthreads();
@@ -973,18 +1010,29 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 if (it == 0 && p.trace_mode == 1) stamp(17);
                 if (r - lane < nr) rows(IntC<1>{}, r);
                 if (it == 0 && p.trace_mode == 1) stamp(18);
+                // midpoint and half-width per candidate; the slack covers the fp32 lane and warp sums.
+                // The 2 NC butterfly sums run interleaved (same per-value order as warp_sum_f).
+                float vs[NC], es[NC];
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     const float E = fmaf(2.f * kScreenK2, fmaf((float)efn[c], sh.candn[c], efx[c]),
                                          fmaf(kD2Round, eff[c], 4e-42f * (float)efn[c]));
-                    // midpoint and half-width; the slack covers the fp32 lane and warp sums
-                    const float v = warp_sum_f(0.5f * E - red[c]);
-                    const float e = warp_sum_f(0.5005f * E + 1e-5f * red[c]);
-                    if (lane == 0) {
-                        sh.wsum[warp][c] = (double)v;
-                        sh.werr[warp][c] = (double)e;
-                    }
+                    vs[c] = 0.5f * E - red[c];
+                    es[c] = 0.5005f * E + 1e-5f * red[c];
                 }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        vs[c] += __shfl_xor_sync(0xffffffffu, vs[c], o);
+                        es[c] += __shfl_xor_sync(0xffffffffu, es[c], o);
+                    }
+                if (lane == 0)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        sh.wsum[warp][c] = (double)vs[c];
+                        sh.werr[warp][c] = (double)es[c];
+                    }
                 if (it == 0 && p.trace_mode == 1) stamp(19);
             };
             // (b) exact pass (only when (a) cannot separate the winner): exact distances for every
@@ -1335,43 +1383,56 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 for (int j = 0; j < k; ++j) {
                     const int a = max(sh.cstart[j], lo), b = min(sh.cstart[j + 1], hi);
                     if (a >= b) continue;  // warp-uniform
-                    double acc[U], cj[U], accc[U];
+                    double acc[U], cj[U], accc[U], acc2[U], accc2[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         acc[u] = 0.0;
                         accc[u] = 0.0;
+                        acc2[u] = 0.0;
+                        accc2[u] = 0.0;
                         const int d = q * U + u;
                         cj[u] = (active_unit && d < NP) ? Cm[j * NP + d] : 0.0;
                     }
                     const unsigned char* sbytes = reinterpret_cast<const unsigned char*>(samp);
-                    auto add_row = [&](int row) {  // row: perm entry (see the scatter above)
+                    // row: perm entry (see the scatter above); two accumulator sets (even / odd steps)
+                    // halve the fp64 dependency chains; the order stays fixed
+                    auto add_row = [&](int row, double(&sa)[U], double(&sc)[U]) {
                         if constexpr (G::VEC16 && sizeof(T) == 4) {
                             const float4 v = *reinterpret_cast<const float4*>(sbytes + ((row ^ q) << 4));
                             const double xv[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                acc[u] += xv[u];
+                                sa[u] += xv[u];
                                 const double diff = xv[u] - cj[u];
-                                accc[u] = fma(diff, diff, accc[u]);
+                                sc[u] = fma(diff, diff, sc[u]);
                             }
                         } else if constexpr (G::VEC16) {
                             const double2 v = *reinterpret_cast<const double2*>(sbytes + ((row ^ q) << 4));
-                            acc[0] += v.x;
-                            acc[1] += v.y;
+                            sa[0] += v.x;
+                            sa[1] += v.y;
                             const double d0 = v.x - cj[0], d1 = v.y - cj[1];
-                            accc[0] = fma(d0, d0, accc[0]);
-                            accc[1] = fma(d1, d1, accc[1]);
+                            sc[0] = fma(d0, d0, sc[0]);
+                            sc[1] = fma(d1, d1, sc[1]);
                         } else {
                             const double xv = (double)samp[G::elem_off(row, q)];
-                            acc[0] += xv;
+                            sa[0] += xv;
                             const double diff = xv - cj[0];
-                            accc[0] = fma(diff, diff, accc[0]);
+                            sc[0] = fma(diff, diff, sc[0]);
                         }
                     };
                     if (active_unit) {
                         int p0 = a + gi;
-#pragma unroll 4
-                        for (; p0 < b; p0 += RPS) add_row(wperm[p0]);
+#pragma unroll 2
+                        for (; p0 + RPS < b; p0 += 2 * RPS) {
+                            add_row(wperm[p0], acc, accc);
+                            add_row(wperm[p0 + RPS], acc2, accc2);
+                        }
+                        if (p0 < b) add_row(wperm[p0], acc, accc);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            acc[u] += acc2[u];
+                            accc[u] += accc2[u];
+                        }
                     }
                     // fold the row groups (fixed tree): lanes gi == 0 hold the sums
 #pragma unroll

@@ -388,33 +388,109 @@ __device__ __forceinline__ bool slot_live(const WState& st) {
     return st.seed_stop == 0 && st.next < st.n_pending;
 }
 
-// block CDF totals: rows of a block summed sequentially (the order the draw re-walks)
+// ---- K-means++ CDF on HBM-resident samples (seeding.hpp:81-92), warp-parallel and deterministic.
+// A 256-row block is one warp: lane L owns rows r0 + 8L .. r0 + 8L + 7 (summed sequentially), the
+// lanes combine by an exclusive shuffle scan, and the in-block cumulative value of row i is
+// fl(excl_L + run_{L,i}). The block total T_q is DEFINED as that value at the block's last row, so the
+// draw, which recomputes the same values, always finds its crossing inside the block it selected.
+// Block prefixes P_{q+1} = fl(P_q + T_q) run sequentially over the blocks (one warp per worker, from
+// shared memory), so cum is monotone across blocks and exactly one row is the first with cum > u
+// (rng.hpp:83-93; CDF rounding differs from the reference's row-sequential sum only in the last bits:
+// the documented CDF-boundary tie class).
+constexpr int kLaneRows = kSeedRows / 32;
+
+struct BlockScan {  // one lane's view of a 256-row block
+    double run[kLaneRows];  // sequential running sums of the lane's rows
+    double excl;            // exclusive prefix of the lanes below (shuffle scan)
+    int nrows;              // rows of this lane (0 past the end of the sample)
+};
+
+__device__ __forceinline__ BlockScan block_scan(const double* __restrict__ d2, int64_t r0, int64_t r1, int lane) {
+    BlockScan b;
+    const int64_t a = r0 + (int64_t)lane * kLaneRows;
+    const int64_t left = r1 - a;
+    b.nrows = left <= 0 ? 0 : (left >= kLaneRows ? kLaneRows : (int)left);
+    double v[kLaneRows];
+#pragma unroll
+    for (int j = 0; j < kLaneRows; ++j) v[j] = j < b.nrows ? d2[a + j] : 0.0;
+    double run = 0.0;
+#pragma unroll
+    for (int j = 0; j < kLaneRows; ++j) {
+        run += v[j];
+        b.run[j] = run;
+    }
+    double incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    b.excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) b.excl = 0.0;
+    return b;
+}
+
+// block totals: one warp per (block, worker)
 __global__ void wide_cdf_kernel(const StepParams p, WideBufs b, int nblk) {
     const int w = blockIdx.y;
     if (!slot_live(b.st[w])) return;
-    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (blk >= nblk) return;
     const int64_t s = p.s, r0 = (int64_t)blk * kSeedRows, r1 = min(s, r0 + kSeedRows);
-    const double* d2 = b.d2 + (int64_t)w * s;
-    double run = 0.0;
-    for (int64_t i = r0; i < r1; ++i) run += d2[i];
-    b.btot[(int64_t)w * nblk + blk] = run;
+    const BlockScan bs = block_scan(b.d2 + (int64_t)w * s, r0, r1, lane);
+    // T_q := the cumulative value at the block's last row, exactly as the draw computes it
+    const int last_lane = (int)((r1 - 1 - r0) / kLaneRows);
+    if (lane == last_lane) {
+        const int j = bs.nrows - 1;
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kLaneRows; ++q)
+            if (q == j) t = bs.excl + bs.run[q];
+        b.btot[(int64_t)w * (nblk + 1) + blk] = t;
+    }
 }
 
-// inverse-CDF draw of candidate c (seeding.hpp:85-92; rng.hpp:83-93): first row with cum > u,
-// cum = P_block + (sequential run within the block); no crossing -> row s-1
+// block prefixes in place: btot[q] <- P_q (exclusive, sequential over blocks), btot[nblk] <- total.
+// One warp per worker: the totals are staged in shared memory by the warp, lane 0 runs the chain.
+__global__ void wide_cdfscan_kernel(WideBufs b, int nblk, int staged) {
+    extern __shared__ double sbuf[];
+    const int w = blockIdx.x;
+    if (!slot_live(b.st[w])) return;
+    double* bt = b.btot + (int64_t)w * (nblk + 1);
+    double* sb = staged ? sbuf : bt;  // very long samples: the chain runs on the global copy
+    if (staged)
+        for (int q = threadIdx.x; q < nblk; q += blockDim.x) sb[q] = bt[q];
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        double P = 0.0;
+#pragma unroll 8
+        for (int q = 0; q < nblk; ++q) {
+            const double t = sb[q];
+            sb[q] = P;
+            P += t;
+        }
+        sb[nblk] = P;
+    }
+    __syncwarp();
+    if (staged)
+        for (int q = threadIdx.x; q <= nblk; q += blockDim.x) bt[q] = sb[q];
+}
+
+// inverse-CDF draw of candidate c (seeding.hpp:85-92; rng.hpp:83-93): first row with cum > u; no
+// crossing -> row s-1. One warp per (candidate, worker): binary search of the block prefixes, then
+// the block's cumulative values recomputed exactly as wide_cdf_kernel did.
 template <typename T>
 __global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nblk) {
-    const int c = blockIdx.x, w = blockIdx.y, wl = w0 + w;
+    const int c = blockIdx.x, w = blockIdx.y, wl = w0 + w, lane = threadIdx.x;
     WState* stp = b.st + w;
-    if (!slot_live(*stp) || threadIdx.x != 0) return;
+    if (!slot_live(*stp)) return;
     const int64_t s = p.s;
     const int n = p.n;
-    const double* bt = b.btot + (int64_t)w * nblk;
-    double total = 0.0;
-    for (int q = 0; q < nblk; ++q) total += bt[q];
+    const double* P = b.btot + (int64_t)w * (nblk + 1);
+    const double total = P[nblk];
     if (!(total > 0.0)) {  // distinct rows exhausted (seeding.hpp:87)
-        if (c == 0) stp->seed_stop = 1;
+        if (c == 0 && lane == 0) stp->seed_stop = 1;
         return;
     }
     const int it = stp->it, next = stp->next, ncand = p.candidates;
@@ -422,27 +498,34 @@ __global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nbl
                                          : philox_unit(p.key, p.round, (uint32_t)(p.worker_base + wl),
                                                        (uint32_t)(0x10000 + next * kMaxCandidates + c));
     const double u = unit * total;
+    // first block q with P_{q+1} > u (P is non-decreasing); none -> the fallback row
+    int lo = 0, hi = nblk;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (P[mid + 1] > u)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
     int64_t row = s - 1;
-    double P = 0.0;
-    for (int q = 0; q < nblk; ++q) {
-        if (P + bt[q] > u) {
-            const double* d2 = b.d2 + (int64_t)w * s;
-            const int64_t r0 = (int64_t)q * kSeedRows, r1 = min(s, r0 + kSeedRows);
-            double run = 0.0;
-            for (int64_t i = r0; i < r1; ++i) {
-                run += d2[i];
-                if (P + run > u) {
-                    row = i;
-                    break;
-                }
-            }
-            break;
+    if (lo < nblk) {
+        const int64_t r0 = (int64_t)lo * kSeedRows, r1 = min(s, r0 + kSeedRows);
+        const BlockScan bs = block_scan(b.d2 + (int64_t)w * s, r0, r1, lane);
+        const double Pq = P[lo];
+        int hit = kLaneRows;
+#pragma unroll
+        for (int j = kLaneRows - 1; j >= 0; --j)
+            if (j < bs.nrows && Pq + (bs.excl + bs.run[j]) > u) hit = j;
+        const unsigned m = __ballot_sync(0xffffffffu, hit < kLaneRows);
+        if (m) {
+            const int src = __ffs(m) - 1;
+            const int h = __shfl_sync(0xffffffffu, hit, src);
+            row = r0 + (int64_t)src * kLaneRows + h;
         }
-        P += bt[q];
     }
     const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + row) * n;
     double* cd = b.cand + ((int64_t)w * kMaxCandidates + c) * n;
-    for (int d = 0; d < n; ++d) cd[d] = (double)x[d];
+    for (int d = lane; d < n; d += 32) cd[d] = (double)x[d];
 }
 
 // candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): an fp32 screen decides
@@ -524,24 +607,31 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
     }
 }
 
-// winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot
+// winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot. Warp c
+// sums candidate c's block partials (lanes strided, then a shuffle tree: a fixed order).
 __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
     const int w = blockIdx.x, n = p.n, k = p.k, ncand = p.candidates;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WState* stp = b.st + w;
     if (!slot_live(*stp)) return;
+    __shared__ double tot_s[kMaxCandidates];
     __shared__ int best_s;
+    if (warp < ncand) {
+        const double* bc_c = b.bcost + ((int64_t)w * kMaxCandidates + warp) * nblk;
+        double t = 0.0;
+        for (int q = lane; q < nblk; q += 32) t += bc_c[q];
+        t = warp_sum(t);
+        if (lane == 0) tot_s[warp] = t;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
         double bc = __longlong_as_double(0x7ff0000000000000LL);
         int best = 0;
-        for (int c = 0; c < ncand; ++c) {
-            const double* bc_c = b.bcost + ((int64_t)w * kMaxCandidates + c) * nblk;
-            double t = 0.0;
-            for (int q = 0; q < nblk; ++q) t += bc_c[q];
-            if (t < bc) {
-                bc = t;
+        for (int c = 0; c < ncand; ++c)
+            if (tot_s[c] < bc) {
+                bc = tot_s[c];
                 best = c;
             }
-        }
         best_s = best;
     }
     __syncthreads();
@@ -1040,7 +1130,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     };
     const size_t oS = take((size_t)Wb * s * n * sizeof(T)), oC = take((size_t)Wb * kn * 8),
                  od2 = take((size_t)Wb * s * 8), odc = take((size_t)Wb * kMaxCandidates * s * 8),
-                 ocand = take((size_t)Wb * kMaxCandidates * n * 8), obt = take((size_t)Wb * nblk * 8),
+                 ocand = take((size_t)Wb * kMaxCandidates * n * 8), obt = take((size_t)Wb * (nblk + 1) * 8),
                  obc = take((size_t)Wb * kMaxCandidates * nblk * 8), opart = take((size_t)Wb * G * pd * 8),
                  olc = take((size_t)Wb * k * 8), ofl = take((size_t)Wb * k), opend = take((size_t)Wb * k * 4),
                  olab = take((size_t)Wb * s * 4), oact = take(4), ost = take((size_t)Wb * sizeof(WState)),
@@ -1090,12 +1180,19 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         e = cudaFuncSetAttribute(wide_cost_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem);
         if (e != cudaSuccess) return e;
     }
+    const int staged = (size_t)(nblk + 1) * 8 <= 200 * 1024 ? 1 : 0;
+    const size_t scan_smem = staged ? (size_t)(nblk + 1) * 8 : 0;
+    if (slots > 0 && scan_smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(wide_cdfscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem);
+        if (e != cudaSuccess) return e;
+    }
     for (int it = 0; it < slots; ++it) {
-        wide_cdf_kernel<<<dim3((unsigned)((nblk + 63) / 64), (unsigned)Wb), 64, 0, st>>>(p, b, nblk);
+        wide_cdf_kernel<<<dim3((unsigned)((nblk + 7) / 8), (unsigned)Wb), 256, 0, st>>>(p, b, nblk);
+        wide_cdfscan_kernel<<<(unsigned)Wb, 32, scan_smem, st>>>(b, nblk, staged);
         wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
         wide_cost_kernel<T><<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, cost_smem, st>>>(
             p, b, nblk);
-        wide_decide_kernel<<<Wb, 128, 0, st>>>(p, b, nblk);
+        wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
         wide_d2upd_kernel<<<rows_grid, kWT, 0, st>>>(p, b, it);
     }
     // Lloyd: passes until every worker of the batch stopped
