@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda.h>
 #include <dlfcn.h>
@@ -45,6 +46,13 @@ int fail(int code, const std::string& msg) {
     } while (0)
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
+
+// Every entry point binds its device and clears this host thread's last CUDA error first: a failed
+// runtime call elsewhere in the process (non-sticky) must not surface as this call's launch error.
+inline void bind_device(int device) {
+    cudaSetDevice(device);
+    cudaGetLastError();
+}
 
 // ------------------------------------------------------------ device buffers
 struct DevBuf {
@@ -905,13 +913,18 @@ int hpcg_ctx_create(int device, hpcg_ctx** out) {
     }
     c->own_stream = true;
     c->rec_slot = acquire_rec_slot();
+    // L2 fetch granularity for the random 64-B sample rows (diagnostic switch while it is measured)
+    if (const char* g = getenv("HPCG_L2_FETCH")) {
+        const size_t v = (size_t)atoi(g);
+        if (v) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, v);
+    }
     *out = c;
     return HPCG_OK;
 }
 
 int hpcg_ctx_destroy(hpcg_ctx* ctx) {
     if (!ctx) return HPCG_OK;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (ctx->rec_slot >= 0) {
         cudaDeviceSynchronize();  // no launch of this context may still read its record slot
         release_rec_slot(ctx->rec_slot);
@@ -926,7 +939,7 @@ int hpcg_ctx_destroy(hpcg_ctx* ctx) {
 
 int hpcg_ctx_set_stream(hpcg_ctx* ctx, void* st) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     ctx->stream = static_cast<cudaStream_t>(st);  // NULL: legacy default stream
     ctx->own_stream = false;
@@ -934,7 +947,7 @@ int hpcg_ctx_set_stream(hpcg_ctx* ctx, void* st) {
 }
 
 int hpcg_ctx_synchronize(hpcg_ctx* ctx) {
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     CU(cudaStreamSynchronize(ctx->stream));
     return HPCG_OK;
 }
@@ -956,7 +969,7 @@ int hpcg_ctx_enable_timing(hpcg_ctx* ctx, int enable) {
 
 int hpcg_ctx_kernel_times(hpcg_ctx* ctx, int64_t* counts, double* total_ms) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     for (int c = 0; c < 2; ++c) {
         for (auto& ev : ctx->pending[c]) {
             float ms = 0.f;
@@ -976,7 +989,7 @@ int hpcg_ctx_kernel_times(hpcg_ctx* ctx, int64_t* counts, double* total_ms) {
 
 int hpcg_probe_fma_peak(hpcg_ctx* ctx, double* tfma) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     DevBuf out;
@@ -1005,7 +1018,7 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
                         hpcg_dataset** out) {
     if (m < 1 || n < 1) return fail(HPCG_EINVAL, "Dataset: needs at least one row and one column");
     if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     void* d = nullptr;
     const size_t bytes = (size_t)m * (size_t)n * dsize(dtype);
     size_t have = 0;
@@ -1071,7 +1084,7 @@ int hpcg_dataset_wrap_sharded(hpcg_ctx* ctx, const void* const* shard_dev, const
     }
     // shards resident on other devices of this process: the gathers read them over NVLink (peer
     // access; IPC-opened shards of other processes are already mapped)
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     for (int i = 0; i < nshards; ++i) {
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, shard_dev[i]) != cudaSuccess) {
@@ -1129,7 +1142,7 @@ int hpcg_ipc_export(const void* dev_ptr, void* handle_out) {
 }
 
 int hpcg_ipc_open(hpcg_ctx* ctx, const void* handle, void** dev_ptr_out) {
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     cudaIpcMemHandle_t h;
     uint64_t off = 0;
     std::memcpy(&h, handle, sizeof h);
@@ -1141,7 +1154,7 @@ int hpcg_ipc_open(hpcg_ctx* ctx, const void* handle, void** dev_ptr_out) {
 }
 
 int hpcg_ipc_close(hpcg_ctx* ctx, void* dev_ptr, const void* handle) {
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     uint64_t off = 0;
     std::memcpy(&off, static_cast<const char*>(handle) + sizeof(cudaIpcMemHandle_t), 8);
     CU(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - off));
@@ -1162,7 +1175,7 @@ const void* hpcg_dataset_device_ptr(const hpcg_dataset* ds) { return ds->X; }
 int hpcg_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_host, const uint8_t* deg, int64_t k,
                 int require_valid, int32_t* labels_host, int64_t* counts_host, double* cost, int64_t* n_d) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (k < 1) return fail(HPCG_EINVAL, "assign: need at least one centroid");
     const int64_t n = ds->n;
     std::vector<double> cv;
@@ -1213,7 +1226,7 @@ int hpcg_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_host, con
 int hpcg_assign_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_dev, int64_t k_valid,
                     int32_t* labels_dev, double* cost_dev) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (k_valid < 1) return fail(HPCG_EINVAL, "assign: need at least one centroid");
     if (int rc = check_shape(ds->dtype, ds->n, k_valid)) return rc;
     if (ctx->s_b.bytes < (size_t)k_valid * 4) {
@@ -1234,7 +1247,7 @@ int hpcg_assign_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_dev, 
 // ---------------------------------------------------------------- gather
 int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, int64_t s, void* S_host) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (s < 1 || s > ds->m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
     for (int64_t i = 0; i < s; ++i)
         if (idx_host[i] < 0 || idx_host[i] >= ds->m) return fail(HPCG_EINVAL, "gather: row index out of range");
@@ -1271,7 +1284,7 @@ int hpcg_sample_indices(hpcg_ctx* ctx, int64_t m, int64_t s, uint64_t key, uint3
     if (!ctx || !idx_out) return fail(HPCG_EINVAL, "sample_indices: null argument");
     if (s < 1 || s > m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     uint32_t a, b;
     float inv_b;
     SamplePRP::moduli((uint64_t)m, a, b, inv_b);
@@ -1292,7 +1305,7 @@ int hpcg_sample_gather_dev(hpcg_ctx* ctx, const hpcg_dataset* ds, int64_t W, int
     if (s < 1 || s > ds->m) return fail(HPCG_EINVAL, "draw_sample: sample size must be in [1, m]");
     if (W < 1 || W > 65535) return fail(HPCG_EINVAL, "sample_gather: worker count must be in [1, 65535]");
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     ShardTable t;
     t.n = ds->nshards;
     for (int i = 0; i < ds->nshards; ++i) {
@@ -1381,7 +1394,7 @@ int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_
                              int32_t* stop, int64_t* n_d, int32_t* filled, int32_t* labels, int64_t* counts,
                              double* history, int32_t hist_cap, int32_t* hist_len) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     const int64_t n = ds->n;
     if (W < 1) return fail(HPCG_EINVAL, "worker_step: need at least one worker");
     if (s < 1) return fail(HPCG_EINVAL, "seeding: empty sample");
@@ -1509,6 +1522,7 @@ int hpcg_worker_step_batched(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_
 struct hpcg_engine {
     hpcg_ctx* ctx = nullptr;
     const hpcg_dataset* ds = nullptr;
+    int device = 0;  // the context's device (destroy must not read a context freed before it)
     hpcg_engine_cfg cfg{};
     int64_t W = 0, k = 0, n = 0, s = 0, R = 0;
     int64_t round = 0;
@@ -1868,7 +1882,7 @@ int hpcg_ctx_attach_comm(hpcg_ctx* ctx, int32_t nranks, int32_t rank, const void
     const NcclApi& a = nccl_api();
     if (!a.ok) return fail(HPCG_ENCCL, a.why);
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (ctx->comm) {
         a.comm_destroy(ctx->comm);
         ctx->comm = nullptr;
@@ -1893,7 +1907,7 @@ int hpcg_ctx_comm_info(const hpcg_ctx* ctx, int32_t* nranks, int32_t* rank) {
 
 int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_cfg* c, hpcg_engine** out) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     hpcg_engine_cfg cfg = *c;
     if (cfg.strategy == HPCG_INNER) cfg.n_workers = 1;  // engine.hpp:446
     // EngineConfig::validate (engine.hpp:70-86)
@@ -1922,6 +1936,7 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
 
     auto* e = new hpcg_engine;
     e->ctx = ctx;
+    e->device = ctx->device;
     e->ds = ds;
     e->cfg = cfg;
     e->W = cfg.n_workers;
@@ -2007,7 +2022,7 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
 int hpcg_engine_set_exchange(hpcg_engine* e, int32_t nranks, int32_t rank, hpcg_allgather_fn fn, void* user) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HPCG_EINVAL, "set_exchange: bad rank layout");
     if (e->round > 0) return fail(HPCG_EINVAL, "set_exchange: rounds already run");
     if (!fn && nranks > 1 && (!ctx->comm || ctx->nranks != nranks || ctx->rank != rank))
@@ -2050,7 +2065,7 @@ int hpcg_engine_set_exchange(hpcg_engine* e, int32_t nranks, int32_t rank, hpcg_
 int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     cudaStream_t st = ctx->stream;
     const int64_t W = e->W, k = e->k, kn = k * e->n;
     e->cfg.master_seed = master_seed;
@@ -2084,7 +2099,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
 int hpcg_engine_import_best(hpcg_engine* e, double obj, int64_t worker, const double* C, const uint8_t* f) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     cudaStream_t st = ctx->stream;
     int64_t ver = 0;
     CU(d2h(&ver, e->sh_ver.as<int64_t>(), 1, st));
@@ -2102,7 +2117,7 @@ int hpcg_engine_import_best(hpcg_engine* e, double obj, int64_t worker, const do
 
 int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
-    cudaSetDevice(e->ctx->device);
+    bind_device(e->ctx->device);
     for (int64_t i = 0; i < n_rounds; ++i) {
         if (e->round >= e->R) return fail(HPCG_EINVAL, "engine: max_samples rounds already run");
         const double now = !e->wall ? 0.0 : e->xr > 1 ? (e->round ? e->common_now : 0.0) : e->elapsed();
@@ -2113,7 +2128,7 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
 
 int hpcg_engine_run(hpcg_engine* e) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
-    cudaSetDevice(e->ctx->device);
+    bind_device(e->ctx->device);
     while (e->round < e->R) {
         // run_wall_clock (engine.hpp:353-357): one clock reading per round decides the stop,
         // the phase and the carry-over
@@ -2136,7 +2151,7 @@ int hpcg_engine_set_trace(hpcg_engine* e, int64_t* trace_dev, int32_t mode) {
 
 int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
-    cudaSetDevice(e->ctx->device);
+    bind_device(e->ctx->device);
     unsigned long long v = 0;
     CU(d2h(&v, e->nd_total.as<unsigned long long>(), 1, e->ctx->stream));
     CU(cudaStreamSynchronize(e->ctx->stream));
@@ -2146,7 +2161,7 @@ int hpcg_engine_distance_evals(hpcg_engine* e, int64_t* n_d) {
 
 int hpcg_engine_export_best(hpcg_engine* e, double* obj_out, int64_t* worker_out, double* C_out, uint8_t* f_out) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
-    cudaSetDevice(e->ctx->device);
+    bind_device(e->ctx->device);
     hpcg_ctx* ctx = e->ctx;
     int32_t wk = -1;
     if (obj_out) CU(d2h(obj_out, e->sh_obj.as<double>(), 1, ctx->stream));
@@ -2324,7 +2339,7 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
                        int64_t* trace_len) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     if (e->xr > 1) {
         (void)publications;
         (void)pub_cap;  // multi-rank: read the (replicated) log with hpcg_engine_publications
@@ -2483,7 +2498,7 @@ int hpcg_engine_round_outcome(hpcg_engine* e, double* objective, int32_t* iterat
                               uint8_t* accepted, int32_t* filled) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     const size_t W = (size_t)e->W;
     if (objective) CU(d2h(objective, e->objb.as<double>(), W, ctx->stream));
     if (iterations) CU(d2h(iterations, e->iters.as<int32_t>(), W, ctx->stream));
@@ -2498,7 +2513,7 @@ int hpcg_engine_round_outcome(hpcg_engine* e, double* objective, int32_t* iterat
 int hpcg_engine_publications(hpcg_engine* e, double* publications, int64_t cap, int64_t* n_out) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     int64_t npub = 0;
     CU(d2h(&npub, e->pub_count.as<int64_t>(), 1, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -2514,7 +2529,7 @@ int hpcg_engine_publications(hpcg_engine* e, double* publications, int64_t cap, 
 int hpcg_engine_worker_incumbents(hpcg_engine* e, double* C_out, uint8_t* f_out, double* obj_out) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     hpcg_ctx* ctx = e->ctx;
-    cudaSetDevice(ctx->device);
+    bind_device(ctx->device);
     const int64_t W = e->W, k = e->k, kn = k * e->n;
     if (C_out) CU(d2h(C_out, e->inc_c.as<double>(), (size_t)(W * kn), ctx->stream));
     if (f_out) CU(d2h(f_out, e->inc_f.as<uint8_t>(), (size_t)(W * k), ctx->stream));
@@ -2525,7 +2540,7 @@ int hpcg_engine_worker_incumbents(hpcg_engine* e, double* C_out, uint8_t* f_out,
 
 int hpcg_engine_destroy(hpcg_engine* e) {
     if (e) {
-        cudaSetDevice(e->ctx->device);
+        bind_device(e->device);
         delete e;
     }
     return HPCG_OK;
