@@ -725,11 +725,36 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         auto d2_update_flagged = [&](int c, bool tr) {
             int cnt = 0;
             const double* cd = sh.cand[c];
+            // exact distances of the listed rows, up to two per lane with interleaved fp64 chains
+            // (narrow rows; wider rows one per lane); flushed once 64 are listed (list_cap >= 96)
+            constexpr int kPer = NP * sizeof(T) <= 64 ? 2 : 1;
             auto flush = [&](bool all) {
-                while (cnt >= 32 || (all && cnt > 0)) {
-                    const int take = cnt < 32 ? cnt : 32;
+                while (cnt >= 32 * kPer || (all && cnt > 0)) {
+                    const int take = cnt < 32 * kPer ? cnt : 32 * kPer;
                     if (tr && lane == 0) atomicAdd(&sh.exact_rows1, take);
-                    if (lane < take) {
+                    if constexpr (kPer == 2) {
+                        if (lane + 32 < take) {
+                            const int ra = (int)wlist[lane], rb = (int)wlist[lane + 32];
+                            T xa[NP], xb[NP];
+                            load_row_T<T, NP>(samp, ra, xa);
+                            load_row_T<T, NP>(samp, rb, xb);
+                            double a = 0.0, b = 0.0;
+#pragma unroll
+                            for (int d = 0; d < NP; ++d) {
+                                const double cv = cd[d];
+                                const double ea = __dsub_rn((double)xa[d], cv), eb = __dsub_rn((double)xb[d], cv);
+                                a = __dadd_rn(a, __dmul_rn(ea, ea));
+                                b = __dadd_rn(b, __dmul_rn(eb, eb));
+                            }
+                            d2[ra] = fmin(d2[ra], a);
+                            d2[rb] = fmin(d2[rb], b);
+                        } else if (lane < take) {
+                            const int r = (int)wlist[lane];
+                            T xr[NP];
+                            load_row_T<T, NP>(samp, r, xr);
+                            d2[r] = fmin(d2[r], exact_dist_regs<T, NP>(xr, cd));
+                        }
+                    } else if (lane < take) {
                         const int r = (int)wlist[lane];
                         T xr[NP];
                         load_row_T<T, NP>(samp, r, xr);
@@ -1110,8 +1135,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
                 if (it == 0 && p.trace_mode == 1 && !exact) stamp(20);
                 // lane e < 2*ncand sums column e over ranks (rank order), then broadcast
                 double col = 0.0;
-                if (lane < 2 * ncand)
-                    for (int rr = 0; rr < C; ++rr) col += rxc[rr * xs + lane];
+                if (lane < 2 * ncand) {
+                    double v[16];  // the loads first (independent), then the rank-order sum
+#pragma unroll
+                    for (int rr = 0; rr < 16; ++rr) v[rr] = rr < C ? rxc[rr * xs + lane] : 0.0;
+#pragma unroll
+                    for (int rr = 0; rr < 16; ++rr)
+                        if (rr < C) col += v[rr];
+                }
                 double tc[kMaxCandidates], te[kMaxCandidates];
                 double bc = __longlong_as_double(0x7ff0000000000000LL), be = 0.0;
                 best = 0;

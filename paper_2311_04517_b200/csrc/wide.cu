@@ -17,6 +17,7 @@
 // sub/mul/add), so labels and argmins are exact by construction. Every reduction is in a fixed
 // order (row blocks in order, CTAs in order), so results are deterministic.
 #include <algorithm>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include "launch.h"
@@ -42,9 +43,10 @@ struct WState {
 
 struct WideBufs {  // device scratch for one worker batch
     void* S = nullptr;
-    double *Cm = nullptr, *d2 = nullptr, *dc = nullptr, *cand = nullptr, *btot = nullptr, *bcost = nullptr,
+    double *Cm = nullptr, *d2 = nullptr, *cand = nullptr, *btot = nullptr, *bcost = nullptr,
            *part = nullptr, *lastcnt = nullptr;
     uint8_t* flags = nullptr;
+    uint8_t* rflag = nullptr;  // [Wb][s] per-row candidate flags of the current K-means++ slot
     int32_t *pend = nullptr, *labels = nullptr, *active = nullptr;
     WState* st = nullptr;
 };
@@ -274,32 +276,57 @@ __device__ __forceinline__ void exact_ties(unsigned tie, const T* __restrict__ S
 }
 
 // ---------------------------------------------------------------- gather + init
-template <typename T>
-__global__ void wide_gather_kernel(const StepParams p, int w0, T* __restrict__ S) {
-    const int w = blockIdx.y, wl = w0 + w;
+// Sample rows into S[w][i][:] (engine.hpp:165-177 with the launch's indices): per warp 32 rows, one
+// index per lane (PRP / explicit / contiguous), then the rows' V-byte chunks chunk-major across the
+// warp with the row addresses shuffled -- every lane's loads issued before its stores, so a narrow
+// row (config 5: 32 B) costs one vector load per lane instead of a warp per row.
+template <int V>
+__global__ void __launch_bounds__(256) wide_gather_kernel(const StepParams p, int w0, int64_t rowb,
+                                                          unsigned char* __restrict__ S) {
+    using VT = typename std::conditional<V == 16, uint4, typename std::conditional<V == 8, uint2, uint32_t>::type>::type;
+    const int w = blockIdx.y, wl = w0 + w, lane = threadIdx.x & 31;
     const int64_t s = p.s;
-    const int n = p.n;
+    const int64_t i0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    if (i0 >= s) return;
     SamplePRP prp;
     if (p.sample_mode == 1)
         prp = SamplePRP::make(p.key, p.round, (uint32_t)(p.worker_base + wl), (uint64_t)p.m, p.prp_a, p.prp_b,
                               p.prp_inv_b);
-    const T* X = static_cast<const T*>(p.X);
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (kWT / 32);
-    for (int64_t i = (int64_t)blockIdx.x * (kWT / 32) + (threadIdx.x >> 5); i < s; i += warps) {
-        int64_t g = 0;
-        if (lane == 0) {
-            if (p.sample_mode == 0)
-                g = p.idx[(int64_t)wl * s + i];
-            else if (p.sample_mode == 1)
-                g = (int64_t)prp((uint64_t)i);
-            else
-                g = (int64_t)wl * s + i;
+    const int64_t i = i0 + lane;
+    int64_t g = 0;
+    if (i < s) {
+        if (p.sample_mode == 0)
+            g = p.idx[(int64_t)wl * s + i];
+        else if (p.sample_mode == 1)
+            g = (int64_t)prp((uint64_t)i);
+        else
+            g = (int64_t)wl * s + i;
+    }
+    const unsigned char* src;
+    if (p.nshards > 1) {
+        int sh = 0;
+        while (sh + 1 < p.nshards && g >= p.shard_end[sh]) ++sh;
+        src = static_cast<const unsigned char*>(p.shard_ptr[sh]) + (g - (sh ? p.shard_end[sh - 1] : 0)) * rowb;
+    } else {
+        src = static_cast<const unsigned char*>(p.X) + g * rowb;
+    }
+    unsigned char* dst = S + ((int64_t)w * s + i0) * rowb;
+    const int cpr = (int)(rowb / V), total = 32 * cpr;
+    constexpr int U = 8;
+    for (int e0 = 0; e0 < total; e0 += 32 * U) {
+        VT v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * 32 + lane, r = e / cpr, q = e - r * cpr;
+            const unsigned char* sp = reinterpret_cast<const unsigned char*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), r & 31));
+            if (e < total && i0 + r < s) v[u] = __ldg(reinterpret_cast<const VT*>(sp + (int64_t)q * V));
         }
-        g = __shfl_sync(0xffffffffu, g, 0);
-        const T* src = p.nshards > 1 ? row_ptr<T>(p, g) : X + g * n;
-        T* dst = S + ((int64_t)w * s + i) * n;
-        for (int d = lane; d < n; d += 32) dst[d] = src[d];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * 32 + lane, r = e / cpr;
+            if (e < total && i0 + r < s) reinterpret_cast<VT*>(dst)[e] = v[u];
+        }
     }
 }
 
@@ -528,11 +555,12 @@ __global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nbl
     for (int d = lane; d < n; d += 32) cd[d] = (double)x[d];
 }
 
-// candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): an fp32 screen decides
-// the rows the candidate provably cannot improve (value d2_i, exact); the others get the
-// reference distance. Per-row values are kept for the winner's D^2 update; block partials by warp
-// shuffle trees and then the warps in order, so the costs are exact sums in a fixed order. Each
-// CTA covers kCostBPC consecutive 256-row blocks (records built once).
+// candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93): an fp32 screen decides the
+// rows a candidate provably cannot improve (value d2_i, exact); the others get the reference
+// distance. Per row one flag byte (bit c: candidate c may improve the row) is the work list of the
+// winner's D^2 update, which recomputes only those rows -- no per-candidate value array. Each CTA
+// covers kCostBPC consecutive 256-row blocks; a thread sums its rows in order, then a warp tree and
+// the warps in order give one partial per (CTA, candidate): costs are exact sums in a fixed order.
 constexpr int kCostBPC = 8;  // 256-row blocks per CTA of the candidate-cost pass
 
 template <typename T>
@@ -558,13 +586,20 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
     __syncthreads();
     const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
     const bool vec = sizeof(T) == 4 && (n & 3) == 0;
+    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
     const int64_t s = p.s;
     const int blk0 = blockIdx.x * kCostBPC, blk1 = min(nblk, blk0 + kCostBPC);
-    for (int blk = blk0; blk < blk1; ++blk) {  // the candidate records are built once per CTA
+    const T* Sw = static_cast<const T*>(b.S) + (int64_t)w * s * n;
+    const double* d2w = b.d2 + (int64_t)w * s;
+    uint8_t* flw = b.rflag + (int64_t)w * s;
+    double acc[kMaxCandidates];
+#pragma unroll
+    for (int c = 0; c < kMaxCandidates; ++c) acc[c] = 0.0;
+    for (int blk = blk0; blk < blk1; ++blk) {
         const int64_t i = (int64_t)blk * kSeedRows + threadIdx.x;
-        const bool valid = i < s;
-        const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + (valid ? i : 0)) * n;
-        const double d2i = valid ? b.d2[(int64_t)w * s + i] : 0.0;
+        if (i >= s) break;
+        const T* x = Sw + i * n;
+        const double d2i = d2w[i];
         // screen: s~_c = |c|^2 + x.(-2c); dist~_c = |x|^2 + s~_c
         float2 a[kMaxCandidates], nn = make_float2(0.f, 0.f);
 #pragma unroll
@@ -584,26 +619,32 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
         }
         const float xx = nn.x + nn.y, xn = sqrtf(xx) * 1.0001f;
         const float f2 = __double2float_ru(d2i);
-        for (int c = 0; c < ncand; ++c) {
-            double v = 0.0;
-            if (valid) {
-                v = d2i;
-                const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
-                const float dt = xx + (a[c].x + a[c].y);
-                if (!(dt - kappa * sc * sc > f2))  // may improve: the reference distance
-                    v = fmin(d2i, dist1<T>(x, n, cand + (int64_t)c * n, sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0));
-                b.dc[((int64_t)w * kMaxCandidates + c) * s + i] = v;
+        uint32_t fl = 0;
+#pragma unroll
+        for (int c = 0; c < kMaxCandidates; ++c) {
+            if (c >= ncand) break;
+            double v = d2i;
+            const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
+            const float dt = xx + (a[c].x + a[c].y);
+            if (!(dt - kappa * sc * sc > f2)) {  // may improve: the reference distance
+                v = fmin(d2i, dist1<T>(x, n, cand + (int64_t)c * n, vecd));
+                fl |= 1u << c;
             }
-            v = warp_sum(v);  // block partial: warp trees, then the warps in order (fixed order)
-            if (lane == 0) wred[c][warp] = v;
+            acc[c] += v;
         }
-        __syncthreads();
-        if (threadIdx.x < ncand) {
-            double tot = 0.0;
-            for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
-            b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blk] = tot;
-        }
-        __syncthreads();
+        flw[i] = (uint8_t)fl;
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCandidates; ++c) {
+        if (c >= ncand) break;
+        const double v = warp_sum(acc[c]);  // warp trees, then the warps in order (fixed order)
+        if (lane == 0) wred[c][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ncand) {
+        double tot = 0.0;
+        for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
+        b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
     }
 }
 
@@ -616,10 +657,11 @@ __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
     if (!slot_live(*stp)) return;
     __shared__ double tot_s[kMaxCandidates];
     __shared__ int best_s;
-    if (warp < ncand) {
+    if (warp < ncand) {  // one partial per cost CTA (wide_cost_kernel)
         const double* bc_c = b.bcost + ((int64_t)w * kMaxCandidates + warp) * nblk;
+        const int ncta = (nblk + kCostBPC - 1) / kCostBPC;
         double t = 0.0;
-        for (int q = lane; q < nblk; q += 32) t += bc_c[q];
+        for (int q = lane; q < ncta; q += 32) t += bc_c[q];
         t = warp_sum(t);
         if (lane == 0) tot_s[warp] = t;
     }
@@ -650,12 +692,22 @@ __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
     }
 }
 
+// D^2 update with the slot's winner (seeding.hpp:100-103): only rows its cost pass flagged can
+// change; they get min(d2, the reference distance) -- the same value the cost pass added
+template <typename T>
 __global__ void wide_d2upd_kernel(const StepParams p, WideBufs b, int it_expect) {
     const int w = blockIdx.y;
     const WState& st = b.st[w];
     if (st.it != it_expect + 1 || st.seed_stop) return;  // this slot was decided for w
     const int64_t s = p.s, i = (int64_t)blockIdx.x * kWT + threadIdx.x;
-    if (i < s) b.d2[(int64_t)w * s + i] = b.dc[((int64_t)w * kMaxCandidates + st.best) * s + i];
+    if (i >= s) return;
+    if (!((b.rflag[(int64_t)w * s + i] >> st.best) & 1u)) return;
+    const int n = p.n;
+    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
+    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
+    const double* cd = b.cand + ((int64_t)w * kMaxCandidates + st.best) * n;
+    double* d2 = b.d2 + (int64_t)w * s + i;
+    *d2 = fmin(*d2, dist1<T>(x, n, cd, vecd));
 }
 
 // ---------------------------------------------------------------- Lloyd
@@ -1113,7 +1165,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     static const int rpc = getenv("HPCG_WIDE_RPC") ? atoi(getenv("HPCG_WIDE_RPC")) : 24;  // diagnostics
     // the geometry of a batch of the engine's size (p.geo_W), so CTA partitions -- and the sums --
     // do not depend on how many workers this rank holds
-    const size_t per_worker_b = (size_t)s * ((size_t)n * sizeof(T) + 8 * (kMaxCandidates + 1) + 4) + 1024;
+    const size_t per_worker_b = (size_t)s * ((size_t)n * sizeof(T) + 8 + 1 + 4) + 1024;
     const int Wgeo = p.geo_W > 0 ? (int)std::max<size_t>(1, std::min<size_t>((size_t)p.geo_W, ((size_t)4 << 30) /
                                                                                         std::max<size_t>(per_worker_b, 1)))
                                  : Wb;
@@ -1129,7 +1181,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         return o;
     };
     const size_t oS = take((size_t)Wb * s * n * sizeof(T)), oC = take((size_t)Wb * kn * 8),
-                 od2 = take((size_t)Wb * s * 8), odc = take((size_t)Wb * kMaxCandidates * s * 8),
+                 od2 = take((size_t)Wb * s * 8), orf = take((size_t)Wb * s),
                  ocand = take((size_t)Wb * kMaxCandidates * n * 8), obt = take((size_t)Wb * (nblk + 1) * 8),
                  obc = take((size_t)Wb * kMaxCandidates * nblk * 8), opart = take((size_t)Wb * G * pd * 8),
                  olc = take((size_t)Wb * k * 8), ofl = take((size_t)Wb * k), opend = take((size_t)Wb * k * 4),
@@ -1146,7 +1198,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     b.S = c8 + oS;
     b.Cm = reinterpret_cast<double*>(c8 + oC);
     b.d2 = reinterpret_cast<double*>(c8 + od2);
-    b.dc = reinterpret_cast<double*>(c8 + odc);
+    b.rflag = reinterpret_cast<uint8_t*>(c8 + orf);
     b.cand = reinterpret_cast<double*>(c8 + ocand);
     b.btot = reinterpret_cast<double*>(c8 + obt);
     b.bcost = reinterpret_cast<double*>(c8 + obc);
@@ -1159,8 +1211,18 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     b.st = reinterpret_cast<WState*>(c8 + ost);
 
     const dim3 rows_grid((unsigned)((s + kWT - 1) / kWT), (unsigned)Wb);
-    wide_gather_kernel<T><<<dim3((unsigned)std::min<int64_t>((s + 7) / 8, 4096), (unsigned)Wb), kWT, 0, st>>>(
-        p, w0, static_cast<T*>(b.S));
+    {
+        const int64_t rowb = (int64_t)n * sizeof(T);
+        const dim3 gg((unsigned)((s + 255) / 256), (unsigned)Wb);
+        unsigned char* Sb = static_cast<unsigned char*>(b.S);
+        const bool aligned = p.nshards > 1 || (reinterpret_cast<uintptr_t>(p.X) & 15) == 0;
+        if (rowb % 16 == 0 && aligned)
+            wide_gather_kernel<16><<<gg, 256, 0, st>>>(p, w0, rowb, Sb);
+        else if (rowb % 8 == 0)
+            wide_gather_kernel<8><<<gg, 256, 0, st>>>(p, w0, rowb, Sb);
+        else
+            wide_gather_kernel<4><<<gg, 256, 0, st>>>(p, w0, rowb, Sb);
+    }
     wide_init_kernel<T><<<Wb, kWT, 0, st>>>(p, w0, b);
     {
         const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
@@ -1193,7 +1255,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         wide_cost_kernel<T><<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, cost_smem, st>>>(
             p, b, nblk);
         wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
-        wide_d2upd_kernel<<<rows_grid, kWT, 0, st>>>(p, b, it);
+        wide_d2upd_kernel<T><<<rows_grid, kWT, 0, st>>>(p, b, it);
     }
     // Lloyd: passes until every worker of the batch stopped
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
@@ -1263,7 +1325,7 @@ cudaError_t launch_objective_wide(int dtype, const ObjParams& p, int* nblocks, c
 // pass accumulator in shared memory), any s; workers in batches bounded by the scratch size.
 cudaError_t launch_step_wide(int dtype, const StepParams& p, cudaStream_t st, std::string* why) {
     const size_t row_bytes = (size_t)p.n * (dtype == 0 ? 4 : 8);
-    const size_t per_worker = (size_t)p.s * (row_bytes + 8 * (kMaxCandidates + 1) + 4) + 1024;
+    const size_t per_worker = (size_t)p.s * (row_bytes + 8 + 1 + 4) + 1024;
     const size_t budget = (size_t)4 << 30;
     const int Wb = (int)std::max<size_t>(1, std::min<size_t>((size_t)p.W, budget / std::max<size_t>(per_worker, 1)));
     for (int w0 = 0; w0 < p.W; w0 += Wb) {
