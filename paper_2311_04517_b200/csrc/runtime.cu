@@ -913,11 +913,6 @@ int hpcg_ctx_create(int device, hpcg_ctx** out) {
     }
     c->own_stream = true;
     c->rec_slot = acquire_rec_slot();
-    // L2 fetch granularity for the random 64-B sample rows (diagnostic switch while it is measured)
-    if (const char* g = getenv("HPCG_L2_FETCH")) {
-        const size_t v = (size_t)atoi(g);
-        if (v) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, v);
-    }
     *out = c;
     return HPCG_OK;
 }
@@ -1272,16 +1267,6 @@ int hpcg_gather(hpcg_ctx* ctx, const hpcg_dataset* ds, const int64_t* idx_host, 
 }
 
 // the device sample definition of RngMode::philox (SamplePRP), for tests and reproduction
-// every worker's sample indices of one PHILOX round (the step kernel then gathers from explicit
-// indices -- the same rows -- and can prefetch a later worker's rows into L2)
-__global__ void round_indices_kernel(uint64_t m, uint32_t a, uint32_t b, float inv_b, uint64_t key, uint32_t round,
-                                     int32_t worker_base, int64_t s, int64_t* out) {
-    const int w = blockIdx.y;
-    const SamplePRP prp = SamplePRP::make(key, round, (uint32_t)(worker_base + w), m, a, b, inv_b);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < s) out[(int64_t)w * s + i] = (int64_t)prp((uint64_t)i);
-}
-
 __global__ void sample_prp_kernel(uint64_t m, uint32_t a, uint32_t b, float inv_b, uint64_t key, uint32_t round,
                                   uint32_t worker, int64_t s, int64_t* out) {
     const SamplePRP prp = SamplePRP::make(key, round, worker, m, a, b, inv_b);
@@ -1558,8 +1543,6 @@ struct hpcg_engine {
     DevBuf xsend, xrecv, xerr;
     std::vector<unsigned char> xhost;  // host staging of a caller collective
     double common_now = 0.0;           // wall clock, multi-rank: the latest clock of the last exchange
-    bool pre_idx = false;              // PHILOX: indices precomputed per round (explicit-index gather)
-    int pf_stride = 0;                 // L2 prefetch distance in workers (0: off)
     // reference-RNG replay state
     std::vector<Mt64> streams;
     std::vector<int64_t> h_idx, h_fr;
@@ -1783,21 +1766,6 @@ int engine_round(hpcg_engine* e, double now) {
     p.geo_W = (int)std::max<int64_t>(W, e->xWtot);
     p.sample_mode = reference ? 0 : 1;
     p.idx = e->d_idx.as<int64_t>();
-    if (e->pre_idx) {
-        const dim3 g((unsigned)((s + 255) / 256), (unsigned)W);
-        round_indices_kernel<<<g, 256, 0, ctx->stream>>>((uint64_t)p.m, p.prp_a, p.prp_b, p.prp_inv_b, e->key,
-                                                        (uint32_t)r, e->cfg.worker_base, s, e->d_idx.as<int64_t>());
-        CU(cudaGetLastError());
-        ctx->launches += 1;
-        p.sample_mode = 0;
-        if (e->pf_stride > 0) {
-            StepGeometry g2;
-            std::string w2;
-            if (step_geometry(e->ds->dtype, (int)n, s, (int)k, (int)e->cfg.candidates,
-                              (int)std::max<int64_t>(W, e->xWtot), &g2, &w2) == cudaSuccess)
-                p.pf_stride = std::max(1, g2.active_clusters) * e->pf_stride;
-        }
-    }
     p.key = e->key;
     p.round = (uint32_t)r;
     p.worker_base = e->cfg.worker_base;
@@ -2013,13 +1981,6 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     e->ucap = std::max<int64_t>(1, k * cfg.candidates);
     ALLOC(d_fr, W * 8);
     ALLOC(d_un, W * e->ucap * 8);
-    {
-        const char* pi = getenv("HPCG_PRE_IDX");
-        e->pre_idx = !reference && (pi ? atoi(pi) != 0 : false);
-        const char* pf = getenv("HPCG_PF");
-        e->pf_stride = e->pre_idx && pf ? atoi(pf) : 0;
-    }
-    if (e->pre_idx) ALLOC(d_idx, W * e->s * 8);
     if (reference) {
         ALLOC(d_idx, W * e->s * 8);
         e->h_idx.assign((size_t)(W * e->s), 0);

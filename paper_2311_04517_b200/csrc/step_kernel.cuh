@@ -88,9 +88,6 @@ struct StepParams {
     uint8_t* inc_f;
     double* inc_obj;
     uint8_t* accepted;
-    // L2 prefetch of a later worker's sample rows (explicit indices only): every CTA of worker wl
-    // prefetches its row range of worker wl + pf_stride (the one the next free cluster will take)
-    int32_t pf_stride;
     // optional phase timeline (ns, %globaltimer) per CTA: [W*C][kTraceSlots]
     int64_t* trace;
     int32_t trace_mode;  // 0: first Lloyd pass in detail, 1: first K-means++ slot in detail
@@ -607,15 +604,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
         sh.n_valid = nv;
     }
     mark();  // 2: sample landed
-    if (p.pf_stride > 0 && p.sample_mode == 0 && wl + p.pf_stride < p.W) {
-        // rows of the worker a cluster will take after this one: into L2 (evict_last) now, so its
-        // gather hits L2 instead of HBM; one coalesced index load + one prefetch per row
-        const int64_t* nidx = p.idx + (int64_t)(wl + p.pf_stride) * s + r0;
-        for (int li = tid; li < nr; li += kStepThreads) {
-            const T* rp = row_ptr<T>(p, nidx[li]);
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(rp));
-        }
-    }
     cluster.sync();  // sample rows of every CTA now visible cluster-wide (DSMEM)
     mark();  // 3: cluster synced
 

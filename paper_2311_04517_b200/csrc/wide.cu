@@ -104,6 +104,22 @@ __device__ __forceinline__ double dist1(const T* __restrict__ x, int n, const do
     return acc;
 }
 
+// fixed-order tree sum over a CTA of AT threads; result in every thread
+template <int AT>
+__device__ double cta_sum_t(double v, double* red) {
+    const int tid = threadIdx.x;
+    red[tid] = v;
+    __syncthreads();
+#pragma unroll
+    for (int o = AT / 2; o > 0; o >>= 1) {
+        if (tid < o) red[tid] = red[tid] + red[tid + o];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
 // fixed-order tree sum over the CTA (kWT threads); result valid in thread 0
 __device__ double cta_sum(double v, double* red) {
     const int tid = threadIdx.x;
@@ -725,8 +741,9 @@ __global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
 // one pass for CTA g of worker w: rows chunk_range(s, G, g) in rounds of kWT; labels by exact
 // strict-< argmin (core.hpp:146-157); per-cluster sums of each round's rows (label-sorted, row
 // order) and its cost tree-sum are added to the CTA accumulators in round order
-template <typename T>
-__global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
+template <typename T, int AT>
+__global__ void __launch_bounds__(AT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
+    constexpr int AW = AT / 32;  // warps
     extern __shared__ double wsm[];
     const int w = blockIdx.y, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (b.st[w].done) return;
@@ -735,14 +752,14 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
     double* acc = wsm;                  // [k*n] sums
     double* cnt = acc + kn;             // [k] counts
-    double* red = cnt + k;              // [kWT] tree
-    float* rec = reinterpret_cast<float*>(red + kWT + ((kn + k + kWT) & 1));  // [kpad][n4], 16-B aligned
+    double* red = cnt + k;              // [AT] tree
+    float* rec = reinterpret_cast<float*>(red + AT + ((kn + k + AT) & 1));  // [kpad][n4], 16-B aligned
     float* ccs = rec + (int64_t)kpad * n4;             // [kpad]
-    int* wcnt = reinterpret_cast<int*>(ccs + kpad);    // [8][k] per-warp label counts
-    int* cstart = wcnt + 8 * k;         // [k+1]
-    int* sorted = cstart + k + 1;       // [kWT] label-sorted round rows
+    int* wcnt = reinterpret_cast<int*>(ccs + kpad);    // [AW][k] per-warp label counts
+    int* cstart = wcnt + AW * k;        // [k+1]
+    int* sorted = cstart + k + 1;       // [AT] label-sorted round rows
     __shared__ float cmax_s;
-    for (int64_t e = tid; e < kn + k; e += kWT) acc[e] = 0.0;
+    for (int64_t e = tid; e < kn + k; e += AT) acc[e] = 0.0;
     double cost = 0.0;
     int64_t r0, r1;
     chunk_range(s, G, g, r0, r1);
@@ -761,7 +778,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
     const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
     const bool vec = sizeof(T) == 4 && (n & 3) == 0;                           // float4 screen loads
     const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;           // 16-B sum loads
-    for (int64_t base = r0; base < r1; base += kWT) {
+    for (int64_t base = r0; base < r1; base += AT) {
         const int64_t i = base + tid;
         const bool valid = i < r1;
         int lab = 0;
@@ -783,7 +800,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
             labels[i] = lab;
         }
         // stable counting sort of the round's rows by label
-        for (int e = tid; e < 8 * k; e += kWT) wcnt[e] = 0;
+        for (int e = tid; e < AW * k; e += AT) wcnt[e] = 0;
         __syncthreads();
         const unsigned peers = __match_any_sync(0xffffffffu, valid ? lab : -1);
         const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -795,7 +812,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
                 const int j = j0 + lane;
                 int col = 0;
                 if (j < k)
-                    for (int q = 0; q < 8; ++q) col += wcnt[q * k + j];
+                    for (int q = 0; q < AW; ++q) col += wcnt[q * k + j];
                 int incl = col;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -805,7 +822,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
                 if (j < k) {
                     int run = base + incl - col;
                     cstart[j] = run;
-                    for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < AW; ++q) {
                         const int c = wcnt[q * k + j];
                         wcnt[q * k + j] = run;
                         run += c;
@@ -817,7 +834,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         }
         __syncthreads();
         if (valid) sorted[wcnt[warp * k + lab] + rank] = tid;
-        cost += valid ? bestd : 0.0;  // per-thread running sum (thread t: rows r0 + t + kWT*i, in order)
+        cost += valid ? bestd : 0.0;  // per-thread running sum (thread t: rows r0 + t + AT*i, in order)
         __syncthreads();              // sorted[] complete before the sums read it
         // per-cluster sums of this round: warp w takes clusters w, w+8, ..., walks the cluster's
         // rows in order with lanes over dims (coalesced row loads), then adds to the CTA
@@ -826,7 +843,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
         // lane summing rows gi, gi + RPS, ... in order, then a fixed shuffle tree over gi
         const int LR = n <= 4 ? 1 : n <= 8 ? 2 : n <= 16 ? 4 : n <= 32 ? 8 : n <= 64 ? 16 : 32;
         const int RPS = 32 / LR, gi = lane / LR, dq = (lane % LR) * 4;
-        for (int j = warp; j < k && n <= 128; j += kWT / 32) {
+        for (int j = warp; j < k && n <= 128; j += AW) {
             const int q0 = cstart[j], q1 = cstart[j + 1];
             if (q0 == q1) continue;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -855,7 +872,7 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
                 if (dq + 3 < n) aj[3] += a3;
             }
         }
-        for (int j = warp; j < k && n > 128; j += kWT / 32) {
+        for (int j = warp; j < k && n > 128; j += AW) {
             const int q0 = cstart[j], q1 = cstart[j + 1];
             if (q0 == q1) continue;
             for (int d0 = lane * 4; d0 < n; d0 += 128) {
@@ -876,13 +893,13 @@ __global__ void __launch_bounds__(kWT) wide_assign_kernel(const StepParams p, Wi
                 if (d0 + 3 < n) aj[3] += a3;
             }
         }
-        for (int j = tid; j < k; j += kWT) cnt[j] += (double)(cstart[j + 1] - cstart[j]);
+        for (int j = tid; j < k; j += AT) cnt[j] += (double)(cstart[j + 1] - cstart[j]);
         __syncthreads();
     }
     const int64_t pd = kn + k + 1;
     double* out = b.part + ((int64_t)w * G + g) * pd;
-    for (int64_t e = tid; e < kn + k; e += kWT) out[e] = acc[e];
-    cost = cta_sum(cost, red);  // fixed tree over the threads' running sums
+    for (int64_t e = tid; e < kn + k; e += AT) out[e] = acc[e];
+    cost = cta_sum_t<AT>(cost, red);  // fixed tree over the threads' running sums
     if (tid == 0) out[kn + k] = cost;
 }
 
@@ -1260,9 +1277,11 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     // Lloyd: passes until every worker of the batch stopped
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
-    const size_t smem = (size_t)(kn + k + kWT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
-                        (size_t)(8 * k + k + 1 + kWT) * 4;
-    e = cudaFuncSetAttribute(wide_assign_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the assign pass in rounds of kAT rows (fewer round barriers per row than kWT)
+    constexpr int kAT = 512;
+    const size_t smem = (size_t)(kn + k + kAT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
+                        (size_t)((kAT / 32) * k + k + 1 + kAT) * 4;
+    e = cudaFuncSetAttribute(wide_assign_kernel<T, kAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         if (why) *why = "wide step: k*n too large for the pass accumulator";
         return e;
@@ -1284,7 +1303,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
                                         : launch_wide_tc<2, 16>(p, b, ccw, Wb, sms, stmap, st));
                 if (e != cudaSuccess) return e;
             }
-            wide_assign_kernel<T><<<dim3((unsigned)G, (unsigned)Wb), kWT, smem, st>>>(p, b, G, tc ? 1 : 0);
+            wide_assign_kernel<T, kAT><<<dim3((unsigned)G, (unsigned)Wb), kAT, smem, st>>>(p, b, G, tc ? 1 : 0);
             wide_lloyd_reduce_kernel<<<Wb, kWT, 0, st>>>(p, b, G, w0);
             if ((pass & 3) == 3 || pass == p.max_iters + 1) {  // stop check every few passes
                 wide_count_active_kernel<<<1, 256, 0, st>>>(b, Wb);
