@@ -742,7 +742,7 @@ __global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
 // strict-< argmin (core.hpp:146-157); per-cluster sums of each round's rows (label-sorted, row
 // order) and its cost tree-sum are added to the CTA accumulators in round order
 template <typename T, int AT>
-__global__ void __launch_bounds__(AT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
+__global__ void __launch_bounds__(AT, 1024 / AT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
     constexpr int AW = AT / 32;  // warps
     extern __shared__ double wsm[];
     const int w = blockIdx.y, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1278,7 +1278,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
     // the assign pass in rounds of kAT rows (fewer round barriers per row than kWT)
-    constexpr int kAT = 512;
+    constexpr int kAT = 256;
     const size_t smem = (size_t)(kn + k + kAT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
                         (size_t)((kAT / 32) * k + k + 1 + kAT) * 4;
     e = cudaFuncSetAttribute(wide_assign_kernel<T, kAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
