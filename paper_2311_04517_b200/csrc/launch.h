@@ -28,6 +28,7 @@ cudaError_t step_geometry(int dtype, int n, int64_t s, int k, int ncand, int W, 
 // Grid-wide worker step over samples materialised in HBM (wide.cu): any n, k (k*n <= kWideMaxKN),
 // any s. launch_step falls back to it when the cluster-resident kernel cannot hold the shape.
 constexpr int64_t kWideMaxKN = 16384;
+constexpr int64_t kInnerWideRows = 65536;  // W == 1 from this sample size on: the grid-wide path
 constexpr int kWideMaxN = 4096, kWideMaxK = 4096;
 cudaError_t launch_step_wide(int dtype, const StepParams& p, cudaStream_t st, std::string* why);
 cudaError_t launch_objective_wide(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st);

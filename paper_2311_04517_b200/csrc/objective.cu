@@ -34,7 +34,10 @@ cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeo
     // cluster's shared memory), the grid-wide HBM path otherwise
     const int np = pick_np(dtype, p.n);
     static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
-    if (np != 0 && p.k <= kMaxK && p.candidates <= kMaxCandidates && !force_wide) {
+    // one worker with a large sample (the inner strategy, engine.hpp:243-246, 446): the grid-wide
+    // path spreads its rows over every SM (G CTAs per pass) instead of one <= 16-CTA cluster
+    const bool one_big = (p.geo_W > 0 ? p.geo_W : p.W) == 1 && p.s >= kInnerWideRows;
+    if (np != 0 && p.k <= kMaxK && p.candidates <= kMaxCandidates && !force_wide && !one_big) {
         StepGeometry tmp;
         std::string w2;
         if (step_geometry(dtype, p.n, p.s, p.k, p.candidates, p.geo_W > 0 ? p.geo_W : p.W, &tmp, &w2) == cudaSuccess)
@@ -146,6 +149,7 @@ static cudaError_t launch_tc(const ObjParams& p, const CUtensorMap& tmap, int* n
     nblocks[0] = sms;
     kern<<<sms, TG::THREADS, smem, st>>>(p, tmap);
     if (p.launched) *p.launched += 1;
+    if (p.finalized) *p.finalized = p.cost_out ? 1 : 0;  // the last CTA wrote the fixed-order total
     return cudaGetLastError();
 }
 
@@ -246,6 +250,7 @@ static cudaError_t launch_tcw(const ObjParams& p, int* nblocks, cudaStream_t st)
 }
 
 cudaError_t launch_objective(int dtype, const ObjParams& p, int* nblocks, cudaStream_t st) {
+    if (p.finalized) *p.finalized = 0;  // set by the launchers whose kernel sums its own blocks
     const int np = pick_np(dtype, p.n);
     static const bool force_wide = getenv("HPCG_WIDE") != nullptr;
     static const bool no_tc = getenv("HPCG_OBJ_NO_TC") != nullptr;

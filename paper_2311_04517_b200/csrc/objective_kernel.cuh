@@ -36,7 +36,37 @@ struct ObjParams {
                            // the north star's fp32 mode (1e-5 relative); 0: exact fp64 row cost
     const float* nclo;     // fast_cost: [kv x n] -(c - fl32(c)), the low part of each centre, so a row's
                            // difference is (x - c_hi) - c_lo: error ~2^-24 |x - c| whatever |c| / |x - c|
+                           // (wide-row kernel; the tensor-core kernel derives it in its prologue)
+    double* cost_out;      // optional: the kernel's last CTA sums block_cost in the fixed order of
+    unsigned int* done_ctr;  //   sum_blocks_kernel<<<1, 256>>> into *cost_out (done_ctr: zeroed counter)
+    int* finalized;        // host: set to 1 by a launcher whose kernel wrote *cost_out, else 0
 };
+
+// the fixed-order block-partial sum of sum_blocks_kernel<<<1, 256>>>, run by threads 0..255 of the
+// grid's last CTA (the CTAs' partials published by __threadfence + a ticket counter)
+HPCG_DEV void finalize_block_sums(const ObjParams& p, double* s32) {
+    __shared__ unsigned int s_ticket;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_ticket = atomicAdd(p.done_ctr, 1u);
+    __syncthreads();
+    if (s_ticket != gridDim.x - 1) return;
+    __threadfence();
+    const int tid = threadIdx.x;
+    if (tid < 256) {
+        double v = 0.0;
+        for (int i = tid; i < (int)gridDim.x; i += 256) v += __ldcg(p.block_cost + i);
+        v = warp_sum(v);
+        if ((tid & 31) == 0) s32[tid >> 5] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += s32[w];
+        *p.cost_out = t;
+        *p.done_ctr = 0u;  // ready for the next launch (stream-ordered)
+    }
+}
 
 // valid centre count: the device value when given (the host launched with an upper bound)
 HPCG_DEV int obj_kv(const ObjParams& p) {

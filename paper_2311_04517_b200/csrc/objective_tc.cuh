@@ -141,7 +141,12 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
         const float c2 = j < kv ? (float)(-2.0 * p.C[(int64_t)j * NP + d]) : 0.f;
         Bt[G::elem_off(j, d)] = tf32_rna(c2);
         s_rec[j][d] = c2;
-        s_clo[j][d] = (p.fast_cost && j < kv && d < p.n) ? p.nclo[(int64_t)j * p.n + d] : 0.f;
+        if (p.fast_cost && j < kv) {  // the centre's low part: -(c - fl32(c))
+            const double c = p.C[(int64_t)j * NP + d];
+            s_clo[j][d] = (float)-(c - (double)(float)c);
+        } else {
+            s_clo[j][d] = 0.f;
+        }
     }
     if (tid < N) {
         float cc = 1e38f;
@@ -440,6 +445,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
         for (int w = 0; w < EW; ++w) t += s_wcost[w];
         p.block_cost[blockIdx.x] = t;
     }
+    if (p.cost_out) finalize_block_sums(p, s_wcost);  // s_wcost reused as the 8 warp partials
 }
 
 }  // namespace hpcg

@@ -210,6 +210,7 @@ struct hpcg_ctx {
     int fp32_exact_cost = 0;               // f(C,X) over fp32 data: 1 = exact fp64 row cost, 0 = fp32 mode
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
     DevBuf clo;                           // low parts of the centres of the fp32-mode f(C,X) cost
+    DevBuf done_ctr;                      // CTA ticket counter of the self-finalising f(C,X) kernel
     int rec_slot = -1;                     // constant-bank slot of the objective records
     DevBuf rec_scratch;
     // per-kernel-class event timing (class 0 worker step, 1 objective)
@@ -829,7 +830,7 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
     int launched = 0;
     op.launched = &launched;
     op.fast_cost = (ds->dtype == HPCG_F32 && !ctx->fp32_exact_cost) ? 1 : 0;
-    if (op.fast_cost) {
+    if (op.fast_cost && (ds->n == 64 || ds->n == 128)) {  // the wide-row kernel reads them from global
         const int64_t cnt = (int64_t)kv * ds->n;
         CU(ctx->clo.reserve((size_t)std::max<int64_t>(cnt, 4) * sizeof(float)));
         centre_lo_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 64), 256, 0, ctx->stream>>>(
@@ -853,13 +854,25 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
         op.X = ds->X;
         op.m = ds->m;
         op.labels = labels_dev;
+        // the tensor-core kernel's last CTA writes the total (no separate sum launch)
+        if (!ctx->done_ctr.p) {
+            CU(ctx->done_ctr.reserve(16));
+            CU(cudaMemsetAsync(ctx->done_ctr.p, 0, 16, ctx->stream));
+        }
+        op.cost_out = cost_dev;
+        op.done_ctr = ctx->done_ctr.as<unsigned int>();
+        int fin = 0;
+        op.finalized = &fin;
         int used = nb;
         KTimer kt(ctx, 1);
         CU(launch_objective(ds->dtype, op, &used, ctx->stream));
         kt.done();
-        sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, cost_dev);
-        CU(cudaGetLastError());
-        ctx->launches += launched + 1;
+        if (!fin) {
+            sum_blocks_kernel<<<1, 256, 0, ctx->stream>>>(blocks.as<double>(), used, cost_dev);
+            CU(cudaGetLastError());
+            ctx->launches += 1;
+        }
+        ctx->launches += launched;
         return HPCG_OK;
     }
     // row-sharded X: one pass per shard (labels at the shard's global offset), the shard sums in
