@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
 // to the fp64 centre my_c (lane p's); tb: this warp's 32 x 33 doubles. Per 32-dim chunk the 2 np
 // loads are issued before any use (memory-level parallelism), then the terms go through shared
 // memory so that lane p can add its own pair's terms in ascending d.
-__device__ __noinline__ double warp_exact_pairs(const float* __restrict__ S, int n, int64_t my_row, const double* my_c, int np,
+__device__ double warp_exact_pairs(const float* __restrict__ S, int n, int64_t my_row, const double* my_c, int np,
                                    double* tb) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
@@ -811,14 +811,13 @@ __global__ void __launch_bounds__(kWT) wide_cost_wrow_kernel(const StepParams p,
                         q_c = c;
                         q_d2 = d2i;
                     }
-                    ++nq;
+                    if (++nq == 32) drain();
                 } else if (lane == 0) {
                     acc[c] += d2i;
                 }
             }
             if (lane == 0) flw[i] = (uint8_t)fl;
         }
-        if (nq > 32 - RG * kMaxCandidates) drain();  // one call site: the queue holds a group's pairs
     }
     if (nq) drain();
     if (lane == 0)
