@@ -672,30 +672,23 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
 // terms in ascending d -- the reference distance (core.hpp:100-108) exactly.
 
 // lane p (< np) returns the reference distance of pair p: row my_row (held by lane p; fp32, n dims)
-// to the fp64 centre my_c (lane p's); tb: this warp's 32 x 33 doubles. Per 32-dim chunk the 2 np
-// loads are issued before any use (memory-level parallelism), then the terms go through shared
-// memory so that lane p can add its own pair's terms in ascending d.
+// to the fp64 centre my_c (lane p's); tb: this warp's 32 x 33 doubles
 __device__ double warp_exact_pairs(const float* __restrict__ S, int n, int64_t my_row, const double* my_c, int np,
                                    double* tb) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
     for (int d0 = 0; d0 < n; d0 += 32) {
         const int d = d0 + lane;
-        float xv[32];
-        double cv[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < np; ++q) {
             const int64_t r = __shfl_sync(0xffffffffu, my_row, q);
             const double* c = reinterpret_cast<const double*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_c), q));
-            const bool ok = q < np && d < n;
-            xv[q] = ok ? __ldg(S + r * n + d) : 0.f;
-            cv[q] = ok ? __ldg(c + d) : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const double diff = __dsub_rn((double)xv[q], cv[q]);
-            tb[q * 33 + lane] = __dmul_rn(diff, diff);
+            double t = 0.0;
+            if (d < n) {
+                const double diff = __dsub_rn((double)__ldg(S + r * n + d), c[d]);
+                t = __dmul_rn(diff, diff);
+            }
+            tb[q * 33 + lane] = t;
         }
         __syncwarp();
         if (lane < np) {
@@ -753,71 +746,47 @@ __global__ void __launch_bounds__(kWT) wide_cost_wrow_kernel(const StepParams p,
         }
         nq = 0;
     };
-    constexpr int RG = 8;  // rows per group: their loads are issued together
-    for (int64_t i0 = r0; i0 < r1; i0 += RG) {
-        float a[RG][kMaxCandidates], nn[RG];
+    for (int64_t i = r0; i < r1; ++i) {
+        const float* x = Sw + i * n;
+        float a[kMaxCandidates], nn = 0.f;
 #pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            nn[g] = 0.f;
-#pragma unroll
-            for (int c = 0; c < kMaxCandidates; ++c) a[g][c] = 0.f;
-        }
+        for (int c = 0; c < kMaxCandidates; ++c) a[c] = 0.f;
         for (int d = 4 * lane; d < n; d += 128) {
-            float4 xv[RG];
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + d));
+            nn = fmaf(xv.x, xv.x, fmaf(xv.y, xv.y, fmaf(xv.z, xv.z, fmaf(xv.w, xv.w, nn))));
 #pragma unroll
-            for (int g = 0; g < RG; ++g)
-                xv[g] = i0 + g < r1 ? __ldg(reinterpret_cast<const float4*>(Sw + (i0 + g) * n + d))
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int g = 0; g < RG; ++g) {
-                nn[g] = fmaf(xv[g].x, xv[g].x, fmaf(xv[g].y, xv[g].y, fmaf(xv[g].z, xv[g].z, fmaf(xv[g].w, xv[g].w, nn[g]))));
-#pragma unroll
-                for (int c = 0; c < kMaxCandidates; ++c)
-                    if (c < ncand) {
-                        const float4 cv = *reinterpret_cast<const float4*>(crec + c * n + d);
-                        a[g][c] = fmaf(xv[g].x, cv.x, fmaf(xv[g].y, cv.y, fmaf(xv[g].z, cv.z, fmaf(xv[g].w, cv.w, a[g][c]))));
-                    }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int g = 0; g < RG; ++g) {
-                nn[g] += __shfl_xor_sync(0xffffffffu, nn[g], o);
-#pragma unroll
-                for (int c = 0; c < kMaxCandidates; ++c)
-                    if (c < ncand) a[g][c] += __shfl_xor_sync(0xffffffffu, a[g][c], o);
-            }
-        double d2g[RG];
-#pragma unroll
-        for (int g = 0; g < RG; ++g) d2g[g] = i0 + g < r1 ? d2w[i0 + g] : 0.0;
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            const int64_t i = i0 + g;
-            if (i >= r1) break;
-            const double d2i = d2g[g];
-            const float f2 = __double2float_ru(d2i);
-            const float xn = sqrtf(nn[g]) * 1.0001f;
-            uint32_t fl = 0;
-#pragma unroll
-            for (int c = 0; c < kMaxCandidates; ++c) {
-                if (c >= ncand) break;
-                const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
-                const float dt = nn[g] + (ccn[c] + a[g][c]);
-                if (!(dt - kappa * sc * sc > f2)) {  // may improve: queue (row, c) for the exact distance
-                    fl |= 1u << c;
-                    if (lane == nq) {
-                        q_row = i;
-                        q_c = c;
-                        q_d2 = d2i;
-                    }
-                    if (++nq == 32) drain();
-                } else if (lane == 0) {
-                    acc[c] += d2i;
+            for (int c = 0; c < kMaxCandidates; ++c)
+                if (c < ncand) {
+                    const float4 cv = *reinterpret_cast<const float4*>(crec + c * n + d);
+                    a[c] = fmaf(xv.x, cv.x, fmaf(xv.y, cv.y, fmaf(xv.z, cv.z, fmaf(xv.w, cv.w, a[c]))));
                 }
-            }
-            if (lane == 0) flw[i] = (uint8_t)fl;
         }
+        nn = warp_sum_f(nn);
+#pragma unroll
+        for (int c = 0; c < kMaxCandidates; ++c)
+            if (c < ncand) a[c] = warp_sum_f(a[c]);
+        const double d2i = d2w[i];
+        const float f2 = __double2float_ru(d2i);
+        const float xn = sqrtf(nn) * 1.0001f;
+        uint32_t fl = 0;
+#pragma unroll
+        for (int c = 0; c < kMaxCandidates; ++c) {
+            if (c >= ncand) break;
+            const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
+            const float dt = nn + (ccn[c] + a[c]);
+            if (!(dt - kappa * sc * sc > f2)) {  // may improve: queue (row, c) for the exact distance
+                fl |= 1u << c;
+                if (lane == nq) {
+                    q_row = i;
+                    q_c = c;
+                    q_d2 = d2i;
+                }
+                if (++nq == 32) drain();
+            } else if (lane == 0) {
+                acc[c] += d2i;
+            }
+        }
+        if (lane == 0) flw[i] = (uint8_t)fl;
     }
     if (nq) drain();
     if (lane == 0)
