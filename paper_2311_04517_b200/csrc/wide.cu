@@ -664,184 +664,6 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
     }
 }
 
-// ---- wide fp32 rows (n % 4 == 0, n >= 64: config 4): the candidate-cost pass and the D^2 update
-// with coalesced row access. A warp screens one row at a time (lane l holds dims 4l.., a butterfly
-// sum gives the candidates' screen values), queues the (row, candidate) pairs the screen cannot
-// settle, and evaluates 32 queued pairs at once: per 32-dim chunk the lanes compute the pairs'
-// terms fl(fl(x_d - c_d)^2) (coalesced row reads) into shared memory, then lane p adds its pair's
-// terms in ascending d -- the reference distance (core.hpp:100-108) exactly.
-
-// lane p (< np) returns the reference distance of pair p: row my_row (held by lane p; fp32, n dims)
-// to the fp64 centre my_c (lane p's); tb: this warp's 32 x 33 doubles
-__device__ double warp_exact_pairs(const float* __restrict__ S, int n, int64_t my_row, const double* my_c, int np,
-                                   double* tb) {
-    const int lane = threadIdx.x & 31;
-    double acc = 0.0;
-    for (int d0 = 0; d0 < n; d0 += 32) {
-        const int d = d0 + lane;
-        for (int q = 0; q < np; ++q) {
-            const int64_t r = __shfl_sync(0xffffffffu, my_row, q);
-            const double* c = reinterpret_cast<const double*>(
-                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_c), q));
-            double t = 0.0;
-            if (d < n) {
-                const double diff = __dsub_rn((double)__ldg(S + r * n + d), c[d]);
-                t = __dmul_rn(diff, diff);
-            }
-            tb[q * 33 + lane] = t;
-        }
-        __syncwarp();
-        if (lane < np) {
-            const int jn = min(32, n - d0);
-            for (int j = 0; j < jn; ++j) acc = __dadd_rn(acc, tb[lane * 33 + j]);
-        }
-        __syncwarp();
-    }
-    return acc;
-}
-
-__global__ void __launch_bounds__(kWT) wide_cost_wrow_kernel(const StepParams p, WideBufs b, int nblk) {
-    __shared__ double wred[kMaxCandidates][kWT / 32];
-    extern __shared__ __align__(16) unsigned char wsm_raw[];
-    const int w = blockIdx.y, n = p.n, ncand = p.candidates;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (!slot_live(b.st[w])) return;
-    float* crec = reinterpret_cast<float*>(wsm_raw);                       // [ncand][n] -2c (fp32)
-    double* tball = reinterpret_cast<double*>(wsm_raw + (((size_t)kMaxCandidates * n * 4 + 15) & ~(size_t)15));
-    double* tb = tball + warp * 32 * 33;
-    __shared__ float ccn[kMaxCandidates];
-    const double* cand = b.cand + (int64_t)w * kMaxCandidates * n;
-    for (int e = threadIdx.x; e < ncand * n; e += kWT) crec[e] = (float)(-2.0 * cand[e]);
-    if (threadIdx.x < ncand) {
-        double a = 0.0;
-        for (int d = 0; d < n; ++d) a += cand[(int64_t)threadIdx.x * n + d] * cand[(int64_t)threadIdx.x * n + d];
-        ccn[threadIdx.x] = (float)a;
-    }
-    __syncthreads();
-    const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
-    const int64_t s = p.s;
-    const float* Sw = static_cast<const float*>(b.S) + (int64_t)w * s * n;
-    const double* d2w = b.d2 + (int64_t)w * s;
-    uint8_t* flw = b.rflag + (int64_t)w * s;
-    // this warp's rows: a contiguous slice of the CTA's kCostBPC blocks
-    const int64_t c0 = (int64_t)blockIdx.x * kCostBPC * kSeedRows, c1 = min(s, c0 + (int64_t)kCostBPC * kSeedRows);
-    int64_t r0, r1;
-    chunk_range(c1 - c0, kWT / 32, warp, r0, r1);
-    r0 += c0;
-    r1 += c0;
-    double acc[kMaxCandidates];  // lane 0 holds the warp's per-candidate sums (a fixed order)
-#pragma unroll
-    for (int c = 0; c < kMaxCandidates; ++c) acc[c] = 0.0;
-    int64_t q_row = 0;  // lane q's queued pair
-    int q_c = 0, nq = 0;
-    double q_d2 = 0.0;
-    auto drain = [&]() {
-        const double dist = warp_exact_pairs(Sw, n, q_row, cand + (int64_t)q_c * n, nq, tb);
-        const double v = lane < nq ? fmin(q_d2, dist) : 0.0;
-#pragma unroll
-        for (int c = 0; c < kMaxCandidates; ++c) {
-            if (c >= ncand) break;
-            const double vc = warp_sum(lane < nq && q_c == c ? v : 0.0);
-            if (lane == 0) acc[c] += vc;
-        }
-        nq = 0;
-    };
-    for (int64_t i = r0; i < r1; ++i) {
-        const float* x = Sw + i * n;
-        float a[kMaxCandidates], nn = 0.f;
-#pragma unroll
-        for (int c = 0; c < kMaxCandidates; ++c) a[c] = 0.f;
-        for (int d = 4 * lane; d < n; d += 128) {
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + d));
-            nn = fmaf(xv.x, xv.x, fmaf(xv.y, xv.y, fmaf(xv.z, xv.z, fmaf(xv.w, xv.w, nn))));
-#pragma unroll
-            for (int c = 0; c < kMaxCandidates; ++c)
-                if (c < ncand) {
-                    const float4 cv = *reinterpret_cast<const float4*>(crec + c * n + d);
-                    a[c] = fmaf(xv.x, cv.x, fmaf(xv.y, cv.y, fmaf(xv.z, cv.z, fmaf(xv.w, cv.w, a[c]))));
-                }
-        }
-        nn = warp_sum_f(nn);
-#pragma unroll
-        for (int c = 0; c < kMaxCandidates; ++c)
-            if (c < ncand) a[c] = warp_sum_f(a[c]);
-        const double d2i = d2w[i];
-        const float f2 = __double2float_ru(d2i);
-        const float xn = sqrtf(nn) * 1.0001f;
-        uint32_t fl = 0;
-#pragma unroll
-        for (int c = 0; c < kMaxCandidates; ++c) {
-            if (c >= ncand) break;
-            const float sc = xn + sqrtf(ccn[c]) * 1.0001f;
-            const float dt = nn + (ccn[c] + a[c]);
-            if (!(dt - kappa * sc * sc > f2)) {  // may improve: queue (row, c) for the exact distance
-                fl |= 1u << c;
-                if (lane == nq) {
-                    q_row = i;
-                    q_c = c;
-                    q_d2 = d2i;
-                }
-                if (++nq == 32) drain();
-            } else if (lane == 0) {
-                acc[c] += d2i;
-            }
-        }
-        if (lane == 0) flw[i] = (uint8_t)fl;
-    }
-    if (nq) drain();
-    if (lane == 0)
-#pragma unroll
-        for (int c = 0; c < kMaxCandidates; ++c)
-            if (c < ncand) wred[c][warp] = acc[c];
-    __syncthreads();
-    if (threadIdx.x < ncand) {
-        double tot = 0.0;
-        for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
-        b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
-    }
-}
-
-// D^2 update for wide fp32 rows: each warp queues its slice's winner-flagged rows and evaluates
-// them 32 at a time with warp_exact_pairs
-__global__ void __launch_bounds__(kWT) wide_d2upd_wrow_kernel(const StepParams p, WideBufs b, int it_expect) {
-    extern __shared__ double tball2[];
-    const int w = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const WState& st = b.st[w];
-    if (st.it != it_expect + 1 || st.seed_stop) return;
-    const int n = p.n, best = st.best;
-    const int64_t s = p.s;
-    const int64_t c0 = (int64_t)blockIdx.x * kWT * 8, c1 = min(s, c0 + (int64_t)kWT * 8);  // 2048 rows per CTA
-    if (c0 >= s) return;
-    int64_t r0, r1;
-    chunk_range(c1 - c0, kWT / 32, warp, r0, r1);
-    r0 += c0;
-    r1 += c0;
-    const float* Sw = static_cast<const float*>(b.S) + (int64_t)w * s * n;
-    const double* cd = b.cand + ((int64_t)w * kMaxCandidates + best) * n;
-    double* d2w = b.d2 + (int64_t)w * s;
-    const uint8_t* flw = b.rflag + (int64_t)w * s;
-    double* tb = tball2 + warp * 32 * 33;
-    for (int64_t base = r0; base < r1; base += 32) {
-        const int64_t i = base + lane;
-        const bool f = i < r1 && ((flw[i] >> best) & 1u);
-        const unsigned m = __ballot_sync(0xffffffffu, f);
-        if (!m) continue;
-        const int rank = __popc(m & ((1u << lane) - 1u));
-        // compact the flagged rows to lanes 0..np-1
-        int64_t my_row = 0;
-        for (int q = 0; q < 32; ++q) {
-            const int64_t rq = __shfl_sync(0xffffffffu, i, q);
-            const bool fq = (m >> q) & 1u;
-            const int rk = __popc(m & ((1u << q) - 1u));
-            if (fq && rk == lane) my_row = rq;
-        }
-        (void)rank;
-        const int np = __popc(m);
-        const double dist = warp_exact_pairs(Sw, n, my_row, cd, np, tb);
-        if (lane < np) d2w[my_row] = fmin(d2w[my_row], dist);
-    }
-}
-
 // winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot. Warp c
 // sums candidate c's block partials (lanes strided, then a shuffle tree: a fixed order).
 __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
@@ -1433,16 +1255,6 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     const size_t cost_smem = (size_t)ncand * ((n + 3) & ~3) * 4;
-    // wide fp32 rows: the warp-cooperative cost pass and D^2 update (coalesced rows)
-    const bool wrow = sizeof(T) == 4 && n % 4 == 0 && n >= 64 && !getenv("HPCG_WIDE_ROWCOST");
-    const size_t wrow_smem = (((size_t)kMaxCandidates * n * 4 + 15) & ~(size_t)15) + (size_t)(kWT / 32) * 32 * 33 * 8;
-    if (slots > 0 && wrow) {
-        e = cudaFuncSetAttribute(wide_cost_wrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wrow_smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(wide_d2upd_wrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((kWT / 32) * 32 * 33 * 8));
-        if (e != cudaSuccess) return e;
-    }
     if (slots > 0) {
         e = cudaFuncSetAttribute(wide_cost_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem);
         if (e != cudaSuccess) return e;
@@ -1457,18 +1269,10 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         wide_cdf_kernel<<<dim3((unsigned)((nblk + 7) / 8), (unsigned)Wb), 256, 0, st>>>(p, b, nblk);
         wide_cdfscan_kernel<<<(unsigned)Wb, 32, scan_smem, st>>>(b, nblk, staged);
         wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
-        if (wrow) {
-            wide_cost_wrow_kernel<<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, wrow_smem,
-                                    st>>>(p, b, nblk);
-            wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
-            wide_d2upd_wrow_kernel<<<dim3((unsigned)((s + kWT * 8 - 1) / (kWT * 8)), (unsigned)Wb), kWT,
-                                     (size_t)(kWT / 32) * 32 * 33 * 8, st>>>(p, b, it);
-        } else {
-            wide_cost_kernel<T><<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, cost_smem,
-                                  st>>>(p, b, nblk);
-            wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
-            wide_d2upd_kernel<T><<<rows_grid, kWT, 0, st>>>(p, b, it);
-        }
+        wide_cost_kernel<T><<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, cost_smem, st>>>(
+            p, b, nblk);
+        wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
+        wide_d2upd_kernel<T><<<rows_grid, kWT, 0, st>>>(p, b, it);
     }
     // Lloyd: passes until every worker of the batch stopped
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
