@@ -88,16 +88,6 @@ HPCG_DEV void tmem_ld16(uint32_t addr, uint32_t* v) {
         : "r"(addr));
 }
 HPCG_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// the same wait, tied to the 16 destination registers of an earlier tcgen05.ld so that no use of
-// them can be scheduled before it
-HPCG_DEV void tmem_wait_ld16(uint32_t* v) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
-                   "+r"(v[15])
-                 :
-                 : "memory");
-}
 HPCG_DEV float tf32_rna(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -122,7 +112,7 @@ HPCG_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 // KPS: centre pairs screened (ceil(kv / 2) of the N / 2 columns pairs; a compile-time count keeps
 // the top-2 branch free)
 template <int NP, int N, int KPS>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
     objective_tc_kernel(const ObjParams p, const __grid_constant__ CUtensorMap tmap) {
     using TG = TcGeo<NP, N>;
     using G = Geo<float, NP>;
@@ -270,35 +260,17 @@ __global__ void __maxnreg__(112)
         uint32_t pb = 0;
         int64_t row = ((int64_t)blockIdx.x + (int64_t)tp * gridDim.x) * TG::TM + rb * TG::M + r;
         const int64_t row_step = STEP * (int64_t)gridDim.x * TG::TM;
-        // the screened values of a tile: tcgen05.ld issued one tile ahead (N = 16), so the TMEM
-        // latency of tile i + STEP hides under the epilogue of tile i
-        constexpr bool kPipe = N == 16;
-        uint32_t v[N];
-        auto tmem_issue = [&](int bb, uint32_t(&vv)[N]) {
-            const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((bb * TG::TR + rb) * N);
-            tmem_ld16(taddr, vv);
-            if constexpr (N == 32) tmem_ld16(taddr + 16, vv + 16);
-        };
-        auto tmem_release = [&](int bb, uint32_t(&vv)[N]) {
-            tmem_wait_ld16(vv);
-            if constexpr (N == 32) tmem_wait_ld16(vv + 16);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[bb]);
-        };
-        if (kPipe && tp < my) {
+        for (int i = tp; i < my; i += STEP, row += row_step) {
             mbar_wait_sleep(&tfull[b], pb);
             tc_fence_after();
-            tmem_issue(b, v);
-            tmem_release(b, v);
-        }
-        for (int i = tp; i < my; i += STEP, row += row_step) {
-            if constexpr (!kPipe) {
-                mbar_wait_sleep(&tfull[b], pb);
-                tc_fence_after();
-                tmem_issue(b, v);
-                tmem_release(b, v);
-            }
+            uint32_t v[N];
+            const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((b * TG::TR + rb) * N);
+            tmem_ld16(taddr, v);
+            if constexpr (N == 32) tmem_ld16(taddr + 16, v + 16);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
             // the row: its stage has landed (the MMAs that read it have completed)
             const float* tile = reinterpret_cast<const float*>(ring + s * TILE);
             float x[NP];
@@ -316,13 +288,6 @@ __global__ void __maxnreg__(112)
             if (b += STEP, b >= NB) {
                 b -= NB;
                 pb ^= 1u;
-            }
-            const bool nxt = kPipe && i + STEP < my;
-            uint32_t vn[N];
-            if (nxt) {  // the next tile's values, in flight during this row's epilogue
-                mbar_wait_sleep(&tfull[b], pb);
-                tc_fence_after();
-                tmem_issue(b, vn);
             }
             {
                 // top-2 of d~_j = |c_j|^2 - 2 x.c_j over all N columns (unused ones screen to 1e38);
@@ -465,11 +430,6 @@ __global__ void __maxnreg__(112)
                     if (labels_out) labels_out[row] = remap[lab];
                     if (counts_out) atomicAdd(counts_out + remap[lab], 1ULL);
                 }
-            }
-            if (nxt) {
-                tmem_release(b, vn);
-#pragma unroll
-                for (int q = 0; q < N; ++q) v[q] = vn[q];
             }
         }
         cost = warp_sum(cost);
