@@ -19,8 +19,12 @@
 
 namespace hpcg {
 
-constexpr int kStepThreads = 512;  // one CTA per SM, 16 warps
+#ifndef HPCG_STEP_THREADS
+#define HPCG_STEP_THREADS 512
+#endif
+constexpr int kStepThreads = HPCG_STEP_THREADS;  // 512: one CTA per SM, 16 warps; 256: two CTAs per SM
 constexpr int kStepWarps = kStepThreads / 32;
+constexpr int kStepMinBlocks = 512 / kStepThreads;  // keeps the register cap at 128 per thread
 constexpr int kMaxK = 32;          // label fits u8 and the per-warp partial table fits smem
 constexpr int kMaxCandidates = 4;  // K-means++ candidates per slot (reference default 3) in one sweep
 
@@ -185,7 +189,7 @@ __host__ __device__ inline SmemLayout step_layout(int rows_cap, int k, int ncand
     L.labels = L.scratch;
     L.pos = up(L.labels + rows_cap);
     L.perm = up(L.pos + rows_cap * 2);
-    L.wpart = up(L.perm + (rows_cap + (kStepWarps + 1) * G::GROUP) * 2);
+    L.wpart = up(L.perm + rows_cap * 2);
     const int lloyd_end = L.wpart + kStepWarps * part_d * 8;
     L.d2 = L.scratch;    // seeding only
     L.gidx = L.scratch;  // gather only
@@ -214,8 +218,8 @@ struct StepShared {  // static smem: per-step scalars and exchange slots
     uint32_t whit[kStepWarps][kMaxCandidates];
     double units[kMaxK][kMaxCandidates];     // K-means++ draws of every slot (unit interval)
     float cnorm[kMaxK];  // |c_j| (fp32, rounded up) of the current screen records
-    int32_t wcnt[kStepWarps][kMaxK];  // per-warp label counts (counting sort)
-    int32_t woff[kStepWarps][kMaxK];  // sorted-order offset of (warp, label)
+    uint16_t wcnt[kStepWarps][kMaxK];  // per-warp label counts (counting sort; rows per CTA < 2^16)
+    uint16_t woff[kStepWarps][kMaxK];  // sorted-order offset of (warp, label)
     int32_t cstart[kMaxK + 1];        // sorted-order start of each cluster
     int32_t decision;  // 0 continue, 1 done
     int32_t exact_passes;  // K-means++ slots that needed the exact cost pass (diagnostic)
@@ -307,6 +311,15 @@ HPCG_DEV float fmin3f(float a, float b, float c) {  // three-input min (sm_100 F
     return r;
 }
 
+// |x|^2 of a row in fp32 (one FFMA2 chain)
+template <int NPF>
+HPCG_DEV float row_sq(const float2 (&x)[NPF / 2]) {
+    float2 nn = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NPF / 2; ++q) nn = __ffma2_rn(x[q], x[q], nn);
+    return nn.x + nn.y;
+}
+
 // K-means++ screens, expanded form: dist ~ s + x.(-2c), s = |x|^2 + |c|^2, with the seed
 // (s, or s minus the bound) folded into the first chain; two rows per call, four independent
 // FFMA2 chains. |screen - exact| <= kScreenK (|x| + |c|)^2 <= 2 kScreenK s (the fp32 rounding
@@ -391,7 +404,7 @@ HPCG_DEV double exact_dist(const T* samp, int row, const double* c, int n) {
 
 // ------------------------------------------------------------------ the kernel
 template <typename T, int NP>
-__global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const StepParams p) {
+__global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kernel(const StepParams p) {
     using G = Geo<T, NP>;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
@@ -616,8 +629,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
     if (sh.n_pending > 0) {
         const int np_ = sh.n_pending;
         const int ncand = p.candidates;
-        float* xsq = reinterpret_cast<float*>(smem + L.xnorm);  // |x|^2 (fp32) per local row
         uint32_t* wlist = reinterpret_cast<uint32_t*>(smem + L.wlist) + warp * list_cap(ncand);
+        float* xsq = reinterpret_cast<float*>(smem + L.xnorm);  // |x|^2 (fp32) per local row
         uint8_t* nflag = smem + L.nflag;  // bit c: the cost screen could not settle (row, candidate c)
         // screen bound B = kScreenK2 * s (see screen_exp2); s itself is rounded, hence the 1.001
         constexpr float kScreenK2 = 2.002f * 2.0f * (float)(G::NPF / 2 + 12) * 5.9604645e-8f;
@@ -628,10 +641,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) worker_step_kernel(const Step
             d2[li] = __longlong_as_double(0x7ff0000000000000LL);
             float2 x2[G::NPF / 2];
             load_row_f32<T, NP>(samp, li, x2);
-            float2 nn = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int q = 0; q < G::NPF / 2; ++q) nn = __ffma2_rn(x2[q], x2[q], nn);
-            xsq[li] = nn.x + nn.y;
+            xsq[li] = row_sq<G::NPF>(x2);
         }
         // fp32 screen record of slot c of sh.cand (-2c and |c|^2); one warp, caller syncs
         auto make_candf = [&](int c) {
