@@ -24,7 +24,7 @@ namespace hpcg {
 #endif
 constexpr int kStepThreads = HPCG_STEP_THREADS;  // 512: one CTA per SM, 16 warps; 256: two CTAs per SM
 constexpr int kStepWarps = kStepThreads / 32;
-constexpr int kStepMinBlocks = 512 / kStepThreads;  // keeps the register cap at 128 per thread
+constexpr int kStepMinBlocks = kStepThreads >= 512 ? 1 : 512 / kStepThreads;  // 256: two CTAs per SM at 128 registers
 constexpr int kMaxK = 32;          // label fits u8 and the per-warp partial table fits smem
 constexpr int kMaxCandidates = 4;  // K-means++ candidates per slot (reference default 3) in one sweep
 
@@ -128,7 +128,7 @@ struct Geo {
     static constexpr int NPF = (NP + 1) & ~1;                  // fp32 screen dims (pairs)
     static constexpr int CSR = ((NPF + 2) + 3) & ~3;           // screen record floats (16-B mult)
     static constexpr int RST = NPF + 2;                        // centre-pair record stride (float2)
-    static constexpr int R = NP <= 16 ? 4 : 2;                 // rows per thread in the assign pass
+    static constexpr int R = (NP <= 16 && kStepThreads <= 512) ? 4 : 2;  // rows per thread in the assign pass
     static constexpr int GROUP = 32 * R;                       // rows per warp group
     static constexpr int LPR = NP <= 1 ? 1 : NP <= 2 ? 2 : NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;
     static constexpr int RPS = 32 / LPR;                       // rows per warp step in the update
@@ -221,7 +221,9 @@ struct StepShared {  // static smem: per-step scalars and exchange slots
     uint16_t wcnt[kStepWarps][kMaxK];  // per-warp label counts (counting sort; rows per CTA < 2^16)
     uint16_t woff[kStepWarps][kMaxK];  // sorted-order offset of (warp, label)
     int32_t cstart[kMaxK + 1];        // sorted-order start of each cluster
-    int32_t decision;  // 0 continue, 1 done
+    int32_t decision;  // K-means++ slot: 1 = the approximate costs decided the winner
+    int32_t best_c;    // K-means++ slot: winning candidate
+    double cdf_P, cdf_T;  // K-means++ slot: this rank's CDF offset and the cluster total
     int32_t exact_passes;  // K-means++ slots that needed the exact cost pass (diagnostic)
     int32_t exact_rows;    // rows given an exact distance in the D^2 updates (diagnostic)
     int32_t exact_rows1;   // ... in the first K-means++ slot's update (diagnostic)
@@ -451,8 +453,10 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
     double* rx1 = part + 2 * C * kXchSmall;            // [2][C][sl]   reduce-scatter inputs
     double* rx2 = rx1 + 2 * C * sl;                    // [2][C*sl]    all-gathered totals
     uint32_t xcount = 0, xph[2] = {0u, 0u};
-    // all-to-all of nv <= kXchSmall scalars: returns [C][xs] slots in rank order
-    auto exchange = [&](int nv, auto&& value_of) -> const double* {
+    // all-to-all of nv <= kXchSmall scalars: returns [C][xs] slots in rank order. w0_only: only
+    // warp 0 waits for (and may read) the slots; it publishes what the others need through shared
+    // memory before a __syncthreads
+    auto exchange = [&](int nv, auto&& value_of, bool w0_only = false) -> const double* {
         const int par = (int)(xcount++ & 1);
         double* rx = rxs + par * C * xs;
         uint64_t* bar = &sh.xbar[par];
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             const double v = value_of(e);
             for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(slot_local + e * 8, r), v, mapa_u32(rbar_local, r));
         }
-        mbar_wait_cluster(bar, xph[par]);
+        if (!w0_only || warp == 0) mbar_wait_cluster(bar, xph[par]);
         xph[par] ^= 1u;
         return rx;
     };
@@ -899,21 +903,22 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             }
             __syncthreads();
             if (it == 0 && p.trace_mode == 1) mark();  // 5: CDF local done
-            const double* rxt = exchange(1, [&](int) { return sh.cta_total; });
+            const double* rxt = exchange(1, [&](int) { return sh.cta_total; }, true);
             if (it == 0 && p.trace_mode == 1) mark();  // 6: CDF exchange complete
-            // P = sum of lower ranks' totals (rank order); total = P_{C-1} + T_{C-1}
-            double P = 0.0, total = 0.0;
-            {
-                double acc = 0.0;
-                for (int rr = 0; rr < C; ++rr) {
-                    const double tr = rxt[rr * xs];
-                    if (rr == cr) P = acc;
-                    if (rr == C - 1)
-                        total = acc + tr;
-                    else
-                        acc += tr;
+            // P = sum of lower ranks' totals (rank order); total = P_{C-1} + T_{C-1}: one thread,
+            // published to the CTA
+            if (tid == 0) {
+                double acc = 0.0, P0 = 0.0;
+                for (int rr = 0; rr < C - 1; ++rr) {
+                    if (rr == cr) P0 = acc;
+                    acc += rxt[rr * xs];
                 }
+                if (cr == C - 1) P0 = acc;
+                sh.cdf_P = P0;
+                sh.cdf_T = acc + rxt[(C - 1) * xs];
             }
+            __syncthreads();
+            const double P = sh.cdf_P, total = sh.cdf_T;
             if (!(total > 0.0)) break;  // distinct rows exhausted (seeding.hpp:87)
             // (2) candidate draws u_c = unit * total; first global row with cum > u_c
             double u[kMaxCandidates];
@@ -1039,11 +1044,13 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                     for (int i = 0; i < R; ++i)
                         if (rbase + i * kStepThreads < nr) nflag[rbase + i * kStepThreads] = (uint8_t)fl[i];
                 };
-                // two rows per thread per step while any lane of the warp has a second row
+                // two rows per thread per step while any lane of the warp has a second row (wider
+                // CTAs run at a lower register cap: one row per step)
                 int r = tid;
-                for (; r - lane + kStepThreads < nr; r += 2 * kStepThreads) rows(IntC<2>{}, r);
+                if constexpr (kStepThreads <= 512)
+                    for (; r - lane + kStepThreads < nr; r += 2 * kStepThreads) rows(IntC<2>{}, r);
                 if (it == 0 && p.trace_mode == 1) stamp(17);
-                if (r - lane < nr) rows(IntC<1>{}, r);
+                for (; r - lane < nr; r += kStepThreads) rows(IntC<1>{}, r);
                 if (it == 0 && p.trace_mode == 1) stamp(18);
                 // midpoint and half-width per candidate; the slack covers the fp32 lane and warp sums.
                 // The 2 NC butterfly sums run interleaved (same per-value order as warp_sum_f).
@@ -1135,45 +1142,51 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             int best = 0;
             auto exchange_decide = [&](bool exact) -> bool {
                 __syncthreads();
-                const double* rxc = exchange(2 * ncand, [&](int e) {
-                    const int c = e < ncand ? e : e - ncand;
-                    double v = 0.0;
-                    for (int w2 = 0; w2 < kStepWarps; ++w2) v += e < ncand ? sh.wsum[w2][c] : sh.werr[w2][c];
-                    return v;
-                });
+                const double* rxc = exchange(
+                    2 * ncand,
+                    [&](int e) {
+                        const int c = e < ncand ? e : e - ncand;
+                        double v = 0.0;
+                        for (int w2 = 0; w2 < kStepWarps; ++w2) v += e < ncand ? sh.wsum[w2][c] : sh.werr[w2][c];
+                        return v;
+                    },
+                    true);
                 if (it == 0 && p.trace_mode == 1 && !exact) mark();  // 11: cost exchange complete
                 if (it == 0 && p.trace_mode == 1 && !exact) stamp(20);
-                // lane e < 2*ncand sums column e over ranks (rank order), then broadcast
-                double col = 0.0;
-                if (lane < 2 * ncand) {
-                    double v[16];  // the loads first (independent), then the rank-order sum
+                // warp 0 decides (lane e < 2*ncand sums column e over ranks in rank order) and
+                // publishes the decision to the CTA
+                if (warp == 0) {
+                    double col = 0.0;
+                    if (lane < 2 * ncand)
+                        for (int rr = 0; rr < C; ++rr) col += rxc[rr * xs + lane];
+                    double tc[kMaxCandidates], te[kMaxCandidates];
+                    double bc = __longlong_as_double(0x7ff0000000000000LL), be = 0.0;
+                    int b0 = 0;
 #pragma unroll
-                    for (int rr = 0; rr < 16; ++rr) v[rr] = rr < C ? rxc[rr * xs + lane] : 0.0;
+                    for (int c = 0; c < kMaxCandidates; ++c) {
+                        tc[c] = (exact ? 0.0 : total) + __shfl_sync(0xffffffffu, col, c);
+                        te[c] = __shfl_sync(0xffffffffu, col, (ncand + c) & 31);
+                        if (c >= ncand) continue;
+                        te[c] += 1e-9 * fabs(tc[c]);  // summation-order slack
+                        if (tc[c] < bc) {
+                            bc = tc[c];
+                            be = te[c];
+                            b0 = c;
+                        }
+                    }
+                    bool dec = true;
+                    if (!exact)
 #pragma unroll
-                    for (int rr = 0; rr < 16; ++rr)
-                        if (rr < C) col += v[rr];
-                }
-                double tc[kMaxCandidates], te[kMaxCandidates];
-                double bc = __longlong_as_double(0x7ff0000000000000LL), be = 0.0;
-                best = 0;
-#pragma unroll
-                for (int c = 0; c < kMaxCandidates; ++c) {
-                    tc[c] = (exact ? 0.0 : total) + __shfl_sync(0xffffffffu, col, c);
-                    te[c] = __shfl_sync(0xffffffffu, col, (ncand + c) & 31);
-                    if (c >= ncand) continue;
-                    te[c] += 1e-9 * fabs(tc[c]);  // summation-order slack
-                    if (tc[c] < bc) {
-                        bc = tc[c];
-                        be = te[c];
-                        best = c;
+                        for (int c = 0; c < kMaxCandidates; ++c)
+                            if (c < ncand && c != b0 && !(tc[c] - te[c] > bc + be)) dec = false;
+                    if (lane == 0) {
+                        sh.best_c = b0;
+                        sh.decision = dec ? 1 : 0;
                     }
                 }
-                bool decided = true;
-                if (!exact)
-#pragma unroll
-                    for (int c = 0; c < kMaxCandidates; ++c)
-                        if (c < ncand && c != best && !(tc[c] - te[c] > bc + be)) decided = false;
-                return decided;
+                __syncthreads();
+                best = sh.best_c;
+                return sh.decision != 0;
             };
             switch (ncand) {
                 case 1: approx_costs(IntC<1>{}); break;
