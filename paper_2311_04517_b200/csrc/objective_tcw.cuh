@@ -25,8 +25,10 @@ struct TcwGeo {
     static constexpr int NPW = 32 * NA;                   // row width (floats)
     static constexpr int SUB = M * 128;                   // bytes per K-atom sub-tile
     static constexpr int TILE = NA * SUB;                 // bytes per stage
-    static constexpr int STAGES = 196608 / TILE < 6 ? 196608 / TILE : 6;
     static constexpr int BSUB = N * 128;                  // bytes per K-atom of the B tile
+    static constexpr int CEN = N * NPW * 4;               // bytes of one fp32 centre table (hi or lo)
+    // ring stages in what is left of 208 KB after the B tile and the two centre tables
+    static constexpr int STAGES = (212992 - NA * BSUB - 2 * CEN) / TILE < 6 ? (212992 - NA * BSUB - 2 * CEN) / TILE : 6;
     static constexpr int TCOLS = 512;
     static constexpr int NB = TCOLS / N;                  // TMEM tile buffers
     static constexpr int EPI_WARPS = 8;
@@ -39,8 +41,13 @@ struct TcwGeo {
 template <int NA>
 __host__ __device__ inline int objective_tcw_smem() {
     using TG = TcwGeo<NA>;
-    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB + TG::N * TG::NPW * 4;  // + fp32 -c (fp32-mode cost)
+    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB + 2 * TG::CEN;  // + fp32 -c hi / lo (fp32-mode cost)
 }
+
+// fp32 centre tables of the row cost: chunk-major [NPW/4][N][4], so 32 lanes reading chunk c of 32
+// different centres touch 32 distinct 16-B slots of one 512-B span (no bank conflicts)
+template <int N>
+HPCG_DEV int cen_off(int j, int d) { return (((d >> 2) * N + j) << 2) + (d & 3); }
 
 // byte offset of float d of row r inside a tile of NA [rows x 128 B] SWIZZLE_128B atoms
 HPCG_DEV uint32_t sw128_off(int rows, int r, int d) {
@@ -64,12 +71,16 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
     const int kv = obj_kv(p);
     const double* __restrict__ Cg = p.C;  // [kv x NPW] fp64 centres (L1-resident)
 
-    float* negc = reinterpret_cast<float*>(Bt + NA * TG::BSUB);  // [N][NPW] fp32 -c (fp32-mode row cost)
+    // fp32 -c as hi + lo (hi = -fl32(c), lo = -(c - fl32(c))) for the fp32-mode row cost
+    float* negc = reinterpret_cast<float*>(Bt + NA * TG::BSUB);
+    float* neglo = negc + N * NPW;
     for (int e = tid; e < N * NPW; e += TG::THREADS) {
         const int j = e / NPW, d = e - j * NPW;
-        const float c2 = j < kv ? (float)(-2.0 * Cg[(int64_t)j * NPW + d]) : 0.f;
+        const double c = j < kv ? Cg[(int64_t)j * NPW + d] : 0.0;
+        const float c2 = (float)(-2.0 * c);
         *reinterpret_cast<float*>(Bt + sw128_off(N, j, d)) = tf32_rna(c2);
-        negc[e] = 0.5f * c2;  // exact: -fl32(c)
+        negc[cen_off<N>(j, d)] = 0.5f * c2;  // exact: -fl32(c)
+        neglo[cen_off<N>(j, d)] = (float)-(c - (double)(float)c);
     }
     if (tid < N) {
         float cc = 1e38f;
@@ -203,37 +214,43 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
                     p1[q] = fminf(p1[q], p1[q + w]);
                 }
             int lab = __float_as_int(p1[0]) & TMASK;
-            // one pass over the row: |x|^2 (fp32) and the fp64 cost to the screened centre
-            auto row_cost = [&](int j, float* nn_out) -> double {
-                if (p.fast_cost) {  // fp32 mode: (x - c~)^2 in fp32 FFMA2 chains, widened once per row
-                    const float* nc = negc + j * NPW;
-                    const float* nl = p.nclo + (int64_t)j * NPW;  // low parts (L1-resident, 16 KB)
-                    float2 a0 = make_float2(0.f, 0.f), a1 = a0, nn2 = a0;
+            // the fp64 cost to the screened centre, one pass over the row's chunks of the stage
+            // (row base and swizzle phase hoisted: chunk c of the row is atom c / 8, slot (c % 8) ^ (r % 8))
+            const unsigned char* rowp = tile + r * 128;
+            const int rsw = r & 7;
+            auto xchunk = [&](int c) -> float4 {
+                return *reinterpret_cast<const float4*>(rowp + (c >> 3) * (TG::M * 128) + (((c & 7) ^ rsw) << 4));
+            };
+            auto row_cost = [&](int j) -> double {
+                if (p.fast_cost) {  // fp32 mode: ((x + hi) + lo)^2 in fp32 FFMA2 chains, widened once per row
+                    const float4* hc = reinterpret_cast<const float4*>(negc) + j;
+                    const float4* lc = reinterpret_cast<const float4*>(neglo) + j;
+                    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll 4
-                    for (int c = 0; c < NPW / 4; ++c) {
-                        const float4 x4 = *reinterpret_cast<const float4*>(tile + sw128_off(TG::M, r, 4 * c));
-                        const float4 c4 = *reinterpret_cast<const float4*>(nc + 4 * c);
-                        const float4 l4 = __ldg(reinterpret_cast<const float4*>(nl + 4 * c));
-                        nn2 = __ffma2_rn(make_float2(x4.x, x4.y), make_float2(x4.x, x4.y), nn2);
-                        nn2 = __ffma2_rn(make_float2(x4.z, x4.w), make_float2(x4.z, x4.w), nn2);
+                    for (int c = 0; c < NPW / 4; c += 2) {
+                        const float4 x4 = xchunk(c), y4 = xchunk(c + 1);
+                        const float4 c4 = hc[c * N], d4 = hc[(c + 1) * N];
+                        const float4 l4 = lc[c * N], m4 = lc[(c + 1) * N];
                         const float2 e0 = __fadd2_rn(__fadd2_rn(make_float2(x4.x, x4.y), make_float2(c4.x, c4.y)),
                                                      make_float2(l4.x, l4.y));
                         const float2 e1 = __fadd2_rn(__fadd2_rn(make_float2(x4.z, x4.w), make_float2(c4.z, c4.w)),
                                                      make_float2(l4.z, l4.w));
+                        const float2 e2 = __fadd2_rn(__fadd2_rn(make_float2(y4.x, y4.y), make_float2(d4.x, d4.y)),
+                                                     make_float2(m4.x, m4.y));
+                        const float2 e3 = __fadd2_rn(__fadd2_rn(make_float2(y4.z, y4.w), make_float2(d4.z, d4.w)),
+                                                     make_float2(m4.z, m4.w));
                         a0 = __ffma2_rn(e0, e0, a0);
                         a1 = __ffma2_rn(e1, e1, a1);
+                        a2 = __ffma2_rn(e2, e2, a2);
+                        a3 = __ffma2_rn(e3, e3, a3);
                     }
-                    if (nn_out) *nn_out = nn2.x + nn2.y;
-                    return (double)((a0.x + a0.y) + (a1.x + a1.y));
+                    return (double)(((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y)));
                 }
                 const double* cj = Cg + (int64_t)j * NPW;
                 double a[4] = {0.0, 0.0, 0.0, 0.0};
-                float2 nn2 = make_float2(0.f, 0.f);
 #pragma unroll 4
                 for (int c = 0; c < NPW / 4; ++c) {
-                    const float4 x4 = *reinterpret_cast<const float4*>(tile + sw128_off(TG::M, r, 4 * c));
-                    nn2 = __ffma2_rn(make_float2(x4.x, x4.y), make_float2(x4.x, x4.y), nn2);
-                    nn2 = __ffma2_rn(make_float2(x4.z, x4.w), make_float2(x4.z, x4.w), nn2);
+                    const float4 x4 = xchunk(c);
                     const double2 c01 = __ldg(reinterpret_cast<const double2*>(cj + 4 * c));
                     const double2 c23 = __ldg(reinterpret_cast<const double2*>(cj + 4 * c + 2));
                     const double e0 = (double)x4.x - c01.x, e1 = (double)x4.y - c01.y;
@@ -243,12 +260,14 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
                     a[2] = fma(e2, e2, a[2]);
                     a[3] = fma(e3, e3, a[3]);
                 }
-                if (nn_out) *nn_out = nn2.x + nn2.y;
                 return (a[0] + a[1]) + (a[2] + a[3]);
             };
-            float nn = 0.f;
-            double rc = row_cost(valid ? lab : 0, &nn);
+            double rc = row_cost(valid ? lab : 0);
             const int lab0 = lab;
+            // |x|^2 bound of the screens' error terms from the cost just computed: |x| <= |x - c| + |c|
+            // (1.0001 covers the fp32-mode cost and the rounded |c|^2)
+            const float sxc = (sqrtf(fmaxf((float)rc, 0.f)) + sqrtf(s_cc[valid ? lab : 0])) * 1.0001f;
+            const float nn = valid ? sxc * sxc : 0.f;
             const float btc = kap2 * (nn + cmax2);
             unsigned tie = __ballot_sync(0xffffffffu, valid && !(p2[0] - p1[0] > btc));
             if (tie) {
@@ -325,7 +344,7 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
                     }
                     if (lane == src) lab = dj;
                 }
-                if (valid && lab != lab0) rc = row_cost(lab, nullptr);
+                if (valid && lab != lab0) rc = row_cost(lab);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are read
