@@ -26,9 +26,9 @@ struct TcwGeo {
     static constexpr int SUB = M * 128;                   // bytes per K-atom sub-tile
     static constexpr int TILE = NA * SUB;                 // bytes per stage
     static constexpr int BSUB = N * 128;                  // bytes per K-atom of the B tile
-    static constexpr int CEN = N * NPW * 4;               // bytes of one fp32 centre table (hi or lo)
-    // ring stages in what is left of 208 KB after the B tile and the two centre tables
-    static constexpr int STAGES = (212992 - NA * BSUB - 2 * CEN) / TILE < 6 ? (212992 - NA * BSUB - 2 * CEN) / TILE : 6;
+    static constexpr int CEN = N * NPW * 4;               // bytes of the fp32 low-part centre table
+    // ring stages in what is left of 224 KB after the B tile and the low-part table
+    static constexpr int STAGES = (229376 - NA * BSUB - CEN) / TILE < 6 ? (229376 - NA * BSUB - CEN) / TILE : 6;
     static constexpr int TCOLS = 512;
     static constexpr int NB = TCOLS / N;                  // TMEM tile buffers
     static constexpr int EPI_WARPS = 8;
@@ -41,10 +41,10 @@ struct TcwGeo {
 template <int NA>
 __host__ __device__ inline int objective_tcw_smem() {
     using TG = TcwGeo<NA>;
-    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB + 2 * TG::CEN;  // + fp32 -c hi / lo (fp32-mode cost)
+    return 1024 + TG::STAGES * TG::TILE + NA * TG::BSUB + TG::CEN;  // + fp32 low parts (fp32-mode cost)
 }
 
-// fp32 centre tables of the row cost: chunk-major [NPW/4][N][4], so 32 lanes reading chunk c of 32
+// fp32 low-part table of the row cost: chunk-major [NPW/4][N][4], so 32 lanes reading chunk c of 32
 // different centres touch 32 distinct 16-B slots of one 512-B span (no bank conflicts)
 template <int N>
 HPCG_DEV int cen_off(int j, int d) { return (((d >> 2) * N + j) << 2) + (d & 3); }
@@ -71,16 +71,15 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
     const int kv = obj_kv(p);
     const double* __restrict__ Cg = p.C;  // [kv x NPW] fp64 centres (L1-resident)
 
-    // fp32 -c as hi + lo (hi = -fl32(c), lo = -(c - fl32(c))) for the fp32-mode row cost
-    float* negc = reinterpret_cast<float*>(Bt + NA * TG::BSUB);
-    float* neglo = negc + N * NPW;
+    // -c for the fp32-mode row cost as hi + lo: hi = B / 2 (exact: the tf32 -2c of the MMA operand,
+    // read from the B tile), lo = fl32(-c - hi) (|lo| <= 2^-11 |c|, so hi + lo is -c to 2^-35 |c|)
+    float* neglo = reinterpret_cast<float*>(Bt + NA * TG::BSUB);
     for (int e = tid; e < N * NPW; e += TG::THREADS) {
         const int j = e / NPW, d = e - j * NPW;
         const double c = j < kv ? Cg[(int64_t)j * NPW + d] : 0.0;
-        const float c2 = (float)(-2.0 * c);
-        *reinterpret_cast<float*>(Bt + sw128_off(N, j, d)) = tf32_rna(c2);
-        negc[cen_off<N>(j, d)] = 0.5f * c2;  // exact: -fl32(c)
-        neglo[cen_off<N>(j, d)] = (float)-(c - (double)(float)c);
+        const float b = tf32_rna((float)(-2.0 * c));
+        *reinterpret_cast<float*>(Bt + sw128_off(N, j, d)) = b;
+        neglo[cen_off<N>(j, d)] = (float)(-c - 0.5 * (double)b);
     }
     if (tid < N) {
         float cc = 1e38f;
@@ -223,21 +222,26 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
             };
             auto row_cost = [&](int j) -> double {
                 if (p.fast_cost) {  // fp32 mode: ((x + hi) + lo)^2 in fp32 FFMA2 chains, widened once per row
-                    const float4* hc = reinterpret_cast<const float4*>(negc) + j;
+                    const unsigned char* bj = Bt + j * 128;  // centre j's row of the B tile
+                    const int jsw = j & 7;
+                    auto bchunk = [&](int c) -> float4 {
+                        return *reinterpret_cast<const float4*>(bj + (c >> 3) * TG::BSUB + (((c & 7) ^ jsw) << 4));
+                    };
                     const float4* lc = reinterpret_cast<const float4*>(neglo) + j;
+                    const float2 h = make_float2(0.5f, 0.5f);
                     float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll 4
                     for (int c = 0; c < NPW / 4; c += 2) {
                         const float4 x4 = xchunk(c), y4 = xchunk(c + 1);
-                        const float4 c4 = hc[c * N], d4 = hc[(c + 1) * N];
+                        const float4 c4 = bchunk(c), d4 = bchunk(c + 1);
                         const float4 l4 = lc[c * N], m4 = lc[(c + 1) * N];
-                        const float2 e0 = __fadd2_rn(__fadd2_rn(make_float2(x4.x, x4.y), make_float2(c4.x, c4.y)),
+                        const float2 e0 = __fadd2_rn(__ffma2_rn(make_float2(c4.x, c4.y), h, make_float2(x4.x, x4.y)),
                                                      make_float2(l4.x, l4.y));
-                        const float2 e1 = __fadd2_rn(__fadd2_rn(make_float2(x4.z, x4.w), make_float2(c4.z, c4.w)),
+                        const float2 e1 = __fadd2_rn(__ffma2_rn(make_float2(c4.z, c4.w), h, make_float2(x4.z, x4.w)),
                                                      make_float2(l4.z, l4.w));
-                        const float2 e2 = __fadd2_rn(__fadd2_rn(make_float2(y4.x, y4.y), make_float2(d4.x, d4.y)),
+                        const float2 e2 = __fadd2_rn(__ffma2_rn(make_float2(d4.x, d4.y), h, make_float2(y4.x, y4.y)),
                                                      make_float2(m4.x, m4.y));
-                        const float2 e3 = __fadd2_rn(__fadd2_rn(make_float2(y4.z, y4.w), make_float2(d4.z, d4.w)),
+                        const float2 e3 = __fadd2_rn(__ffma2_rn(make_float2(d4.z, d4.w), h, make_float2(y4.z, y4.w)),
                                                      make_float2(m4.z, m4.w));
                         a0 = __ffma2_rn(e0, e0, a0);
                         a1 = __ffma2_rn(e1, e1, a1);
