@@ -201,8 +201,28 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
     // narrow rows (fp64 n <= 3, fp32 n = 2): bulk-copy ring + centre-pair screen
     static const bool no_rows = getenv("HPCG_OBJ_NO_ROWS") != nullptr;
     if constexpr ((sizeof(T) == 8 && NP <= 3) || (sizeof(T) == 4 && NP == 2)) {
-        if (!old && !no_rows && p.n == NP && (reinterpret_cast<uintptr_t>(p.X) & 15) == 0)
+        if (!old && !no_rows && p.n == NP && (reinterpret_cast<uintptr_t>(p.X) & 15) == 0) {
+            static const bool no_grid = getenv("HPCG_OBJ_NO_GRID") != nullptr;
+            if (p.grid && p.kv <= 32 && !no_grid) {  // cell filter: the masks, then the pass
+                auto kern = objective_rows_kernel<T, NP, true>;
+                const int smem = objective_rows_smem<T, NP, true>(p.kv);
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                if (e != cudaSuccess) return e;
+                int per_sm = 0, dev = 0, sms = 148;
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kObjThreads, smem);
+                if (e != cudaSuccess) return e;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                if (per_sm >= 1 && nblocks[0] >= sms * per_sm) {
+                    grid_mask_kernel<NP><<<kGridCells / 256, 256, 0, st>>>(p);
+                    e = cudaGetLastError();
+                    if (e != cudaSuccess) return e;
+                    if (p.launched) *p.launched += 1;
+                }
+                return launch_grid(kern, smem, p, tmap, nblocks, st);
+            }
             return launch_grid(objective_rows_kernel<T, NP>, objective_rows_smem<T, NP>(p.kv), p, tmap, nblocks, st);
+        }
     }
     p.use_tma = (!getenv("HPCG_NO_TMA") && tma_ok<T, NP>(p) && make_tmap<T>(p, ObjGeo<T, NP>::GR, &tmap)) ? 1 : 0;
     return launch_grid(objective_kernel<T, NP>, objective_smem<T, NP>(p.kv), p, tmap, nblocks, st);

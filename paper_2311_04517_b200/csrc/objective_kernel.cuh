@@ -17,6 +17,11 @@ namespace hpcg {
 constexpr int kObjThreads = 256;
 constexpr int kObjMaxK = 256;
 
+constexpr int kGridCells = 4096;  // cells of the narrow-row filter (objective_rows.cuh)
+struct GridHdr {                  // after the kGridCells masks in ObjParams::grid
+    double lo[3], inv_w[3];
+};
+
 struct ObjParams {
     const void* X;
     int64_t m;
@@ -34,12 +39,10 @@ struct ObjParams {
     int* launched;         // optional: kernels launched are added here
     int32_t fast_cost;     // fp32 data: row cost in fp32 (direct form, FFMA2), accumulated in fp64 --
                            // the north star's fp32 mode (1e-5 relative); 0: exact fp64 row cost
-    const float* nclo;     // fast_cost: [kv x n] -(c - fl32(c)), the low part of each centre, so a row's
-                           // difference is (x - c_hi) - c_lo: error ~2^-24 |x - c| whatever |c| / |x - c|
-                           // (wide-row kernel; the tensor-core kernel derives it in its prologue)
     double* cost_out;      // optional: the kernel's last CTA sums block_cost in the fixed order of
     unsigned int* done_ctr;  //   sum_blocks_kernel<<<1, 256>>> into *cost_out (done_ctr: zeroed counter)
     int* finalized;        // host: set to 1 by a launcher whose kernel wrote *cost_out, else 0
+    uint32_t* grid;        // optional scratch of the narrow-row cell filter (kGridCells masks + GridHdr)
 };
 
 // the fixed-order block-partial sum of sum_blocks_kernel<<<1, 256>>>, run by threads 0..255 of the

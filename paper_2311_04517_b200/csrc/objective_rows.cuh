@@ -18,25 +18,121 @@
 
 namespace hpcg {
 
-template <typename T, int NP>
+// Cell filter for rows of n <= 3 (GRID variant): the centres' bounding box, padded, is cut into
+// kGridCells cells (G per dimension); per cell a mask of the centres that can be the nearest to some
+// point of the cell (grid_mask_kernel). A row inside the grid computes the exact reference distance
+// to its cell's candidates only; rows outside it (or kv > 32) take every centre.
+template <int NP>
+struct GridGeo {
+    static constexpr int G = NP == 1 ? 4096 : NP == 2 ? 64 : 16;  // cells per dimension (kGridCells cells)
+};
+
+template <typename T, int NP, bool GRID = false>
 struct RowsGeo {
     static constexpr int R = 4;                              // rows per lane
     static constexpr int GR = 32 * R;                        // rows per stage
     static constexpr int RB = NP * (int)sizeof(T);           // row bytes
     static constexpr int STAGE = GR * RB;                    // bytes per stage (multiple of 16)
     static constexpr int WARPS = 8;
-    static constexpr int STAGES = 98304 / (WARPS * STAGE) < 8 ? 98304 / (WARPS * STAGE) : 8;
+    static constexpr int RING = GRID ? 81920 : 98304;        // ring bytes (GRID: + 16 KB of cell masks)
+    static constexpr int STAGES = RING / (WARPS * STAGE) < 8 ? RING / (WARPS * STAGE) : 8;
     static constexpr int RST = ((NP + 2) / 2) * 2;           // record stride (float2, even: 16-B loads)
     static constexpr int CDS = NP | 1;                       // fp64 centre stride: odd (8-B loads)
     static constexpr float kappa = 2.0f * (float)(NP + 12) * 5.9604645e-8f;
     static_assert(STAGE % 16 == 0 && STAGES >= 2, "stage geometry");
 };
 
-template <typename T, int NP>
+template <typename T, int NP, bool GRID = false>
 __host__ __device__ inline int objective_rows_smem(int kv) {
-    using RG = RowsGeo<T, NP>;
+    using RG = RowsGeo<T, NP, GRID>;
     const int kp = (kv + 1) / 2;
-    return ((kp * RG::RST * 8 + kv * RG::CDS * 8 + 127) & ~127) + RG::WARPS * RG::STAGES * RG::STAGE + 128;
+    return ((kp * RG::RST * 8 + kv * RG::CDS * 8 + 127) & ~127) + RG::WARPS * RG::STAGES * RG::STAGE + 128 +
+           (GRID ? kGridCells * 4 : 0);
+}
+
+// The cell masks (one thread per cell). Cell box = [lo + i w, lo + (i + 1) w] per dimension, widened
+// by 1e-6 w (the fp64 cell index of a row is exact to far less). z* = the centre nearest the cell's
+// midpoint; centre j is dropped iff max over the box of 2 x.(c_j - z*) < |c_j|^2 - |z*|^2 - delta,
+// i.e. every point of the box is nearer z* than c_j by more than delta = 1e-9 (|x|max + |c|max)^2 in
+// exact arithmetic -- far above the rounding of the reference distance (~1e-15 of the same scale),
+// so the fp64 distances keep that order and a dropped centre can neither be the nearest nor tie it.
+template <int NP>
+__global__ void __launch_bounds__(256) grid_mask_kernel(const ObjParams p) {
+    constexpr int G = GridGeo<NP>::G;
+    __shared__ double sc[32][3], s_n2[32], s_lo[3], s_w[3], s_rc;
+    const int kv = obj_kv(p);
+    for (int e = threadIdx.x; e < 32 * 3; e += blockDim.x) {
+        const int j = e / 3, d = e - j * 3;
+        sc[j][d] = (j < kv && d < NP) ? p.C[(int64_t)j * NP + d] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int j = threadIdx.x;
+        s_n2[j] = sc[j][0] * sc[j][0] + sc[j][1] * sc[j][1] + sc[j][2] * sc[j][2];
+    }
+    if (threadIdx.x == 0) {
+        double rc = 0.0;
+        for (int j = 0; j < kv; ++j) rc = fmax(rc, sqrt(sc[j][0] * sc[j][0] + sc[j][1] * sc[j][1] + sc[j][2] * sc[j][2]));
+        s_rc = rc;
+        for (int d = 0; d < 3; ++d) {
+            double mn = kv > 0 ? sc[0][d] : 0.0, mx = mn;
+            for (int j = 1; j < kv; ++j) {
+                mn = fmin(mn, sc[j][d]);
+                mx = fmax(mx, sc[j][d]);
+            }
+            const double span = mx - mn;
+            const double pad = 0.15 * span + 1e-3 * (fabs(mn) + fabs(mx)) + 1e-3;
+            s_lo[d] = mn - pad;
+            s_w[d] = (span + 2.0 * pad) / G;
+        }
+        if (blockIdx.x == 0) {
+            GridHdr* h = reinterpret_cast<GridHdr*>(p.grid + kGridCells);
+            for (int d = 0; d < 3; ++d) {
+                h->lo[d] = s_lo[d];
+                h->inv_w[d] = 1.0 / s_w[d];
+            }
+        }
+    }
+    __syncthreads();
+    for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < kGridCells; cell += gridDim.x * blockDim.x) {
+        double blo[3] = {0.0, 0.0, 0.0}, bhi[3] = {0.0, 0.0, 0.0}, mid[3] = {0.0, 0.0, 0.0};
+        int rest = cell;
+        double rb2 = 0.0;
+        for (int d = NP - 1; d >= 0; --d) {
+            const int i = rest % G;
+            rest /= G;
+            blo[d] = s_lo[d] + ((double)i - 1e-6) * s_w[d];
+            bhi[d] = s_lo[d] + ((double)i + 1.0 + 1e-6) * s_w[d];
+            mid[d] = 0.5 * (blo[d] + bhi[d]);
+            rb2 += fmax(blo[d] * blo[d], bhi[d] * bhi[d]);
+        }
+        int zs = 0;
+        double bd = __longlong_as_double(0x7ff0000000000000LL);
+        for (int j = 0; j < kv; ++j) {
+            double dd = 0.0;
+            for (int d = 0; d < NP; ++d) dd += (mid[d] - sc[j][d]) * (mid[d] - sc[j][d]);
+            if (dd < bd) {
+                bd = dd;
+                zs = j;
+            }
+        }
+        const double sr = sqrt(rb2) + s_rc;
+        const double delta = 1e-9 * sr * sr;
+        uint32_t mask = 0;
+        for (int j = 0; j < kv; ++j) {
+            bool keep = j == zs;
+            if (!keep) {
+                double mx = 0.0;
+                for (int d = 0; d < NP; ++d) {
+                    const double w = sc[j][d] - sc[zs][d];
+                    mx += fmax(blo[d] * w, bhi[d] * w);
+                }
+                keep = !(2.0 * mx < (s_n2[j] - s_n2[zs]) - delta);
+            }
+            if (keep) mask |= 1u << j;
+        }
+        p.grid[cell] = mask;
+    }
 }
 
 HPCG_DEV void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -46,9 +142,9 @@ HPCG_DEV void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* 
         : "memory");
 }
 
-template <typename T, int NP>
+template <typename T, int NP, bool GRID = false>
 __global__ void __launch_bounds__(256, 2) objective_rows_kernel(const ObjParams p, const __grid_constant__ CUtensorMap) {
-    using RG = RowsGeo<T, NP>;
+    using RG = RowsGeo<T, NP, GRID>;
     constexpr int R = RG::R, GR = RG::GR, RST = RG::RST, CDS = RG::CDS, WARPS = RG::WARPS, STAGES = RG::STAGES;
     extern __shared__ __align__(16) unsigned char osm[];
     const int kvl = p.kv, kpl = (kvl + 1) / 2;  // launch bound: smem layout, uniform trip count
@@ -56,6 +152,7 @@ __global__ void __launch_bounds__(256, 2) objective_rows_kernel(const ObjParams 
     float2* rp = reinterpret_cast<float2*>(osm);
     double* Cd = reinterpret_cast<double*>(osm + kpl * RST * 8);
     unsigned char* rings = osm + ((kpl * RST * 8 + kvl * CDS * 8 + 127) & ~127);
+    uint32_t* s_mask = reinterpret_cast<uint32_t*>(rings + WARPS * STAGES * RG::STAGE + 128);  // GRID only
     __shared__ __align__(8) uint64_t s_bar[WARPS][STAGES];
     __shared__ float s_cmax;
     __shared__ double s_wcost[WARPS];
@@ -77,6 +174,8 @@ __global__ void __launch_bounds__(256, 2) objective_rows_kernel(const ObjParams 
         rec[2 * NP] = j < kv ? (float)cc : 1e38f;
         for (int d = NP + 1; d < RST; ++d) rec[2 * d] = 0.f;
     }
+    if constexpr (GRID)
+        for (int e = tid; e < kGridCells; e += 256) s_mask[e] = p.grid[e];
     if (lane == 0) {
         for (int st = 0; st < STAGES; ++st) mbar_init(&s_bar[warp][st], 1);
         mbar_init_fence();
@@ -98,6 +197,13 @@ __global__ void __launch_bounds__(256, 2) objective_rows_kernel(const ObjParams 
     const int tmask = (1 << tbits) - 1;
     const float kap = RG::kappa + __int_as_float((127 + tbits - 22) << 23);  // + 2^(tb-22)
 
+    // cell filter: the grid's origin and inverse cell widths in registers (GRID only)
+    double glo[NP], giw[NP];
+#pragma unroll
+    for (int d = 0; d < NP; ++d) {
+        glo[d] = GRID ? reinterpret_cast<const GridHdr*>(p.grid + kGridCells)->lo[d] : 0.0;
+        giw[d] = GRID ? reinterpret_cast<const GridHdr*>(p.grid + kGridCells)->inv_w[d] : 0.0;
+    }
     const T* X = static_cast<const T*>(p.X);
     const int64_t m = p.m;
     const int64_t ngroups = (m + GR - 1) / GR, nfull = m / GR;
@@ -143,6 +249,41 @@ __global__ void __launch_bounds__(256, 2) objective_rows_kernel(const ObjParams 
         }
         __syncwarp();
         issue(i + STAGES);
+        if constexpr (GRID) {
+            // the cell's candidates, exact reference distances (core.hpp:146-157: ascending j, strict <)
+            constexpr int G = GridGeo<NP>::G;
+            const uint32_t all = kv >= 32 ? 0xffffffffu : ((1u << kv) - 1u);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int64_t row = row0 + r * 32 + lane;
+                const bool valid = full || row < m;
+                bool in = true;
+                int cell = 0;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    const double t = ((double)x[r][d] - glo[d]) * giw[d];
+                    in &= (t >= 0.0) & (t < (double)G);
+                    cell = cell * G + (in ? __double2int_rz(t) : 0);
+                }
+                uint32_t msk = in ? s_mask[cell] : all;
+                int lab = msk ? __ffs(msk) - 1 : 0;
+                double dv = __longlong_as_double(0x7ff0000000000000LL);
+                for (; msk; msk &= msk - 1) {
+                    const int j = __ffs(msk) - 1;
+                    const double dd = exact_dist_regs<T, NP>(x[r], Cd + j * CDS);
+                    if (dd < dv) {
+                        dv = dd;
+                        lab = j;
+                    }
+                }
+                if (valid) {
+                    cost += dv;
+                    if (p.labels) p.labels[row] = p.remap[lab];
+                    if (p.counts) atomicAdd(p.counts + p.remap[lab], 1ULL);
+                }
+            }
+            continue;
+        }
         float xf[R][NP];
 #pragma unroll
         for (int r = 0; r < R; ++r)

@@ -209,7 +209,7 @@ struct hpcg_ctx {
     std::atomic<int64_t> upload_bytes{0};  // host -> device bytes of dataset uploads (hpcg_dataset_upload)
     int fp32_exact_cost = 0;               // f(C,X) over fp32 data: 1 = exact fp64 row cost, 0 = fp32 mode
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f;  // scratch for one-shot calls
-    DevBuf clo;                           // low parts of the centres of the fp32-mode f(C,X) cost
+    DevBuf grid;                          // cell masks of the narrow-row f(C,X) filter
     DevBuf done_ctr;                      // CTA ticket counter of the self-finalising f(C,X) kernel
     int rec_slot = -1;                     // constant-bank slot of the objective records
     DevBuf rec_scratch;
@@ -812,12 +812,6 @@ cudaError_t d2h(T* dst, const T* src, size_t count, cudaStream_t st) {
     return cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, st);
 }
 
-// low parts of the valid centres for the fp32-mode row cost: nclo = -(c - fl32(c))
-__global__ void centre_lo_kernel(const double* C, int64_t count, float* nclo) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
-        nclo[e] = (float)-(C[e] - (double)(float)C[e]);
-}
-
 // Full-data assignment on device: valid centres C_valid_dev [kv x n], remap [kv];
 // labels_dev may be null; counts_dev (u64 x k) may be null; cost to cost_dev.
 int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev, const int32_t* remap_dev, int kv,
@@ -830,14 +824,9 @@ int run_assign(hpcg_ctx* ctx, const hpcg_dataset* ds, const double* C_valid_dev,
     int launched = 0;
     op.launched = &launched;
     op.fast_cost = (ds->dtype == HPCG_F32 && !ctx->fp32_exact_cost) ? 1 : 0;
-    if (op.fast_cost && (ds->n == 64 || ds->n == 128)) {  // the wide-row kernel reads them from global
-        const int64_t cnt = (int64_t)kv * ds->n;
-        CU(ctx->clo.reserve((size_t)std::max<int64_t>(cnt, 4) * sizeof(float)));
-        centre_lo_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 64), 256, 0, ctx->stream>>>(
-            C_valid_dev, cnt, ctx->clo.as<float>());
-        CU(cudaGetLastError());
-        ctx->launches += 1;
-        op.nclo = ctx->clo.as<float>();
+    if (ds->n <= 3 && kv <= 32) {  // narrow rows: the cell filter's masks (objective_rows.cuh)
+        CU(ctx->grid.reserve((size_t)kGridCells * 4 + sizeof(GridHdr)));
+        op.grid = ctx->grid.as<uint32_t>();
     }
     op.rec_slot = -1;
     if (ctx->rec_slot >= 0 && ctx->rec_scratch.reserve((size_t)kRecSlotF4 * sizeof(float4)) == cudaSuccess) {
