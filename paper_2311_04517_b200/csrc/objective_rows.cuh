@@ -34,7 +34,7 @@ struct RowsGeo {
     static constexpr int RB = NP * (int)sizeof(T);           // row bytes
     static constexpr int STAGE = GR * RB;                    // bytes per stage (multiple of 16)
     static constexpr int WARPS = 8;
-    static constexpr int RING = GRID ? 81920 : 98304;        // ring bytes (GRID: + 16 KB of cell masks)
+    static constexpr int RING = GRID ? 49152 : 98304;        // ring bytes (GRID: + 16 KB of cell masks, 3 CTAs/SM)
     static constexpr int STAGES = RING / (WARPS * STAGE) < 8 ? RING / (WARPS * STAGE) : 8;
     static constexpr int RST = ((NP + 2) / 2) * 2;           // record stride (float2, even: 16-B loads)
     static constexpr int CDS = NP | 1;                       // fp64 centre stride: odd (8-B loads)
@@ -143,7 +143,7 @@ HPCG_DEV void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* 
 }
 
 template <typename T, int NP, bool GRID = false>
-__global__ void __launch_bounds__(256, 2) objective_rows_kernel(const ObjParams p, const __grid_constant__ CUtensorMap) {
+__global__ void __launch_bounds__(256, GRID ? 3 : 2) objective_rows_kernel(const ObjParams p, const __grid_constant__ CUtensorMap) {
     using RG = RowsGeo<T, NP, GRID>;
     constexpr int R = RG::R, GR = RG::GR, RST = RG::RST, CDS = RG::CDS, WARPS = RG::WARPS, STAGES = RG::STAGES;
     extern __shared__ __align__(16) unsigned char osm[];
