@@ -396,11 +396,11 @@ __global__ void wide_init_kernel(const StepParams p, int w0, WideBufs b) {
 
 // D^2 from every valid centre (including a first centre just drawn): the screen's argmin over
 // the valid centres (near ties exact) and the reference distance to it
-template <typename T>
+template <typename T, int NP = 0>
 __global__ void __launch_bounds__(kWT) wide_d2init_kernel(const StepParams p, WideBufs b) {
     extern __shared__ __align__(16) float wrec[];
     __shared__ float red_f[1];
-    const int w = blockIdx.y, k = p.k, n = p.n;
+    const int w = blockIdx.y, k = p.k, n = NP ? NP : p.n;
     const int64_t s = p.s;
     if (b.st[w].n_pending == 0) return;
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
@@ -408,6 +408,25 @@ __global__ void __launch_bounds__(kWT) wide_d2init_kernel(const StepParams p, Wi
     float* ccs = rec + (int64_t)kpad * n4;
     const double* Cm = b.Cm + (int64_t)w * k * n;
     const uint8_t* fl = b.flags + (int64_t)w * k;
+    __shared__ int s_nv, s_j;
+    if (threadIdx.x == 0) {
+        int nv = 0, j1 = 0;
+        for (int j = 0; j < k; ++j)
+            if (!fl[j]) {
+                if (nv++ == 0) j1 = j;
+            }
+        s_nv = nv;
+        s_j = j1;
+    }
+    __syncthreads();
+    if (s_nv == 1) {  // one valid centre (round 0: the first centre just drawn): D^2 is its distance
+        const int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x;
+        if (i >= s) return;
+        const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
+        const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
+        b.d2[(int64_t)w * s + i] = dist1<T>(S + i * n, n, Cm + (int64_t)s_j * n, vecd);
+        return;
+    }
     build_records(Cm, k, kpad, n, n4, rec, ccs, fl);
     const float cmax = records_cmax(ccs, kpad, red_f);
     const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
@@ -473,14 +492,34 @@ __device__ __forceinline__ BlockScan block_scan(const double* __restrict__ d2, i
     return b;
 }
 
-// block totals: one warp per (block, worker)
-__global__ void wide_cdf_kernel(const StepParams p, WideBufs b, int nblk) {
+// block totals: one warp per (block, worker). From the second slot on, the lanes first apply the
+// previous slot's D^2 update to their rows (seeding.hpp:100-103): only rows that slot's cost pass
+// flagged for its winner can change, and they take min(d2, the reference distance) -- the value the
+// cost pass added. (After the last slot D^2 is not read again, so no separate update pass runs.)
+template <typename T, int NP = 0>
+__global__ void wide_cdf_kernel(const StepParams p, WideBufs b, int nblk, int it) {
     const int w = blockIdx.y;
-    if (!slot_live(b.st[w])) return;
+    const WState& st = b.st[w];
+    if (!slot_live(st)) return;
     const int lane = threadIdx.x & 31;
     const int blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (blk >= nblk) return;
     const int64_t s = p.s, r0 = (int64_t)blk * kSeedRows, r1 = min(s, r0 + kSeedRows);
+    if (it > 0 && st.it == it) {
+        const int n = NP ? NP : p.n, best = st.best;
+        const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
+        const double* cd = b.cand + ((int64_t)w * kMaxCandidates + best) * n;
+        const int64_t a = r0 + (int64_t)lane * kLaneRows;
+        for (int j = 0; j < kLaneRows; ++j) {
+            const int64_t i = a + j;
+            if (i >= r1) break;
+            if ((b.rflag[(int64_t)w * s + i] >> best) & 1u) {
+                const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
+                double* d2 = b.d2 + (int64_t)w * s + i;
+                *d2 = fmin(*d2, dist1<T>(x, n, cd, vecd));
+            }
+        }
+    }
     const BlockScan bs = block_scan(b.d2 + (int64_t)w * s, r0, r1, lane);
     // T_q := the cumulative value at the block's last row, exactly as the draw computes it
     const int last_lane = (int)((r1 - 1 - r0) / kLaneRows);
@@ -664,6 +703,119 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
     }
 }
 
+// The same pass for a compile-time row width NP (n = 8 / 16 / 32: config 5 and the like): rows in
+// registers, candidates' fp32 records and fp64 coordinates in shared memory (broadcast loads), the
+// screen bounds' |c| terms hoisted; identical arithmetic and summation order to wide_cost_kernel, so
+// the partials are bit-identical to it.
+template <typename T, int NP>
+__global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, WideBufs b, int nblk) {
+    __shared__ double wred[kMaxCandidates][kWT / 32];
+    __shared__ __align__(16) float crec[kMaxCandidates][NP];
+    __shared__ __align__(16) double cdv[kMaxCandidates][NP];
+    __shared__ float ccn[kMaxCandidates], ccr[kMaxCandidates];
+    const int w = blockIdx.y, ncand = p.candidates;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (!slot_live(b.st[w])) return;
+    const double* cand = b.cand + (int64_t)w * kMaxCandidates * NP;
+    for (int e = threadIdx.x; e < kMaxCandidates * NP; e += kWT) {
+        const int c = e / NP, d = e - c * NP;
+        const double v = c < ncand ? cand[(int64_t)c * NP + d] : 0.0;
+        cdv[c][d] = v;
+        crec[c][d] = (float)(-2.0 * v);
+    }
+    if (threadIdx.x < kMaxCandidates) {
+        const int c = threadIdx.x;
+        double a = 0.0;
+        if (c < ncand)
+            for (int d = 0; d < NP; ++d) a += cand[(int64_t)c * NP + d] * cand[(int64_t)c * NP + d];
+        ccn[c] = (float)a;
+        ccr[c] = sqrtf((float)a) * 1.0001f;
+    }
+    __syncthreads();
+    constexpr float kappa = 2.0f * (float)((NP + 1) / 2 + 12) * 5.9604645e-8f;
+    const int64_t s = p.s;
+    const int blk0 = blockIdx.x * kCostBPC, blk1 = min(nblk, blk0 + kCostBPC);
+    const T* Sw = static_cast<const T*>(b.S) + (int64_t)w * s * NP;
+    const double* d2w = b.d2 + (int64_t)w * s;
+    uint8_t* flw = b.rflag + (int64_t)w * s;
+    double acc[kMaxCandidates];
+#pragma unroll
+    for (int c = 0; c < kMaxCandidates; ++c) acc[c] = 0.0;
+    for (int blk = blk0; blk < blk1; ++blk) {
+        const int64_t i = (int64_t)blk * kSeedRows + threadIdx.x;
+        if (i >= s) break;
+        T x[NP];
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+            for (int q = 0; q < NP / 4; ++q) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(Sw + i * NP) + q);
+                x[4 * q] = v.x;
+                x[4 * q + 1] = v.y;
+                x[4 * q + 2] = v.z;
+                x[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < NP / 2; ++q) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(Sw + i * NP) + q);
+                x[2 * q] = v.x;
+                x[2 * q + 1] = v.y;
+            }
+        }
+        const double d2i = d2w[i];
+        float2 a[kMaxCandidates], nn = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < kMaxCandidates; ++c) a[c] = make_float2(ccn[c], 0.f);
+#pragma unroll
+        for (int d = 0; d < NP; d += 4) {
+            const float2 xa = make_float2((float)x[d], (float)x[d + 1]), xb = make_float2((float)x[d + 2], (float)x[d + 3]);
+            nn = __ffma2_rn(xa, xa, nn);
+            nn = __ffma2_rn(xb, xb, nn);
+#pragma unroll
+            for (int c = 0; c < kMaxCandidates; ++c)
+                if (c < ncand) {
+                    const float4 cv = *reinterpret_cast<const float4*>(&crec[c][d]);
+                    a[c] = __ffma2_rn(xa, make_float2(cv.x, cv.y), a[c]);
+                    a[c] = __ffma2_rn(xb, make_float2(cv.z, cv.w), a[c]);
+                }
+        }
+        const float xx = nn.x + nn.y, xn = sqrtf(xx) * 1.0001f;
+        const float f2 = __double2float_ru(d2i);
+        uint32_t fl = 0;
+#pragma unroll
+        for (int c = 0; c < kMaxCandidates; ++c) {
+            if (c >= ncand) break;
+            double v = d2i;
+            const float sc = xn + ccr[c];
+            const float dt = xx + (a[c].x + a[c].y);
+            if (!(dt - kappa * sc * sc > f2)) {  // may improve: the reference distance
+                double e = 0.0;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    const double diff = __dsub_rn((double)x[d], cdv[c][d]);
+                    e = __dadd_rn(e, __dmul_rn(diff, diff));
+                }
+                v = fmin(d2i, e);
+                fl |= 1u << c;
+            }
+            acc[c] += v;
+        }
+        flw[i] = (uint8_t)fl;
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCandidates; ++c) {
+        if (c >= ncand) break;
+        const double v = warp_sum(acc[c]);
+        if (lane == 0) wred[c][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ncand) {
+        double tot = 0.0;
+        for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
+        b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
+    }
+}
+
 // winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot. Warp c
 // sums candidate c's block partials (lanes strided, then a shuffle tree: a fixed order).
 __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
@@ -708,24 +860,6 @@ __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
     }
 }
 
-// D^2 update with the slot's winner (seeding.hpp:100-103): only rows its cost pass flagged can
-// change; they get min(d2, the reference distance) -- the same value the cost pass added
-template <typename T>
-__global__ void wide_d2upd_kernel(const StepParams p, WideBufs b, int it_expect) {
-    const int w = blockIdx.y;
-    const WState& st = b.st[w];
-    if (st.it != it_expect + 1 || st.seed_stop) return;  // this slot was decided for w
-    const int64_t s = p.s, i = (int64_t)blockIdx.x * kWT + threadIdx.x;
-    if (i >= s) return;
-    if (!((b.rflag[(int64_t)w * s + i] >> st.best) & 1u)) return;
-    const int n = p.n;
-    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
-    const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
-    const double* cd = b.cand + ((int64_t)w * kMaxCandidates + st.best) * n;
-    double* d2 = b.d2 + (int64_t)w * s + i;
-    *d2 = fmin(*d2, dist1<T>(x, n, cd, vecd));
-}
-
 // ---------------------------------------------------------------- Lloyd
 __global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
     const int w = blockIdx.x, k = p.k;
@@ -741,13 +875,13 @@ __global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
 // one pass for CTA g of worker w: rows chunk_range(s, G, g) in rounds of kWT; labels by exact
 // strict-< argmin (core.hpp:146-157); per-cluster sums of each round's rows (label-sorted, row
 // order) and its cost tree-sum are added to the CTA accumulators in round order
-template <typename T, int AT>
+template <typename T, int AT, int NP = 0>  // NP: the row width as a compile-time constant (0: p.n)
 __global__ void __launch_bounds__(AT, 1024 / AT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
     constexpr int AW = AT / 32;  // warps
     extern __shared__ double wsm[];
     const int w = blockIdx.y, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (b.st[w].done) return;
-    const int k = p.k, n = p.n;
+    const int k = p.k, n = NP ? NP : p.n;
     const int64_t s = p.s, kn = (int64_t)k * n;
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
     double* acc = wsm;                  // [k*n] sums
@@ -1244,9 +1378,16 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     {
         const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
         const size_t rs = (size_t)kpad * n4 * 4 + (size_t)kpad * 4;
-        e = cudaFuncSetAttribute(wide_d2init_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs);
+        auto go = [&](auto kern) -> cudaError_t {
+            cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs);
+            if (e2 != cudaSuccess) return e2;
+            kern<<<rows_grid, kWT, rs, st>>>(p, b);
+            return cudaSuccess;
+        };
+        e = n == 8 ? go(wide_d2init_kernel<T, 8>) : n == 16 ? go(wide_d2init_kernel<T, 16>)
+            : n == 32 ? go(wide_d2init_kernel<T, 32>) : n == 128 ? go(wide_d2init_kernel<T, 128>)
+                      : go(wide_d2init_kernel<T, 0>);
         if (e != cudaSuccess) return e;
-        wide_d2init_kernel<T><<<rows_grid, kWT, rs, st>>>(p, b);
     }
     // K-means++ slots: as many host iterations as the worker with the most pending slots
     int32_t slots = 0;
@@ -1266,13 +1407,27 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         if (e != cudaSuccess) return e;
     }
     for (int it = 0; it < slots; ++it) {
-        wide_cdf_kernel<<<dim3((unsigned)((nblk + 7) / 8), (unsigned)Wb), 256, 0, st>>>(p, b, nblk);
+        const dim3 fgrid((unsigned)((nblk + 7) / 8), (unsigned)Wb);
+        if (n == 8)
+            wide_cdf_kernel<T, 8><<<fgrid, 256, 0, st>>>(p, b, nblk, it);
+        else if (n == 16)
+            wide_cdf_kernel<T, 16><<<fgrid, 256, 0, st>>>(p, b, nblk, it);
+        else if (n == 128)
+            wide_cdf_kernel<T, 128><<<fgrid, 256, 0, st>>>(p, b, nblk, it);
+        else
+            wide_cdf_kernel<T, 0><<<fgrid, 256, 0, st>>>(p, b, nblk, it);
         wide_cdfscan_kernel<<<(unsigned)Wb, 32, scan_smem, st>>>(b, nblk, staged);
         wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
-        wide_cost_kernel<T><<<dim3((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb), kWT, cost_smem, st>>>(
-            p, b, nblk);
+        const dim3 cgrid((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb);
+        if (n == 8)
+            wide_cost_np_kernel<T, 8><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+        else if (n == 16)
+            wide_cost_np_kernel<T, 16><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+        else if (n == 32)
+            wide_cost_np_kernel<T, 32><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+        else
+            wide_cost_kernel<T><<<cgrid, kWT, cost_smem, st>>>(p, b, nblk);
         wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
-        wide_d2upd_kernel<T><<<rows_grid, kWT, 0, st>>>(p, b, it);
     }
     // Lloyd: passes until every worker of the batch stopped
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
@@ -1281,7 +1436,11 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     constexpr int kAT = 256;
     const size_t smem = (size_t)(kn + k + kAT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
                         (size_t)((kAT / 32) * k + k + 1 + kAT) * 4;
-    e = cudaFuncSetAttribute(wide_assign_kernel<T, kAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the assign pass specialised for common row widths (index and loop arithmetic at compile time)
+    auto assign_kern = n == 8 ? wide_assign_kernel<T, kAT, 8> : n == 16 ? wide_assign_kernel<T, kAT, 16>
+                       : n == 32 ? wide_assign_kernel<T, kAT, 32> : n == 64 ? wide_assign_kernel<T, kAT, 64>
+                       : n == 128 ? wide_assign_kernel<T, kAT, 128> : wide_assign_kernel<T, kAT, 0>;
+    e = cudaFuncSetAttribute(assign_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         if (why) *why = "wide step: k*n too large for the pass accumulator";
         return e;
@@ -1303,7 +1462,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
                                         : launch_wide_tc<2, 16>(p, b, ccw, Wb, sms, stmap, st));
                 if (e != cudaSuccess) return e;
             }
-            wide_assign_kernel<T, kAT><<<dim3((unsigned)G, (unsigned)Wb), kAT, smem, st>>>(p, b, G, tc ? 1 : 0);
+            assign_kern<<<dim3((unsigned)G, (unsigned)Wb), kAT, smem, st>>>(p, b, G, tc ? 1 : 0);
             wide_lloyd_reduce_kernel<<<Wb, kWT, 0, st>>>(p, b, G, w0);
             if ((pass & 3) == 3 || pass == p.max_iters + 1) {  // stop check every few passes
                 wide_count_active_kernel<<<1, 256, 0, st>>>(b, Wb);

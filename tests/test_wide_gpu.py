@@ -48,7 +48,11 @@ def test_wide_kmeans_vs_oracle(dtype, n, k, s, W):
 
 
 @pytest.mark.parametrize("dtype,n,k,s,npend", [(np.float64, 48, 10, 3000, 10), (np.float32, 128, 25, 2000, 7),
-                                               (np.float64, 3, 40, 2500, 40)])
+                                               (np.float64, 3, 40, 2500, 40),
+                                               # k > 32 keeps these on the grid-wide path: the cost pass
+                                               # specialised for n = 8 / 16 / 32
+                                               (np.float32, 8, 40, 3000, 40), (np.float64, 16, 36, 2500, 30),
+                                               (np.float32, 32, 34, 2000, 20)])
 def test_wide_seeding_with_reference_draws(dtype, n, k, s, npend):
     X = mixture(s, n, k, seed=31 + k, dtype=dtype)
     rs = np.random.default_rng(5)
