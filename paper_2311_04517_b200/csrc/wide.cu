@@ -816,6 +816,146 @@ __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, W
     }
 }
 
+// The same pass for wide fp32 rows (n = 64 / 128: config 4), warp-cooperative so the row loads are
+// coalesced: a warp takes 8 rows at a time, lane L holding dims 4L.. of each (n = 128; n = 64: lanes
+// 0-15 of two row halves... simply the dims 4L < n). Each lane forms its partial |x|^2 and x.(-2c)
+// for the 8 rows, a transposing butterfly (31 shuffles) leaves lane L = 4r + q with the total of row
+// r's quantity q (q = 0: |x|^2, q = 1..3: candidate q-1), which tests its (row, candidate) pair
+// exactly like wide_cost_kernel and, when the candidate may improve, evaluates the reference
+// distance (ascending d, non-fused, one lane per pair). Sums: per candidate over rows in a fixed
+// order (the lanes' running sums, then a fixed tree and the warps in order).
+template <int NP>
+__global__ void __launch_bounds__(kWT) wide_cost_rows_kernel(const StepParams p, WideBufs b, int nblk) {
+    static_assert(NP % 4 == 0 && NP <= 128, "row width");
+    __shared__ double wred[kMaxCandidates][kWT / 32];
+    __shared__ __align__(16) float crec[3][NP];
+    __shared__ float ccn[3], ccr[3];
+    const int w = blockIdx.y, ncand = p.candidates;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (!slot_live(b.st[w])) return;
+    const double* cand = b.cand + (int64_t)w * kMaxCandidates * NP;
+    for (int e = threadIdx.x; e < 3 * NP; e += kWT) {
+        const int c = e / NP, d = e - c * NP;
+        crec[c][d] = c < ncand ? (float)(-2.0 * cand[(int64_t)c * NP + d]) : 0.f;
+    }
+    if (threadIdx.x < 3) {
+        const int c = threadIdx.x;
+        double a = 0.0;
+        if (c < ncand)
+            for (int d = 0; d < NP; ++d) a += cand[(int64_t)c * NP + d] * cand[(int64_t)c * NP + d];
+        ccn[c] = (float)a;
+        ccr[c] = sqrtf((float)a) * 1.0001f;
+    }
+    __syncthreads();
+    constexpr float kappa = 2.0f * (float)((NP + 1) / 2 + 12) * 5.9604645e-8f;
+    const int64_t s = p.s;
+    const int64_t row_lo = (int64_t)blockIdx.x * kCostBPC * kSeedRows;
+    const int64_t row_hi = min(s, row_lo + (int64_t)kCostBPC * kSeedRows);
+    const float* Sw = static_cast<const float*>(b.S) + (int64_t)w * s * NP;
+    const double* d2w = b.d2 + (int64_t)w * s;
+    uint8_t* flw = b.rflag + (int64_t)w * s;
+    const int d0 = 4 * lane;              // this lane's dims in the screen
+    const bool has = d0 < NP;
+    const int r = lane >> 2, q = lane & 3;  // the (row, quantity) this lane ends up owning
+    const int c = q - 1;
+    float4 cv[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) cv[cc] = has ? *reinterpret_cast<const float4*>(&crec[cc][d0]) : make_float4(0, 0, 0, 0);
+    double acc = 0.0;  // lane's running cost of candidate c (q >= 1)
+    const int64_t gstep = (int64_t)(kWT / 32) * 8;
+    float4 xn8[8];  // the next group's rows, loaded while the current group is screened
+    auto load_group = [&](int64_t g0) {
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+            const int64_t i = g0 + rr;
+            xn8[rr] = (has && i < row_hi) ? __ldg(reinterpret_cast<const float4*>(Sw + i * NP + d0))
+                                          : make_float4(0, 0, 0, 0);
+        }
+    };
+    load_group(row_lo + (int64_t)warp * 8);
+    for (int64_t i0 = row_lo + (int64_t)warp * 8; i0 < row_hi; i0 += gstep) {
+        float4 xc[8];
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) xc[rr] = xn8[rr];
+        if (i0 + gstep < row_hi) load_group(i0 + gstep);
+        float v[32];
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+            const float4 x = xc[rr];
+            const float2 xa = make_float2(x.x, x.y), xb = make_float2(x.z, x.w);
+            float2 nn = __ffma2_rn(xa, xa, make_float2(0.f, 0.f));
+            nn = __ffma2_rn(xb, xb, nn);
+            v[rr * 4] = nn.x + nn.y;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                float2 a = __ffma2_rn(xa, make_float2(cv[cc].x, cv[cc].y), make_float2(0.f, 0.f));
+                a = __ffma2_rn(xb, make_float2(cv[cc].z, cv[cc].w), a);
+                v[rr * 4 + 1 + cc] = a.x + a.y;
+            }
+        }
+        // transposing butterfly: after the stage with offset o, the lane keeps the half of its values
+        // selected by its bit o; finally lane L holds the warp total of value L
+#pragma unroll
+        for (int o = 16, m = 32; o > 0; o >>= 1, m >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int t = 0; t < m / 2; ++t) {
+                const float send = up ? v[t] : v[t + m / 2];
+                const float keep = up ? v[t + m / 2] : v[t];
+                v[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        const float tot = v[0];  // row r's quantity q
+        const float xx = __shfl_sync(0xffffffffu, tot, lane & ~3);
+        const int64_t i = i0 + r;
+        const bool valid = i < row_hi;
+        const double d2i = valid ? d2w[i] : 0.0;
+        bool may = false;
+        if (q >= 1 && c < ncand && valid) {
+            const float xn = sqrtf(xx) * 1.0001f, f2 = __double2float_ru(d2i);
+            const float sc = xn + ccr[c];
+            const float dt = xx + (ccn[c] + tot);
+            may = !(dt - kappa * sc * sc > f2);
+            double vv = d2i;
+            if (may) {  // the reference distance (core.hpp:100-108), this lane alone
+                const float* xr = Sw + i * NP;
+                const double* cd = cand + (int64_t)c * NP;
+                double e = 0.0;
+#pragma unroll 8
+                for (int d = 0; d < NP; d += 4) {
+                    const float4 x4 = __ldg(reinterpret_cast<const float4*>(xr + d));
+                    const double2 c01 = __ldg(reinterpret_cast<const double2*>(cd + d));
+                    const double2 c23 = __ldg(reinterpret_cast<const double2*>(cd + d + 2));
+                    double df = __dsub_rn((double)x4.x, c01.x);
+                    e = __dadd_rn(e, __dmul_rn(df, df));
+                    df = __dsub_rn((double)x4.y, c01.y);
+                    e = __dadd_rn(e, __dmul_rn(df, df));
+                    df = __dsub_rn((double)x4.z, c23.x);
+                    e = __dadd_rn(e, __dmul_rn(df, df));
+                    df = __dsub_rn((double)x4.w, c23.y);
+                    e = __dadd_rn(e, __dmul_rn(df, df));
+                }
+                vv = fmin(d2i, e);
+            }
+            acc += vv;
+        }
+        // the row's flag byte: bit c from lane 4r + 1 + c
+        const unsigned bal = __ballot_sync(0xffffffffu, may);
+        if (q == 0 && valid) flw[i] = (uint8_t)((bal >> (lane + 1)) & 7u);
+    }
+    // candidate c: lanes 4r + 1 + c (r = 0..7), a fixed tree, then the warps in order
+    double t = acc;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane >= 1 && lane <= 3) wred[lane - 1][warp] = t;
+    __syncthreads();
+    if (threadIdx.x < ncand) {
+        double tot2 = 0.0;
+        for (int q2 = 0; q2 < kWT / 32; ++q2) tot2 += wred[threadIdx.x][q2];
+        b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot2;
+    }
+}
+
 // winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot. Warp c
 // sums candidate c's block partials (lanes strided, then a shuffle tree: a fixed order).
 __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
@@ -875,8 +1015,11 @@ __global__ void wide_lloyd_begin_kernel(const StepParams p, WideBufs b) {
 // one pass for CTA g of worker w: rows chunk_range(s, G, g) in rounds of kWT; labels by exact
 // strict-< argmin (core.hpp:146-157); per-cluster sums of each round's rows (label-sorted, row
 // order) and its cost tree-sum are added to the CTA accumulators in round order
-template <typename T, int AT, int NP = 0>  // NP: the row width as a compile-time constant (0: p.n)
-__global__ void __launch_bounds__(AT, 1024 / AT) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
+#ifndef WIDE_ASSIGN_MINB
+#define WIDE_ASSIGN_MINB 3  // CTAs per SM the register cap is set for (80 registers at 256 threads)
+#endif
+template <typename T, int AT, int NP = 0, int AR = 1>  // NP: the row width at compile time (0: p.n); AR rows per thread per round
+__global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const StepParams p, WideBufs b, int G, int tc_codes) {
     constexpr int AW = AT / 32;  // warps
     extern __shared__ double wsm[];
     const int w = blockIdx.y, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -889,9 +1032,9 @@ __global__ void __launch_bounds__(AT, 1024 / AT) wide_assign_kernel(const StepPa
     double* red = cnt + k;              // [AT] tree
     float* rec = reinterpret_cast<float*>(red + AT + ((kn + k + AT) & 1));  // [kpad][n4], 16-B aligned
     float* ccs = rec + (int64_t)kpad * n4;             // [kpad]
-    int* wcnt = reinterpret_cast<int*>(ccs + kpad);    // [AW][k] per-warp label counts
-    int* cstart = wcnt + AW * k;        // [k+1]
-    int* sorted = cstart + k + 1;       // [AT] label-sorted round rows
+    int* wcnt = reinterpret_cast<int*>(ccs + kpad);    // [AR][AW][k] per-(slot, warp) label counts
+    int* cstart = wcnt + AR * AW * k;   // [k+1]
+    int* sorted = cstart + k + 1;       // [AT * AR] label-sorted round rows
     __shared__ float cmax_s;
     for (int64_t e = tid; e < kn + k; e += AT) acc[e] = 0.0;
     double cost = 0.0;
@@ -912,41 +1055,55 @@ __global__ void __launch_bounds__(AT, 1024 / AT) wide_assign_kernel(const StepPa
     const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
     const bool vec = sizeof(T) == 4 && (n & 3) == 0;                           // float4 screen loads
     const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;           // 16-B sum loads
-    for (int64_t base = r0; base < r1; base += AT) {
-        const int64_t i = base + tid;
-        const bool valid = i < r1;
-        int lab = 0;
-        double bestd = 0.0;
-        float m1 = 0.f, m2 = 0.f, xx = 0.f;
-        unsigned tie;
-        if (tc_codes) {  // the tensor-core screen's code: label, bit 31 = still a near tie
-            const int32_t code = valid ? labels[i] : 0;
-            lab = code & 0x7fffffff;
-            tie = __ballot_sync(0xffffffffu, valid && code < 0);
-        } else {
-            if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
-            const float sc = sqrtf(xx) * 1.0001f + cmax;
-            tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+    for (int64_t base = r0; base < r1; base += (int64_t)AT * AR) {
+        // R rows per thread per round (rows base + tid + AT r): the round's sort and fold barriers
+        // are shared by AT * AR rows; thread t still visits rows r0 + t + AT i in order
+        int labr[AR];
+        double bestd[AR];
+        bool validr[AR];
+#pragma unroll
+        for (int r = 0; r < AR; ++r) {
+            const int64_t i = base + tid + (int64_t)AT * r;
+            const bool valid = i < r1;
+            validr[r] = valid;
+            int lab = 0;
+            float m1 = 0.f, m2 = 0.f, xx = 0.f;
+            unsigned tie;
+            if (tc_codes) {  // the tensor-core screen's code: label, bit 31 = still a near tie
+                const int32_t code = valid ? labels[i] : 0;
+                lab = code & 0x7fffffff;
+                tie = __ballot_sync(0xffffffffu, valid && code < 0);
+            } else {
+                if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
+                const float sc = sqrtf(xx) * 1.0001f + cmax;
+                tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+            }
+            if (tie) exact_ties<T>(tie, S, base + (int64_t)AT * r + warp * 32, n, k, Cm, lab);
+            bestd[r] = 0.0;
+            if (valid) {  // the row's cost: the reference distance to its centre
+                bestd[r] = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
+                labels[i] = lab;
+            }
+            labr[r] = lab;
         }
-        if (tie) exact_ties<T>(tie, S, base + warp * 32, n, k, Cm, lab);
-        if (valid) {  // the row's cost: the reference distance to its centre
-            bestd = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
-            labels[i] = lab;
+        // stable counting sort of the round's rows by label: (row slot r, warp) major, lane minor
+        for (int e = tid; e < AR * AW * k; e += AT) wcnt[e] = 0;
+        __syncthreads();
+        unsigned peersr[AR];
+#pragma unroll
+        for (int r = 0; r < AR; ++r) {
+            peersr[r] = __match_any_sync(0xffffffffu, validr[r] ? labr[r] : -1);
+            if (validr[r] && (peersr[r] & ((1u << lane) - 1u)) == 0)
+                wcnt[(r * AW + warp) * k + labr[r]] = __popc(peersr[r]);
         }
-        // stable counting sort of the round's rows by label
-        for (int e = tid; e < AW * k; e += AT) wcnt[e] = 0;
         __syncthreads();
-        const unsigned peers = __match_any_sync(0xffffffffu, valid ? lab : -1);
-        const int rank = __popc(peers & ((1u << lane) - 1u));
-        if (valid && rank == 0) wcnt[warp * k + lab] = __popc(peers);
-        __syncthreads();
-        if (warp == 0) {  // cluster-major, warp-minor offsets: a shuffle scan over 32 clusters at a time
-            int base = 0;
+        if (warp == 0) {  // cluster-major, (slot, warp)-minor offsets: a shuffle scan over 32 clusters at a time
+            int base2 = 0;
             for (int j0 = 0; j0 < k; j0 += 32) {
                 const int j = j0 + lane;
                 int col = 0;
                 if (j < k)
-                    for (int q = 0; q < AW; ++q) col += wcnt[q * k + j];
+                    for (int q = 0; q < AR * AW; ++q) col += wcnt[q * k + j];
                 int incl = col;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -954,21 +1111,25 @@ __global__ void __launch_bounds__(AT, 1024 / AT) wide_assign_kernel(const StepPa
                     if (lane >= o) incl += y;
                 }
                 if (j < k) {
-                    int run = base + incl - col;
+                    int run = base2 + incl - col;
                     cstart[j] = run;
-                    for (int q = 0; q < AW; ++q) {
+                    for (int q = 0; q < AR * AW; ++q) {
                         const int c = wcnt[q * k + j];
                         wcnt[q * k + j] = run;
                         run += c;
                     }
                 }
-                base += __shfl_sync(0xffffffffu, incl, 31);
+                base2 += __shfl_sync(0xffffffffu, incl, 31);
             }
-            if (lane == 0) cstart[k] = base;
+            if (lane == 0) cstart[k] = base2;
         }
         __syncthreads();
-        if (valid) sorted[wcnt[warp * k + lab] + rank] = tid;
-        cost += valid ? bestd : 0.0;  // per-thread running sum (thread t: rows r0 + t + AT*i, in order)
+#pragma unroll
+        for (int r = 0; r < AR; ++r) {
+            if (validr[r])
+                sorted[wcnt[(r * AW + warp) * k + labr[r]] + __popc(peersr[r] & ((1u << lane) - 1u))] = tid + AT * r;
+            cost += validr[r] ? bestd[r] : 0.0;  // per-thread running sum (thread t: rows r0 + t + AT*i, in order)
+        }
         __syncthreads();              // sorted[] complete before the sums read it
         // per-cluster sums of this round: warp w takes clusters w, w+8, ..., walks the cluster's
         // rows in order with lanes over dims (coalesced row loads), then adds to the CTA
@@ -1425,6 +1586,10 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
             wide_cost_np_kernel<T, 16><<<cgrid, kWT, 0, st>>>(p, b, nblk);
         else if (n == 32)
             wide_cost_np_kernel<T, 32><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+        else if (sizeof(T) == 4 && n == 128 && ncand <= 3)
+            wide_cost_rows_kernel<128><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+        else if (sizeof(T) == 4 && n == 64 && ncand <= 3)
+            wide_cost_rows_kernel<64><<<cgrid, kWT, 0, st>>>(p, b, nblk);
         else
             wide_cost_kernel<T><<<cgrid, kWT, cost_smem, st>>>(p, b, nblk);
         wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
@@ -1433,13 +1598,16 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
     // the assign pass in rounds of kAT rows (fewer round barriers per row than kWT)
-    constexpr int kAT = 256;
+    constexpr int kAT = 256, kAR = 4;  // 1024 rows per round
     const size_t smem = (size_t)(kn + k + kAT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
-                        (size_t)((kAT / 32) * k + k + 1 + kAT) * 4;
+                        (size_t)(kAR * (kAT / 32) * k + k + 1 + kAT * kAR) * 4;
     // the assign pass specialised for common row widths (index and loop arithmetic at compile time)
-    auto assign_kern = n == 8 ? wide_assign_kernel<T, kAT, 8> : n == 16 ? wide_assign_kernel<T, kAT, 16>
-                       : n == 32 ? wide_assign_kernel<T, kAT, 32> : n == 64 ? wide_assign_kernel<T, kAT, 64>
-                       : n == 128 ? wide_assign_kernel<T, kAT, 128> : wide_assign_kernel<T, kAT, 0>;
+    auto assign_kern = n == 8     ? wide_assign_kernel<T, kAT, 8, kAR>
+                       : n == 16  ? wide_assign_kernel<T, kAT, 16, kAR>
+                       : n == 32  ? wide_assign_kernel<T, kAT, 32, kAR>
+                       : n == 64  ? wide_assign_kernel<T, kAT, 64, kAR>
+                       : n == 128 ? wide_assign_kernel<T, kAT, 128, kAR>
+                                  : wide_assign_kernel<T, kAT, 0, kAR>;
     e = cudaFuncSetAttribute(assign_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         if (why) *why = "wide step: k*n too large for the pass accumulator";
