@@ -161,7 +161,7 @@ static cudaError_t launch_obj_t(const ObjParams& p_in, int* nblocks, cudaStream_
     static const bool old = getenv("HPCG_OBJ_OLD") != nullptr || getenv("HPCG_NO_TMA") != nullptr;
     static const bool no_tc = getenv("HPCG_OBJ_NO_TC") != nullptr;
     if constexpr (sizeof(T) == 4 && (NP == 8 || NP == 16 || NP == 32)) {  // tensor-core screen
-        if (!old && !no_tc && p.kv >= 1 && p.kv <= 32 && tma_ok<T, NP>(p) && make_tmap<T>(p, TcGeo<NP, 16>::TM, &tmap)) {
+        if (!old && !no_tc && p.kv >= 1 && p.kv <= 32 && tma_ok<T, NP>(p) && make_tmap<T>(p, TcGeo<NP, 16>::BOX, &tmap)) {
             p.use_tma = 1;
             switch ((p.kv + 1) / 2) {  // screened centre pairs
                 case 1: return launch_tc<NP, 16, 1>(p, tmap, nblocks, st);

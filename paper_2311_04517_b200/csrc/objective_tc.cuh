@@ -25,8 +25,10 @@
 #pragma once
 #include "objective_kernel.cuh"
 
-#ifndef HPCG_TC_TR
-#define HPCG_TC_TR 2
+
+
+#ifndef HPCG_TC_EPI
+#define HPCG_TC_EPI 16  // epilogue warps of the tensor-core f(C,X) kernel
 #endif
 
 namespace hpcg {
@@ -34,15 +36,19 @@ namespace hpcg {
 template <int NP, int N>
 struct TcGeo {
     static constexpr int M = 128;                     // rows per MMA (= TMEM lanes)
-    static constexpr int TR = HPCG_TC_TR;             // MMA row blocks per tile (one commit per tile)
+    static constexpr int TR = NP <= 16 ? 2 : 1;       // MMA row blocks per tile (one commit per tile)
+    static constexpr int RPT = (NP == 8 && N == 16) ? 2 : 1;  // row blocks an epilogue thread takes per tile (n = 8:
+                                                      // both; n = 16 would spill at the 96-register cap)
+    static constexpr int BOX = TR * M < 256 ? TR * M : 256;   // TMA box rows (<= 256): TM / BOX loads per tile
     static constexpr int TM = M * TR;                 // rows per tile (= TMA box rows)
     static constexpr int RS = NP * 4;                 // row bytes (= swizzle span)
     static constexpr int TILE = TM * RS;              // bytes per stage
     static constexpr int STAGES = 196608 / TILE;     // 192 KB ring: tiles in flight from HBM
     static constexpr int TCOLS = 512;                 // all of TMEM (one CTA per SM)
     static constexpr int NB = TCOLS / (TR * N);       // TMEM tile buffers (even: 2 epilogue groups)
-    static constexpr int EPI_WARPS = 16;              // 4 groups of 4 warps: (tile phase, row block)
-    static constexpr int GSTEP = EPI_WARPS / 4 / TR;  // tile phases: a group takes every GSTEP-th tile
+    static constexpr int EPI_WARPS = HPCG_TC_EPI;     // groups of 4 warps, one per tile phase
+    static constexpr int GSTEP = EPI_WARPS / 4 / (TR / RPT);  // tile phases: a group = (phase, RPT row blocks)
+                                                              // takes every GSTEP-th tile
     static constexpr int THREADS = (EPI_WARPS + 2) * 32;
     static constexpr int CDS = NP + 1;                // fp64 centre stride (doubles): odd, so the 8-B
                                                       // loads of up to 16 distinct centres in a half-warp
@@ -169,11 +175,11 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 4 * TG::TR);
+            mbar_init(&empty[s], 4 * (TG::TR / TG::RPT));  // the warps of the tile's groups
         }
         for (int b = 0; b < NB; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4 * TG::TR);
+            mbar_init(&tempty[b], 4 * (TG::TR / TG::RPT));
         }
         mbar_init_fence();
     }
@@ -194,8 +200,10 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
             for (int i = 0; i < my; ++i) {
                 if (i >= STAGES) mbar_wait_cta(&empty[s], pl ^ 1u);
                 mbar_expect_tx(&full[s], (uint32_t)TILE);
-                tma_load_2d(ring + s * TILE, &tmap, 0, (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::TM),
-                            &full[s]);
+#pragma unroll
+                for (int h = 0; h < TG::TM / TG::BOX; ++h)
+                    tma_load_2d(ring + s * TILE + h * TG::BOX * TG::RS, &tmap, 0,
+                                (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::TM + h * TG::BOX), &full[s]);
                 if (++s == STAGES) {
                     s = 0;
                     pl ^= 1u;
@@ -239,12 +247,13 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                 }
             }
         }
-    } else {  // ---- epilogue: group g = (tile parity tp, row block rb): local tiles tp, tp + 2, ...,
-              // rows rb*128 + r of each; warp quarter wq = its TMEM lanes
+    } else {  // ---- epilogue: group g = (tile phase tp, row blocks rbase..rbase+RPT-1): local tiles tp,
+              // tp + GSTEP, ..., rows rb*128 + r of those blocks; warp quarter wq = its TMEM lanes
         constexpr int KP = KPS;
         static_assert(KPS >= 1 && KPS <= N / 2, "screened pairs");
         constexpr int STEP = TG::GSTEP;
-        const int g = warp >> 2, wq = warp & 3, tp = g / TG::TR, rb = g % TG::TR;
+        constexpr int RPT = TG::RPT;
+        const int g = warp >> 2, wq = warp & 3, tp = g / (TG::TR / RPT), rbase = (g % (TG::TR / RPT)) * RPT;
         const int r = wq * 32 + lane;  // row within the 128-row block (= TMEM lane)
         const float2* cc = reinterpret_cast<const float2*>(s_cc);  // broadcast loads (registers are scarce)
         float cmax = 0.f;
@@ -258,36 +267,60 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
         const int32_t* const remap = p.remap;
         int s = tp, b = tp;
         uint32_t pb = 0;
-        int64_t row = ((int64_t)blockIdx.x + (int64_t)tp * gridDim.x) * TG::TM + rb * TG::M + r;
+        int64_t row0 = ((int64_t)blockIdx.x + (int64_t)tp * gridDim.x) * TG::TM + rbase * TG::M + r;
         const int64_t row_step = STEP * (int64_t)gridDim.x * TG::TM;
-        for (int i = tp; i < my; i += STEP, row += row_step) {
+        for (int i = tp; i < my; i += STEP, row0 += row_step) {
             mbar_wait_sleep(&tfull[b], pb);
             tc_fence_after();
+            // the first row block's screened values: tcgen05.ld in flight while the rows are read
             uint32_t v[N];
-            const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((b * TG::TR + rb) * N);
-            tmem_ld16(taddr, v);
-            if constexpr (N == 32) tmem_ld16(taddr + 16, v + 16);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[b]);
-            // the row: its stage has landed (the MMAs that read it have completed)
-            const float* tile = reinterpret_cast<const float*>(ring + s * TILE);
-            float x[NP];
-#pragma unroll
-            for (int q = 0; q < NP / 4; ++q) {
-                const float4 t4 = *reinterpret_cast<const float4*>(tile + G::elem_off(rb * TG::M + r, q * 4));
-                x[4 * q] = t4.x;
-                x[4 * q + 1] = t4.y;
-                x[4 * q + 2] = t4.z;
-                x[4 * q + 3] = t4.w;
+            {
+                const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((b * TG::TR + rbase) * N);
+                tmem_ld16(taddr, v);
+                if constexpr (N == 32) tmem_ld16(taddr + 16, v + 16);
+                if constexpr (RPT == 1) {  // one row block: its values read, the TMEM buffer share is free
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[b]);
+                }
             }
+            // the rows of this group's row blocks: their stage has landed (the MMAs that read it completed)
+            const float* tile = reinterpret_cast<const float*>(ring + s * TILE);
+            float xr[RPT][NP];
+#pragma unroll
+            for (int rb = 0; rb < RPT; ++rb)
+#pragma unroll
+                for (int q = 0; q < NP / 4; ++q) {
+                    const float4 t4 =
+                        *reinterpret_cast<const float4*>(tile + G::elem_off((rbase + rb) * TG::M + r, q * 4));
+                    xr[rb][4 * q] = t4.x;
+                    xr[rb][4 * q + 1] = t4.y;
+                    xr[rb][4 * q + 2] = t4.z;
+                    xr[rb][4 * q + 3] = t4.w;
+                }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            const int bcur = b;
             if (s += STEP, s >= STAGES) s -= STAGES;
             if (b += STEP, b >= NB) {
                 b -= NB;
                 pb ^= 1u;
+            }
+#pragma unroll
+            for (int rb = 0; rb < RPT; ++rb) {
+            const int64_t row = row0 + rb * TG::M;
+            const float* x = xr[rb];
+            if (rb > 0) {
+                const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((bcur * TG::TR + rbase + rb) * N);
+                tmem_ld16(taddr, v);
+                if constexpr (N == 32) tmem_ld16(taddr + 16, v + 16);
+            }
+            if constexpr (RPT > 1) tmem_wait_ld();
+            if (RPT > 1 && rb == RPT - 1) {  // this group's values read: its share of the TMEM buffer is free
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[bcur]);
             }
             {
                 // top-2 of d~_j = |c_j|^2 - 2 x.c_j over all N columns (unused ones screen to 1e38);
@@ -431,6 +464,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                     if (counts_out) atomicAdd(counts_out + remap[lab], 1ULL);
                 }
             }
+            }  // row blocks
         }
         cost = warp_sum(cost);
         if (lane == 0) s_wcost[warp] = cost;
