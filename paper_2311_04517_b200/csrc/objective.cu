@@ -135,7 +135,8 @@ static cudaError_t launch_grid(K kern, int smem, const ObjParams& p, const CUten
 template <int NP, int N, int KPS>
 static cudaError_t launch_tc(const ObjParams& p, const CUtensorMap& tmap, int* nblocks, cudaStream_t st) {
     using TG = TcGeo<NP, N>;
-    auto kern = objective_tc_kernel<NP, N, KPS>;
+    // the cost-only pass (no labels / counts) compiles without the output path: fewer live registers
+    auto kern = (p.labels || p.counts) ? objective_tc_kernel<NP, N, KPS, true> : objective_tc_kernel<NP, N, KPS, false>;
     const int smem = objective_tc_smem<NP, N>(p.kv);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

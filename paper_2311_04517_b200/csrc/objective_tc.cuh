@@ -114,10 +114,26 @@ HPCG_DEV bool mbar_try(uint64_t* bar, uint32_t phase) {
 HPCG_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
     while (!mbar_try(bar, phase)) __nanosleep(40);
 }
+// the same on a shared-memory address already converted (hot loops keep the u32 base)
+HPCG_DEV void mbar_wait_sleep_u32(uint32_t addr, uint32_t phase) {
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(addr), "r"(phase)
+            : "memory");
+        if (ok) return;
+        __nanosleep(40);
+    }
+}
+HPCG_DEV void mbar_arrive_u32(uint32_t addr) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 
 // KPS: centre pairs screened (ceil(kv / 2) of the N / 2 columns pairs; a compile-time count keeps
 // the top-2 branch free)
-template <int NP, int N, int KPS>
+template <int NP, int N, int KPS, bool OUT = true>  // OUT: labels / counts requested (else cost only)
 __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
     objective_tc_kernel(const ObjParams p, const __grid_constant__ CUtensorMap tmap) {
     using TG = TcGeo<NP, N>;
@@ -269,38 +285,49 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
         uint32_t pb = 0;
         int64_t row0 = ((int64_t)blockIdx.x + (int64_t)tp * gridDim.x) * TG::TM + rbase * TG::M + r;
         const int64_t row_step = STEP * (int64_t)gridDim.x * TG::TM;
+        // loop invariants: barrier addresses, this lane's TMEM column base, its rows' chunk offsets in a stage
+        const uint32_t tfull_u = smem_u32(&tfull[0]), tempty_u = smem_u32(&tempty[0]), empty_u = smem_u32(&empty[0]);
+        const uint32_t tbase = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)(rbase * N);
+        const uint32_t ring_u = smem_u32(ring);
+        uint32_t xoff[RPT][NP / 4];
+#pragma unroll
+        for (int rb = 0; rb < RPT; ++rb)
+#pragma unroll
+            for (int q = 0; q < NP / 4; ++q) xoff[rb][q] = (uint32_t)G::elem_off((rbase + rb) * TG::M + r, q * 4) * 4u;
         for (int i = tp; i < my; i += STEP, row0 += row_step) {
-            mbar_wait_sleep(&tfull[b], pb);
+            mbar_wait_sleep_u32(tfull_u + 8u * (uint32_t)b, pb);
             tc_fence_after();
             // the first row block's screened values: tcgen05.ld in flight while the rows are read
             uint32_t v[N];
             {
-                const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((b * TG::TR + rbase) * N);
+                const uint32_t taddr = tbase + (uint32_t)(b * TG::TR * N);
                 tmem_ld16(taddr, v);
                 if constexpr (N == 32) tmem_ld16(taddr + 16, v + 16);
                 if constexpr (RPT == 1) {  // one row block: its values read, the TMEM buffer share is free
                     tmem_wait_ld();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[b]);
+                    if (lane == 0) mbar_arrive_u32(tempty_u + 8u * (uint32_t)b);
                 }
             }
             // the rows of this group's row blocks: their stage has landed (the MMAs that read it completed)
-            const float* tile = reinterpret_cast<const float*>(ring + s * TILE);
+            const uint32_t tile_u = ring_u + (uint32_t)(s * TILE);
             float xr[RPT][NP];
 #pragma unroll
             for (int rb = 0; rb < RPT; ++rb)
 #pragma unroll
                 for (int q = 0; q < NP / 4; ++q) {
-                    const float4 t4 =
-                        *reinterpret_cast<const float4*>(tile + G::elem_off((rbase + rb) * TG::M + r, q * 4));
+                    float4 t4;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(t4.x), "=f"(t4.y), "=f"(t4.z), "=f"(t4.w)
+                                 : "r"(tile_u + xoff[rb][q]));
                     xr[rb][4 * q] = t4.x;
                     xr[rb][4 * q + 1] = t4.y;
                     xr[rb][4 * q + 2] = t4.z;
                     xr[rb][4 * q + 3] = t4.w;
                 }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            if (lane == 0) mbar_arrive_u32(empty_u + 8u * (uint32_t)s);
             const int bcur = b;
             if (s += STEP, s >= STAGES) s -= STAGES;
             if (b += STEP, b >= NB) {
@@ -312,7 +339,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
             const int64_t row = row0 + rb * TG::M;
             const float* x = xr[rb];
             if (rb > 0) {
-                const uint32_t taddr = tm + ((uint32_t)(wq * 32) << 16) + (uint32_t)((bcur * TG::TR + rbase + rb) * N);
+                const uint32_t taddr = tbase + (uint32_t)((bcur * TG::TR + rb) * N);
                 tmem_ld16(taddr, v);
                 if constexpr (N == 32) tmem_ld16(taddr + 16, v + 16);
             }
@@ -320,7 +347,7 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
             if (RPT > 1 && rb == RPT - 1) {  // this group's values read: its share of the TMEM buffer is free
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[bcur]);
+                if (lane == 0) mbar_arrive_u32(tempty_u + 8u * (uint32_t)bcur);
             }
             {
                 // top-2 of d~_j = |c_j|^2 - 2 x.c_j over all N columns (unused ones screen to 1e38);
@@ -460,8 +487,10 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                         }
                         cost += (a[0] + a[1]) + (a[2] + a[3]);
                     }
-                    if (labels_out) labels_out[row] = remap[lab];
-                    if (counts_out) atomicAdd(counts_out + remap[lab], 1ULL);
+                    if constexpr (OUT) {
+                        if (labels_out) labels_out[row] = remap[lab];
+                        if (counts_out) atomicAdd(counts_out + remap[lab], 1ULL);
+                    }
                 }
             }
             }  // row blocks
