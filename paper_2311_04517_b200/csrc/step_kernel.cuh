@@ -405,7 +405,7 @@ HPCG_DEV double exact_dist(const T* samp, int row, const double* c, int n) {
 }
 
 // ------------------------------------------------------------------ the kernel
-template <typename T, int NP>
+template <typename T, int NP, bool TRACE = false>  // TRACE: the phase timeline (diagnostics) compiled in
 __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kernel(const StepParams p) {
     using G = Geo<T, NP>;
     cg::cluster_group cluster = cg::this_cluster();
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
 
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ StepShared sh;
-    int64_t* trace = p.trace ? p.trace + (int64_t)blockIdx.x * kTraceSlots : nullptr;
+    int64_t* trace = (TRACE && p.trace) ? p.trace + (int64_t)blockIdx.x * kTraceSlots : nullptr;
     int tslot = 0;
     auto mark = [&]() {
         if (trace && tid == 0 && tslot < kTraceSlots) trace[tslot] = gtimer();
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             if (p.sample_mode == 1) return (int64_t)prp((uint64_t)i);
             return (int64_t)wl * s + i;
         };
-        if (p.trace_mode == 0) stamp(16);
+        if ((TRACE && p.trace_mode == 0)) stamp(16);
         const int rowb = n * (int)sizeof(T);
         if constexpr (G::VEC16 && 32 % G::CPR == 0) {
             if (n == NP) {  // whole rows of 16-B chunks. Per warp step: every lane computes one
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 }
             }
         }
-        if (p.trace_mode == 0) stamp(17);
+        if ((TRACE && p.trace_mode == 0)) stamp(17);
         if (NP > n)
             for (int e = tid; e < nr * (NP - n); e += kStepThreads) {
                 const int li = e / (NP - n), d = n + (e - li * (NP - n));
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
         mbar_init(&sh.cbar, 1);
         mbar_init_fence();
     }
-    if (p.trace_mode == 0) stamp(18);
+    if ((TRACE && p.trace_mode == 0)) stamp(18);
     mark();  // 1: copies issued
     cp_async_wait_all();
     __syncthreads();  // gx (aliases d2) fully consumed before seeding reuses the region
@@ -902,9 +902,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 sh.cta_total = texcl + run;
             }
             __syncthreads();
-            if (it == 0 && p.trace_mode == 1) mark();  // 5: CDF local done
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 5: CDF local done
             const double* rxt = exchange(1, [&](int) { return sh.cta_total; }, true);
-            if (it == 0 && p.trace_mode == 1) mark();  // 6: CDF exchange complete
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 6: CDF exchange complete
             // P = sum of lower ranks' totals (rank order); total = P_{C-1} + T_{C-1}: one thread,
             // published to the CTA
             if (tid == 0) {
@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 if (lane == 0) sh.whit[warp][c] = h;
             }
             __syncthreads();
-            if (it == 0 && p.trace_mode == 1) mark();  // 7: search done
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 7: search done
             // cum is monotone across the cluster and P equals the previous rank's last cum
             // exactly, so exactly one CTA holds the first global row with cum > u_c: the CTA with a
             // local crossing and P <= u_c (rank 0: P = 0); if no row crosses, rank C-1 takes the
@@ -982,11 +982,11 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             }
             mbar_wait_cluster(&sh.cbar, cph);
             cph ^= 1u;
-            if (it == 0 && p.trace_mode == 1) mark();  // 8: candidates received
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 8: candidates received
             for (int c = warp; c < ncand; c += kStepWarps) make_candf(c);
             __syncthreads();
-            if (it == 0 && p.trace_mode == 1) mark();  // 9: candidates fetched
-            if (it == 0 && p.trace_mode == 1) stamp(16);
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 9: candidates fetched
+            if (it == 0 && (TRACE && p.trace_mode == 1)) stamp(16);
             // (3) candidate costs sum_i min(d2_i, dist(S_i, cand_c)) (seeding.hpp:93). First from
             // the fp32 screen with a rigorous per-row error budget; only if two candidates are
             // within their budgets (or tie) are the costs recomputed with exact distances.
@@ -1049,9 +1049,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 int r = tid;
                 if constexpr (kStepThreads <= 512)
                     for (; r - lane + kStepThreads < nr; r += 2 * kStepThreads) rows(IntC<2>{}, r);
-                if (it == 0 && p.trace_mode == 1) stamp(17);
+                if (it == 0 && (TRACE && p.trace_mode == 1)) stamp(17);
                 for (; r - lane < nr; r += kStepThreads) rows(IntC<1>{}, r);
-                if (it == 0 && p.trace_mode == 1) stamp(18);
+                if (it == 0 && (TRACE && p.trace_mode == 1)) stamp(18);
                 // midpoint and half-width per candidate; the slack covers the fp32 lane and warp sums.
                 // The 2 NC butterfly sums run interleaved (same per-value order as warp_sum_f).
                 float vs[NC], es[NC];
@@ -1075,7 +1075,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                         sh.wsum[warp][c] = (double)vs[c];
                         sh.werr[warp][c] = (double)es[c];
                     }
-                if (it == 0 && p.trace_mode == 1) stamp(19);
+                if (it == 0 && (TRACE && p.trace_mode == 1)) stamp(19);
             };
             // (b) exact pass (only when (a) cannot separate the winner): exact distances for every
             //     row the screen cannot settle, compacted into the warp's work list
@@ -1151,8 +1151,8 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                         return v;
                     },
                     true);
-                if (it == 0 && p.trace_mode == 1 && !exact) mark();  // 11: cost exchange complete
-                if (it == 0 && p.trace_mode == 1 && !exact) stamp(20);
+                if (it == 0 && (TRACE && p.trace_mode == 1) && !exact) mark();  // 11: cost exchange complete
+                if (it == 0 && (TRACE && p.trace_mode == 1) && !exact) stamp(20);
                 // warp 0 decides (lane e < 2*ncand sums column e over ranks in rank order) and
                 // publishes the decision to the CTA
                 if (warp == 0) {
@@ -1194,7 +1194,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 case 3: approx_costs(IntC<3>{}); break;
                 default: approx_costs(IntC<kMaxCandidates>{}); break;
             }
-            if (it == 0 && p.trace_mode == 1) mark();  // 10: costs local done
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 10: costs local done
             if (!exchange_decide(false)) {
                 __syncthreads();  // all reads of this exchange precede the exact pass's pushes
                 if (tid == 0) ++sh.exact_passes;
@@ -1205,12 +1205,12 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             const int j = sh.pending[next];
             for (int d = tid; d < NP; d += kStepThreads) Cm[j * NP + d] = d < n ? sh.cand[best][d] : 0.0;
             if (tid == 0) sh.flags[j] = 0;
-            if (it == 0 && p.trace_mode == 1) stamp(21);
-            d2_update_flagged(best, it == 0 && p.trace_mode == 1);
+            if (it == 0 && (TRACE && p.trace_mode == 1)) stamp(21);
+            d2_update_flagged(best, it == 0 && (TRACE && p.trace_mode == 1));
             ++filled;
             __syncthreads();
-            if (it == 0 && p.trace_mode == 1) mark();  // 12: d2 updated (slot done)
-            if (it == 0 && p.trace_mode == 1) stamp(24);
+            if (it == 0 && (TRACE && p.trace_mode == 1)) mark();  // 12: d2 updated (slot done)
+            if (it == 0 && (TRACE && p.trace_mode == 1)) stamp(24);
         }
         __syncthreads();
     }
@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             // max |c_j| over the centroids (records made by the previous means phase)
             const float cmax =
                 __uint_as_float(__reduce_max_sync(0xffffffffu, lane < k ? __float_as_uint(sh.cnorm[lane]) : 0u));
-            if (pass == 0 && p.trace_mode == 0) mark();  // 5: prep done
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 5: prep done
             // ---- assign: fp32 FFMA2 screen, exact fp64 recheck of near ties. Rows are dealt
             // to warps as 32-row chunks (chunk c -> warp c % NW) and each warp screens 4, 2 or 1
             // of its chunks at a time, so warps differ by at most one chunk of work.
@@ -1380,7 +1380,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 }
                 if (t < nchw) screen_chunks(IntC<1>{}, t);
             }
-            if (pass == 0 && p.trace_mode == 0) mark();  // 6: assign done
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 6: assign done
             __syncthreads();
             // CTA-wide stable counting sort by label: cluster ranges + (warp, label) offsets
             if (warp == 0) {
@@ -1413,7 +1413,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                         (uint16_t)(G::VEC16 ? row * G::CPR + G::swz(row) : row);
             }
             __syncthreads();
-            if (pass == 0 && p.trace_mode == 0) mark();  // 7: sort done
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 7: sort done
             // ---- update: sums / cost of the warp's own rows, cluster by cluster along its
             // label-sorted segment; per cluster the lanes cover ROWS_PER_STEP rows x
             // LANES_PER_ROW units (16-B chunks or single elements) so every smem read is a
@@ -1505,20 +1505,20 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 if (lane == 0) wp[k * NP + k] = cost_w;
             }
             __syncthreads();
-            if (pass == 0 && p.trace_mode == 0) mark();  // 8: update done
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 8: update done
             // ---- CTA partial (warps in order) pushed to every CTA; totals in rank order
             const double* totx = reduce_all(part_d, [&](int e) {
                 double v = 0.0;
                 for (int w2 = 0; w2 < kStepWarps; ++w2) v += wpart[w2 * part_d + e];
                 return v;
             });
-            if (pass == 0 && p.trace_mode == 0) mark();  // 9: partials pushed
-            if (pass == 0 && p.trace_mode == 0) mark();  // 10: exchange complete
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 9: partials pushed
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 10: exchange complete
             __syncthreads();  // every warp partial consumed before tot overwrites wpart
             double* tot = wpart;
             for (int e = tid; e < part_d; e += kStepThreads) tot[e] = totx[e];
             __syncthreads();
-            if (pass == 0 && p.trace_mode == 0) mark();  // 11: cluster reduce done
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 11: cluster reduce done
             const double f = tot[k * NP + k];
             if (hist_len > 0 && f > last * (1.0 + 1e-12)) {  // lloyd.hpp:114-121
                 if (tid == 0) sh.err = kErrMonotone;
@@ -1572,7 +1572,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             }
             closing = go_close;
             __syncthreads();
-            if (pass == 0 && p.trace_mode == 0) mark();  // 12: means done
+            if (pass == 0 && (TRACE && p.trace_mode == 0)) mark();  // 12: means done
         }
         // outputs of the last pass: labels (sample order), flags = empty clusters
         if (stop >= 0) {
@@ -1624,7 +1624,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
         }
     }
     if (trace && tid == 0) {
-        if (p.trace_mode == 1) {
+        if ((TRACE && p.trace_mode == 1)) {
             trace[kTraceSlots - 3] = sh.exact_passes;
             trace[kTraceSlots - 4] = sh.exact_rows;
             trace[kTraceSlots - 7] = sh.exact_rows1;

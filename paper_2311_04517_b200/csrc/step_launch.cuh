@@ -125,7 +125,14 @@ cudaError_t launch_step_t(const StepParams& p_in, cudaStream_t st, StepGeometry*
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, worker_step_kernel<T, NP>, p);
+    if (p.trace) {  // the diagnostic timeline build (same geometry: the attributes are set for both)
+        auto kt = worker_step_kernel<T, NP, true>;
+        cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+        cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaLaunchKernelEx(&cfg, kt, p);
+    } else {
+        e = cudaLaunchKernelEx(&cfg, worker_step_kernel<T, NP>, p);
+    }
     if (geo_out) *geo_out = g;
     static const bool dbg = getenv("HPCG_DEBUG") != nullptr;
     if (dbg)
