@@ -7,6 +7,6 @@ for v in "$@"; do
   if [ "$v" = main ]; then unset HPCG_LIB_OVERRIDE; else export HPCG_LIB_OVERRIDE=$PWD/$v; fi
   for c in 5 4; do
     ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_${nm}_$c.csv python tools/prof_wide.py $c 1 > /dev/null 2>&1
-    echo "== $nm config $c"; python tools/launch_table.py gpurun_out/${T}_${nm}_$c.csv 6
+    echo "== $nm config $c"; python tools/launch_summary.py gpurun_out/${T}_${nm}_$c.csv 6
   done
 done
