@@ -36,6 +36,7 @@ constexpr int kJT = 8;             // centroids per distance tile (registers)
 struct WState {
     int32_t n_pending, n_valid, next, it, filled, seed_stop;  // seeding progress
     int32_t best;                                             // winner of the current slot
+    int32_t ambig;  // the slot's interval costs did not separate the winner: exact cost pass pending
     int32_t iters, stop, hist_len, closing, done, err, run_lloyd;
     int64_t nd;
     double f_prev, last, f_final;
@@ -43,6 +44,7 @@ struct WState {
 
 struct WideBufs {  // device scratch for one worker batch
     void* S = nullptr;
+    double* bcost_hi = nullptr;  // upper ends of the candidate-cost partials (interval pass)
     double *Cm = nullptr, *d2 = nullptr, *cand = nullptr, *btot = nullptr, *bcost = nullptr,
            *part = nullptr, *lastcnt = nullptr;
     uint8_t* flags = nullptr;
@@ -618,14 +620,14 @@ __global__ void wide_draw_kernel(const StepParams p, int w0, WideBufs b, int nbl
 // the warps in order give one partial per (CTA, candidate): costs are exact sums in a fixed order.
 constexpr int kCostBPC = 8;  // 256-row blocks per CTA of the candidate-cost pass
 
-template <typename T>
+template <typename T, bool IV>  // exact either way (hi = lo); !IV: only the workers the interval decision left open
 __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, WideBufs b, int nblk) {
     __shared__ double wred[kMaxCandidates][kWT / 32];
     extern __shared__ __align__(16) float crec_raw[];  // [ncand][n4] -2 * candidate (fp32)
     __shared__ float ccn[kMaxCandidates];
     const int w = blockIdx.y, n = p.n, ncand = p.candidates;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (!slot_live(b.st[w])) return;
+    if (!slot_live(b.st[w]) || (!IV && !b.st[w].ambig)) return;
     const int n4 = (n + 3) & ~3;
     auto crec = [&](int c) { return crec_raw + (int64_t)c * n4; };
     const double* cand = b.cand + (int64_t)w * kMaxCandidates * n;
@@ -700,6 +702,7 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
         double tot = 0.0;
         for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
         b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
+        b.bcost_hi[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
     }
 }
 
@@ -707,7 +710,7 @@ __global__ void __launch_bounds__(kWT) wide_cost_kernel(const StepParams p, Wide
 // registers, candidates' fp32 records and fp64 coordinates in shared memory (broadcast loads), the
 // screen bounds' |c| terms hoisted; identical arithmetic and summation order to wide_cost_kernel, so
 // the partials are bit-identical to it.
-template <typename T, int NP>
+template <typename T, int NP, bool IV>  // exact (hi = lo: the first decision is final); IV false: gated re-run
 __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, WideBufs b, int nblk) {
     __shared__ double wred[kMaxCandidates][kWT / 32];
     __shared__ __align__(16) float crec[kMaxCandidates][NP];
@@ -715,7 +718,7 @@ __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, W
     __shared__ float ccn[kMaxCandidates], ccr[kMaxCandidates];
     const int w = blockIdx.y, ncand = p.candidates;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (!slot_live(b.st[w])) return;
+    if (!slot_live(b.st[w]) || (!IV && !b.st[w].ambig)) return;
     const double* cand = b.cand + (int64_t)w * kMaxCandidates * NP;
     for (int e = threadIdx.x; e < kMaxCandidates * NP; e += kWT) {
         const int c = e / NP, d = e - c * NP;
@@ -788,7 +791,10 @@ __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, W
             double v = d2i;
             const float sc = xn + ccr[c];
             const float dt = xx + (a[c].x + a[c].y);
-            if (!(dt - kappa * sc * sc > f2)) {  // may improve: the reference distance
+            const float B = kappa * sc * sc;
+            if (!(dt - B > f2)) {  // may improve: the reference distance (narrow rows: about what interval
+                                   // bookkeeping would cost, so this pass is exact and the decision final)
+                fl |= 1u << c;
                 double e = 0.0;
 #pragma unroll
                 for (int d = 0; d < NP; ++d) {
@@ -796,16 +802,15 @@ __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, W
                     e = __dadd_rn(e, __dmul_rn(diff, diff));
                 }
                 v = fmin(d2i, e);
-                fl |= 1u << c;
             }
             acc[c] += v;
         }
-        flw[i] = (uint8_t)fl;
+        if (IV) flw[i] = (uint8_t)fl;
     }
 #pragma unroll
     for (int c = 0; c < kMaxCandidates; ++c) {
         if (c >= ncand) break;
-        const double v = warp_sum(acc[c]);
+        const double v = warp_sum(acc[c]);  // warp trees, then the warps in order (fixed order)
         if (lane == 0) wred[c][warp] = v;
     }
     __syncthreads();
@@ -813,6 +818,7 @@ __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, W
         double tot = 0.0;
         for (int q = 0; q < kWT / 32; ++q) tot += wred[threadIdx.x][q];
         b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
+        b.bcost_hi[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot;
     }
 }
 
@@ -824,15 +830,16 @@ __global__ void __launch_bounds__(kWT) wide_cost_np_kernel(const StepParams p, W
 // exactly like wide_cost_kernel and, when the candidate may improve, evaluates the reference
 // distance (ascending d, non-fused, one lane per pair). Sums: per candidate over rows in a fixed
 // order (the lanes' running sums, then a fixed tree and the warps in order).
-template <int NP>
+template <int NP, bool IV>  // IV: interval pass; else the exact pass for the workers it left undecided
 __global__ void __launch_bounds__(kWT) wide_cost_rows_kernel(const StepParams p, WideBufs b, int nblk) {
     static_assert(NP % 4 == 0 && NP <= 128, "row width");
     __shared__ double wred[kMaxCandidates][kWT / 32];
+    __shared__ double wred_hi[kMaxCandidates][kWT / 32];
     __shared__ __align__(16) float crec[3][NP];
     __shared__ float ccn[3], ccr[3];
     const int w = blockIdx.y, ncand = p.candidates;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (!slot_live(b.st[w])) return;
+    if (!slot_live(b.st[w]) || (!IV && !b.st[w].ambig)) return;
     const double* cand = b.cand + (int64_t)w * kMaxCandidates * NP;
     for (int e = threadIdx.x; e < 3 * NP; e += kWT) {
         const int c = e / NP, d = e - c * NP;
@@ -861,7 +868,7 @@ __global__ void __launch_bounds__(kWT) wide_cost_rows_kernel(const StepParams p,
     float4 cv[3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) cv[cc] = has ? *reinterpret_cast<const float4*>(&crec[cc][d0]) : make_float4(0, 0, 0, 0);
-    double acc = 0.0;  // lane's running cost of candidate c (q >= 1)
+    double acc = 0.0, acch = 0.0;  // lane's running cost interval of candidate c (q >= 1)
     const int64_t gstep = (int64_t)(kWT / 32) * 8;
     float4 xn8[8];  // the next group's rows, loaded while the current group is screened
     auto load_group = [&](int64_t g0) {
@@ -915,9 +922,13 @@ __global__ void __launch_bounds__(kWT) wide_cost_rows_kernel(const StepParams p,
             const float xn = sqrtf(xx) * 1.0001f, f2 = __double2float_ru(d2i);
             const float sc = xn + ccr[c];
             const float dt = xx + (ccn[c] + tot);
-            may = !(dt - kappa * sc * sc > f2);
-            double vv = d2i;
-            if (may) {  // the reference distance (core.hpp:100-108), this lane alone
+            const float B = kappa * sc * sc;
+            may = !(dt - B > f2);
+            double vv = d2i, vh = d2i;
+            if (IV && may) {  // the true min(d2, dist) lies in [min(d2, dt - B), min(d2, dt + B)]
+                vv = fmin(d2i, (double)fmaxf(dt - B, 0.f));
+                vh = fmin(d2i, (double)(dt + B));
+            } else if (may) {  // the reference distance (core.hpp:100-108), this lane alone
                 const float* xr = Sw + i * NP;
                 const double* cd = cand + (int64_t)c * NP;
                 double e = 0.0;
@@ -935,57 +946,96 @@ __global__ void __launch_bounds__(kWT) wide_cost_rows_kernel(const StepParams p,
                     df = __dsub_rn((double)x4.w, c23.y);
                     e = __dadd_rn(e, __dmul_rn(df, df));
                 }
-                vv = fmin(d2i, e);
+                vv = vh = fmin(d2i, e);
             }
             acc += vv;
+            acch += vh;
         }
         // the row's flag byte: bit c from lane 4r + 1 + c
         const unsigned bal = __ballot_sync(0xffffffffu, may);
-        if (q == 0 && valid) flw[i] = (uint8_t)((bal >> (lane + 1)) & 7u);
+        if (IV && q == 0 && valid) flw[i] = (uint8_t)((bal >> (lane + 1)) & 7u);
     }
     // candidate c: lanes 4r + 1 + c (r = 0..7), a fixed tree, then the warps in order
-    double t = acc;
+    double t = acc, th = acch;
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane >= 1 && lane <= 3) wred[lane - 1][warp] = t;
+    for (int o = 4; o < 32; o <<= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+        th += __shfl_xor_sync(0xffffffffu, th, o);
+    }
+    if (lane >= 1 && lane <= 3) {
+        wred[lane - 1][warp] = t;
+        wred_hi[lane - 1][warp] = th;
+    }
     __syncthreads();
     if (threadIdx.x < ncand) {
-        double tot2 = 0.0;
-        for (int q2 = 0; q2 < kWT / 32; ++q2) tot2 += wred[threadIdx.x][q2];
+        double tot2 = 0.0, toth2 = 0.0;
+        for (int q2 = 0; q2 < kWT / 32; ++q2) {
+            tot2 += wred[threadIdx.x][q2];
+            toth2 += wred_hi[threadIdx.x][q2];
+        }
         b.bcost[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = tot2;
+        b.bcost_hi[((int64_t)w * kMaxCandidates + threadIdx.x) * nblk + blockIdx.x] = toth2;
     }
 }
 
 // winner of the slot (strict <, first candidate wins ties: seeding.hpp:94-98) into its slot. Warp c
 // sums candidate c's block partials (lanes strided, then a shuffle tree: a fixed order).
+// EXACT = false: after the interval pass. The cost of candidate c lies in [lo_c, hi_c] (sums of the
+// per-row interval ends, a 1e-9 relative slack for the summation order); if one candidate's hi is
+// below every other's lo it is the strict winner of the exact costs and the slot is decided, else
+// the worker is marked for the exact pass. EXACT = true: after the exact pass, for marked workers.
+template <bool EXACT>
 __global__ void wide_decide_kernel(const StepParams p, WideBufs b, int nblk) {
     const int w = blockIdx.x, n = p.n, k = p.k, ncand = p.candidates;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WState* stp = b.st + w;
-    if (!slot_live(*stp)) return;
-    __shared__ double tot_s[kMaxCandidates];
+    if (!slot_live(*stp) || (EXACT && !stp->ambig)) return;
+    __shared__ double tot_s[kMaxCandidates], toth_s[kMaxCandidates];
     __shared__ int best_s;
-    if (warp < ncand) {  // one partial per cost CTA (wide_cost_kernel)
+    if (warp < ncand) {  // one partial per cost CTA
         const double* bc_c = b.bcost + ((int64_t)w * kMaxCandidates + warp) * nblk;
+        const double* bh_c = b.bcost_hi + ((int64_t)w * kMaxCandidates + warp) * nblk;
         const int ncta = (nblk + kCostBPC - 1) / kCostBPC;
-        double t = 0.0;
-        for (int q = lane; q < ncta; q += 32) t += bc_c[q];
+        double t = 0.0, th = 0.0;
+        for (int q = lane; q < ncta; q += 32) {
+            t += bc_c[q];
+            th += bh_c[q];
+        }
         t = warp_sum(t);
-        if (lane == 0) tot_s[warp] = t;
+        th = warp_sum(th);
+        if (lane == 0) {
+            tot_s[warp] = t;
+            toth_s[warp] = th;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double bc = __longlong_as_double(0x7ff0000000000000LL);
         int best = 0;
-        for (int c = 0; c < ncand; ++c)
-            if (tot_s[c] < bc) {
-                bc = tot_s[c];
-                best = c;
-            }
+        bool exact = true;
+        for (int c = 0; c < ncand; ++c) exact &= tot_s[c] == toth_s[c];
+        if (EXACT || exact) {  // strict <, the first candidate wins ties (seeding.hpp:94-98)
+            for (int c = 0; c < ncand; ++c)
+                if (tot_s[c] < bc) {
+                    bc = tot_s[c];
+                    best = c;
+                }
+        } else {
+            for (int c = 0; c < ncand; ++c)
+                if (toth_s[c] < bc) {
+                    bc = toth_s[c];
+                    best = c;
+                }
+            const double hb = toth_s[best] * (1.0 + 1e-9);
+            for (int c = 0; c < ncand; ++c)
+                if (c != best && !(hb < tot_s[c] * (1.0 - 1e-9))) best = -1;
+        }
         best_s = best;
+        stp->ambig = best < 0 ? 1 : 0;
     }
     __syncthreads();
     const int best = best_s;
+    if (best < 0) return;  // the exact pass decides
     const int j = b.pend[(int64_t)w * k + stp->next];
     const double* cd = b.cand + ((int64_t)w * kMaxCandidates + best) * n;
     for (int d = threadIdx.x; d < n; d += blockDim.x) b.Cm[((int64_t)w * k + j) * n + d] = cd[d];
@@ -1495,7 +1545,8 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     const size_t oS = take((size_t)Wb * s * n * sizeof(T)), oC = take((size_t)Wb * kn * 8),
                  od2 = take((size_t)Wb * s * 8), orf = take((size_t)Wb * s),
                  ocand = take((size_t)Wb * kMaxCandidates * n * 8), obt = take((size_t)Wb * (nblk + 1) * 8),
-                 obc = take((size_t)Wb * kMaxCandidates * nblk * 8), opart = take((size_t)Wb * G * pd * 8),
+                 obc = take((size_t)Wb * kMaxCandidates * nblk * 8), obch = take((size_t)Wb * kMaxCandidates * nblk * 8),
+                 opart = take((size_t)Wb * G * pd * 8),
                  olc = take((size_t)Wb * k * 8), ofl = take((size_t)Wb * k), opend = take((size_t)Wb * k * 4),
                  olab = take((size_t)Wb * s * 4), oact = take(4), ost = take((size_t)Wb * sizeof(WState)),
                  occw = take((size_t)Wb * (kTcwN + 1) * 4);
@@ -1514,6 +1565,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     b.cand = reinterpret_cast<double*>(c8 + ocand);
     b.btot = reinterpret_cast<double*>(c8 + obt);
     b.bcost = reinterpret_cast<double*>(c8 + obc);
+    b.bcost_hi = reinterpret_cast<double*>(c8 + obch);
     b.part = reinterpret_cast<double*>(c8 + opart);
     b.lastcnt = reinterpret_cast<double*>(c8 + olc);
     b.flags = reinterpret_cast<uint8_t*>(c8 + ofl);
@@ -1558,7 +1610,9 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     if (e != cudaSuccess) return e;
     const size_t cost_smem = (size_t)ncand * ((n + 3) & ~3) * 4;
     if (slots > 0) {
-        e = cudaFuncSetAttribute(wide_cost_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem);
+        e = cudaFuncSetAttribute(wide_cost_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wide_cost_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem);
         if (e != cudaSuccess) return e;
     }
     const int staged = (size_t)(nblk + 1) * 8 <= 200 * 1024 ? 1 : 0;
@@ -1580,19 +1634,29 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         wide_cdfscan_kernel<<<(unsigned)Wb, 32, scan_smem, st>>>(b, nblk, staged);
         wide_draw_kernel<T><<<dim3((unsigned)ncand, (unsigned)Wb), 32, 0, st>>>(p, w0, b, nblk);
         const dim3 cgrid((unsigned)((nblk + kCostBPC - 1) / kCostBPC), (unsigned)Wb);
-        if (n == 8)
-            wide_cost_np_kernel<T, 8><<<cgrid, kWT, 0, st>>>(p, b, nblk);
-        else if (n == 16)
-            wide_cost_np_kernel<T, 16><<<cgrid, kWT, 0, st>>>(p, b, nblk);
-        else if (n == 32)
-            wide_cost_np_kernel<T, 32><<<cgrid, kWT, 0, st>>>(p, b, nblk);
-        else if (sizeof(T) == 4 && n == 128 && ncand <= 3)
-            wide_cost_rows_kernel<128><<<cgrid, kWT, 0, st>>>(p, b, nblk);
-        else if (sizeof(T) == 4 && n == 64 && ncand <= 3)
-            wide_cost_rows_kernel<64><<<cgrid, kWT, 0, st>>>(p, b, nblk);
-        else
-            wide_cost_kernel<T><<<cgrid, kWT, cost_smem, st>>>(p, b, nblk);
-        wide_decide_kernel<<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
+        // the interval pass and its decision, then the exact pass + decision for undecided workers
+        const bool interval = sizeof(T) == 4 && (n == 128 || n == 64) && ncand <= 3;
+        auto cost_pass = [&](auto ivc) {
+            constexpr bool IV = decltype(ivc)::value != 0;
+            if (n == 8)
+                wide_cost_np_kernel<T, 8, IV><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+            else if (n == 16)
+                wide_cost_np_kernel<T, 16, IV><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+            else if (n == 32)
+                wide_cost_np_kernel<T, 32, IV><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+            else if (sizeof(T) == 4 && n == 128 && ncand <= 3)
+                wide_cost_rows_kernel<128, IV><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+            else if (sizeof(T) == 4 && n == 64 && ncand <= 3)
+                wide_cost_rows_kernel<64, IV><<<cgrid, kWT, 0, st>>>(p, b, nblk);
+            else
+                wide_cost_kernel<T, IV><<<cgrid, kWT, cost_smem, st>>>(p, b, nblk);
+        };
+        cost_pass(IntC<1>{});
+        wide_decide_kernel<false><<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
+        if (interval) {  // only the wide-row pass leaves workers undecided
+            cost_pass(IntC<0>{});
+            wide_decide_kernel<true><<<Wb, 32 * kMaxCandidates, 0, st>>>(p, b, nblk);
+        }
     }
     // Lloyd: passes until every worker of the batch stopped
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);

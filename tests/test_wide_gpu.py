@@ -70,6 +70,27 @@ def test_wide_seeding_with_reference_draws(dtype, n, k, s, npend):
     assert rng.next_u64() == o.next_u64(r2)
 
 
+@pytest.mark.parametrize("n", [64, 128])
+def test_wide_seeding_duplicate_rows_exact_fallback(n):
+    # a sample of 12 distinct rows repeated: K-means++ candidates coincide, their costs tie exactly, the
+    # interval pass of the wide-row cost kernel cannot separate them and the exact pass decides (strict <,
+    # the first candidate wins: seeding.hpp:94-98)
+    rs = np.random.default_rng(n)
+    base = rs.normal(0.0, 2.0, (12, n))
+    X = (base[rs.integers(0, 12, 3000)] + 0.0).astype(np.float32)
+    k = 20
+    init = np.zeros((k, n))
+    deg = np.ones(k, np.uint8)
+    rng = hp.RngStream(4242 + n)
+    Cg, fg = hp.reinit_degenerate(init, deg, X, hp.SeedConfig(), rng)
+    o = orc()
+    r2 = o.rng(seed=4242 + n)
+    Co, fo, _ = o.reinit(X.astype(np.float64), init, deg, r2)
+    assert np.array_equal(fg, fo)
+    assert np.array_equal(Cg, Co)
+    assert rng.next_u64() == o.next_u64(r2)
+
+
 @pytest.mark.parametrize("dtype,n,k", [(np.float32, 128, 25), (np.float64, 33, 7), (np.float32, 8, 300)])
 def test_wide_objective_vs_oracle(dtype, n, k):
     X = mixture(60001, n, min(k, 30), seed=7 + n, dtype=dtype)
