@@ -544,19 +544,78 @@ __global__ void wide_cdf_kernel(const StepParams p, WideBufs b, int nblk, int it
     if (blk >= nblk) return;
     const int64_t s = p.s, r0 = (int64_t)blk * kSeedRows, r1 = min(s, r0 + kSeedRows);
     if (it > 0 && st.it == it) {
+        // the block's flagged rows, compacted across the warp (an exclusive shuffle scan of the lanes'
+        // counts), then up to kCdfIL of them per lane with their exact chains interleaved: each chain is
+        // still the reference's sequential distance, only the latency of several overlaps
+        constexpr int kCdfIL = 4;
+        __shared__ uint16_t flist[256 / 32][kSeedRows];
         const int n = NP ? NP : p.n, best = st.best;
-        const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
         const double* cd = b.cand + ((int64_t)w * kMaxCandidates + best) * n;
         const int64_t a = r0 + (int64_t)lane * kLaneRows;
-        for (int j = 0; j < kLaneRows; ++j) {
-            const int64_t i = a + j;
-            if (i >= r1) break;
-            if ((b.rflag[(int64_t)w * s + i] >> best) & 1u) {
-                const T* x = static_cast<const T*>(b.S) + ((int64_t)w * s + i) * n;
-                double* d2 = b.d2 + (int64_t)w * s + i;
-                *d2 = fmin(*d2, dist1<T>(x, n, cd, vecd));
-            }
+        uint32_t fm = 0;
+#pragma unroll
+        for (int j = 0; j < kLaneRows; ++j)
+            if (a + j < r1 && ((b.rflag[(int64_t)w * s + a + j] >> best) & 1u)) fm |= 1u << j;
+        const int cnt = __popc(fm);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        uint16_t* fl_w = flist[threadIdx.x >> 5];
+        for (int e = incl - cnt; fm; fm &= fm - 1, ++e) fl_w[e] = (uint16_t)(lane * kLaneRows + __ffs(fm) - 1);
+        __syncwarp();
+        for (int e0 = 0; e0 < total; e0 += 32 * kCdfIL) {
+            const T* xr[kCdfIL];
+            double acc[kCdfIL];
+            bool on[kCdfIL];
+#pragma unroll
+            for (int q = 0; q < kCdfIL; ++q) {
+                const int e = e0 + q * 32 + lane;
+                on[q] = e < total;
+                xr[q] = static_cast<const T*>(b.S) + ((int64_t)w * s + r0 + (on[q] ? fl_w[e] : 0)) * n;
+                acc[q] = 0.0;
+            }
+            int d = 0;
+            if constexpr (sizeof(T) == 4) {
+                if ((n & 3) == 0)
+                    for (; d < n; d += 4) {  // 16-B row loads; the four steps of each chain in order
+                        const double2 c01 = __ldg(reinterpret_cast<const double2*>(cd + d));
+                        const double2 c23 = __ldg(reinterpret_cast<const double2*>(cd + d + 2));
+                        float4 xv[kCdfIL];
+#pragma unroll
+                        for (int q = 0; q < kCdfIL; ++q) xv[q] = __ldg(reinterpret_cast<const float4*>(xr[q] + d));
+#pragma unroll
+                        for (int q = 0; q < kCdfIL; ++q) {
+                            double diff = __dsub_rn((double)xv[q].x, c01.x);
+                            acc[q] = __dadd_rn(acc[q], __dmul_rn(diff, diff));
+                            diff = __dsub_rn((double)xv[q].y, c01.y);
+                            acc[q] = __dadd_rn(acc[q], __dmul_rn(diff, diff));
+                            diff = __dsub_rn((double)xv[q].z, c23.x);
+                            acc[q] = __dadd_rn(acc[q], __dmul_rn(diff, diff));
+                            diff = __dsub_rn((double)xv[q].w, c23.y);
+                            acc[q] = __dadd_rn(acc[q], __dmul_rn(diff, diff));
+                        }
+                    }
+            }
+            for (; d < n; ++d) {
+                const double cv = __ldg(cd + d);
+#pragma unroll
+                for (int q = 0; q < kCdfIL; ++q) {
+                    const double diff = __dsub_rn((double)__ldg(xr[q] + d), cv);
+                    acc[q] = __dadd_rn(acc[q], __dmul_rn(diff, diff));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kCdfIL; ++q)
+                if (on[q]) {
+                    double* d2 = b.d2 + (int64_t)w * s + r0 + fl_w[e0 + q * 32 + lane];
+                    *d2 = fmin(*d2, acc[q]);
+                }
+        }
+        __syncwarp();  // every updated D^2 of the block visible to the lanes that scan it
     }
     const BlockScan bs = block_scan(b.d2 + (int64_t)w * s, r0, r1, lane);
     // T_q := the cumulative value at the block's last row, exactly as the draw computes it
