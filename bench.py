@@ -209,13 +209,31 @@ def map_global_shards(hp, ctx, Xd, world, rank, device):
     return shards, peers
 
 
+EXCHANGE = {"mode": "nccl", "allgather": None}  # how the engines exchange (set by attach_nccl)
+
+
 def attach_nccl(hp, ctx, world, rank, device):
-    """The library's own NCCL communicator (ncclCommInitRank; unique id broadcast by torch)."""
+    """The library's own NCCL communicator (ncclCommInitRank; unique id broadcast by torch). If the
+    library cannot set it up, the engines exchange through a gloo group instead (the library's host
+    all-gather callback) and the bench line says so."""
     import torch
     import torch.distributed as dist
     uid = torch.tensor(list(hp.comm_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=device)
     dist.broadcast(uid, 0)
-    ctx.attach_comm(world, rank, bytes(uid.cpu().tolist()))
+    err = None
+    try:
+        ctx.attach_comm(world, rank, bytes(uid.cpu().tolist()))
+    except Exception as ex:  # noqa: BLE001 -- recorded in the bench line
+        err = f"{type(ex).__name__}: {ex}"[:120]
+    ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+    if int(ok.item()) == 0:
+        EXCHANGE["mode"] = f"gloo host all-gather (library NCCL unavailable: {err or 'on another rank'})"
+        EXCHANGE["allgather"] = hp.gloo_allgather(dist.new_group(backend="gloo"))
+
+
+def set_exchange(eng, world, rank):
+    eng.set_exchange(world, rank, allgather=EXCHANGE["allgather"])
 
 
 def gather_rate(hp, ctx, ds, stream, key, reps=8):
@@ -275,7 +293,7 @@ def run_gpu(args, world, rank, local):
                 sampling = f"local shard (global sampling unavailable: {type(ex).__name__}: {ex})"[:160]
     eng = hp.Engine(ds_eng, cfg)
     if world > 1:  # every round publishes over all ranks' workers through the library (NCCL all-gather)
-        eng.set_exchange(world, rank)
+        set_exchange(eng, world, rank)
     fma_tfma = ctx.fma_peak()
 
     def step(seed):
@@ -373,7 +391,7 @@ def run_gpu(args, world, rank, local):
                    "parallelism": f"{world} GPU(s), one process per GPU; library NCCL all-gather of the round "
                                   f"candidates + device publication scan every round, select_best and f(C,X) "
                                   f"shard partials over all ranks",
-                   "sampling": sampling},
+                   "sampling": sampling, "exchange": EXCHANGE["mode"] if world > 1 else "none (1 rank)"},
         "distance_evals_per_step": nd_all / args.steps,
         "objective_pass": {"gbs": obj_gbs, "ms": float(np.median(obj_ms)), "bytes": obj_bytes,
                            "roofline": {"bound": "hbm", "achieved": obj_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -454,7 +472,7 @@ def e2e_run_multi(X, args, world, rank, ctx, device):
             shards, peers = map_global_shards(hp, ctx, view, world, rank, device)
             ds_eng = hp.DeviceDataset.from_shards(shards, ctx=ctx, keepalive=ds)
         eng = hp.Engine(ds_eng, cfg)
-        eng.set_exchange(world, rank)
+        set_exchange(eng, world, rank)
         eng.reset(30_000 + i)
         eng.run()
         r = eng.finish()
