@@ -452,11 +452,12 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
     const int sl = xch_slice(k, NP, C);
     double* rx1 = part + 2 * C * kXchSmall;            // [2][C][sl]   reduce-scatter inputs
     double* rx2 = rx1 + 2 * C * sl;                    // [2][C*sl]    all-gathered totals
-    uint32_t xcount = 0, xph[2] = {0u, 0u};
+    uint32_t xcount = 0;  // exchanges so far: buffer = count & 1, its mbarrier phase = (count >> 1) & 1
     // all-to-all of nv <= kXchSmall scalars: returns [C][xs] slots in rank order. w0_only: only
     // warp 0 waits for (and may read) the slots; it publishes what the others need through shared
     // memory before a __syncthreads
     auto exchange = [&](int nv, auto&& value_of, bool w0_only = false) -> const double* {
+        const uint32_t ph = (xcount >> 1) & 1u;
         const int par = (int)(xcount++ & 1);
         double* rx = rxs + par * C * xs;
         uint64_t* bar = &sh.xbar[par];
@@ -466,14 +467,14 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             const double v = value_of(e);
             for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(slot_local + e * 8, r), v, mapa_u32(rbar_local, r));
         }
-        if (!w0_only || warp == 0) mbar_wait_cluster(bar, xph[par]);
-        xph[par] ^= 1u;
+        if (!w0_only || warp == 0) mbar_wait_cluster(bar, ph);
         return rx;
     };
     // cluster-wide sum of nv values per CTA, reduced in rank order by the element's owner rank
     // (reduce-scatter) and broadcast (all-gather): returns the nv totals, identical in every CTA
-    uint32_t rcount = 0, rph1[2] = {0u, 0u}, rph2[2] = {0u, 0u};
+    uint32_t rcount = 0;  // reductions so far (buffers / mbarrier phases as for the exchanges)
     auto reduce_all = [&](int nv, auto&& value_of) -> const double* {
+        const uint32_t ph = (rcount >> 1) & 1u;
         const int par = (int)(rcount++ & 1);
         double* in = rx1 + par * C * sl;
         double* tot = rx2 + par * C * sl;
@@ -490,16 +491,14 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
             const int o = e / sl;
             st_async_f64(mapa_u32(in_l + (e - o * sl) * 8, o), v, mapa_u32(b1_l, o));
         }
-        mbar_wait_cluster(b1, rph1[par]);
-        rph1[par] ^= 1u;
+        mbar_wait_cluster(b1, ph);
         const uint32_t tot_l = smem_u32(tot), b2_l = smem_u32(b2);
         for (int e = tid; e < mylen; e += kStepThreads) {
             double t = in[e];
             for (int r = 1; r < C; ++r) t += in[r * sl + e];
             for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(tot_l + (mylo + e) * 8, r), t, mapa_u32(b2_l, r));
         }
-        mbar_wait_cluster(b2, rph2[par]);
-        rph2[par] ^= 1u;
+        mbar_wait_cluster(b2, ph);
         return tot;
     };
 
