@@ -97,6 +97,11 @@ int hpcg_probe_fma_peak(hpcg_ctx* ctx, double* tfma_per_s);
 /* ---- datasets: X (m x n, row-major) resident in HBM  (core.hpp:34-50 Dataset) ------------ */
 int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n,
                         hpcg_dataset** out);
+/* Page-lock caller-owned host memory for the lifetime of an ingest buffer (io.hpp:68-102 load_dataset
+ * fills a std::vector; registered, its upload runs at the full PCIe rate instead of through the
+ * driver's staging copies). The memory stays the caller's; unregister before freeing it. */
+int hpcg_host_register(void* host, int64_t bytes);
+int hpcg_host_unregister(void* host);
 int hpcg_dataset_wrap(hpcg_ctx* ctx, const void* X_dev, hpcg_dtype dtype, int64_t m, int64_t n,
                       hpcg_dataset** out); /* borrows X_dev (must outlive the handle) */
 /* Row-sharded X (multi-GPU global sampling): shard i holds shard_rows[i] rows at

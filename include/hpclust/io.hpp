@@ -84,6 +84,41 @@ inline Dataset load_dataset(const std::string& path, const TableFormat& fmt = {}
     return d;
 }
 
+// Ingest to pinned host memory (additive): the parsed values stay in the
+// Dataset's own vector, page-locked for the holder's lifetime (hpcg_host_register), so
+// DeviceDataset(holder.X) / run(holder.X, cfg) upload at the full PCIe rate. Do not resize
+// holder.X.values while it is pinned.
+struct PinnedDataset {
+    Dataset X;
+    bool pinned = false;
+    PinnedDataset() = default;
+    explicit PinnedDataset(Dataset&& d) : X(std::move(d)) {
+        pinned = !X.values.empty() &&
+                 hpcg_host_register(X.values.data(), (std::int64_t)(X.values.size() * sizeof(double))) == HPCG_OK;
+    }
+    PinnedDataset(PinnedDataset&& o) noexcept : X(std::move(o.X)), pinned(o.pinned) { o.pinned = false; }
+    PinnedDataset& operator=(PinnedDataset&& o) noexcept {
+        release();
+        X = std::move(o.X);
+        pinned = o.pinned;
+        o.pinned = false;
+        return *this;
+    }
+    PinnedDataset(const PinnedDataset&) = delete;
+    PinnedDataset& operator=(const PinnedDataset&) = delete;
+    ~PinnedDataset() { release(); }
+
+private:
+    void release() {
+        if (pinned) hpcg_host_unregister(X.values.data());
+        pinned = false;
+    }
+};
+
+inline PinnedDataset load_dataset_pinned(const std::string& path, const TableFormat& fmt = {}) {
+    return PinnedDataset(load_dataset(path, fmt));
+}
+
 inline void save_dataset(const Dataset& X, const std::string& path, const TableFormat& fmt = {}) {
     std::ofstream out(path, std::ios::binary);
     if (!out) throw std::runtime_error("cannot open file for writing: " + path);

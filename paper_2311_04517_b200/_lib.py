@@ -25,7 +25,8 @@ EXPORTS = (
     "hpcg_engine_reset", "hpcg_engine_import_best", "hpcg_engine_set_trace", "hpcg_engine_worker_incumbents",
     "hpcg_engine_publications", "hpcg_sample_gather_dev", "hpcg_philox_seed_draws", "hpcg_engine_round_outcome",
     "hpcg_engine_philox_key", "hpcg_comm_unique_id", "hpcg_ctx_attach_comm", "hpcg_ctx_comm_info",
-    "hpcg_engine_set_exchange", "hpcg_ctx_upload_bytes", "hpcg_ctx_set_fp32_cost",
+    "hpcg_engine_set_exchange", "hpcg_ctx_upload_bytes", "hpcg_ctx_set_fp32_cost", "hpcg_host_register",
+    "hpcg_host_unregister",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -119,6 +120,8 @@ def _load():
         "hpcg_ipc_export": (C.c_int, [P, P]),
         "hpcg_ipc_open": (C.c_int, [P, P, P]),
         "hpcg_ipc_close": (C.c_int, [P, P, P]),
+        "hpcg_host_register": (C.c_int, [P, C.c_int64]),
+        "hpcg_host_unregister": (C.c_int, [P]),
         "hpcg_dataset_wrap": (C.c_int, [P, P, C.c_int, I64, I64, P]),
         "hpcg_dataset_destroy": (C.c_int, [P]),
         "hpcg_dataset_device_ptr": (P, [P]),

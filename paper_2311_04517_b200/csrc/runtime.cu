@@ -1011,6 +1011,26 @@ int hpcg_probe_fma_peak(hpcg_ctx* ctx, double* tfma) {
 }
 
 // ------------------------------------------------------------------ datasets
+int hpcg_host_register(void* host, int64_t bytes) {
+    if (!host || bytes < 1) return fail(HPCG_EINVAL, "host_register: empty range");
+    cudaError_t e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HPCG_ECUDA, cudaGetErrorString(e));
+    }
+    return HPCG_OK;
+}
+
+int hpcg_host_unregister(void* host) {
+    if (!host) return fail(HPCG_EINVAL, "host_unregister: null pointer");
+    cudaError_t e = cudaHostUnregister(host);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HPCG_ECUDA, cudaGetErrorString(e));
+    }
+    return HPCG_OK;
+}
+
 int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n,
                         hpcg_dataset** out) {
     if (m < 1 || n < 1) return fail(HPCG_EINVAL, "Dataset: needs at least one row and one column");
