@@ -201,6 +201,15 @@ typedef struct hpcg_engine_cfg {
     int32_t worker_base;  /* global id of worker 0 on this rank (multi-GPU), else 0 */
     double time_limit;    /* seconds; > 0: wall-clock schedule (engine.hpp:348-374) with max_samples an
                              optional per-worker cap (0 = none); 0: lockstep over max_samples rounds */
+    int32_t free_running; /* wall-clock schedule only. 0: round granularity (every worker of a round starts
+                             from the round's snapshot). 1: free-running workers with immediate publication
+                             (engine.hpp:355-371): groups of workers advance on their own streams, each step
+                             draws its init from a device-side versioned incumbent under a lock and an
+                             accepted cooperative result is published the moment its group's step ends;
+                             the device clock decides stop and phase per worker. Philox streams, one rank,
+                             cluster-resident shapes. */
+    int32_t free_group;   /* workers per free-running group (0 = automatic: ceil(W / 16)); 1 = every
+                             worker publishes on its own */
 } hpcg_engine_cfg;
 
 typedef struct hpcg_run_out {
@@ -228,6 +237,10 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds);
  * first round end past phase_t1 seconds, trace timestamps are seconds). */
 int hpcg_engine_run(hpcg_engine* e);
 int64_t hpcg_engine_round_index(const hpcg_engine* e);
+/* Per-worker progress (WorkerState::samples_processed and t_w, engine.hpp:100, 250): the rounds run and
+ * the last round's clock for the round-granular schedules, each worker's own count and clock for
+ * the free-running schedule. Either pointer may be NULL. */
+int hpcg_engine_worker_progress(hpcg_engine* e, int64_t* samples, double* t_w);
 /* Diagnostics: per-CTA phase timestamps (%globaltimer ns) of subsequent rounds written to
  * trace_dev[W * cluster * 32] (NULL disables); mode 0 details the first Lloyd pass, mode 1
  * the first K-means++ slot. */

@@ -563,6 +563,10 @@ struct EngineConfig {
     bool compute_full_objective = true;
     bool compute_assignment = false;
     RngMode rng_mode = RngMode::reference;  // extension (not in the reference)
+    // extension, wall-clock schedule only: free-running workers with immediate publication
+    // (run_wall_clock, engine.hpp:348-374) instead of round granularity; needs RngMode::philox
+    bool free_running = false;
+    std::size_t free_group = 0;  // workers per free-running group (0 = automatic, 1 = every worker alone)
 
     bool deterministic_mode() const { return !std::isfinite(time_limit) && max_samples.has_value(); }
     double budget() const { return deterministic_mode() ? (double)*max_samples : time_limit; }
@@ -805,6 +809,8 @@ inline ClusteringResult detail::run_ds(hpcg_dataset* ds, std::size_t rows, std::
     ec.compute_full_objective = cfg.compute_full_objective ? 1 : 0;
     ec.compute_assignment = cfg.compute_assignment ? 1 : 0;
     ec.rng_mode = cfg.rng_mode == RngMode::reference ? HPCG_RNG_REFERENCE : HPCG_RNG_PHILOX;
+    ec.free_running = cfg.free_running && !cfg.deterministic_mode() ? 1 : 0;
+    ec.free_group = (int32_t)cfg.free_group;
     hpcg_engine* e = nullptr;
     gpu::check(hpcg_engine_create(gpu::context(), ds, &ec, &e));
     std::unique_ptr<hpcg_engine, int (*)(hpcg_engine*)> guard(e, hpcg_engine_destroy);
@@ -825,6 +831,9 @@ inline ClusteringResult detail::run_ds(hpcg_dataset* ds, std::size_t rows, std::
     std::vector<double> incC(W * k * n);
     std::vector<std::uint8_t> incF(W * k);
     gpu::check(hpcg_engine_worker_incumbents(e, incC.data(), incF.data(), nullptr));
+    std::vector<std::int64_t> w_samples(W);
+    std::vector<double> w_clock(W);
+    gpu::check(hpcg_engine_worker_progress(e, w_samples.data(), w_clock.data()));
     if (o.has_full_objective) res.full_objective = o.full_objective;
     if (cfg.compute_assignment) {
         Assignment a;
@@ -850,8 +859,8 @@ inline ClusteringResult detail::run_ds(hpcg_dataset* ds, std::size_t rows, std::
         std::copy_n(incC.data() + w * k * n, k * n, ws.incumbent.centers.data());
         std::copy_n(incF.data() + w * k, k, ws.incumbent.degenerate.data());
         ws.incumbent_objective = wobj[w];
-        ws.samples_processed = R;
-        ws.t_w = o.last_timestamp;  // the clock read after the worker's last step (engine.hpp:250)
+        ws.samples_processed = (std::size_t)w_samples[w];
+        ws.t_w = w_clock[w];  // the clock read after the worker's last step (engine.hpp:250)
         for (std::int64_t t = 0; t < tlen[w]; ++t)
             ws.update_trace.push_back({traces[(w * R + (std::size_t)t) * 2], traces[(w * R + (std::size_t)t) * 2 + 1]});
     }

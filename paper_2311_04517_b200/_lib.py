@@ -26,7 +26,7 @@ EXPORTS = (
     "hpcg_engine_publications", "hpcg_sample_gather_dev", "hpcg_philox_seed_draws", "hpcg_engine_round_outcome",
     "hpcg_engine_philox_key", "hpcg_comm_unique_id", "hpcg_ctx_attach_comm", "hpcg_ctx_comm_info",
     "hpcg_engine_set_exchange", "hpcg_ctx_upload_bytes", "hpcg_ctx_set_fp32_cost", "hpcg_host_register",
-    "hpcg_host_unregister",
+    "hpcg_host_unregister", "hpcg_engine_worker_progress",
 )
 
 HPCG_OK, HPCG_EINVAL, HPCG_ELOGIC, HPCG_ENOSOL, HPCG_ECUDA, HPCG_ENCCL, HPCG_EUNSUPPORTED = range(7)
@@ -85,7 +85,7 @@ class EngineCfg(C.Structure):
                 ("phase_t2", C.c_double), ("master_seed", C.c_uint64), ("candidates", C.c_int64),
                 ("max_iters", C.c_int64), ("rel_tol", C.c_double), ("compute_full_objective", C.c_int32),
                 ("compute_assignment", C.c_int32), ("rng_mode", C.c_int32), ("worker_base", C.c_int32),
-                ("time_limit", C.c_double)]
+                ("time_limit", C.c_double), ("free_running", C.c_int32), ("free_group", C.c_int32)]
 
 
 class RunOut(C.Structure):
@@ -122,6 +122,7 @@ def _load():
         "hpcg_ipc_close": (C.c_int, [P, P, P]),
         "hpcg_host_register": (C.c_int, [P, C.c_int64]),
         "hpcg_host_unregister": (C.c_int, [P]),
+        "hpcg_engine_worker_progress": (C.c_int, [P, P, P]),
         "hpcg_dataset_wrap": (C.c_int, [P, P, C.c_int, I64, I64, P]),
         "hpcg_dataset_destroy": (C.c_int, [P]),
         "hpcg_dataset_device_ptr": (P, [P]),

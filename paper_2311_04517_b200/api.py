@@ -572,6 +572,8 @@ class EngineConfig:
     rng: str = "reference"  # "reference" (bit-parity streams) or "philox" (device)
     worker_base: int = 0
     time_limit: float = 0.0  # seconds; > 0: wall-clock schedule (engine.hpp:348-374), max_samples a cap
+    free_running: bool = False  # wall clock: free-running workers, immediate publication (engine.hpp:355-371)
+    free_group: int = 0  # workers per free-running group (0 = automatic)
 
     def to_c(self) -> _lib.EngineCfg:
         if self.strategy not in STRATEGIES:
@@ -581,7 +583,7 @@ class EngineConfig:
                               self.candidates, self.max_iters, self.rel_tol, int(self.compute_full_objective),
                               int(self.compute_assignment),
                               _lib.RNG_REFERENCE if self.rng == "reference" else _lib.RNG_PHILOX, self.worker_base,
-                              float(self.time_limit))
+                              float(self.time_limit), int(self.free_running), int(self.free_group))
 
 
 @dataclass
@@ -660,6 +662,12 @@ class Engine:
         nd, acc, fl = np.empty(W, np.int64), np.empty(W, np.uint8), np.empty(W, np.int32)
         check(lib.hpcg_engine_round_outcome(self.h, ptr(obj), ptr(it), ptr(st), ptr(nd), ptr(acc), ptr(fl)))
         return dict(objective=obj, iterations=it, stop=st, n_d=nd, accepted=acc.astype(bool), filled=fl)
+
+    def worker_progress(self):
+        """(samples_processed[W], t_w[W]) -- WorkerState fields engine.hpp:100, 250."""
+        smp, tw = np.zeros(self.W, np.int64), np.zeros(self.W)
+        check(lib.hpcg_engine_worker_progress(self.h, ptr(smp), ptr(tw)))
+        return smp, tw
 
     def worker_incumbents(self):
         k, n, W = self.cfg.k, self.ds.n, self.W

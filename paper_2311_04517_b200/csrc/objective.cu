@@ -44,6 +44,10 @@ cudaError_t launch_step(int dtype, const StepParams& p, cudaStream_t st, StepGeo
             return dtype == 0 ? launch_step_f32(p, st, g, why, np) : launch_step_f64(p, st, g, why, np);
     }
     if (g) *g = StepGeometry{};
+    if (p.go) {  // per-worker go flags are read by the cluster-resident kernel only
+        if (why) *why = "the free-running schedule needs a cluster-resident shape";
+        return cudaErrorNotSupported;
+    }
     return launch_step_wide(dtype, p, st, why);
 }
 

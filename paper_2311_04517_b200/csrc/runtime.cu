@@ -1572,6 +1572,10 @@ struct hpcg_engine {
     int64_t ucap = 0;
     int64_t* trace_buf = nullptr;  // optional phase timeline (hpcg_engine_set_trace)
     int32_t trace_mode = 0;
+    // free-running schedule (cfg.free_running): per-worker progress, init snapshots and traces
+    bool free_mode = false;
+    int64_t fr_cap = 0;  // trace entries kept per worker
+    DevBuf fr_t0, fr_go, fr_coop, fr_entered, fr_samples, fr_tw, fr_init_c, fr_init_f, fr_tcnt, fr_trace, fr_lock;
 };
 
 namespace {
@@ -1880,6 +1884,344 @@ int engine_round(hpcg_engine* e, double now) {
     ++e->round;
     return HPCG_OK;
 }
+
+// ------------------------------------------------------------------------------------------
+// Free-running wall-clock schedule with immediate publication (run_wall_clock, engine.hpp:348-374).
+// The workers are cut into groups; each group advances on its own stream as a chain
+//   between(prep) -> step -> between(post + prep) -> step -> ... -> between(post)
+// and the groups run concurrently. `between` is one warp that does, per worker of the group and in
+// worker-id order, what the reference's worker thread does around worker_step:
+//   post: ++samples_processed, t_w = clock, trace entry of an accepted step (timestamp nudged with
+//         nextafter, engine.hpp:258-262), SharedBest::try_publish of an accepted cooperative step
+//         (engine.hpp:368-370) -- at once, not at a round end;
+//   prep: the loop head (engine.hpp:353-365): one clock reading decides stop (time limit, sample
+//         cap), phase, and the hybrid entry publication; then step_init (engine.hpp:337-343): the
+//         snapshot of the shared best -- or the worker's own incumbent -- copied to the worker's
+//         init slot, which the step kernel reads.
+// The shared best is the device-side versioned incumbent: {version, objective, worker, centroids,
+// flags} guarded by a spin lock taken by one lane (the mutex of engine.hpp:114-157), so snapshots
+// are never torn and publications are strict-< in lock order. The clock is %globaltimer.
+struct FreeParams {
+    int W, k, n, worker_base, strategy;
+    double t1, limit;
+    int64_t max_samples;
+    const unsigned long long* t0;
+    const uint8_t* accepted;
+    const double* inc_obj;
+    const double* inc_c;
+    const uint8_t* inc_f;
+    const int64_t* nd;
+    const int32_t* err;
+    int32_t* err_first;
+    int32_t* go;
+    uint8_t* coop;
+    uint8_t* entered;
+    int64_t* samples;
+    double* tw;
+    double* init_c;
+    uint8_t* init_f;
+    int64_t* trace_cnt;
+    double* trace;  // [W x trace_cap x 2]
+    int64_t trace_cap;
+    unsigned long long* nd_total;
+    int* lock;
+    int64_t* sh_version;
+    double* sh_obj;
+    int32_t* sh_worker;
+    double* sh_c;
+    uint8_t* sh_f;
+    double* pub_log;
+    int64_t* pub_count;
+    int64_t pub_cap;
+};
+
+__device__ __forceinline__ unsigned long long free_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// t0 such that (globaltimer - t0) continues the host's elapsed() (seconds since the engine's t0)
+__global__ void free_t0_kernel(unsigned long long* t0, unsigned long long elapsed_ns) { *t0 = free_gtimer() - elapsed_ns; }
+
+__device__ __forceinline__ void free_lock(int* lock, int lane) {
+    if (lane == 0)
+        while (atomicCAS(lock, 0, 1) != 0) __nanosleep(100);
+    __syncwarp();
+    __threadfence();
+}
+__device__ __forceinline__ void free_unlock(int* lock, int lane) {
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicExch(lock, 0);
+}
+
+// SharedBest::try_publish (engine.hpp:126-136); the caller's warp holds the lock
+__device__ void free_try_publish(const FreeParams& q, int w, double obj, double ts, int lane) {
+    if (!(obj < *(volatile double*)q.sh_obj)) return;
+    const int kn = q.k * q.n;
+    for (int e = lane; e < kn; e += 32) ((volatile double*)q.sh_c)[e] = q.inc_c[(int64_t)w * kn + e];
+    for (int e = lane; e < q.k; e += 32) ((volatile uint8_t*)q.sh_f)[e] = q.inc_f[(int64_t)w * q.k + e];
+    if (lane == 0) {
+        const int64_t ver = *(volatile int64_t*)q.sh_version + 1;
+        *(volatile int64_t*)q.sh_version = ver;
+        *(volatile double*)q.sh_obj = obj;
+        *(volatile int32_t*)q.sh_worker = q.worker_base + w;
+        const int64_t at = *(volatile int64_t*)q.pub_count;
+        if (at < q.pub_cap) {
+            double* rec = q.pub_log + at * 4;
+            rec[0] = (double)ver;
+            rec[1] = (double)(q.worker_base + w);
+            rec[2] = obj;
+            rec[3] = ts;
+        }
+        *(volatile int64_t*)q.pub_count = at + 1;
+    }
+}
+
+__global__ void __launch_bounds__(32) free_between_kernel(const FreeParams q, int w0, int g, int do_post, int do_prep) {
+    const int lane = threadIdx.x;
+    const int kn = q.k * q.n;
+    // every finished step of the group is accounted for (and published) before any worker of the
+    // group takes its next snapshot, so a snapshot sees the group's freshest results
+    for (int i = 0; i < g; ++i) {
+        const int w = w0 + i;
+        if (do_post && q.go[w]) {  // the step this worker was prepared for has run
+            const bool acc = q.accepted[w] != 0;
+            double ts = 0.0;
+            if (lane == 0) {
+                ts = (double)(free_gtimer() - *q.t0) * 1e-9;  // the clock is read once, after the sample
+                q.samples[w] += 1;
+                q.tw[w] = ts;
+                atomicAdd(q.nd_total, (unsigned long long)q.nd[w]);
+                if (q.err[w] != 0 && q.err_first[w] == 0) q.err_first[w] = q.err[w];
+                if (acc) {
+                    const int64_t cnt = q.trace_cnt[w];
+                    double* tr = q.trace + (int64_t)w * q.trace_cap * 2;
+                    if (cnt > 0) {
+                        const double last = tr[(min(cnt, q.trace_cap) - 1) * 2];
+                        if (!(ts > last)) ts = nextafter(last, (double)INFINITY);
+                    }
+                    const int64_t at = min(cnt, q.trace_cap - 1);  // a full trace keeps its latest entry last
+                    tr[at * 2] = ts;
+                    tr[at * 2 + 1] = q.inc_obj[w];
+                    q.trace_cnt[w] = cnt + 1;
+                }
+            }
+            ts = __shfl_sync(0xffffffffu, ts, 0);
+            if (acc && q.coop[w]) {
+                free_lock(q.lock, lane);
+                free_try_publish(q, w, q.inc_obj[w], ts, lane);
+                free_unlock(q.lock, lane);
+            }
+        }
+    }
+    if (!do_prep) return;
+    __syncwarp();
+    for (int i = 0; i < g; ++i) {
+        const int w = w0 + i;
+        int flags = 0;
+        double now = 0.0;
+        if (lane == 0) {
+            now = (double)(free_gtimer() - *q.t0) * 1e-9;
+            const bool go = now < q.limit && (q.max_samples < 1 || q.samples[w] < q.max_samples) && q.err_first[w] == 0;
+            const bool coop = q.strategy == HPCG_COOPERATIVE || (q.strategy == HPCG_HYBRID && now >= q.t1);
+            const bool enter = go && coop && q.strategy == HPCG_HYBRID && !q.entered[w];
+            q.go[w] = go ? 1 : 0;
+            q.coop[w] = coop ? 1 : 0;
+            if (enter) q.entered[w] = 1;
+            flags = (go ? 1 : 0) | (coop ? 2 : 0) | (enter ? 4 : 0);
+        }
+        flags = __shfl_sync(0xffffffffu, flags, 0);
+        now = __shfl_sync(0xffffffffu, now, 0);
+        if (!(flags & 1)) continue;
+        double* ic = q.init_c + (int64_t)w * kn;
+        uint8_t* ifl = q.init_f + (int64_t)w * q.k;
+        if (flags & 2) {
+            free_lock(q.lock, lane);
+            if (flags & 4) {  // engine.hpp:359-364: the phase-1 incumbent enters the shared best
+                const double obj = q.inc_obj[w];
+                if (isfinite(obj)) free_try_publish(q, w, obj, now, lane);
+                __syncwarp();
+            }
+            const int64_t ver = *(volatile int64_t*)q.sh_version;  // snapshot(): nullopt while version == 0
+            for (int e = lane; e < kn; e += 32) ic[e] = ver ? ((volatile double*)q.sh_c)[e] : 0.0;
+            for (int e = lane; e < q.k; e += 32) ifl[e] = ver ? ((volatile uint8_t*)q.sh_f)[e] : (uint8_t)1;
+            free_unlock(q.lock, lane);
+        } else {
+            for (int e = lane; e < kn; e += 32) ic[e] = q.inc_c[(int64_t)w * kn + e];
+            for (int e = lane; e < q.k; e += 32) ifl[e] = q.inc_f[(int64_t)w * q.k + e];
+        }
+    }
+}
+
+int engine_run_free(hpcg_engine* e) {
+    hpcg_ctx* ctx = e->ctx;
+    const int64_t W = e->W, k = e->k, n = e->n, kn = k * n;
+    cudaStream_t st0 = ctx->stream;
+    if (e->round > 0 || e->free_mode) return fail(HPCG_EINVAL, "free-running schedule: the engine has already run");
+    const int gsz = (int)(e->cfg.free_group > 0 ? std::min<int64_t>(e->cfg.free_group, W) : std::max<int64_t>(1, (W + 15) / 16));
+    const int G = (int)((W + gsz - 1) / gsz);
+    const int S = std::min(G, 16);
+    e->fr_cap = 512;
+    CU(e->fr_t0.reserve(8));
+    CU(e->fr_go.reserve((size_t)W * 4));
+    CU(e->fr_coop.reserve((size_t)W));
+    CU(e->fr_entered.reserve((size_t)W));
+    CU(e->fr_samples.reserve((size_t)W * 8));
+    CU(e->fr_tw.reserve((size_t)W * 8));
+    CU(e->fr_init_c.reserve((size_t)(W * kn) * 8));
+    CU(e->fr_init_f.reserve((size_t)(W * k)));
+    CU(e->fr_tcnt.reserve((size_t)W * 8));
+    CU(e->fr_trace.reserve((size_t)(W * e->fr_cap) * 16));
+    CU(e->fr_lock.reserve(4));
+    CU(cudaMemsetAsync(e->fr_go.p, 0, (size_t)W * 4, st0));
+    CU(cudaMemsetAsync(e->fr_coop.p, 0, (size_t)W, st0));
+    CU(cudaMemsetAsync(e->fr_entered.p, 0, (size_t)W, st0));
+    CU(cudaMemsetAsync(e->fr_samples.p, 0, (size_t)W * 8, st0));
+    CU(cudaMemsetAsync(e->fr_tw.p, 0, (size_t)W * 8, st0));
+    CU(cudaMemsetAsync(e->fr_tcnt.p, 0, (size_t)W * 8, st0));
+    CU(cudaMemsetAsync(e->fr_lock.p, 0, 4, st0));
+    const int64_t want_pubs = std::max<int64_t>(e->pub_cap, 16384);
+    CU(e->pub_log.grow((size_t)want_pubs * 32, (size_t)e->pub_cap * 32, st0));
+    e->pub_cap = want_pubs;
+    e->free_mode = true;
+
+    FreeParams q = {};
+    q.W = (int)W;
+    q.k = (int)k;
+    q.n = (int)n;
+    q.worker_base = e->cfg.worker_base;
+    q.strategy = e->cfg.strategy;
+    q.t1 = e->cfg.phase_t1;
+    q.limit = e->cfg.time_limit;
+    q.max_samples = e->cfg.max_samples;
+    q.t0 = e->fr_t0.as<unsigned long long>();
+    q.accepted = e->acc.as<uint8_t>();
+    q.inc_obj = e->inc_obj.as<double>();
+    q.inc_c = e->inc_c.as<double>();
+    q.inc_f = e->inc_f.as<uint8_t>();
+    q.nd = e->nd.as<int64_t>();
+    q.err = e->err.as<int32_t>();
+    q.err_first = e->err_first.as<int32_t>();
+    q.go = e->fr_go.as<int32_t>();
+    q.coop = e->fr_coop.as<uint8_t>();
+    q.entered = e->fr_entered.as<uint8_t>();
+    q.samples = e->fr_samples.as<int64_t>();
+    q.tw = e->fr_tw.as<double>();
+    q.init_c = e->fr_init_c.as<double>();
+    q.init_f = e->fr_init_f.as<uint8_t>();
+    q.trace_cnt = e->fr_tcnt.as<int64_t>();
+    q.trace = e->fr_trace.as<double>();
+    q.trace_cap = e->fr_cap;
+    q.nd_total = e->nd_total.as<unsigned long long>();
+    q.lock = e->fr_lock.as<int>();
+    q.sh_version = e->sh_ver.as<int64_t>();
+    q.sh_obj = e->sh_obj.as<double>();
+    q.sh_worker = e->sh_worker.as<int32_t>();
+    q.sh_c = e->sh_c.as<double>();
+    q.sh_f = e->sh_f.as<uint8_t>();
+    q.pub_log = e->pub_log.as<double>();
+    q.pub_count = e->pub_count.as<int64_t>();
+    q.pub_cap = e->pub_cap;
+
+    StepParams p = {};
+    p.X = e->ds->X;
+    set_shards(p, e->ds);
+    p.m = e->ds->m;
+    SamplePRP::moduli((uint64_t)p.m, p.prp_a, p.prp_b, p.prp_inv_b);
+    p.n = (int)n;
+    p.s = e->s;
+    p.geo_W = (int)W;  // the cluster geometry of the whole engine, whatever the group size
+    p.sample_mode = 1;
+    p.key = e->key;
+    p.init_stride = kn;
+    p.initf_stride = k;
+    p.shared_version = nullptr;
+    p.candidates = (int)e->cfg.candidates;
+    p.seed_mode = 1;
+    p.units_stride = (int)e->ucap;
+    p.k = (int)k;
+    p.max_iters = (int)std::min<int64_t>(e->cfg.max_iters, INT32_MAX);
+    p.rel_tol = e->cfg.rel_tol;
+    p.do_lloyd = 1;
+
+    std::vector<cudaStream_t> streams((size_t)S, nullptr);
+    std::vector<cudaEvent_t> ev((size_t)(2 * S), nullptr);
+    auto cleanup = [&]() {
+        for (auto s_ : streams)
+            if (s_) {
+                cudaStreamSynchronize(s_);
+                cudaStreamDestroy(s_);
+            }
+        for (auto v : ev)
+            if (v) cudaEventDestroy(v);
+    };
+    for (auto& s_ : streams)
+        if (cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking) != cudaSuccess) {
+            cleanup();
+            return fail(HPCG_ECUDA, "free-running schedule: stream creation failed");
+        }
+    for (auto& v : ev)
+        if (cudaEventCreateWithFlags(&v, cudaEventDisableTiming) != cudaSuccess) {
+            cleanup();
+            return fail(HPCG_ECUDA, "free-running schedule: event creation failed");
+        }
+    // the device clock continues the engine's host clock (seconds since t0)
+    free_t0_kernel<<<1, 1, 0, st0>>>(e->fr_t0.as<unsigned long long>(), (unsigned long long)(e->elapsed() * 1e9));
+    cudaError_t ce = cudaStreamSynchronize(st0);
+    ctx->launches += 1;
+    int64_t laps = 0;
+    std::string why;
+    for (; ce == cudaSuccess; ++laps) {
+        if (e->elapsed() >= e->cfg.time_limit) break;
+        if (e->cfg.max_samples > 0 && laps >= e->cfg.max_samples) break;
+        // at most two laps in flight per stream: the host does not run ahead of the device clock
+        if (laps >= 2)
+            for (int si = 0; si < S && ce == cudaSuccess; ++si) ce = cudaEventSynchronize(ev[(size_t)((laps & 1) * S + si)]);
+        for (int grp = 0; grp < G && ce == cudaSuccess; ++grp) {
+            cudaStream_t st = streams[(size_t)(grp % S)];
+            const int w0 = grp * gsz, g = (int)std::min<int64_t>(gsz, W - w0);
+            free_between_kernel<<<1, 32, 0, st>>>(q, w0, g, laps > 0 ? 1 : 0, 1);
+            p.W = g;
+            p.round = (uint32_t)laps;
+            p.worker_base = e->cfg.worker_base + w0;
+            p.init_c = e->fr_init_c.as<double>() + (int64_t)w0 * kn;
+            p.init_f = e->fr_init_f.as<uint8_t>() + (int64_t)w0 * k;
+            p.first_row = e->d_fr.as<int64_t>() + w0;
+            p.units = e->d_un.as<double>() + (int64_t)w0 * e->ucap;
+            p.out_obj = e->objb.as<double>() + w0;
+            p.out_iters = e->iters.as<int32_t>() + w0;
+            p.out_stop = e->stopb.as<int32_t>() + w0;
+            p.out_nd = e->nd.as<int64_t>() + w0;
+            p.out_filled = e->filled.as<int32_t>() + w0;
+            p.out_err = e->err.as<int32_t>() + w0;
+            p.inc_c = e->inc_c.as<double>() + (int64_t)w0 * kn;
+            p.inc_f = e->inc_f.as<uint8_t>() + (int64_t)w0 * k;
+            p.inc_obj = e->inc_obj.as<double>() + w0;
+            p.accepted = e->acc.as<uint8_t>() + w0;
+            p.go = e->fr_go.as<int32_t>() + w0;
+            ce = launch_step(e->ds->dtype, p, st, nullptr, &why);
+            ctx->launches += 2;
+        }
+        for (int si = 0; si < S && ce == cudaSuccess; ++si) ce = cudaEventRecord(ev[(size_t)((laps & 1) * S + si)], streams[(size_t)si]);
+    }
+    if (ce == cudaSuccess && laps > 0)
+        for (int grp = 0; grp < G; ++grp) {  // account for the last prepared steps
+            const int w0 = grp * gsz, g = (int)std::min<int64_t>(gsz, W - w0);
+            free_between_kernel<<<1, 32, 0, streams[(size_t)(grp % S)]>>>(q, w0, g, 1, 0);
+            ctx->launches += 1;
+        }
+    for (auto s_ : streams) {
+        cudaError_t e2 = cudaStreamSynchronize(s_);
+        if (ce == cudaSuccess) ce = e2;
+    }
+    if (ce == cudaSuccess) ce = cudaGetLastError();
+    cleanup();
+    if (ce != cudaSuccess) return fail(HPCG_ECUDA, std::string("free-running schedule: ") + cudaGetErrorString(ce) + " " + why);
+    e->round = laps;  // laps enqueued: an upper bound of every worker's sample count
+    return HPCG_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1950,6 +2292,21 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     if (cfg.candidates > kMaxCandidates) return fail(HPCG_EUNSUPPORTED, "more than 4 K-means++ candidates per centre");
     if (int rc = check_shape(ds->dtype, ds->n, cfg.k)) return rc;
     // shapes without a cluster-resident geometry run on the grid-wide path (launch_step decides)
+    if (cfg.free_running) {
+        if (!wall) return fail(HPCG_EINVAL, "EngineConfig: the free-running schedule needs a time limit");
+        if (cfg.free_group < 0) return fail(HPCG_EINVAL, "EngineConfig: free_group must be nonnegative");
+        if (cfg.rng_mode != HPCG_RNG_PHILOX)
+            return fail(HPCG_EUNSUPPORTED, "the free-running schedule draws on the device: rng_mode must be philox");
+        StepGeometry g_;
+        std::string why_;
+        if (cfg.k > kMaxK || cfg.n_workers > INT32_MAX ||
+            step_geometry(ds->dtype, (int)ds->n, cfg.sample_size, (int)cfg.k, (int)cfg.candidates, (int)cfg.n_workers, &g_,
+                          &why_) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(HPCG_EUNSUPPORTED, "the free-running schedule needs a cluster-resident shape (n <= 32, k <= 32, "
+                                           "sample within a cluster's shared memory)");
+        }
+    }
 
     auto* e = new hpcg_engine;
     e->ctx = ctx;
@@ -2046,6 +2403,8 @@ int hpcg_engine_set_exchange(hpcg_engine* e, int32_t nranks, int32_t rank, hpcg_
         return fail(HPCG_ENCCL, "set_exchange: no matching NCCL communicator attached to the context");
     if (e->cfg.strategy == HPCG_INNER && nranks > 1)
         return fail(HPCG_EUNSUPPORTED, "the inner strategy runs one worker: no multi-rank exchange");
+    if (e->cfg.free_running && nranks > 1)
+        return fail(HPCG_EUNSUPPORTED, "the free-running schedule runs on one rank");
     e->xr = nranks;
     e->xrank = rank;
     e->xfn = fn;
@@ -2110,6 +2469,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     e->pub_ub = 0;
     e->entered_coop = false;
     e->common_now = 0.0;
+    e->free_mode = false;
     return HPCG_OK;
 }
 
@@ -2135,6 +2495,7 @@ int hpcg_engine_import_best(hpcg_engine* e, double obj, int64_t worker, const do
 int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     bind_device(e->ctx->device);
+    if (e->cfg.free_running) return fail(HPCG_EINVAL, "engine: the free-running schedule has no rounds (hpcg_engine_run)");
     for (int64_t i = 0; i < n_rounds; ++i) {
         if (e->round >= e->R) return fail(HPCG_EINVAL, "engine: max_samples rounds already run");
         const double now = !e->wall ? 0.0 : e->xr > 1 ? (e->round ? e->common_now : 0.0) : e->elapsed();
@@ -2146,6 +2507,7 @@ int hpcg_engine_rounds(hpcg_engine* e, int64_t n_rounds) {
 int hpcg_engine_run(hpcg_engine* e) {
     std::lock_guard<std::mutex> lk(e->ctx->mu);
     bind_device(e->ctx->device);
+    if (e->cfg.free_running) return engine_run_free(e);
     while (e->round < e->R) {
         // run_wall_clock (engine.hpp:353-357): one clock reading per round decides the stop,
         // the phase and the carry-over
@@ -2159,6 +2521,26 @@ int hpcg_engine_run(hpcg_engine* e) {
 
 int64_t hpcg_engine_round_index(const hpcg_engine* e) { return e->round; }
 uint64_t hpcg_engine_philox_key(const hpcg_engine* e) { return e->key; }
+
+int hpcg_engine_worker_progress(hpcg_engine* e, int64_t* samples, double* t_w) {
+    std::lock_guard<std::mutex> lk(e->ctx->mu);
+    bind_device(e->ctx->device);
+    const size_t W = (size_t)e->W;
+    if (e->free_mode) {
+        if (samples) CU(d2h(samples, e->fr_samples.as<int64_t>(), W, e->ctx->stream));
+        if (t_w) CU(d2h(t_w, e->fr_tw.as<double>(), W, e->ctx->stream));
+        CU(cudaStreamSynchronize(e->ctx->stream));
+        return HPCG_OK;
+    }
+    // round-granular schedules: every worker has processed `round` samples; t_w is the round count
+    // (lockstep, engine.hpp:413) or the last round end in seconds
+    const double tw = e->round == 0 ? 0.0 : e->wall && !e->t_end.empty() ? e->t_end.back() : (double)e->round;
+    for (size_t w = 0; w < W; ++w) {
+        if (samples) samples[w] = e->round;
+        if (t_w) t_w[w] = tw;
+    }
+    return HPCG_OK;
+}
 
 int hpcg_engine_set_trace(hpcg_engine* e, int64_t* trace_dev, int32_t mode) {
     e->trace_buf = trace_dev;
@@ -2363,7 +2745,8 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
         return engine_finish_multi(e, out, centroids, flags, labels, worker_obj, traces, trace_cap, trace_len);
     }
     cudaStream_t st = ctx->stream;
-    const int64_t W = e->W, k = e->k, n = e->n, kn = k * n, R = e->round;
+    // free-running schedule: no per-round logs (R = 0 below); the per-worker traces are read further down
+    const int64_t W = e->W, k = e->k, n = e->n, kn = k * n, R = e->free_mode ? 0 : e->round;
     const int64_t Rw = std::max<int64_t>(R, 1) * W;
     const bool want_obj = e->cfg.compute_full_objective || e->cfg.compute_assignment;
     const bool want_labels = e->cfg.compute_assignment && labels;
@@ -2458,6 +2841,38 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     o.clustering_time = min_last;  // engine.hpp:472-475
     // every worker has t_w = R in lockstep, so the first finisher is worker 0 (engine.hpp:477-481)
     o.clustering_time_first_finisher = last_ts[0] >= 0 ? last_ts[0] : 0.0;
+    int64_t free_samples = 0;
+    double free_last = 0.0;
+    if (e->free_mode) {  // each worker's own trace, sample count and clock
+        std::vector<int64_t> cnt((size_t)W), smp((size_t)W);
+        std::vector<double> tw((size_t)W), tr((size_t)(W * e->fr_cap * 2));
+        CU(d2h(cnt.data(), e->fr_tcnt.as<int64_t>(), (size_t)W, st));
+        CU(d2h(smp.data(), e->fr_samples.as<int64_t>(), (size_t)W, st));
+        CU(d2h(tw.data(), e->fr_tw.as<double>(), (size_t)W, st));
+        CU(d2h(tr.data(), e->fr_trace.as<double>(), tr.size(), st));
+        CU(cudaStreamSynchronize(st));
+        min_last = kInf;
+        int64_t first = 0;
+        for (int64_t w = 0; w < W; ++w) {
+            const int64_t kept = std::min(cnt[(size_t)w], e->fr_cap);
+            const double* t = tr.data() + w * e->fr_cap * 2;
+            if (traces)
+                for (int64_t i = 0; i < std::min(kept, trace_cap); ++i) {
+                    // a trace longer than the caller's buffer keeps its latest entries
+                    const int64_t src = kept > trace_cap ? kept - trace_cap + i : i;
+                    traces[(w * trace_cap + i) * 2 + 0] = t[src * 2];
+                    traces[(w * trace_cap + i) * 2 + 1] = t[src * 2 + 1];
+                }
+            if (trace_len) trace_len[w] = std::min(kept, trace_cap);
+            last_ts[(size_t)w] = kept > 0 ? t[(kept - 1) * 2] : -1.0;
+            if (kept > 0) min_last = std::min(min_last, last_ts[(size_t)w]);
+            free_samples += smp[(size_t)w];
+            free_last = std::max(free_last, tw[(size_t)w]);
+            if (tw[(size_t)w] < tw[(size_t)first]) first = w;  // engine.hpp:477-479, strict <
+        }
+        o.clustering_time = min_last;
+        o.clustering_time_first_finisher = last_ts[(size_t)first] >= 0 ? last_ts[(size_t)first] : 0.0;
+    }
     std::vector<double> bc(h_bc, h_bc + kn);
     std::vector<uint8_t> bf(h_bf, h_bf + k);
     if (centroids) std::memcpy(centroids, bc.data(), (size_t)kn * 8);
@@ -2496,8 +2911,8 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
         o.has_full_objective = 1;
         final_nd = e->ds->m * (int64_t)remap.size();
     }
-    o.last_timestamp = R > 0 ? ts_of(R - 1) : 0.0;  // every worker's t_w (engine.hpp:250)
-    o.total_samples = (uint64_t)(W * R);
+    o.last_timestamp = e->free_mode ? free_last : R > 0 ? ts_of(R - 1) : 0.0;  // every worker's t_w (engine.hpp:250)
+    o.total_samples = e->free_mode ? (uint64_t)free_samples : (uint64_t)(W * R);
     o.distance_evals = (int64_t)ndt + final_nd;
     o.n_publications = npub;
     if (publications && npub > 0) {

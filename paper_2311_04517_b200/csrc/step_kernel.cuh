@@ -92,6 +92,9 @@ struct StepParams {
     uint8_t* inc_f;
     double* inc_obj;
     uint8_t* accepted;
+    // free-running schedule: go[wl] == 0 -> this worker's cluster does nothing (its deadline or
+    // sample cap was reached when the schedule prepared the step); null -> every worker runs
+    const int32_t* go;
     // optional phase timeline (ns, %globaltimer) per CTA: [W*C][kTraceSlots]
     int64_t* trace;
     int32_t trace_mode;  // 0: first Lloyd pass in detail, 1: first K-means++ slot in detail
@@ -412,6 +415,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
     const int C = (int)cluster.num_blocks();
     const int cr = (int)cluster.block_rank();
     const int wl = blockIdx.x / C;
+    if (p.go && p.go[wl] == 0) return;  // the whole cluster reads one flag: uniform exit before any barrier
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = p.n, k = p.k;
     const int64_t s = p.s;
