@@ -275,6 +275,43 @@ HPCG_DEV void cp_async4(void* sdst, const void* gsrc) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
+// Gather variants for random sample rows: without a prefetch size the L2 fills a whole 128-B line per
+// missed sector pair (measured: 609 MB of DRAM reads for 328 MB of random 64-B rows, unchanged by
+// cudaLimitMaxL2FetchGranularity = 32/64/128); `.L2::64B` caps the fill at the 64 B that hold the row
+// (315 MB for the same gather). Streaming readers keep the default.
+HPCG_DEV void cp_async16_row(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+#ifdef HPCG_NO_ROW_HINT  // A/B switch (tools/ab.sh)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+#else
+    asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+#endif
+}
+HPCG_DEV void cp_async8_row(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+HPCG_DEV void cp_async4_row(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+// register-staged row chunk (16 / 8 / 4 bytes) with the same fill cap
+template <typename VT>
+HPCG_DEV VT ld_row_chunk(const void* gsrc) {
+    if constexpr (sizeof(VT) == 16) {
+        uint4 t;
+        asm volatile("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "l"(gsrc));
+        return t;
+    } else if constexpr (sizeof(VT) == 8) {
+        uint2 t;
+        asm volatile("ld.global.nc.L2::64B.v2.u32 {%0,%1}, [%2];" : "=r"(t.x), "=r"(t.y) : "l"(gsrc));
+        return t;
+    } else {
+        uint32_t t;
+        asm volatile("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(t) : "l"(gsrc));
+        return t;
+    }
+}
 HPCG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 HPCG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -410,12 +447,18 @@ HPCG_DEV double exact_dist(const T* samp, int row, const double* c, int n) {
 // ------------------------------------------------------------------ the kernel
 template <typename T, int NP, bool TRACE = false>  // TRACE: the phase timeline (diagnostics) compiled in
 __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kernel(const StepParams p) {
+    if (p.go) {  // free-running schedule: the whole cluster reads one flag -- uniform exit before any barrier.
+        // First statement, on %clusterid (= the local worker): placed after the index setup it cost the
+        // kernel its register allocation (4 -> 196 bytes of spills, +3 % per step)
+        unsigned cid;
+        asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        if (p.go[cid] == 0) return;
+    }
     using G = Geo<T, NP>;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
     const int cr = (int)cluster.block_rank();
     const int wl = blockIdx.x / C;
-    if (p.go && p.go[wl] == 0) return;  // the whole cluster reads one flag: uniform exit before any barrier
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = p.n, k = p.k;
     const int64_t s = p.s;
@@ -546,7 +589,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                     for (int j = 0; j < G::CPR; ++j) {
                         const int rl = j * RPI + lane / G::CPR, row = g * 32 + rl;
                         const int64_t src = __shfl_sync(0xffffffffu, gi, rl);
-                        if (row < nr) cp_async16(samp + G::elem_off(row, q * EPC), row_ptr<T>(p, src) + q * EPC);
+                        if (row < nr) cp_async16_row(samp + G::elem_off(row, q * EPC), row_ptr<T>(p, src) + q * EPC);
                     }
                 }
             }
@@ -561,19 +604,19 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks) worker_step_kern
                 constexpr int EPC = 16 / (int)sizeof(T);
                 for (int e = tid; e < nr * cpr; e += kStepThreads) {
                     const int li = e / cpr, q = e - li * cpr;
-                    cp_async16(samp + G::elem_off(li, q * EPC), row_ptr<T>(p, gx[li]) + q * EPC);
+                    cp_async16_row(samp + G::elem_off(li, q * EPC), row_ptr<T>(p, gx[li]) + q * EPC);
                 }
             } else if ((rowb & 7) == 0) {  // 8-B chunks
                 const int cpr = rowb >> 3;
                 constexpr int EPC = 8 / (int)sizeof(T);
                 for (int e = tid; e < nr * cpr; e += kStepThreads) {
                     const int li = e / cpr, q = e - li * cpr;
-                    cp_async8(samp + G::elem_off(li, q * EPC), row_ptr<T>(p, gx[li]) + q * EPC);
+                    cp_async8_row(samp + G::elem_off(li, q * EPC), row_ptr<T>(p, gx[li]) + q * EPC);
                 }
             } else {  // 4-B elements (fp32, odd n)
                 for (int e = tid; e < nr * n; e += kStepThreads) {
                     const int li = e / n, d = e - li * n;
-                    cp_async4(samp + G::elem_off(li, d), row_ptr<T>(p, gx[li]) + d);
+                    cp_async4_row(samp + G::elem_off(li, d), row_ptr<T>(p, gx[li]) + d);
                 }
             }
         }

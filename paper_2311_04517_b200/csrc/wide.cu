@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(256) wide_gather_kernel(const StepParams p, in
             const int e = e0 + u * 32 + lane, r = e / cpr, q = e - r * cpr;
             const unsigned char* sp = reinterpret_cast<const unsigned char*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), r & 31));
-            if (e < total && i0 + r < s) v[u] = __ldg(reinterpret_cast<const VT*>(sp + (int64_t)q * V));
+            if (e < total && i0 + r < s) v[u] = ld_row_chunk<VT>(sp + (int64_t)q * V);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
