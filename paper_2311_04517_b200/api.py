@@ -586,6 +586,30 @@ class EngineConfig:
                               float(self.time_limit), int(self.free_running), int(self.free_group))
 
 
+class _Traces:
+    """Per-worker update traces (WorkerState::update_trace): worker w -> rows (timestamp, objective).
+    A view over the finish buffers, sliced on access (building W arrays eagerly costs more host time
+    than a round of 256 workers takes on the device)."""
+
+    def __init__(self, buf, lens):
+        self._buf, self._len = buf, lens
+
+    def __len__(self):
+        return len(self._len)
+
+    def __getitem__(self, w):
+        if isinstance(w, slice):
+            return [self[i] for i in range(*w.indices(len(self)))]
+        if w < 0:
+            w += len(self)
+        if not 0 <= w < len(self):
+            raise IndexError(w)
+        return self._buf[w, : int(self._len[w])]
+
+    def __iter__(self):
+        return (self[w] for w in range(len(self)))
+
+
 @dataclass
 class ClusteringResult:
     """engine.hpp:269-284."""
@@ -616,6 +640,7 @@ class Engine:
         check(lib.hpcg_engine_create(ds.ctx.h, ds.h, C.byref(self._c), C.byref(h)))
         self.h = h
         self.W = 1 if cfg.strategy == "inner" else cfg.n_workers
+        self._nranks = 1
 
     def set_exchange(self, nranks: int, rank: int, allgather=None):
         """Make this engine rank `rank` of `nranks` (cooperative / hybrid publication over every
@@ -625,6 +650,7 @@ class Engine:
         fn = _lib.ALLGATHER_FN() if allgather is None else allgather_callback(allgather, nranks)
         self._xfn = fn  # keep the callback alive as long as the engine
         check(lib.hpcg_engine_set_exchange(self.h, nranks, rank, fn, None))
+        self._nranks = nranks
 
     def rounds(self, n: int = 1):
         check(lib.hpcg_engine_rounds(self.h, n))
@@ -693,11 +719,17 @@ class Engine:
         rounds = max(self.round_index, self.cfg.max_samples)
         wobj = np.empty(W)
         tcap = max(1, rounds)
-        traces = np.zeros((W, tcap, 2))
+        traces = np.empty((W, tcap, 2))
         tlen = np.zeros(W, dtype=np.int64)
-        check(lib.hpcg_engine_finish(self.h, C.byref(out), ptr(cent), ptr(flags), ptr(labels), None, 0,
+        # the publication log in the same call when its size has a bound known here: at most W records per
+        # round plus the hybrid carry-over (one rank, round-granular schedules)
+        bounded = self._nranks == 1 and not self.cfg.free_running
+        pcap = (rounds + 1) * W if bounded else 0
+        pubs = np.empty((max(1, pcap), 4)) if bounded else None
+        check(lib.hpcg_engine_finish(self.h, C.byref(out), ptr(cent), ptr(flags), ptr(labels), ptr(pubs), pcap,
                                      ptr(wobj), ptr(traces), tcap, ptr(tlen)))
-        pubs = self.publications()
+        if not bounded:
+            pubs = self.publications()
         return _result(out, cent, flags, labels, pubs, wobj, traces, tlen)
 
     def publications(self) -> np.ndarray:
@@ -730,8 +762,8 @@ def _result(out, cent, flags, labels, pubs, wobj, traces, tlen) -> ClusteringRes
         clustering_time_first_finisher=float(out.clustering_time_first_finisher),
         wall_seconds=float(out.wall_seconds), total_samples=int(out.total_samples),
         distance_evals=int(out.distance_evals), worker_objectives=wobj,
-        traces=[traces[w, : int(tlen[w])].copy() for w in range(len(tlen))],
-        publications=pubs[: min(npub, len(pubs))].copy())
+        traces=_Traces(traces, tlen),
+        publications=pubs[: min(npub, len(pubs))])
 
 
 def run(X, cfg: EngineConfig, ctx: Context | None = None) -> ClusteringResult:

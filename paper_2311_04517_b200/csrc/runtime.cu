@@ -2774,7 +2774,13 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
         if (rc) return rc;
     }
     // pinned staging: [inc_obj W][lobj Rw][bc kn][f][ndt][npub][sel 2x i32][errf W][lacc Rw][bf k]
-    const size_t need = (size_t)(W + Rw + kn + 3) * 8 + 8 + (size_t)W * 4 + (size_t)Rw + (size_t)k;
+    size_t need = (size_t)(W + Rw + kn + 3) * 8 + 8 + (size_t)W * 4 + (size_t)Rw + (size_t)k;
+    // the publication log rides in the same staging (and the same synchronisation) when the host-known
+    // bound of its length is small; otherwise it is read after the count is known
+    const int64_t pub_stage = (publications && !e->free_mode) ? std::min(e->pub_ub, std::min(pub_cap, e->pub_cap)) : 0;
+    const bool pubs_staged = pub_stage > 0 && pub_stage * 32 <= (1 << 20);
+    const size_t pub_off = (need + 7) & ~(size_t)7;
+    if (pubs_staged) need = pub_off + (size_t)pub_stage * 32;
     if (need > ctx->pin_bytes) {  // context-level: one allocation across engines / calls
         if (ctx->pin) cudaFreeHost(ctx->pin);
         ctx->pin = nullptr;
@@ -2804,6 +2810,8 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     CU(d2h(h_bc, bc_d, (size_t)kn, st));
     CU(d2h(h_bf, bf_d, (size_t)k, st));
     if (dev_obj) CU(d2h(h_f, e->scratch_c.as<double>(), 1, st));
+    double* h_pubs = reinterpret_cast<double*>(static_cast<unsigned char*>(ctx->pin) + pub_off);
+    if (pubs_staged) CU(d2h(h_pubs, e->pub_log.as<double>(), (size_t)(pub_stage * 4), st));
     CU(cudaStreamSynchronize(st));
     const unsigned long long ndt = *h_ndt;
     const int64_t npub = *h_npub;
@@ -2917,8 +2925,12 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     o.n_publications = npub;
     if (publications && npub > 0) {
         const int64_t cnt = std::min(npub, std::min(pub_cap, e->pub_cap));
-        CU(d2h(publications, e->pub_log.as<double>(), (size_t)(cnt * 4), st));
-        CU(cudaStreamSynchronize(st));
+        if (pubs_staged && cnt <= pub_stage) {
+            std::memcpy(publications, h_pubs, (size_t)cnt * 32);
+        } else {
+            CU(d2h(publications, e->pub_log.as<double>(), (size_t)(cnt * 4), st));
+            CU(cudaStreamSynchronize(st));
+        }
     }
     if (worker_obj) std::memcpy(worker_obj, h_obj, (size_t)W * 8);
     o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
