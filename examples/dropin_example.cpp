@@ -39,6 +39,24 @@ int main(int argc, char** argv) {
         hpclust::ClusteringResult rw = hpclust::run(X, wcfg);
         std::printf("{\"wall_seconds\": %.17g, \"wall_samples\": %zu, \"wall_full\": %.17g, ", rw.wall_seconds,
                     rw.total_samples, rw.full_objective.value_or(-1.0));
+        // the same budget with free-running workers and immediate publication (engine.hpp:355-371;
+        // EngineConfig::free_running, an extension): every worker on its own, device Philox streams
+        hpclust::EngineConfig fcfg = wcfg;
+        fcfg.rng_mode = hpclust::RngMode::philox;
+        fcfg.free_running = true;
+        fcfg.free_group = 1;
+        hpclust::ClusteringResult rf = hpclust::run(X, fcfg);
+        std::size_t fsum = 0, fmin = ~std::size_t{0};
+        double tw_max = 0.0;
+        for (const auto& w : rf.per_worker) {
+            fsum += w.samples_processed;
+            fmin = std::min(fmin, w.samples_processed);
+            tw_max = std::max(tw_max, w.t_w);
+        }
+        std::printf("\"free_samples\": %zu, \"free_sum\": %zu, \"free_min\": %zu, \"free_tw_max\": %.17g, "
+                    "\"free_full\": %.17g, \"free_pubs\": %zu, \"free_seconds\": %.17g, ",
+                    rf.total_samples, fsum, fmin, tw_max, rf.full_objective.value_or(-1.0), rf.publications.size(),
+                    rf.wall_seconds);
         std::printf("\"sample0\": %.17g, \"seed_c0\": %.17g, \"lloyd_obj\": %.17g, \"lloyd_iters\": %zu, "
                     "\"lloyd_stop\": \"%s\", \"nd\": %lld, \"f_full\": %.17g, \"run_full\": %.17g, "
                     "\"run_best\": %d, \"run_nd\": %lld, \"run_c0\": %.17g, \"pubs\": %zu}\n",

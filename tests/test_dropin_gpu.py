@@ -53,6 +53,9 @@ def test_dropin_matches_reference_semantics():
     # wall-clock schedule through the drop-in: stops at the first round end past 0.2 s
     assert r["wall_seconds"] >= 0.2 and r["wall_samples"] > 0 and r["wall_samples"] % 3 == 0
     assert r["wall_full"] > 0
+    # free-running workers through the drop-in: per-worker sample counts and clocks (WorkerState)
+    assert r["free_samples"] == r["free_sum"] > 0 and r["free_min"] >= 1
+    assert 0.1 < r["free_tw_max"] <= r["free_seconds"] and r["free_pubs"] >= 1 and r["free_full"] > 0
 
 
 BEXE = ROOT / "examples" / "baselines_example"
