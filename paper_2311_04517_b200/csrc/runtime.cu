@@ -1956,10 +1956,17 @@ __device__ __forceinline__ void free_unlock(int* lock, int lane) {
     if (lane == 0) atomicExch(lock, 0);
 }
 
-// SharedBest::try_publish (engine.hpp:126-136); the caller's warp holds the lock
+// SharedBest::try_publish (engine.hpp:126-136); the caller's warp holds the writers' lock. Readers do
+// not take it: the record is a seqlock (lock[1] is odd while a writer is inside), so the snapshots of
+// concurrent workers do not serialise behind one another -- publications are rare, snapshots are
+// one per sample.
 __device__ void free_try_publish(const FreeParams& q, int w, double obj, double ts, int lane) {
     if (!(obj < *(volatile double*)q.sh_obj)) return;
     const int kn = q.k * q.n;
+    volatile int* seq = q.lock + 1;
+    if (lane == 0) *seq = *seq + 1;  // odd: record in flux
+    __syncwarp();
+    __threadfence();
     for (int e = lane; e < kn; e += 32) ((volatile double*)q.sh_c)[e] = q.inc_c[(int64_t)w * kn + e];
     for (int e = lane; e < q.k; e += 32) ((volatile uint8_t*)q.sh_f)[e] = q.inc_f[(int64_t)w * q.k + e];
     if (lane == 0) {
@@ -1977,48 +1984,65 @@ __device__ void free_try_publish(const FreeParams& q, int w, double obj, double 
         }
         *(volatile int64_t*)q.pub_count = at + 1;
     }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) *seq = *seq + 1;  // even: record stable
 }
 
-__global__ void __launch_bounds__(32) free_between_kernel(const FreeParams q, int w0, int g, int do_post, int do_prep) {
-    const int lane = threadIdx.x;
+constexpr int kFreeWarps = 16;  // warps of the between kernel (one worker each in the parallel phases)
+
+__global__ void __launch_bounds__(32 * kFreeWarps) free_between_kernel(const FreeParams q, int w0, int g, int do_post,
+                                                                      int do_prep) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int kn = q.k * q.n;
-    // every finished step of the group is accounted for (and published) before any worker of the
-    // group takes its next snapshot, so a snapshot sees the group's freshest results
-    for (int i = 0; i < g; ++i) {
-        const int w = w0 + i;
-        if (do_post && q.go[w]) {  // the step this worker was prepared for has run
-            const bool acc = q.accepted[w] != 0;
-            double ts = 0.0;
+    __shared__ double s_ts[64];
+    __shared__ int s_pub[64];
+    // ---- post: bookkeeping of the finished steps, one worker per warp; the publications after it in
+    // worker-id order by warp 0 (so one group of all workers publishes exactly as a lockstep round end)
+    for (int i0 = 0; do_post && i0 < g; i0 += 64) {
+        for (int i = i0 + warp; i < min(g, i0 + 64); i += kFreeWarps) {
+            const int w = w0 + i;
             if (lane == 0) {
-                ts = (double)(free_gtimer() - *q.t0) * 1e-9;  // the clock is read once, after the sample
-                q.samples[w] += 1;
-                q.tw[w] = ts;
-                atomicAdd(q.nd_total, (unsigned long long)q.nd[w]);
-                if (q.err[w] != 0 && q.err_first[w] == 0) q.err_first[w] = q.err[w];
-                if (acc) {
-                    const int64_t cnt = q.trace_cnt[w];
-                    double* tr = q.trace + (int64_t)w * q.trace_cap * 2;
-                    if (cnt > 0) {
-                        const double last = tr[(min(cnt, q.trace_cap) - 1) * 2];
-                        if (!(ts > last)) ts = nextafter(last, (double)INFINITY);
+                int pub = 0;
+                double ts = 0.0;
+                if (q.go[w]) {  // the step this worker was prepared for has run
+                    const bool acc = q.accepted[w] != 0;
+                    ts = (double)(free_gtimer() - *q.t0) * 1e-9;  // the clock is read once, after the sample
+                    q.samples[w] += 1;
+                    q.tw[w] = ts;
+                    atomicAdd(q.nd_total, (unsigned long long)q.nd[w]);
+                    if (q.err[w] != 0 && q.err_first[w] == 0) q.err_first[w] = q.err[w];
+                    if (acc) {
+                        const int64_t cnt = q.trace_cnt[w];
+                        double* tr = q.trace + (int64_t)w * q.trace_cap * 2;
+                        if (cnt > 0) {
+                            const double last = tr[(min(cnt, q.trace_cap) - 1) * 2];
+                            if (!(ts > last)) ts = nextafter(last, (double)INFINITY);
+                        }
+                        const int64_t at = min(cnt, q.trace_cap - 1);  // a full trace keeps its latest entry last
+                        tr[at * 2] = ts;
+                        tr[at * 2 + 1] = q.inc_obj[w];
+                        q.trace_cnt[w] = cnt + 1;
                     }
-                    const int64_t at = min(cnt, q.trace_cap - 1);  // a full trace keeps its latest entry last
-                    tr[at * 2] = ts;
-                    tr[at * 2 + 1] = q.inc_obj[w];
-                    q.trace_cnt[w] = cnt + 1;
+                    pub = (acc && q.coop[w]) ? 1 : 0;
                 }
-            }
-            ts = __shfl_sync(0xffffffffu, ts, 0);
-            if (acc && q.coop[w]) {
-                free_lock(q.lock, lane);
-                free_try_publish(q, w, q.inc_obj[w], ts, lane);
-                free_unlock(q.lock, lane);
+                s_ts[i - i0] = ts;
+                s_pub[i - i0] = pub;
             }
         }
+        __syncthreads();
+        if (warp == 0)
+            for (int i = i0; i < min(g, i0 + 64); ++i)
+                if (s_pub[i - i0]) {
+                    free_lock(q.lock, lane);
+                    free_try_publish(q, w0 + i, q.inc_obj[w0 + i], s_ts[i - i0], lane);
+                    free_unlock(q.lock, lane);
+                }
+        __syncthreads();
     }
     if (!do_prep) return;
-    __syncwarp();
-    for (int i = 0; i < g; ++i) {
+    // ---- prep: the loop head of every worker of the group, one worker per warp
+    for (int i = warp; i < g; i += kFreeWarps) {
         const int w = w0 + i;
         int flags = 0;
         double now = 0.0;
@@ -2038,16 +2062,35 @@ __global__ void __launch_bounds__(32) free_between_kernel(const FreeParams q, in
         double* ic = q.init_c + (int64_t)w * kn;
         uint8_t* ifl = q.init_f + (int64_t)w * q.k;
         if (flags & 2) {
-            free_lock(q.lock, lane);
             if (flags & 4) {  // engine.hpp:359-364: the phase-1 incumbent enters the shared best
                 const double obj = q.inc_obj[w];
-                if (isfinite(obj)) free_try_publish(q, w, obj, now, lane);
-                __syncwarp();
+                if (isfinite(obj)) {
+                    free_lock(q.lock, lane);
+                    free_try_publish(q, w, obj, now, lane);
+                    free_unlock(q.lock, lane);
+                }
             }
-            const int64_t ver = *(volatile int64_t*)q.sh_version;  // snapshot(): nullopt while version == 0
-            for (int e = lane; e < kn; e += 32) ic[e] = ver ? ((volatile double*)q.sh_c)[e] : 0.0;
-            for (int e = lane; e < q.k; e += 32) ifl[e] = ver ? ((volatile uint8_t*)q.sh_f)[e] : (uint8_t)1;
-            free_unlock(q.lock, lane);
+            // snapshot() (engine.hpp:119-124) without the writers' lock: retry while a writer is inside or
+            // the sequence moved under the copy; nullopt while version == 0
+            volatile int* seq = q.lock + 1;
+            for (;;) {
+                int s1 = 0;
+                if (lane == 0) s1 = *seq;
+                s1 = __shfl_sync(0xffffffffu, s1, 0);
+                if (s1 & 1) {
+                    __nanosleep(200);
+                    continue;
+                }
+                __threadfence();
+                const int64_t ver = *(volatile int64_t*)q.sh_version;
+                for (int e = lane; e < kn; e += 32) ic[e] = ver ? ((volatile double*)q.sh_c)[e] : 0.0;
+                for (int e = lane; e < q.k; e += 32) ifl[e] = ver ? ((volatile uint8_t*)q.sh_f)[e] : (uint8_t)1;
+                __threadfence();
+                int s2 = 0;
+                if (lane == 0) s2 = *seq;
+                s2 = __shfl_sync(0xffffffffu, s2, 0);
+                if (s1 == s2) break;
+            }
         } else {
             for (int e = lane; e < kn; e += 32) ic[e] = q.inc_c[(int64_t)w * kn + e];
             for (int e = lane; e < q.k; e += 32) ifl[e] = q.inc_f[(int64_t)w * q.k + e];
@@ -2062,7 +2105,8 @@ int engine_run_free(hpcg_engine* e) {
     if (e->round > 0 || e->free_mode) return fail(HPCG_EINVAL, "free-running schedule: the engine has already run");
     const int gsz = (int)(e->cfg.free_group > 0 ? std::min<int64_t>(e->cfg.free_group, W) : std::max<int64_t>(1, (W + 15) / 16));
     const int G = (int)((W + gsz - 1) / gsz);
-    const int S = std::min(G, 16);
+    static const int max_streams = getenv("HPCG_FREE_STREAMS") ? std::max(1, atoi(getenv("HPCG_FREE_STREAMS"))) : 16;
+    const int S = std::min(G, max_streams);
     e->fr_cap = 512;
     CU(e->fr_t0.reserve(8));
     CU(e->fr_go.reserve((size_t)W * 4));
@@ -2074,14 +2118,14 @@ int engine_run_free(hpcg_engine* e) {
     CU(e->fr_init_f.reserve((size_t)(W * k)));
     CU(e->fr_tcnt.reserve((size_t)W * 8));
     CU(e->fr_trace.reserve((size_t)(W * e->fr_cap) * 16));
-    CU(e->fr_lock.reserve(4));
+    CU(e->fr_lock.reserve(8));  // [0] writers' lock, [1] seqlock sequence
     CU(cudaMemsetAsync(e->fr_go.p, 0, (size_t)W * 4, st0));
     CU(cudaMemsetAsync(e->fr_coop.p, 0, (size_t)W, st0));
     CU(cudaMemsetAsync(e->fr_entered.p, 0, (size_t)W, st0));
     CU(cudaMemsetAsync(e->fr_samples.p, 0, (size_t)W * 8, st0));
     CU(cudaMemsetAsync(e->fr_tw.p, 0, (size_t)W * 8, st0));
     CU(cudaMemsetAsync(e->fr_tcnt.p, 0, (size_t)W * 8, st0));
-    CU(cudaMemsetAsync(e->fr_lock.p, 0, 4, st0));
+    CU(cudaMemsetAsync(e->fr_lock.p, 0, 8, st0));
     const int64_t want_pubs = std::max<int64_t>(e->pub_cap, 16384);
     CU(e->pub_log.grow((size_t)want_pubs * 32, (size_t)e->pub_cap * 32, st0));
     e->pub_cap = want_pubs;
@@ -2182,7 +2226,7 @@ int engine_run_free(hpcg_engine* e) {
         for (int grp = 0; grp < G && ce == cudaSuccess; ++grp) {
             cudaStream_t st = streams[(size_t)(grp % S)];
             const int w0 = grp * gsz, g = (int)std::min<int64_t>(gsz, W - w0);
-            free_between_kernel<<<1, 32, 0, st>>>(q, w0, g, laps > 0 ? 1 : 0, 1);
+            free_between_kernel<<<1, 32 * kFreeWarps, 0, st>>>(q, w0, g, laps > 0 ? 1 : 0, 1);
             p.W = g;
             p.round = (uint32_t)laps;
             p.worker_base = e->cfg.worker_base + w0;
@@ -2209,7 +2253,7 @@ int engine_run_free(hpcg_engine* e) {
     if (ce == cudaSuccess && laps > 0)
         for (int grp = 0; grp < G; ++grp) {  // account for the last prepared steps
             const int w0 = grp * gsz, g = (int)std::min<int64_t>(gsz, W - w0);
-            free_between_kernel<<<1, 32, 0, streams[(size_t)(grp % S)]>>>(q, w0, g, 1, 0);
+            free_between_kernel<<<1, 32 * kFreeWarps, 0, streams[(size_t)(grp % S)]>>>(q, w0, g, 1, 0);
             ctx->launches += 1;
         }
     for (auto s_ : streams) {
