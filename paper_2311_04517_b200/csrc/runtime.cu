@@ -1031,8 +1031,17 @@ int hpcg_host_unregister(void* host) {
     return HPCG_OK;
 }
 
+static int dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n, hpcg_dataset** out,
+                          bool wait);
 int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n,
                         hpcg_dataset** out) {
+    return dataset_upload(ctx, X_host, dtype, m, n, out, true);
+}
+// wait = false (hpcg_run): the copy stays in flight on the context's stream and everything the run
+// enqueues is ordered behind it, so the engine's allocations and the first launches' host work
+// overlap the transfer; the caller synchronises before X_host may change (the run's finish does)
+static int dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int64_t n, hpcg_dataset** out,
+                          bool wait) {
     if (m < 1 || n < 1) return fail(HPCG_EINVAL, "Dataset: needs at least one row and one column");
     if (dtype != HPCG_F32 && dtype != HPCG_F64) return fail(HPCG_EINVAL, "unknown dtype");
     bind_device(ctx->device);
@@ -1054,7 +1063,7 @@ int hpcg_dataset_upload(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int
     }
     cudaError_t e = cudaMemcpyAsync(d, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream);
     ctx->upload_bytes += (int64_t)bytes;
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess && wait) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
         cudaFree(d);
         return fail(HPCG_ECUDA, cudaGetErrorString(e));
@@ -3039,7 +3048,7 @@ int hpcg_run(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int
              int64_t pub_cap, double* worker_obj, double* traces, int64_t trace_cap, int64_t* trace_len) {
     const auto t0 = std::chrono::steady_clock::now();
     hpcg_dataset* ds = nullptr;
-    if (int rc = hpcg_dataset_upload(ctx, X_host, dtype, m, n, &ds)) return rc;
+    if (int rc = dataset_upload(ctx, X_host, dtype, m, n, &ds, false)) return rc;
     hpcg_engine* e = nullptr;
     int rc = hpcg_engine_create(ctx, ds, cfg, &e);
     if (!rc) {
@@ -3049,6 +3058,7 @@ int hpcg_run(hpcg_ctx* ctx, const void* X_host, hpcg_dtype dtype, int64_t m, int
     if (!rc)
         rc = hpcg_engine_finish(e, out, centroids, flags, labels, publications, pub_cap, worker_obj, traces,
                                 trace_cap, trace_len);
+    if (rc) cudaStreamSynchronize(ctx->stream);  // the upload may still read X_host
     hpcg_engine_destroy(e);
     hpcg_dataset_destroy(ds);
     return rc;
