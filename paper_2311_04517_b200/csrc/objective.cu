@@ -142,11 +142,25 @@ static cudaError_t launch_tc(const ObjParams& p, const CUtensorMap& tmap, int* n
     // the cost-only pass (no labels / counts) compiles without the output path: fewer live registers
     auto kern = (p.labels || p.counts) ? objective_tc_kernel<NP, N, KPS, true> : objective_tc_kernel<NP, N, KPS, false>;
     const int smem = objective_tc_smem<NP, N>(p.kv);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148;
+    // per device and instantiation: the opt-in shared-memory size (the largest asked so far) and the SM
+    // count are set / read once -- this launch sits on the critical path of a ~0.13 ms pass
+    static int smem_set[2][16] = {};
+    static int sm_count[16] = {};
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int di = dev & 15, oi = (p.labels || p.counts) ? 1 : 0;
+    cudaError_t e = cudaSuccess;
+    if (smem_set[oi][di] < smem) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        smem_set[oi][di] = smem;
+    }
+    if (sm_count[di] == 0) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sm_count[di] = v;
+    }
+    const int sms = sm_count[di];
     if (nblocks[0] < sms) {
         nblocks[0] = sms;
         return cudaErrorNotReady;

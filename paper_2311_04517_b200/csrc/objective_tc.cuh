@@ -188,7 +188,14 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
                      "r"(TG::TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
+    const int64_t m = p.m;
+    const int64_t ntiles = (m + TG::TM - 1) / TG::TM;
+    const int my = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    // The producer thread initialises the barriers itself and puts the first ring of tiles in flight
+    // BEFORE the CTA-wide barrier below, so the centre tables, the TMEM allocation and the barrier
+    // overlap the first HBM round trip instead of preceding it.
+    const int pre = my < STAGES ? my : STAGES;
+    if (warp == EW && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 4 * (TG::TR / TG::RPT));  // the warps of the tile's groups
@@ -198,22 +205,27 @@ __global__ void __launch_bounds__(TcGeo<NP, N>::THREADS, 1)
             mbar_init(&tempty[b], 4 * (TG::TR / TG::RPT));
         }
         mbar_init_fence();
+        fence_proxy_async();
+        for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(&full[i], (uint32_t)TILE);
+#pragma unroll
+            for (int h = 0; h < TG::TM / TG::BOX; ++h)
+                tma_load_2d(ring + i * TILE + h * TG::BOX * TG::RS, &tmap, 0,
+                            (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::TM + h * TG::BOX), &full[i]);
+        }
     }
     fence_proxy_async();  // B tile (generic stores) -> tensor-core reads (async proxy)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tm = s_tmem;
-    const int64_t m = p.m;
-    const int64_t ntiles = (m + TG::TM - 1) / TG::TM;
-    const int my = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
     double cost = 0.0;
 
     if (warp == EW) {  // ---- TMA producer: stage s, lap parity pl
         if (lane == 0) {
-            int s = 0;
-            uint32_t pl = 0;
-            for (int i = 0; i < my; ++i) {
+            int s = pre == STAGES ? 0 : pre;
+            uint32_t pl = pre == STAGES ? 1u : 0u;
+            for (int i = pre; i < my; ++i) {
                 if (i >= STAGES) mbar_wait_cta(&empty[s], pl ^ 1u);
                 mbar_expect_tx(&full[s], (uint32_t)TILE);
 #pragma unroll
