@@ -151,3 +151,32 @@ def test_free_validation():
     Xw = mixture(4000, 40, 3, seed=2)  # n = 40: the grid-wide path, no cluster-resident geometry
     with pytest.raises(hp.Unsupported, match="cluster-resident"):
         run_engine(Xw, hp.EngineConfig(time_limit=0.1, rng="philox", free_running=True, **kw))
+
+
+def test_free_engine_reset_and_rerun():
+    # hpcg_engine_reset returns a free-running engine to sample 0: the capped competitive schedule is
+    # deterministic, so the second run reproduces the first; a new seed gives a different run
+    X = mixture(30000, 4, 6, seed=25)
+    cfg = hp.EngineConfig(k=6, sample_size=3000, n_workers=5, strategy="competitive", master_seed=9, rng="philox",
+                          max_samples=4, time_limit=1e6, free_running=True, free_group=2)
+    ds = hp.DeviceDataset(X)
+    eng = hp.Engine(ds, cfg)
+    try:
+        eng.run()
+        r1 = eng.finish()
+        o1 = eng.worker_incumbents()[2].copy()
+        with pytest.raises(hp.InvalidArgument, match="already run"):
+            eng.run()
+        eng.reset(9)
+        eng.run()
+        r2 = eng.finish()
+        o2 = eng.worker_incumbents()[2].copy()
+        eng.reset(10)
+        eng.run()
+        o3 = eng.worker_incumbents()[2].copy()
+    finally:
+        eng.close()
+        ds.close()
+    assert np.array_equal(o1, o2) and r1.distance_evals == r2.distance_evals and r1.total_samples == r2.total_samples == 20
+    assert np.array_equal(r1.centroids, r2.centroids) and r1.full_objective == r2.full_objective
+    assert not np.array_equal(o1, o3)
