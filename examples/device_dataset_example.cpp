@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "hpclust/hpclust.hpp"
+#include "hpclust/io.hpp"
 #include "hpclust/parallel.hpp"
 
 int main(int argc, char** argv) {
@@ -53,7 +54,20 @@ int main(int argc, char** argv) {
         hpclust::RngStream sa(9), sb(9);
         const bool acc_a = hpclust::worker_step(wa, sa, dX, wa.incumbent, cfg, [] { return 1.0; });
         const bool acc_b = hpclust::worker_step(wb, sb, X, wb.incumbent, cfg, [] { return 1.0; });
-        std::printf("{\"upload_bytes_100_draws\": %lld, \"draw_same\": %d, \"chk\": %.17g, \"run_same\": %d, "
+        // CSV ingest into page-locked memory (io.hpp load_dataset_pinned): same values as load_dataset,
+        // the holder's rows upload and run like any Dataset
+        hpclust::Dataset head(2000, n);
+        std::copy_n(X.values.begin(), head.values.size(), head.values.begin());
+        const std::string csv = std::string(argv[1]) + ".csv";
+        hpclust::save_dataset(head, csv);
+        hpclust::PinnedDataset pin = hpclust::load_dataset_pinned(csv);
+        const bool pin_same = pin.X.values == hpclust::load_dataset(csv).values && pin.X.rows == 2000;
+        hpclust::EngineConfig pcfg = cfg;
+        pcfg.sample_size = 300;
+        const bool pin_run = hpclust::run(pin.X, pcfg).centroids.centers == hpclust::run(head, pcfg).centroids.centers;
+        std::printf("{\"pinned\": %d, \"pin_same\": %d, \"pin_run\": %d, ", pin.pinned ? 1 : 0, pin_same ? 1 : 0,
+                    pin_run ? 1 : 0);
+        std::printf("\"upload_bytes_100_draws\": %lld, \"draw_same\": %d, \"chk\": %.17g, \"run_same\": %d, "
                     "\"ws_same\": %d, \"ws_obj\": %.17g, \"f_dev\": %.17g, \"f_host\": %.17g, \"policy_chunks\": %zu, "
                     "\"rr\": [%zu, %zu], \"pool_sum\": %.17g}\n",
                     up1 - up0, same ? 1 : 0, chk,

@@ -114,6 +114,7 @@ def test_device_dataset_overloads_no_per_call_upload():
     r = json.loads(out.stdout)
     assert "error" not in r, r
     assert r["upload_bytes_100_draws"] == 0
+    assert r["pinned"] == 1 and r["pin_same"] == 1 and r["pin_run"] == 1  # io.hpp load_dataset_pinned
     assert r["draw_same"] == 1 and r["run_same"] == 1 and r["ws_same"] == 1
     assert r["f_dev"] == r["f_host"]
     assert r["policy_chunks"] == (os.cpu_count() or 1)
