@@ -736,10 +736,39 @@ __global__ void xch_merge_select_kernel(const double* recv, int G, int k, int n,
     }
 }
 
-__global__ void fill_f64_kernel(double* p, int64_t n, double v) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
+// Engine state of sample 0 in ONE launch (was ten memsets and two fills: ~25 us of host API time
+// between a run's finish and the next run's first worker step, with the GPU idle): all-degenerate
+// incumbents at +inf (engine.hpp:456), an empty shared best, cleared error / evaluation / publication
+// counters and accept log.
+struct EngineResetParams {
+    double *inc_c, *inc_obj, *sh_obj, *sh_c;
+    uint8_t *inc_f, *sh_f, *log_acc;
+    int32_t *err_first, *sh_worker;
+    int64_t *sh_ver, *pub_count;
+    unsigned long long* nd_total;
+    int64_t W, k, kn, log_bytes;
+};
+__global__ void engine_reset_kernel(const EngineResetParams q) {
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int64_t i = i0; i < q.W * q.kn; i += step) q.inc_c[i] = 0.0;
+    for (int64_t i = i0; i < q.W * q.k; i += step) q.inc_f[i] = 1;
+    for (int64_t i = i0; i < q.W; i += step) {
+        q.inc_obj[i] = inf;
+        q.err_first[i] = 0;
+    }
+    for (int64_t i = i0; i < q.kn; i += step) q.sh_c[i] = 0.0;
+    for (int64_t i = i0; i < q.k; i += step) q.sh_f[i] = 1;
+    for (int64_t i = i0; i < q.log_bytes; i += step) q.log_acc[i] = 0;
+    if (i0 == 0) {
+        *q.sh_obj = inf;
+        *q.sh_ver = 0;
+        *q.sh_worker = -1;
+        *q.nd_total = 0;
+        *q.pub_count = 0;
+    }
 }
+
 
 // select_best (engine.hpp:180-194: strict <, worker-id order, infinite never wins) and the
 // valid-subset compaction of the winner (engine.hpp:211-229) on the device, so the final
@@ -2317,6 +2346,31 @@ int hpcg_ctx_comm_info(const hpcg_ctx* ctx, int32_t* nranks, int32_t* rank) {
     return HPCG_OK;
 }
 
+static cudaError_t engine_reset_state(hpcg_engine* e, cudaStream_t st) {
+    EngineResetParams q = {};
+    q.inc_c = e->inc_c.as<double>();
+    q.inc_obj = e->inc_obj.as<double>();
+    q.sh_obj = e->sh_obj.as<double>();
+    q.sh_c = e->sh_c.as<double>();
+    q.inc_f = e->inc_f.as<uint8_t>();
+    q.sh_f = e->sh_f.as<uint8_t>();
+    q.log_acc = e->log_acc.as<uint8_t>();
+    q.err_first = e->err_first.as<int32_t>();
+    q.sh_worker = e->sh_worker.as<int32_t>();
+    q.sh_ver = e->sh_ver.as<int64_t>();
+    q.pub_count = e->pub_count.as<int64_t>();
+    q.nd_total = e->nd_total.as<unsigned long long>();
+    q.W = e->W;
+    q.k = e->k;
+    q.kn = e->k * e->n;
+    q.log_bytes = e->log_rounds * e->W;
+    const int64_t work = std::max<int64_t>(q.W * q.kn, q.log_bytes);
+    const unsigned blocks = (unsigned)std::min<int64_t>(296, std::max<int64_t>(1, (work + 255) / 256));
+    engine_reset_kernel<<<blocks, 256, 0, st>>>(q);
+    e->ctx->launches += 1;
+    return cudaGetLastError();
+}
+
 int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_cfg* c, hpcg_engine** out) {
     std::lock_guard<std::mutex> lk(ctx->mu);
     bind_device(ctx->device);
@@ -2427,20 +2481,8 @@ int hpcg_engine_create(hpcg_ctx* ctx, const hpcg_dataset* ds, const hpcg_engine_
     auto chk = [&](cudaError_t x) {
         if (ce == cudaSuccess) ce = x;
     };
-    chk(cudaMemsetAsync(e->inc_c.p, 0, (size_t)(W * kn * 8), st));
-    chk(cudaMemsetAsync(e->inc_f.p, 1, (size_t)(W * k), st));  // all-degenerate incumbents (engine.hpp:456)
-    fill_f64_kernel<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(e->inc_obj.as<double>(), W, kInf);
-    fill_f64_kernel<<<1, 1, 0, st>>>(e->sh_obj.as<double>(), 1, kInf);
-    chk(cudaMemsetAsync(e->sh_ver.p, 0, 8, st));
-    chk(cudaMemsetAsync(e->sh_worker.p, 0xff, 4, st));
-    chk(cudaMemsetAsync(e->sh_c.p, 0, (size_t)(kn * 8), st));
-    chk(cudaMemsetAsync(e->sh_f.p, 1, (size_t)k, st));
-    chk(cudaMemsetAsync(e->err_first.p, 0, (size_t)(W * 4), st));
-    chk(cudaMemsetAsync(e->nd_total.p, 0, 8, st));
-    chk(cudaMemsetAsync(e->pub_count.p, 0, 8, st));
-    chk(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->log_rounds * W), st));
-    chk(cudaGetLastError());
-    ctx->launches += 2;
+    chk(engine_reset_state(e, st));  // all-degenerate incumbents (engine.hpp:456), empty shared best
+    (void)kn;
     if (ce != cudaSuccess) return bad(ce);
     *out = e;
     return HPCG_OK;
@@ -2496,7 +2538,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     hpcg_ctx* ctx = e->ctx;
     bind_device(ctx->device);
     cudaStream_t st = ctx->stream;
-    const int64_t W = e->W, k = e->k, kn = k * e->n;
+    const int64_t W = e->W;
     e->cfg.master_seed = master_seed;
     e->key = splitmix64(master_seed ^ 0x48504331ULL);
     e->round = 0;
@@ -2505,20 +2547,7 @@ int hpcg_engine_reset(hpcg_engine* e, uint64_t master_seed) {
     if (e->cfg.rng_mode == HPCG_RNG_REFERENCE)
         for (int64_t w = 0; w < W; ++w)
             e->streams[(size_t)w] = Mt64::derive(master_seed, 1, (uint64_t)(e->cfg.worker_base + w));
-    CU(cudaMemsetAsync(e->inc_c.p, 0, (size_t)(W * kn * 8), st));
-    CU(cudaMemsetAsync(e->inc_f.p, 1, (size_t)(W * k), st));
-    fill_f64_kernel<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(e->inc_obj.as<double>(), W, kInf);
-    fill_f64_kernel<<<1, 1, 0, st>>>(e->sh_obj.as<double>(), 1, kInf);
-    CU(cudaGetLastError());
-    ctx->launches += 2;
-    CU(cudaMemsetAsync(e->sh_ver.p, 0, 8, st));
-    CU(cudaMemsetAsync(e->sh_worker.p, 0xff, 4, st));
-    CU(cudaMemsetAsync(e->sh_c.p, 0, (size_t)(kn * 8), st));
-    CU(cudaMemsetAsync(e->sh_f.p, 1, (size_t)k, st));
-    CU(cudaMemsetAsync(e->err_first.p, 0, (size_t)(W * 4), st));
-    CU(cudaMemsetAsync(e->nd_total.p, 0, 8, st));
-    CU(cudaMemsetAsync(e->pub_count.p, 0, 8, st));
-    CU(cudaMemsetAsync(e->log_acc.p, 0, (size_t)(e->log_rounds * W), st));
+    CU(engine_reset_state(e, st));
     e->pub_ub = 0;
     e->entered_coop = false;
     e->common_now = 0.0;
