@@ -770,6 +770,32 @@ __global__ void engine_reset_kernel(const EngineResetParams q) {
 }
 
 
+// The result pieces of a finish (incumbent objectives, logs, counters, the winner's centroids, f(C,X))
+// packed into one device staging block, so ONE device-to-host copy carries them: eleven small copies
+// cost ~5 us each on the stream after the f(C,X) pass.
+struct PackSeg {
+    const unsigned char* src;
+    int64_t off, bytes;
+};
+struct PackParams {
+    PackSeg seg[12];
+    int n;
+    unsigned char* dst;
+};
+__global__ void pack_segments_kernel(const PackParams q) {
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+    for (int sg = 0; sg < q.n; ++sg) {
+        const PackSeg g = q.seg[sg];
+        if (((reinterpret_cast<uintptr_t>(g.src) | (uintptr_t)g.off | (uintptr_t)g.bytes) & 7) == 0) {
+            const uint64_t* s8 = reinterpret_cast<const uint64_t*>(g.src);
+            uint64_t* d8 = reinterpret_cast<uint64_t*>(q.dst + g.off);
+            for (int64_t i = i0; i < g.bytes / 8; i += step) d8[i] = s8[i];
+        } else {
+            for (int64_t i = i0; i < g.bytes; i += step) q.dst[g.off + i] = g.src[i];
+        }
+    }
+}
+
 // select_best (engine.hpp:180-194: strict <, worker-id order, infinite never wins) and the
 // valid-subset compaction of the winner (engine.hpp:211-229) on the device, so the final
 // objective launches without a host round trip. sel = {best worker or -1, valid count}.
@@ -1589,7 +1615,7 @@ struct hpcg_engine {
     DevBuf inc_c, inc_f, inc_obj, acc, nd, err, err_first, iters, stopb, filled, objb;
     DevBuf sh_ver, sh_obj, sh_worker, sh_c, sh_f;
     DevBuf log_acc, log_obj, nd_total, pub_log, pub_count;
-    DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks, fin;
+    DevBuf d_idx, d_fr, d_un, scratch_a, scratch_b, scratch_c, blocks, fin, fin_stage;
     int64_t pub_cap = 0;   // publication-log entries allocated (grown on demand)
     int64_t pub_ub = 0;    // upper bound of the entries written so far (<= W per publishing launch)
     int64_t log_rounds = 0;  // rounds the per-round accept/objective logs can hold (grown on demand)
@@ -2880,20 +2906,35 @@ int hpcg_engine_finish(hpcg_engine* e, hpcg_run_out* out, double* centroids, uin
     int32_t* h_errf = h_sel + 2;
     uint8_t* h_lacc = reinterpret_cast<uint8_t*>(h_errf + W);
     uint8_t* h_bf = h_lacc + Rw;
-    CU(d2h(h_obj, e->inc_obj.as<double>(), (size_t)W, st));
-    CU(d2h(h_errf, e->err_first.as<int32_t>(), (size_t)W, st));
-    if (R > 0) {
-        CU(d2h(h_lacc, e->log_acc.as<uint8_t>(), (size_t)(R * W), st));
-        CU(d2h(h_lobj, e->log_obj.as<double>(), (size_t)(R * W), st));
-    }
-    CU(d2h(h_ndt, e->nd_total.as<unsigned long long>(), 1, st));
-    CU(d2h(h_npub, e->pub_count.as<int64_t>(), 1, st));
-    CU(d2h(h_sel, sel_d, 2, st));
-    CU(d2h(h_bc, bc_d, (size_t)kn, st));
-    CU(d2h(h_bf, bf_d, (size_t)k, st));
-    if (dev_obj) CU(d2h(h_f, e->scratch_c.as<double>(), 1, st));
     double* h_pubs = reinterpret_cast<double*>(static_cast<unsigned char*>(ctx->pin) + pub_off);
-    if (pubs_staged) CU(d2h(h_pubs, e->pub_log.as<double>(), (size_t)(pub_stage * 4), st));
+    {
+        CU(e->fin_stage.reserve(need));
+        PackParams pk = {};
+        pk.dst = e->fin_stage.as<unsigned char>();
+        unsigned char* hb = static_cast<unsigned char*>(ctx->pin);
+        auto add = [&](const void* src, const void* host_at, size_t bytes) {
+            if (bytes == 0) return;
+            pk.seg[pk.n++] = PackSeg{static_cast<const unsigned char*>(src),
+                                     (int64_t)(static_cast<const unsigned char*>(host_at) - hb), (int64_t)bytes};
+        };
+        add(e->inc_obj.p, h_obj, (size_t)W * 8);
+        add(e->err_first.p, h_errf, (size_t)W * 4);
+        if (R > 0) {
+            add(e->log_acc.p, h_lacc, (size_t)(R * W));
+            add(e->log_obj.p, h_lobj, (size_t)(R * W) * 8);
+        }
+        add(e->nd_total.p, h_ndt, 8);
+        add(e->pub_count.p, h_npub, 8);
+        add(sel_d, h_sel, 8);
+        add(bc_d, h_bc, (size_t)kn * 8);
+        add(bf_d, h_bf, (size_t)k);
+        if (dev_obj) add(e->scratch_c.p, h_f, 8);
+        if (pubs_staged) add(e->pub_log.p, h_pubs, (size_t)pub_stage * 32);
+        pack_segments_kernel<<<8, 256, 0, st>>>(pk);
+        CU(cudaGetLastError());
+        ctx->launches += 1;
+        CU(cudaMemcpyAsync(ctx->pin, e->fin_stage.p, need, cudaMemcpyDeviceToHost, st));
+    }
     CU(cudaStreamSynchronize(st));
     const unsigned long long ndt = *h_ndt;
     const int64_t npub = *h_npub;
