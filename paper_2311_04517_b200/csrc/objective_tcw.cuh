@@ -70,6 +70,30 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kv = obj_kv(p);
     const double* __restrict__ Cg = p.C;  // [kv x NPW] fp64 centres (L1-resident)
+    const int64_t m = p.m;
+    const int64_t ntiles = (m + TG::M - 1) / TG::M;
+    const int my = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    // the producer thread initialises the barriers and puts the first ring of tiles in flight before the
+    // centre tables are built: the prologue overlaps the first HBM round trip (as in objective_tc.cuh)
+    const int pre = my < STAGES ? my : STAGES;
+    if (warp == EW && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 4);  // the 4 warps of the group that read the tile's rows
+        }
+        for (int b = 0; b < NB; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        mbar_init_fence();
+        fence_proxy_async();
+        for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(&full[i], (uint32_t)TILE);
+            const int row0 = (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::M);
+#pragma unroll
+            for (int a = 0; a < NA; ++a) tma_load_2d(ring + i * TILE + a * TG::SUB, &tmap, 32 * a, row0, &full[i]);
+        }
+    }
 
     // -c for the fp32-mode row cost as hi + lo: hi = B / 2 (exact: the tf32 -2c of the MMA operand,
     // read from the B tile), lo = fl32(-c - hi) (|lo| <= 2^-11 |c|, so hi + lo is -c to 2^-35 |c|)
@@ -98,32 +122,18 @@ __global__ void __launch_bounds__(TcwGeo<NA>::THREADS, 1)
                      "r"(TG::TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 4);  // the 4 warps of the group that read the tile's rows
-        }
-        for (int b = 0; b < NB; ++b) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
-        }
-        mbar_init_fence();
-    }
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tm = s_tmem;
-    const int64_t m = p.m;
-    const int64_t ntiles = (m + TG::M - 1) / TG::M;
-    const int my = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
     double cost = 0.0;
 
     if (warp == EW) {  // ---- TMA producer: NA box loads per tile
         if (lane == 0) {
-            int s = 0;
-            uint32_t pl = 0;
-            for (int i = 0; i < my; ++i) {
+            int s = pre == STAGES ? 0 : pre;
+            uint32_t pl = pre == STAGES ? 1u : 0u;
+            for (int i = pre; i < my; ++i) {
                 if (i >= STAGES) mbar_wait_cta(&empty[s], pl ^ 1u);
                 mbar_expect_tx(&full[s], (uint32_t)TILE);
                 const int row0 = (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * TG::M);
