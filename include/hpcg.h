@@ -1,7 +1,7 @@
 /* hpcg.h — C-ABI of the B200-native HPClust hot path (libhpcg.so).
  *
  * The drop-in boundary: plain pointers, sizes and status codes; no C++ or torch types.
- * The C++ drop-in headers include/hpclust/*.hpp (same namespace, types and signatures as
+ * The C++ drop-in headers include/hpclust/ (*.hpp) (same namespace, types and signatures as
  * the reference's proj/include/hpclust) are implemented on top of these calls, and
  * INTEGRATION.md shows the ctypes binding the Python mirror uses.
  *
