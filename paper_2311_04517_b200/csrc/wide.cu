@@ -1204,7 +1204,6 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
         // R rows per thread per round (rows base + tid + AT r): the round's sort and fold barriers
         // are shared by AT * AR rows; thread t still visits rows r0 + t + AT i in order
         int labr[AR];
-        double bestd[AR];
         bool validr[AR];
 #pragma unroll
         for (int r = 0; r < AR; ++r) {
@@ -1224,11 +1223,7 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
                 tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
             }
             if (tie) exact_ties<T>(tie, S, base + (int64_t)AT * r + warp * 32, n, k, Cm, lab);
-            bestd[r] = 0.0;
-            if (valid) {  // the row's cost: its squared distance to its centre
-                bestd[r] = dist_cost<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
-                labels[i] = lab;
-            }
+            if (valid) labels[i] = lab;
             labr[r] = lab;
         }
         // stable counting sort of the round's rows by label: (row slot r, warp) major, lane minor
@@ -1273,7 +1268,6 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
         for (int r = 0; r < AR; ++r) {
             if (validr[r])
                 sorted[wcnt[(r * AW + warp) * k + labr[r]] + __popc(peersr[r] & ((1u << lane) - 1u))] = tid + AT * r;
-            cost += validr[r] ? bestd[r] : 0.0;  // per-thread running sum (thread t: rows r0 + t + AT*i, in order)
         }
         __syncthreads();              // sorted[] complete before the sums read it
         // per-cluster sums of this round: warp w takes clusters w, w+8, ..., walks the cluster's
@@ -1288,6 +1282,13 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
             if (q0 == q1) continue;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             if (dq < n) {
+                // the rows' objective terms ride along: this lane's four coordinates of centre j stay in
+                // registers and its squared differences go to its own running cost (fixed order: cluster,
+                // then row; reduced over the CTA at the end) -- no second walk over the rows
+                const double* cp = Cm + (int64_t)j * n + dq;
+                const double c0 = cp[0], c1 = dq + 1 < n ? cp[1] : 0.0, c2 = dq + 2 < n ? cp[2] : 0.0,
+                             c3 = dq + 3 < n ? cp[3] : 0.0;
+                double ca = 0.0, cb = 0.0;
 #pragma unroll 4
                 for (int q = q0 + gi; q < q1; q += RPS) {
                     double v[4];
@@ -1296,7 +1297,13 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
                     a1 += v[1];
                     a2 += v[2];
                     a3 += v[3];
+                    const double e0 = v[0] - c0, e1 = v[1] - c1, e2 = v[2] - c2, e3 = v[3] - c3;
+                    ca = fma(e0, e0, ca);
+                    cb = fma(e1, e1, cb);
+                    ca = fma(e2, e2, ca);
+                    cb = fma(e3, e3, cb);
                 }
+                cost += ca + cb;
             }
             for (int o = LR; o < 32; o <<= 1) {
                 a0 += __shfl_xor_sync(0xffffffffu, a0, o);
@@ -1317,6 +1324,10 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
             if (q0 == q1) continue;
             for (int d0 = lane * 4; d0 < n; d0 += 128) {
                 double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                const double* cp = Cm + (int64_t)j * n + d0;
+                const double c0 = cp[0], c1 = d0 + 1 < n ? cp[1] : 0.0, c2 = d0 + 2 < n ? cp[2] : 0.0,
+                             c3 = d0 + 3 < n ? cp[3] : 0.0;
+                double ca = 0.0, cb = 0.0;
 #pragma unroll 4
                 for (int q = q0; q < q1; ++q) {
                     double v[4];
@@ -1325,7 +1336,13 @@ __global__ void __launch_bounds__(AT, WIDE_ASSIGN_MINB) wide_assign_kernel(const
                     a1 += v[1];
                     a2 += v[2];
                     a3 += v[3];
+                    const double e0 = v[0] - c0, e1 = v[1] - c1, e2 = v[2] - c2, e3 = v[3] - c3;
+                    ca = fma(e0, e0, ca);
+                    cb = fma(e1, e1, cb);
+                    ca = fma(e2, e2, ca);
+                    cb = fma(e3, e3, cb);
                 }
+                cost += ca + cb;
                 double* aj = acc + (int64_t)j * n + d0;
                 aj[0] += a0;
                 if (d0 + 1 < n) aj[1] += a1;
