@@ -106,42 +106,6 @@ __device__ __forceinline__ double dist1(const T* __restrict__ x, int n, const do
     return acc;
 }
 
-// a row's squared distance for the Lloyd objective (not an argmin or a D^2 value, so the reference's
-// sequential order is not needed: four interleaved fp64 FMA chains, ~1e-16 relative of the same value)
-template <typename T>
-__device__ __forceinline__ double dist_cost(const T* __restrict__ x, int n, const double* __restrict__ c, bool vec) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int d = 0;
-    if (vec) {
-        if constexpr (sizeof(T) == 4) {
-            for (; d + 4 <= n; d += 4) {
-                const float4 f = __ldg(reinterpret_cast<const float4*>(x + d));
-                const double2 c01 = __ldg(reinterpret_cast<const double2*>(c + d));
-                const double2 c23 = __ldg(reinterpret_cast<const double2*>(c + d + 2));
-                const double e0 = (double)f.x - c01.x, e1 = (double)f.y - c01.y;
-                const double e2 = (double)f.z - c23.x, e3 = (double)f.w - c23.y;
-                a0 = fma(e0, e0, a0);
-                a1 = fma(e1, e1, a1);
-                a2 = fma(e2, e2, a2);
-                a3 = fma(e3, e3, a3);
-            }
-        } else {
-            for (; d + 2 <= n; d += 2) {
-                const double2 f = __ldg(reinterpret_cast<const double2*>(x + d));
-                const double2 c01 = __ldg(reinterpret_cast<const double2*>(c + d));
-                const double e0 = f.x - c01.x, e1 = f.y - c01.y;
-                a0 = fma(e0, e0, a0);
-                a1 = fma(e1, e1, a1);
-            }
-        }
-    }
-    for (; d < n; ++d) {
-        const double e = (double)x[d] - __ldg(c + d);
-        a2 = fma(e, e, a2);
-    }
-    return (a0 + a1) + (a2 + a3);
-}
-
 // fixed-order tree sum over a CTA of AT threads; result in every thread
 template <int AT>
 __device__ double cta_sum_t(double v, double* red) {
