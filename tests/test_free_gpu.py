@@ -180,3 +180,19 @@ def test_free_engine_reset_and_rerun():
     assert np.array_equal(o1, o2) and r1.distance_evals == r2.distance_evals and r1.total_samples == r2.total_samples == 20
     assert np.array_equal(r1.centroids, r2.centroids) and r1.full_objective == r2.full_objective
     assert not np.array_equal(o1, o3)
+
+
+def test_free_config2_scale_many_groups():
+    # the benchmark shape's worker count (256 workers, s = 20,000, k = 10, n = 16) on 16 streams: default
+    # grouping, cooperative; every worker keeps stepping, publications keep improving, nothing stalls
+    rs = np.random.default_rng(26)
+    means = rs.uniform(-10, 10, (10, 16))
+    X = (means[rs.integers(0, 10, 1_000_000)] + rs.standard_normal((1_000_000, 16))).astype(np.float32)
+    W = 256
+    cfg = hp.EngineConfig(k=10, sample_size=20000, n_workers=W, strategy="cooperative", master_seed=6, rng="philox",
+                          time_limit=0.2, free_running=True)
+    r, smp, tw, Cw, fw, ow = run_engine(X, cfg)
+    _check_invariants(r, smp, tw, ow, W)
+    assert smp.min() >= 20 and smp.max() - smp.min() <= 0.5 * smp.max()  # ~1 ms per lap of 256 workers
+    assert len(r.publications) >= 1 and r.publications[-1, 2] == ow.min()
+    assert 0.2 <= r.wall_seconds < 1.5
