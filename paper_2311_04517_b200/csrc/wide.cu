@@ -1738,7 +1738,7 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
     wide_lloyd_begin_kernel<<<Wb, 32, 0, st>>>(p, b);
     const int kpad = (k + kKT - 1) / kKT * kKT, n4 = (n + 3) & ~3;
     // the assign pass in rounds of kAT rows (fewer round barriers per row than kWT)
-    constexpr int kAT = 256, kAR = 4;  // 1024 rows per round
+    constexpr int kAT = 256, kAR = 8;  // 2048 rows per round
     const size_t smem = (size_t)(kn + k + kAT + 1) * 8 + (size_t)kpad * n4 * 4 + (size_t)kpad * 4 +
                         (size_t)(kAR * (kAT / 32) * k + k + 1 + kAT * kAR) * 4;
     // the assign pass specialised for common row widths (index and loop arithmetic at compile time)
