@@ -398,6 +398,7 @@ __global__ void wide_init_kernel(const StepParams p, int w0, WideBufs b) {
 
 // D^2 from every valid centre (including a first centre just drawn): the screen's argmin over
 // the valid centres (near ties exact) and the reference distance to it
+constexpr int kD2Blocks = 8;  // blocks of kWT rows per CTA of the D^2 initialisation
 template <typename T, int NP = 0>
 __global__ void __launch_bounds__(kWT) wide_d2init_kernel(const StepParams p, WideBufs b) {
     extern __shared__ __align__(16) float wrec[];
@@ -421,30 +422,35 @@ __global__ void __launch_bounds__(kWT) wide_d2init_kernel(const StepParams p, Wi
         s_j = j1;
     }
     __syncthreads();
+    // a CTA covers kD2Blocks blocks of kWT rows: the per-CTA prologue (valid-centre scan, records) was
+    // the cost of this pass when every CTA did one row per thread (200 K CTAs at config 5)
+    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
+    const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
     if (s_nv == 1) {  // one valid centre (round 0: the first centre just drawn): D^2 is its distance
-        const int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x;
-        if (i >= s) return;
-        const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
-        const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
-        b.d2[(int64_t)w * s + i] = dist1<T>(S + i * n, n, Cm + (int64_t)s_j * n, vecd);
+        const double* c1 = Cm + (int64_t)s_j * n;
+#pragma unroll 2
+        for (int t = 0; t < kD2Blocks; ++t) {
+            const int64_t i = ((int64_t)blockIdx.x * kD2Blocks + t) * kWT + threadIdx.x;
+            if (i < s) b.d2[(int64_t)w * s + i] = dist1<T>(S + i * n, n, c1, vecd);
+        }
         return;
     }
     build_records(Cm, k, kpad, n, n4, rec, ccs, fl);
     const float cmax = records_cmax(ccs, kpad, red_f);
     const float kappa = 2.0f * (float)((n + 1) / 2 + 12) * 5.9604645e-8f;
     const bool vec = sizeof(T) == 4 && (n & 3) == 0;
-    const int64_t i = (int64_t)blockIdx.x * kWT + threadIdx.x;
-    const bool valid = i < s;
-    const T* S = static_cast<const T*>(b.S) + (int64_t)w * s * n;
-    int lab = 0;
-    float m1 = 0.f, m2 = 0.f, xx = 0.f;
-    if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
-    const float sc = sqrtf(xx) * 1.0001f + cmax;
-    const unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
-    if (tie) exact_ties_masked<T>(tie, S, i - (threadIdx.x & 31), n, k, Cm, fl, lab);
-    if (!valid) return;
-    const bool vecd = sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0;
-    b.d2[(int64_t)w * s + i] = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
+    for (int t = 0; t < kD2Blocks; ++t) {
+        const int64_t i = ((int64_t)blockIdx.x * kD2Blocks + t) * kWT + threadIdx.x;
+        if (i - (threadIdx.x & 31) >= s) break;  // warp-uniform: the whole warp is past the sample
+        const bool valid = i < s;
+        int lab = 0;
+        float m1 = 0.f, m2 = 0.f, xx = 0.f;
+        if (valid) screen_row<T>(S + i * n, n, n4, kpad, rec, ccs, vec, lab, m1, m2, xx);
+        const float sc = sqrtf(xx) * 1.0001f + cmax;
+        const unsigned tie = __ballot_sync(0xffffffffu, valid && !(m2 - m1 > kappa * sc * sc));
+        if (tie) exact_ties_masked<T>(tie, S, i - (threadIdx.x & 31), n, k, Cm, fl, lab);
+        if (valid) b.d2[(int64_t)w * s + i] = dist1<T>(S + i * n, n, Cm + (int64_t)lab * n, vecd);
+    }
 }
 
 // ---------------------------------------------------------------- K-means++ slot
@@ -1670,7 +1676,8 @@ cudaError_t run_batch(const StepParams& p, int w0, int Wb, cudaStream_t st, std:
         auto go = [&](auto kern) -> cudaError_t {
             cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs);
             if (e2 != cudaSuccess) return e2;
-            kern<<<rows_grid, kWT, rs, st>>>(p, b);
+            const dim3 d2_grid((unsigned)((s + (int64_t)kWT * kD2Blocks - 1) / ((int64_t)kWT * kD2Blocks)), (unsigned)Wb);
+            kern<<<d2_grid, kWT, rs, st>>>(p, b);
             return cudaSuccess;
         };
         e = n == 8 ? go(wide_d2init_kernel<T, 8>) : n == 16 ? go(wide_d2init_kernel<T, 16>)
