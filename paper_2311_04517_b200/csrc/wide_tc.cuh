@@ -37,7 +37,7 @@ template <int NA>
 struct WtcGeo {
     static constexpr int N = kTcwN, M = 128, NPW = 32 * NA;
     static constexpr int SUB = M * 128, TILE = NA * SUB;
-    static constexpr int STAGES = 163840 / TILE < 6 ? 163840 / TILE : 6;  // 160 KB ring
+    static constexpr int STAGES = 196608 / TILE < 6 ? 196608 / TILE : 6;  // 192 KB ring (3 stages at n = 128)
     static constexpr int BSUB = N * 128, BT = NA * BSUB;                  // one B buffer
     static constexpr int TCOLS = 512, NB = TCOLS / N;
     static constexpr int EPI_WARPS = 8, THREADS = (EPI_WARPS + 2) * 32;
