@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define HPCG_ABI_VERSION 1
+#define HPCG_ABI_VERSION 2 /* 2: hpcg_engine_cfg gained free_running / free_group */
 #if defined(__GNUC__)
 #pragma GCC visibility push(default)
 #endif

@@ -13,6 +13,8 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("HPCG_LIB_OVERRIDE") or (Path(__file__).resolve().parent / "libhpcg.so"))  # dev A/B
 
 # Every symbol include/hpcg.h declares (checked by tests/test_abi.py).
+ABI_VERSION = 2  # include/hpcg.h HPCG_ABI_VERSION
+
 EXPORTS = (
     "hpcg_last_error", "hpcg_abi_version", "hpcg_ctx_create", "hpcg_ctx_destroy", "hpcg_ctx_set_stream",
     "hpcg_ctx_synchronize", "hpcg_ctx_launch_count", "hpcg_dataset_upload", "hpcg_dataset_wrap",
@@ -104,6 +106,10 @@ def _load():
     if not LIB_PATH.exists():
         raise ImportError(f"{LIB_PATH} is not built (run __graft_entry__.build()); there is no CPU fallback")
     lib = C.CDLL(str(LIB_PATH))
+    lib.hpcg_abi_version.restype = C.c_int
+    if lib.hpcg_abi_version() != ABI_VERSION:  # the structs below mirror one layout of include/hpcg.h
+        raise ImportError(f"{LIB_PATH} has ABI version {lib.hpcg_abi_version()}, this binding expects {ABI_VERSION}: "
+                          "rebuild with __graft_entry__.build()")
     P, I64, I32, U64, D = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_double
     sig = {
         "hpcg_last_error": (C.c_char_p, []),

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(str(_lib.LIB_PATH))
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.hpcg_abi_version() == 1
+    assert lib.hpcg_abi_version() == 2  # hpcg.h HPCG_ABI_VERSION (the binding checks it at load)
 
 
 def test_library_is_sm100a_cuda_code():
