@@ -76,7 +76,12 @@ inline void check(int rc) {
 inline hpcg_ctx* context() {
     struct Holder {
         hpcg_ctx* c = nullptr;
-        Holder() { check(hpcg_ctx_create(0, &c)); }
+        Holder() {
+            // these headers mirror one struct layout of hpcg.h: refuse a library built from another
+            if (hpcg_abi_version() != HPCG_ABI_VERSION)
+                throw std::runtime_error("hpcg: libhpcg.so ABI version differs from include/hpcg.h (rebuild the library)");
+            check(hpcg_ctx_create(0, &c));
+        }
         ~Holder() { hpcg_ctx_destroy(c); }
     };
     static Holder h;
